@@ -1,0 +1,139 @@
+/*
+ * turbo_ns.h -- C ABI of libturbons.so: AOL-preconditioned Newton-Schulz
+ * orthogonalisation ("Turbo-Muon", arxiv 2512.04632) on NVIDIA B200 (sm_100a).
+ *
+ * What is computed (PAPER.md line numbers, "P:Lnnn"):
+ *   Let X be m x n and Xh its short-side orientation (Xh = X if m >= n, else X^T;
+ *   reading R2), N = min(m,n), M = max(m,n).  With coefficients
+ *   (a_k, b_k, c_k), k = 1..T:
+ *     precond = AOL        : A0 = Xh^T Xh (Eq. 7); s_i = (sum_j |A0_ij|)^(-1/2)
+ *                            (Eq. 8); X1 = Xh diag(s) (Eq. 9); A1 = diag(s) A0
+ *                            diag(s) (Alg. 2 l.4) -- the Gram is reused.
+ *     precond = FROBENIUS  : s = 1/||Xh||_F (Eqs. 10-11; Alg. 1).
+ *     precond = NONE       : X1 = Xh (caller guarantees ||X||_2 <= 1).
+ *     for k = 1..T:  A_k = X_k^T X_k   (Eq. 3; k = 1 reuses A1)
+ *                    B_k = b_k A_k + c_k A_k A_k          (Eq. 4)
+ *                    X_{k+1} = a_k X_k + X_k B_k          (Eq. 5)
+ *   The result X_{T+1} (transposed back for m < n) is written in the caller's layout.
+ *
+ * Conventions for every entry point:
+ *   - Matrices are dense row-major, leading dimension = number of columns, in DEVICE
+ *     memory of the current CUDA device, 16-byte aligned.  Element type = `dtype`
+ *     (NS_BF16: bfloat16 storage, fp32 accumulation; NS_FP32: fp32 throughout).
+ *   - `coeffs` is a HOST array of 3*iters floats (a_1,b_1,c_1,a_2,...); it is read
+ *     before the call returns (the caller may free it afterwards).
+ *   - Calls are asynchronous on `stream` (a cudaStream_t; NULL = legacy default
+ *     stream) and never synchronise, except ns_read_flags and the first call for a
+ *     given problem list (plan build: workspace allocation + descriptor upload).
+ *   - Caller-owned memory is never freed by the library.  Workspace (a ping-pong
+ *     buffer of the matrix size plus two N x N buffers and small tables per matrix)
+ *     is owned by the library, cached per problem list, and released by ns_shutdown.
+ *   - All argument checks happen on the host before anything is enqueued; on any
+ *     error nothing is enqueued and no memory is touched.  Numerical conditions
+ *     (zero row-sum, zero matrix, non-finite values) do NOT fail a call: they set
+ *     device flags readable with ns_read_flags (reading R4).
+ *   - Thread-safety: calls are serialised by an internal mutex; distinct streams are
+ *     fine.  Determinism: results are bitwise reproducible for identical inputs,
+ *     independent of how matrices are grouped into calls.
+ */
+#ifndef TURBO_NS_H_
+#define TURBO_NS_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define NS_ABI_VERSION 1
+
+typedef enum {
+  NS_OK = 0,
+  NS_ERR_INVALID_VALUE = 1, /* bad shape / iters / coeffs / enum / NULL pointer      */
+  NS_ERR_NOT_SUPPORTED = 2, /* e.g. misaligned pointer                               */
+  NS_ERR_WORKSPACE = 3,     /* device allocation failed                              */
+  NS_ERR_CUDA = 4           /* a CUDA runtime/driver call or launch failed           */
+} ns_status;
+
+typedef enum {
+  NS_PRECOND_NONE = 0,      /* no scaling; caller guarantees ||X||_2 <= 1             */
+  NS_PRECOND_FROBENIUS = 1, /* Alg. 1: X / ||X||_F   (Muon, Muon+)                   */
+  NS_PRECOND_AOL = 2        /* Alg. 2: AOL column scaling with Gram reuse (Turbo-Muon) */
+} ns_precond;
+
+typedef enum {
+  NS_BF16 = 0, /* bf16 storage of X, A, B; fp32 accumulation (tcgen05 tensor cores) */
+  NS_FP32 = 1  /* fp32 storage and fp32 FFMA arithmetic ("exact" mode)              */
+} ns_dtype;
+
+/* Flag bits reported by ns_read_flags. */
+#define NS_FLAG_ZERO_SCALE 0x1u /* a zero AOL row-sum (zero column) or zero matrix (Frobenius) */
+#define NS_FLAG_NONFINITE 0x2u  /* a non-finite value was produced                        */
+
+/* In place: `batch` matrices of m x n at X, X + m*n, ... (contiguous) are each
+ * overwritten with NS_T(precond(X_i)), T = iters (1..64). */
+ns_status ns_orthogonalize(void* X, int64_t m, int64_t n, int64_t batch, int iters,
+                           const float* coeffs, ns_precond precond, ns_dtype dtype,
+                           void* stream);
+
+/* Grouped: `count` matrices of arbitrary shapes m[i] x n[i].  X is a HOST array of
+ * device pointers (inputs); out is a HOST array of device pointers receiving the
+ * results (out may be NULL, or out[i] == X[i], for in place; out[i] must not
+ * otherwise overlap any X[j]).  Every NS step runs as ONE launch over all matrices
+ * (3*iters + 1 launches in total).  Results are bitwise identical to calling
+ * ns_orthogonalize on each matrix alone. */
+ns_status ns_orthogonalize_batched(void* const* X, void* const* out, const int64_t* m,
+                                   const int64_t* n, int64_t count, int iters,
+                                   const float* coeffs, ns_precond precond, ns_dtype dtype,
+                                   void* stream);
+
+/* Bytes of device workspace the library will hold for this problem list. */
+ns_status ns_workspace_size(const int64_t* m, const int64_t* n, int64_t count,
+                            ns_dtype dtype, size_t* bytes);
+
+/* SYNCHRONISES `stream`, returns the OR of NS_FLAG_* raised since the last read on
+ * the current device, and clears them. */
+ns_status ns_read_flags(void* stream, uint32_t* flags);
+
+/* Number of kernels the library launched on this process since load (host counter). */
+uint64_t ns_launch_count(void);
+
+/* Execution-path override for testing: 0 = auto (tcgen05 for aligned bf16),
+ * 1 = force the SIMT (CUDA-core) kernels.  Returns the previous value. */
+int ns_set_path(int path);
+
+const char* ns_status_string(ns_status s);
+const char* ns_last_error(void); /* detail of the last non-OK status (thread-local) */
+int ns_abi_version(void);
+void ns_shutdown(void); /* synchronises the device, frees workspace and plan caches */
+
+/* ---------------------------------------------------------------------------------
+ * Single-step entry points (each is one step of the path; used by the step-level
+ * parity tests).  X is m x n row-major; N = min(m,n); all outputs are dtype.
+ * --------------------------------------------------------------------------------- */
+
+/* A = Xh^T Xh (N x N, both triangles written)        -- Eq. 3 / Eq. 7. */
+ns_status nsx_gram(const void* X, int64_t m, int64_t n, void* A, ns_dtype dtype,
+                   void* stream);
+
+/* In place on A (N x N symmetric): s from A (AOL: Eq. 8; FROBENIUS: 1/sqrt(trace A) =
+ * 1/||X||_F, Eq. 10), then A <- diag(s) A diag(s) (Alg. 2 l.4).  s: device fp32[N]. */
+ns_status nsx_precondition(void* A, int64_t N, ns_precond precond, float* s,
+                           ns_dtype dtype, void* stream);
+
+/* B = (b A + c A A) diag(s)  (Eq. 4; s == NULL means s = 1). */
+ns_status nsx_poly(const void* A, int64_t N, float b, float c, const float* s, void* B,
+                   ns_dtype dtype, void* stream);
+
+/* Out = a Xh diag(s) + Xh B^T in the caller's (m x n) layout, B as produced by
+ * nsx_poly.  With B = B1 diag(s) this is a X1 + X1 B1 for X1 = Xh diag(s): Eq. 5 with
+ * the AOL scaling of iteration 1 folded in (X1 is never materialised).  s == NULL
+ * means s = 1 (then B is symmetric and B^T = B).  Out must not overlap X. */
+ns_status nsx_update(const void* X, int64_t m, int64_t n, const void* B, float a,
+                     const float* s, void* Out, ns_dtype dtype, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TURBO_NS_H_ */

@@ -1,0 +1,192 @@
+"""Python binding of libturbons.so: argument marshalling only.
+
+Every step of the path runs in the library's CUDA kernels; this module passes device
+pointers, shapes, coefficients and the current CUDA stream through the C ABI
+(include/turbo_ns.h).  PyTorch is used for device memory and streams only.
+"""
+from __future__ import annotations
+
+import ctypes
+from typing import Sequence
+
+import torch
+
+from . import coeffs as _coeffs
+from ._lib import DTYPE_BF16, DTYPE_FP32, PRECOND, check, lib
+
+__all__ = [
+    "orthogonalize", "orthogonalize_list", "workspace_size", "read_flags", "launch_count",
+    "set_path", "shutdown", "gram", "precondition", "poly", "update", "default_coeffs",
+]
+
+
+def _dtype_code(t: torch.Tensor) -> int:
+    if t.dtype == torch.bfloat16:
+        return DTYPE_BF16
+    if t.dtype == torch.float32:
+        return DTYPE_FP32
+    raise TypeError(f"unsupported dtype {t.dtype}; use bfloat16 or float32")
+
+
+def _check_tensor(t: torch.Tensor, name: str = "tensor") -> None:
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous (row-major)")
+
+
+def _stream(t: torch.Tensor | None = None) -> ctypes.c_void_p:
+    dev = t.device if t is not None else None
+    return ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
+
+
+def _coeff_array(iters: int, coeffs, precond: str):
+    if coeffs is None:
+        coeffs = default_coeffs(iters, precond)
+    flat = [float(v) for t in coeffs for v in t] if len(coeffs) and hasattr(coeffs[0], "__len__") \
+        else [float(v) for v in coeffs]
+    if len(flat) != 3 * iters:
+        raise ValueError(f"need {iters} (a, b, c) triples, got {len(flat)} values")
+    return (ctypes.c_float * len(flat))(*flat)
+
+
+def default_coeffs(iters: int = 4, precond: str = "aol"):
+    """Turbo-Muon: the last `iters` Muon+ triples; Muon+ for Frobenius."""
+    return _coeffs.turbo(iters) if precond == "aol" else _coeffs.muon_plus(iters)
+
+
+def orthogonalize(x: torch.Tensor, iters: int = 4, precond: str = "aol", coeffs=None) -> torch.Tensor:
+    """In place: x (m x n, or batch x m x n) <- NS_iters(precond(x)).  Returns x."""
+    _check_tensor(x, "x")
+    if x.dim() == 2:
+        batch, (m, n) = 1, x.shape
+    elif x.dim() == 3:
+        batch, m, n = x.shape
+    else:
+        raise ValueError("x must be 2-D or 3-D")
+    if x.numel() == 0:
+        return x
+    c = _coeff_array(iters, coeffs, precond)
+    with torch.cuda.device(x.device):
+        st = lib.ns_orthogonalize(ctypes.c_void_p(x.data_ptr()), m, n, batch, iters, c,
+                                  PRECOND[precond], _dtype_code(x), _stream(x))
+    check(st, "ns_orthogonalize")
+    return x
+
+
+def orthogonalize_list(xs: Sequence[torch.Tensor], out: Sequence[torch.Tensor] | None = None,
+                       iters: int = 4, precond: str = "aol", coeffs=None) -> list[torch.Tensor]:
+    """Grouped call: one launch per NS step over all matrices.  In place unless `out`."""
+    xs = list(xs)
+    if not xs:
+        return []
+    dt = _dtype_code(xs[0])
+    for i, t in enumerate(xs):
+        _check_tensor(t, f"xs[{i}]")
+        if t.dim() != 2 or _dtype_code(t) != dt or t.device != xs[0].device:
+            raise ValueError("all matrices must be 2-D, same dtype, same device")
+    if out is not None:
+        out = list(out)
+        if len(out) != len(xs):
+            raise ValueError("out must match xs")
+        for i, (o, t) in enumerate(zip(out, xs)):
+            _check_tensor(o, f"out[{i}]")
+            if o.shape != t.shape or o.dtype != t.dtype:
+                raise ValueError("out[i] must match xs[i] in shape and dtype")
+    cnt = len(xs)
+    X = (ctypes.c_void_p * cnt)(*[t.data_ptr() for t in xs])
+    O = (ctypes.c_void_p * cnt)(*[t.data_ptr() for t in out]) if out is not None else None
+    M = (ctypes.c_int64 * cnt)(*[t.shape[0] for t in xs])
+    N = (ctypes.c_int64 * cnt)(*[t.shape[1] for t in xs])
+    c = _coeff_array(iters, coeffs, precond)
+    with torch.cuda.device(xs[0].device):
+        st = lib.ns_orthogonalize_batched(X, O, M, N, cnt, iters, c, PRECOND[precond], dt,
+                                          _stream(xs[0]))
+    check(st, "ns_orthogonalize_batched")
+    return out if out is not None else xs
+
+
+def workspace_size(shapes: Sequence[tuple[int, int]], dtype=torch.bfloat16) -> int:
+    cnt = len(shapes)
+    M = (ctypes.c_int64 * cnt)(*[s[0] for s in shapes])
+    N = (ctypes.c_int64 * cnt)(*[s[1] for s in shapes])
+    out = ctypes.c_size_t(0)
+    check(lib.ns_workspace_size(M, N, cnt, DTYPE_BF16 if dtype == torch.bfloat16 else DTYPE_FP32,
+                                ctypes.byref(out)), "ns_workspace_size")
+    return out.value
+
+
+def read_flags(device=None) -> int:
+    """Synchronises; returns and clears NS_FLAG_* bits (1: zero scale, 2: non-finite)."""
+    f = ctypes.c_uint32(0)
+    with torch.cuda.device(device if device is not None else torch.cuda.current_device()):
+        check(lib.ns_read_flags(_stream(), ctypes.byref(f)), "ns_read_flags")
+    return int(f.value)
+
+
+def launch_count() -> int:
+    return int(lib.ns_launch_count())
+
+
+def set_path(path: int) -> int:
+    """0 = auto (tcgen05 for aligned bf16), 1 = force the CUDA-core kernels."""
+    return int(lib.ns_set_path(int(path)))
+
+
+def shutdown() -> None:
+    lib.ns_shutdown()
+
+
+# ---------------------------------------------------------------------- single steps
+def _short(m: int, n: int) -> int:
+    return min(m, n)
+
+
+def gram(x: torch.Tensor) -> torch.Tensor:
+    """A = Xh^T Xh (N x N), Eq. 3 / Eq. 7."""
+    _check_tensor(x, "x")
+    m, n = x.shape
+    N = _short(m, n)
+    a = torch.empty((N, N), dtype=x.dtype, device=x.device)
+    with torch.cuda.device(x.device):
+        check(lib.nsx_gram(ctypes.c_void_p(x.data_ptr()), m, n, ctypes.c_void_p(a.data_ptr()),
+                           _dtype_code(x), _stream(x)), "nsx_gram")
+    return a
+
+
+def precondition(a: torch.Tensor, precond: str = "aol") -> torch.Tensor:
+    """In place a <- diag(s) a diag(s); returns s (fp32).  Eqs. 8-10, Alg. 2 l.4."""
+    _check_tensor(a, "a")
+    N = a.shape[0]
+    s = torch.empty((N,), dtype=torch.float32, device=a.device)
+    with torch.cuda.device(a.device):
+        check(lib.nsx_precondition(ctypes.c_void_p(a.data_ptr()), N, PRECOND[precond],
+                                   ctypes.c_void_p(s.data_ptr()), _dtype_code(a), _stream(a)),
+              "nsx_precondition")
+    return s
+
+
+def poly(a: torch.Tensor, b: float, c: float, s: torch.Tensor | None = None) -> torch.Tensor:
+    """B = (b A + c A A) diag(s), Eq. 4."""
+    _check_tensor(a, "a")
+    N = a.shape[0]
+    out = torch.empty_like(a)
+    sp = ctypes.c_void_p(s.data_ptr()) if s is not None else None
+    with torch.cuda.device(a.device):
+        check(lib.nsx_poly(ctypes.c_void_p(a.data_ptr()), N, float(b), float(c), sp,
+                           ctypes.c_void_p(out.data_ptr()), _dtype_code(a), _stream(a)), "nsx_poly")
+    return out
+
+
+def update(x: torch.Tensor, bmat: torch.Tensor, a: float, s: torch.Tensor | None = None) -> torch.Tensor:
+    """Out = a Xh diag(s) + Xh B^T in x's layout, Eq. 5 (iteration-1 scaling folded)."""
+    _check_tensor(x, "x")
+    _check_tensor(bmat, "B")
+    m, n = x.shape
+    out = torch.empty_like(x)
+    sp = ctypes.c_void_p(s.data_ptr()) if s is not None else None
+    with torch.cuda.device(x.device):
+        check(lib.nsx_update(ctypes.c_void_p(x.data_ptr()), m, n, ctypes.c_void_p(bmat.data_ptr()),
+                             float(a), sp, ctypes.c_void_p(out.data_ptr()), _dtype_code(x), _stream(x)),
+              "nsx_update")
+    return out

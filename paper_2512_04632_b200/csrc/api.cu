@@ -1,0 +1,773 @@
+// C ABI of libturbons.so (include/turbo_ns.h): argument checking, planning (shape
+// orientation, ping-pong buffers, workspace, TMA descriptors, grouped job tables) and
+// stream-ordered enqueueing of the 3*T + 1 launches of one Newton-Schulz call.
+//
+// The step order follows PAPER.md Alg. 2 (L163-176) and Eqs. 3-5 (L116-118):
+//   k = 1:   GRAM(X0) -> A0 ; PRECOND: s (Eq. 8 / Eq. 10), A1 = diag(s) A0 diag(s)
+//            POLY: B1' = (b1 A1 + c1 A1^2) diag(s)
+//            XB:   X2 = a1 X0 diag(s) + X0 B1'^T    (= a1 X1 + X1 B1, X1 never stored)
+//   k >= 2:  GRAM(Xk) -> Ak ; POLY: Bk = bk Ak + ck Ak^2 ; XB: Xk+1 = ak Xk + Xk Bk
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/turbo_ns.h"
+#include "jobs.h"
+#include "kernels.h"
+
+namespace tns {
+
+// ---------------------------------------------------------------------------- globals
+static std::mutex g_mu;
+static uint64_t g_launches = 0;
+static int g_path = 0;
+static thread_local std::string g_err;
+
+static ns_status fail(ns_status s, const std::string& msg) {
+  g_err = msg;
+  return s;
+}
+#define CU_TRY(expr)                                                                       \
+  do {                                                                                     \
+    cudaError_t _e = (expr);                                                               \
+    if (_e != cudaSuccess)                                                                 \
+      return fail(NS_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e));        \
+  } while (0)
+
+struct DevCtx {
+  bool init = false;
+  int sms = 0;
+  int cc_major = 0, cc_minor = 0;
+  uint32_t* flags = nullptr;  // device word
+};
+static DevCtx g_dev[64];
+static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+
+static ns_status dev_ctx(DevCtx** out) {
+  int dev = 0;
+  CU_TRY(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= 64) return fail(NS_ERR_NOT_SUPPORTED, "device index >= 64");
+  DevCtx& d = g_dev[dev];
+  if (!d.init) {
+    CU_TRY(cudaDeviceGetAttribute(&d.sms, cudaDevAttrMultiProcessorCount, dev));
+    CU_TRY(cudaDeviceGetAttribute(&d.cc_major, cudaDevAttrComputeCapabilityMajor, dev));
+    CU_TRY(cudaDeviceGetAttribute(&d.cc_minor, cudaDevAttrComputeCapabilityMinor, dev));
+    CU_TRY(cudaMalloc(&d.flags, sizeof(uint32_t)));
+    CU_TRY(cudaMemset(d.flags, 0, sizeof(uint32_t)));
+    if (!g_encode) {
+      cudaDriverEntryPointQueryResult q;
+      void* fn = nullptr;
+      CU_TRY(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+      if (q != cudaDriverEntryPointSuccess || !fn)
+        return fail(NS_ERR_CUDA, "cuTensorMapEncodeTiled entry point not found");
+      g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }
+    d.init = true;
+  }
+  *out = &d;
+  return NS_OK;
+}
+
+static inline size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+// Row-major R x C bf16 matrix, 64 x 64 boxes, 128-byte swizzle, zero OOB fill.
+static ns_status encode_tmap(CUtensorMap* tm, const void* base, int64_t rows, int64_t cols) {
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)cols * 2};
+  cuuint32_t box[2] = {64, 64};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = g_encode(tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims,
+                        strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return fail(NS_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+  return NS_OK;
+}
+
+// ---------------------------------------------------------------------------- planning
+struct Mat {
+  void* x;
+  void* out;
+  int64_t m, n, M, N;
+  bool wide;
+  bool copy_in;
+  // workspace byte offsets
+  size_t w_off, a_off, b_off, s_off;
+  // tensormap indices (tcgen05 path)
+  int tm_x, tm_out, tm_w, tm_a, tm_b;
+};
+
+enum PhaseKind { PH_GEMM = 0, PH_SIMT = 1, PH_PRECOND = 2, PH_COPY = 3 };
+struct Phase {
+  PhaseKind kind;
+  size_t dev_off;  // offset of the job array in the device table
+  int njobs;
+  int64_t total;    // tiles (GEMM/SIMT) or items (PRECOND)
+  int64_t total_rows;
+  bool vec8;
+  // copies (PH_COPY)
+  std::vector<std::pair<std::pair<void*, const void*>, size_t>> copies;
+};
+
+struct Plan {
+  int device = 0;
+  ns_dtype dtype = NS_BF16;
+  bool simt = false;
+  int iters = 0;
+  ns_precond precond = NS_PRECOND_AOL;
+  std::vector<Mat> mats;
+  void* ws = nullptr;
+  size_t ws_bytes = 0;
+  void* dtab = nullptr;
+  size_t dtab_bytes = 0;
+  unsigned* barrier = nullptr;
+  std::vector<Phase> phases;
+  uint64_t last_use = 0;
+  ~Plan() {
+    if (ws) cudaFree(ws);
+    if (dtab) cudaFree(dtab);
+  }
+};
+
+static std::map<std::vector<uint64_t>, std::unique_ptr<Plan>> g_plans;
+static uint64_t g_tick = 0;
+static const size_t kMaxPlans = 32;
+
+static size_t elem_size(ns_dtype d) { return d == NS_BF16 ? 2 : 4; }
+
+static bool tma_ok(const Mat& mt, ns_dtype dt) {
+  if (dt != NS_BF16) return false;
+  if ((mt.n % 8) != 0 || (mt.m % 8) != 0) return false;
+  if ((reinterpret_cast<uintptr_t>(mt.x) & 15) || (reinterpret_cast<uintptr_t>(mt.out) & 15)) return false;
+  if (mt.m > (int64_t)1 << 31 || mt.n > (int64_t)1 << 31) return false;
+  return true;
+}
+
+static size_t workspace_bytes_for(const std::vector<Mat>& mats, ns_dtype dt) {
+  size_t off = 256;  // [0,256): barrier counter
+  const size_t es = elem_size(dt);
+  for (const Mat& mt : mats) {
+    off = align_up(off, 256) + (size_t)mt.M * mt.N * es;
+    off = align_up(off, 256) + (size_t)mt.N * mt.N * es;
+    off = align_up(off, 256) + (size_t)mt.N * mt.N * es;
+    off = align_up(off, 256) + (size_t)mt.N * 4;
+  }
+  return align_up(off, 256);
+}
+
+// Host tables assembled for one plan before upload.
+struct HostTables {
+  std::vector<uint8_t> bytes;
+  size_t push(const void* p, size_t n, size_t align = 128) {
+    size_t off = align_up(bytes.size(), align);
+    bytes.resize(off + n);
+    std::memcpy(bytes.data() + off, p, n);
+    return off;
+  }
+};
+
+static ns_status build_plan(Plan& P, HostTables& H, DevCtx* dc, const float* coeffs) {
+  const int T = P.iters;
+  const size_t es = elem_size(P.dtype);
+  const bool bf16 = P.dtype == NS_BF16;
+  // -- workspace layout
+  size_t off = 256;
+  for (Mat& mt : P.mats) {
+    off = align_up(off, 256); mt.w_off = off; off += (size_t)mt.M * mt.N * es;
+    off = align_up(off, 256); mt.a_off = off; off += (size_t)mt.N * mt.N * es;
+    off = align_up(off, 256); mt.b_off = off; off += (size_t)mt.N * mt.N * es;
+    off = align_up(off, 256); mt.s_off = off; off += (size_t)mt.N * 4;
+  }
+  P.ws_bytes = align_up(off, 256);
+  cudaError_t e = cudaMalloc(&P.ws, P.ws_bytes);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(NS_ERR_WORKSPACE, "workspace cudaMalloc(" + std::to_string(P.ws_bytes) + ") failed");
+  }
+  uint8_t* ws = reinterpret_cast<uint8_t*>(P.ws);
+  P.barrier = reinterpret_cast<unsigned*>(ws);
+  auto W = [&](const Mat& mt) { return (void*)(ws + mt.w_off); };
+  auto Am = [&](const Mat& mt) { return (void*)(ws + mt.a_off); };
+  auto Bm = [&](const Mat& mt) { return (void*)(ws + mt.b_off); };
+  auto Sv = [&](const Mat& mt) { return (float*)(ws + mt.s_off); };
+
+  // -- tensormaps (tcgen05 path)
+  std::vector<CUtensorMap> tmaps;
+  if (!P.simt) {
+    for (Mat& mt : P.mats) {
+      CUtensorMap tm;
+      ns_status st;
+      if ((st = encode_tmap(&tm, mt.x, mt.m, mt.n)) != NS_OK) return st;
+      mt.tm_x = (int)tmaps.size(); tmaps.push_back(tm);
+      if (mt.out != mt.x) {
+        if ((st = encode_tmap(&tm, mt.out, mt.m, mt.n)) != NS_OK) return st;
+        mt.tm_out = (int)tmaps.size(); tmaps.push_back(tm);
+      } else {
+        mt.tm_out = mt.tm_x;
+      }
+      if ((st = encode_tmap(&tm, W(mt), mt.m, mt.n)) != NS_OK) return st;
+      mt.tm_w = (int)tmaps.size(); tmaps.push_back(tm);
+      if ((st = encode_tmap(&tm, Am(mt), mt.N, mt.N)) != NS_OK) return st;
+      mt.tm_a = (int)tmaps.size(); tmaps.push_back(tm);
+      if ((st = encode_tmap(&tm, Bm(mt), mt.N, mt.N)) != NS_OK) return st;
+      mt.tm_b = (int)tmaps.size(); tmaps.push_back(tm);
+    }
+  }
+  size_t tm_off = tmaps.empty() ? 0 : H.push(tmaps.data(), tmaps.size() * sizeof(CUtensorMap), 128);
+
+  // Device addresses of tensormaps are known only after allocation: record indices now,
+  // patch pointers after cudaMalloc of the table (two-pass).  We first compute the final
+  // table size by building jobs with placeholder bases, then fix them up.
+  struct Fix { size_t job_off; int ta, tb; };
+  std::vector<Fix> fixes;
+
+  // -- phases
+  if (P.mats.size() > 0) {
+    Phase cp{PH_COPY};
+    for (Mat& mt : P.mats)
+      if (mt.copy_in) cp.copies.push_back({{W(mt), mt.x}, (size_t)mt.m * mt.n * es});
+    if (!cp.copies.empty()) P.phases.push_back(cp);
+  }
+  auto cur_ptr = [&](const Mat& mt, int k) -> void* {  // X_k (k = 1..T+1), caller layout
+    if (k == 1) return mt.copy_in ? W(mt) : mt.x;
+    return ((T - (k - 1)) % 2 == 0) ? mt.out : W(mt);  // dst of iteration k-1
+  };
+  auto cur_tm = [&](const Mat& mt, int k) -> int {
+    if (k == 1) return mt.copy_in ? mt.tm_w : mt.tm_x;
+    return ((T - (k - 1)) % 2 == 0) ? mt.tm_out : mt.tm_w;
+  };
+
+  for (int k = 1; k <= T; ++k) {
+    const float a = coeffs[3 * (k - 1)], b = coeffs[3 * (k - 1) + 1], c = coeffs[3 * (k - 1) + 2];
+    const bool scaled = (k == 1 && P.precond != NS_PRECOND_NONE);
+    for (int step = 0; step < 3; ++step) {
+      const int mode = step;  // GRAM, POLY, XB
+      if (!P.simt) {
+        std::vector<GemmJob> jobs;
+        std::vector<std::pair<int, int>> tmi;
+        int64_t total = 0;
+        for (Mat& mt : P.mats) {
+          GemmJob J;
+          std::memset(&J, 0, sizeof(J));
+          J.mode = mode;
+          int ta = 0, tb = 0;
+          if (mode == MODE_GRAM) {
+            ta = tb = cur_tm(mt, k);
+            J.a_mn = J.b_mn = mt.wide ? 0 : 1;
+            J.sym = 1; J.P = J.Q = (int)mt.N; J.K = (int)mt.M;
+            J.out = Am(mt); J.aux = nullptr; J.ld = mt.N;
+          } else if (mode == MODE_POLY) {
+            ta = tb = mt.tm_a;
+            J.a_mn = J.b_mn = 0;
+            J.sym = 1; J.P = J.Q = J.K = (int)mt.N;
+            J.out = Bm(mt); J.aux = Am(mt); J.ld = mt.N;
+            J.s = scaled ? Sv(mt) : nullptr;
+            J.b = b; J.c = c;
+          } else {
+            if (!mt.wide) {
+              ta = cur_tm(mt, k); tb = mt.tm_b; J.a_mn = 0; J.b_mn = 0;
+              J.P = (int)mt.M; J.Q = (int)mt.N; J.s_by_row = 0;
+            } else {
+              ta = mt.tm_b; tb = cur_tm(mt, k); J.a_mn = 0; J.b_mn = 1;
+              J.P = (int)mt.N; J.Q = (int)mt.M; J.s_by_row = 1;
+            }
+            J.sym = 0; J.K = (int)mt.N;
+            J.out = cur_ptr(mt, k + 1); J.aux = cur_ptr(mt, k); J.ld = mt.n;
+            J.s = scaled ? Sv(mt) : nullptr;
+            J.a = a;
+          }
+          if (J.sym) {
+            const int nb = (J.P + kSymBlock - 1) / kSymBlock;
+            J.tiles = nb * (nb + 1);  // two halves per lower-triangle block
+            J.tiles_q = nb;
+          } else {
+            J.tiles_q = (J.Q + kBN - 1) / kBN;
+            J.tiles = ((J.P + kBM - 1) / kBM) * J.tiles_q;
+          }
+          J.tile_start = total;
+          total += J.tiles;
+          jobs.push_back(J);
+          tmi.push_back({ta, tb});
+        }
+        Phase ph{PH_GEMM};
+        ph.dev_off = H.push(jobs.data(), jobs.size() * sizeof(GemmJob), 64);
+        ph.njobs = (int)jobs.size();
+        ph.total = total;
+        for (size_t j = 0; j < jobs.size(); ++j)
+          fixes.push_back({ph.dev_off + j * sizeof(GemmJob), tmi[j].first, tmi[j].second});
+        P.phases.push_back(ph);
+      } else {
+        std::vector<SimtJob> jobs;
+        int64_t total = 0;
+        for (Mat& mt : P.mats) {
+          SimtJob J;
+          std::memset(&J, 0, sizeof(J));
+          J.mode = mode;
+          if (mode == MODE_GRAM) {
+            void* X = cur_ptr(mt, k);
+            J.A = J.B = X;
+            if (!mt.wide) { J.sa_p = J.sb_q = 1; J.sa_k = J.sb_k = mt.n; }
+            else          { J.sa_p = J.sb_q = mt.n; J.sa_k = J.sb_k = 1; }
+            J.P = J.Q = (int)mt.N; J.K = (int)mt.M;
+            J.out = Am(mt); J.ld = mt.N;
+          } else if (mode == MODE_POLY) {
+            J.A = J.B = Am(mt);
+            J.sa_p = J.sb_q = mt.N; J.sa_k = J.sb_k = 1;
+            J.P = J.Q = J.K = (int)mt.N;
+            J.out = Bm(mt); J.aux = Am(mt); J.ld = mt.N;
+            J.s = scaled ? Sv(mt) : nullptr;
+            J.b = b; J.c = c;
+          } else {
+            void* X = cur_ptr(mt, k);
+            if (!mt.wide) {
+              J.A = X; J.sa_p = mt.n; J.sa_k = 1;
+              J.B = Bm(mt); J.sb_q = mt.N; J.sb_k = 1;
+              J.P = (int)mt.M; J.Q = (int)mt.N; J.s_by_row = 0;
+            } else {
+              J.A = Bm(mt); J.sa_p = mt.N; J.sa_k = 1;
+              J.B = X; J.sb_q = 1; J.sb_k = mt.n;
+              J.P = (int)mt.N; J.Q = (int)mt.M; J.s_by_row = 1;
+            }
+            J.K = (int)mt.N;
+            J.out = cur_ptr(mt, k + 1); J.aux = X; J.ld = mt.n;
+            J.s = scaled ? Sv(mt) : nullptr;
+            J.a = a;
+          }
+          J.tiles_q = (J.Q + kSimtTile - 1) / kSimtTile;
+          J.tiles = ((J.P + kSimtTile - 1) / kSimtTile) * J.tiles_q;
+          J.tile_start = total;
+          total += J.tiles;
+          jobs.push_back(J);
+        }
+        Phase ph{PH_SIMT};
+        ph.dev_off = H.push(jobs.data(), jobs.size() * sizeof(SimtJob), 64);
+        ph.njobs = (int)jobs.size();
+        ph.total = total;
+        P.phases.push_back(ph);
+      }
+      if (mode == MODE_GRAM && scaled) {
+        std::vector<PrecondJob> pj;
+        int64_t rows = 0, items = 0;
+        bool vec8 = bf16;
+        for (Mat& mt : P.mats) vec8 = vec8 && (mt.N % 8 == 0);
+        for (Mat& mt : P.mats) {
+          PrecondJob J;
+          std::memset(&J, 0, sizeof(J));
+          J.A = Am(mt); J.s = Sv(mt); J.N = (int)mt.N; J.precond = (int)P.precond;
+          J.row_start = rows; J.vec_start = items;
+          rows += mt.N;
+          items += vec8 ? (mt.N * mt.N) / 8 : mt.N * mt.N;
+          pj.push_back(J);
+        }
+        Phase ph{PH_PRECOND};
+        ph.dev_off = H.push(pj.data(), pj.size() * sizeof(PrecondJob), 64);
+        ph.njobs = (int)pj.size();
+        ph.total = items;
+        ph.total_rows = rows;
+        ph.vec8 = vec8;
+        P.phases.push_back(ph);
+      }
+    }
+  }
+
+  // -- upload
+  if (!H.bytes.empty()) {
+    P.dtab_bytes = align_up(H.bytes.size(), 256);
+    e = cudaMalloc(&P.dtab, P.dtab_bytes);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      return fail(NS_ERR_WORKSPACE, "job-table cudaMalloc failed");
+    }
+    uint8_t* dbase = reinterpret_cast<uint8_t*>(P.dtab);
+    for (const Fix& f : fixes) {
+      GemmJob* J = reinterpret_cast<GemmJob*>(H.bytes.data() + f.job_off);
+      J->tmA = dbase + tm_off + (size_t)f.ta * sizeof(CUtensorMap);
+      J->tmB = dbase + tm_off + (size_t)f.tb * sizeof(CUtensorMap);
+    }
+    CU_TRY(cudaMemcpy(P.dtab, H.bytes.data(), H.bytes.size(), cudaMemcpyHostToDevice));
+  }
+  (void)dc;
+  return NS_OK;
+}
+
+static ns_status enqueue_plan(Plan& P, DevCtx* dc, cudaStream_t stream) {
+  uint8_t* dbase = reinterpret_cast<uint8_t*>(P.dtab);
+  for (const Phase& ph : P.phases) {
+    switch (ph.kind) {
+      case PH_COPY:
+        for (auto& c : ph.copies)
+          CU_TRY(cudaMemcpyAsync(c.first.first, c.first.second, c.second, cudaMemcpyDeviceToDevice, stream));
+        break;
+      case PH_GEMM:
+        CU_TRY(launch_umma_gemm(reinterpret_cast<const GemmJob*>(dbase + ph.dev_off), ph.njobs, ph.total,
+                                dc->sms, dc->flags, stream));
+        ++g_launches;
+        break;
+      case PH_SIMT:
+        CU_TRY(launch_simt_gemm(reinterpret_cast<const SimtJob*>(dbase + ph.dev_off), ph.njobs, ph.total,
+                                dc->sms, P.dtype == NS_BF16, dc->flags, stream));
+        ++g_launches;
+        break;
+      case PH_PRECOND:
+        CU_TRY(launch_precondition(reinterpret_cast<const PrecondJob*>(dbase + ph.dev_off), ph.njobs,
+                                   ph.total_rows, ph.total, ph.vec8, P.dtype == NS_BF16, P.barrier,
+                                   dc->flags, stream));
+        ++g_launches;
+        break;
+    }
+  }
+  return NS_OK;
+}
+
+// ---------------------------------------------------------------------------- validation
+static ns_status validate_common(int64_t count, int iters, const float* coeffs, ns_precond precond,
+                                 ns_dtype dtype) {
+  if (count < 1) return fail(NS_ERR_INVALID_VALUE, "count/batch must be >= 1");
+  if (iters < 1 || iters > 64) return fail(NS_ERR_INVALID_VALUE, "iters must be in [1, 64]");
+  if (!coeffs) return fail(NS_ERR_INVALID_VALUE, "coeffs is NULL");
+  for (int i = 0; i < 3 * iters; ++i)
+    if (!std::isfinite(coeffs[i])) return fail(NS_ERR_INVALID_VALUE, "non-finite coefficient");
+  if (precond != NS_PRECOND_NONE && precond != NS_PRECOND_FROBENIUS && precond != NS_PRECOND_AOL)
+    return fail(NS_ERR_INVALID_VALUE, "bad precond");
+  if (dtype != NS_BF16 && dtype != NS_FP32) return fail(NS_ERR_INVALID_VALUE, "bad dtype");
+  return NS_OK;
+}
+
+static ns_status validate_mat(const void* x, int64_t m, int64_t n, ns_dtype dtype) {
+  if (!x) return fail(NS_ERR_INVALID_VALUE, "NULL matrix pointer");
+  if (m < 1 || n < 1) return fail(NS_ERR_INVALID_VALUE, "m and n must be >= 1");
+  if (m > ((int64_t)1 << 30) || n > ((int64_t)1 << 30) || m * n > ((int64_t)1 << 40))
+    return fail(NS_ERR_INVALID_VALUE, "matrix too large");
+  if (reinterpret_cast<uintptr_t>(x) % elem_size(dtype))
+    return fail(NS_ERR_NOT_SUPPORTED, "matrix pointer not aligned to its element size");
+  return NS_OK;
+}
+
+static ns_status run(const std::vector<Mat>& mats_in, int iters, const float* coeffs, ns_precond precond,
+                     ns_dtype dtype, cudaStream_t stream) {
+  DevCtx* dc = nullptr;
+  ns_status st = dev_ctx(&dc);
+  if (st != NS_OK) return st;
+  bool simt = (g_path == 1) || dtype != NS_BF16 || dc->cc_major != 10;
+  for (const Mat& mt : mats_in) simt = simt || !tma_ok(mt, dtype);
+  int dev = 0;
+  CU_TRY(cudaGetDevice(&dev));
+  // plan key
+  std::vector<uint64_t> key;
+  key.reserve(mats_in.size() * 4 + 8 + 3 * iters);
+  key.push_back((uint64_t)dev); key.push_back((uint64_t)dtype); key.push_back(simt ? 1 : 0);
+  key.push_back((uint64_t)iters); key.push_back((uint64_t)precond);
+  for (int i = 0; i < 3 * iters; ++i) { uint32_t u; std::memcpy(&u, &coeffs[i], 4); key.push_back(u); }
+  for (const Mat& mt : mats_in) {
+    key.push_back(reinterpret_cast<uint64_t>(mt.x)); key.push_back(reinterpret_cast<uint64_t>(mt.out));
+    key.push_back((uint64_t)mt.m); key.push_back((uint64_t)mt.n);
+  }
+  auto it = g_plans.find(key);
+  Plan* P = nullptr;
+  if (it == g_plans.end()) {
+    if (g_plans.size() >= kMaxPlans) {  // evict least recently used (synchronising)
+      auto victim = g_plans.begin();
+      for (auto jt = g_plans.begin(); jt != g_plans.end(); ++jt)
+        if (jt->second->last_use < victim->second->last_use) victim = jt;
+      cudaDeviceSynchronize();
+      g_plans.erase(victim);
+    }
+    std::unique_ptr<Plan> np(new Plan());
+    np->device = dev; np->dtype = dtype; np->simt = simt; np->iters = iters; np->precond = precond;
+    np->mats = mats_in;
+    HostTables H;
+    st = build_plan(*np, H, dc, coeffs);
+    if (st != NS_OK) return st;
+    P = np.get();
+    g_plans[key] = std::move(np);
+  } else {
+    P = it->second.get();
+  }
+  P->last_use = ++g_tick;
+  return enqueue_plan(*P, dc, stream);
+}
+
+static Mat make_mat(void* x, void* out, int64_t m, int64_t n, int iters) {
+  Mat mt;
+  std::memset(&mt, 0, sizeof(mt));
+  mt.x = x; mt.out = out ? out : x; mt.m = m; mt.n = n;
+  mt.wide = m < n;
+  mt.M = mt.wide ? n : m;
+  mt.N = mt.wide ? m : n;
+  mt.copy_in = (mt.out == mt.x) && (iters % 2 == 1);
+  return mt;
+}
+
+}  // namespace tns
+
+using namespace tns;
+
+extern "C" {
+
+int ns_abi_version(void) { return NS_ABI_VERSION; }
+
+const char* ns_status_string(ns_status s) {
+  switch (s) {
+    case NS_OK: return "NS_OK";
+    case NS_ERR_INVALID_VALUE: return "NS_ERR_INVALID_VALUE";
+    case NS_ERR_NOT_SUPPORTED: return "NS_ERR_NOT_SUPPORTED";
+    case NS_ERR_WORKSPACE: return "NS_ERR_WORKSPACE";
+    case NS_ERR_CUDA: return "NS_ERR_CUDA";
+  }
+  return "NS_ERR_UNKNOWN";
+}
+
+const char* ns_last_error(void) { return g_err.c_str(); }
+
+uint64_t ns_launch_count(void) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  return g_launches;
+}
+
+int ns_set_path(int path) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  int old = g_path;
+  g_path = path;
+  return old;
+}
+
+ns_status ns_orthogonalize(void* X, int64_t m, int64_t n, int64_t batch, int iters, const float* coeffs,
+                           ns_precond precond, ns_dtype dtype, void* stream) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  ns_status st = validate_common(batch, iters, coeffs, precond, dtype);
+  if (st != NS_OK) return st;
+  if ((st = validate_mat(X, m, n, dtype)) != NS_OK) return st;
+  std::vector<Mat> mats;
+  const size_t stride = (size_t)m * n * elem_size(dtype);
+  for (int64_t i = 0; i < batch; ++i) {
+    void* xi = reinterpret_cast<uint8_t*>(X) + i * stride;
+    mats.push_back(make_mat(xi, xi, m, n, iters));
+  }
+  return run(mats, iters, coeffs, precond, dtype, reinterpret_cast<cudaStream_t>(stream));
+}
+
+ns_status ns_orthogonalize_batched(void* const* X, void* const* out, const int64_t* m, const int64_t* n,
+                                   int64_t count, int iters, const float* coeffs, ns_precond precond,
+                                   ns_dtype dtype, void* stream) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  ns_status st = validate_common(count, iters, coeffs, precond, dtype);
+  if (st != NS_OK) return st;
+  if (!X || !m || !n) return fail(NS_ERR_INVALID_VALUE, "NULL array argument");
+  std::vector<Mat> mats;
+  for (int64_t i = 0; i < count; ++i) {
+    if ((st = validate_mat(X[i], m[i], n[i], dtype)) != NS_OK) return st;
+    void* o = out ? out[i] : nullptr;
+    if (o && (st = validate_mat(o, m[i], n[i], dtype)) != NS_OK) return st;
+    mats.push_back(make_mat(X[i], o, m[i], n[i], iters));
+  }
+  return run(mats, iters, coeffs, precond, dtype, reinterpret_cast<cudaStream_t>(stream));
+}
+
+ns_status ns_workspace_size(const int64_t* m, const int64_t* n, int64_t count, ns_dtype dtype, size_t* bytes) {
+  if (!m || !n || !bytes || count < 1) return fail(NS_ERR_INVALID_VALUE, "bad arguments");
+  if (dtype != NS_BF16 && dtype != NS_FP32) return fail(NS_ERR_INVALID_VALUE, "bad dtype");
+  std::vector<Mat> mats;
+  for (int64_t i = 0; i < count; ++i) {
+    if (m[i] < 1 || n[i] < 1) return fail(NS_ERR_INVALID_VALUE, "m and n must be >= 1");
+    mats.push_back(make_mat((void*)16, nullptr, m[i], n[i], 2));
+  }
+  *bytes = workspace_bytes_for(mats, dtype);
+  return NS_OK;
+}
+
+ns_status ns_read_flags(void* stream, uint32_t* flags) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (!flags) return fail(NS_ERR_INVALID_VALUE, "flags is NULL");
+  DevCtx* dc = nullptr;
+  ns_status st = dev_ctx(&dc);
+  if (st != NS_OK) return st;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  uint32_t h = 0;
+  CU_TRY(cudaMemcpyAsync(&h, dc->flags, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+  CU_TRY(cudaMemsetAsync(dc->flags, 0, sizeof(uint32_t), s));
+  CU_TRY(cudaStreamSynchronize(s));
+  *flags = h;
+  return NS_OK;
+}
+
+void ns_shutdown(void) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  cudaDeviceSynchronize();
+  g_plans.clear();
+  for (auto& d : g_dev) {
+    if (d.init && d.flags) cudaFree(d.flags);
+    d = DevCtx();
+  }
+}
+
+// ------------------------------------------------------------------------------ single steps
+// These build a one-off job table, launch one kernel and synchronise (test entry points).
+static ns_status one_gemm(GemmJob J, int ta_rows, int ta_cols, const void* ta_ptr, int tb_rows, int tb_cols,
+                          const void* tb_ptr, SimtJob S, bool simt, ns_dtype dtype, cudaStream_t stream) {
+  DevCtx* dc = nullptr;
+  ns_status st = dev_ctx(&dc);
+  if (st != NS_OK) return st;
+  void* dmem = nullptr;
+  if (!simt) {
+    CUtensorMap tm[2];
+    if ((st = encode_tmap(&tm[0], ta_ptr, ta_rows, ta_cols)) != NS_OK) return st;
+    if ((st = encode_tmap(&tm[1], tb_ptr, tb_rows, tb_cols)) != NS_OK) return st;
+    const size_t bytes = 2 * sizeof(CUtensorMap) + sizeof(GemmJob);
+    CU_TRY(cudaMalloc(&dmem, bytes));
+    uint8_t* d = reinterpret_cast<uint8_t*>(dmem);
+    J.tmA = d;
+    J.tmB = d + sizeof(CUtensorMap);
+    std::vector<uint8_t> h(bytes);
+    std::memcpy(h.data(), tm, sizeof(tm));
+    std::memcpy(h.data() + 2 * sizeof(CUtensorMap), &J, sizeof(J));
+    CU_TRY(cudaMemcpy(dmem, h.data(), bytes, cudaMemcpyHostToDevice));
+    cudaError_t e = launch_umma_gemm(reinterpret_cast<const GemmJob*>(d + 2 * sizeof(CUtensorMap)), 1,
+                                      J.tiles, dc->sms, dc->flags, stream);
+    ++g_launches;
+    cudaError_t e2 = cudaStreamSynchronize(stream);
+    cudaFree(dmem);
+    if (e != cudaSuccess) return fail(NS_ERR_CUDA, std::string("umma launch: ") + cudaGetErrorString(e));
+    if (e2 != cudaSuccess) return fail(NS_ERR_CUDA, std::string("umma exec: ") + cudaGetErrorString(e2));
+  } else {
+    CU_TRY(cudaMalloc(&dmem, sizeof(SimtJob)));
+    CU_TRY(cudaMemcpy(dmem, &S, sizeof(S), cudaMemcpyHostToDevice));
+    cudaError_t e = launch_simt_gemm(reinterpret_cast<const SimtJob*>(dmem), 1, S.tiles, dc->sms,
+                                     dtype == NS_BF16, dc->flags, stream);
+    ++g_launches;
+    cudaError_t e2 = cudaStreamSynchronize(stream);
+    cudaFree(dmem);
+    if (e != cudaSuccess) return fail(NS_ERR_CUDA, std::string("simt launch: ") + cudaGetErrorString(e));
+    if (e2 != cudaSuccess) return fail(NS_ERR_CUDA, std::string("simt exec: ") + cudaGetErrorString(e2));
+  }
+  return NS_OK;
+}
+
+static bool step_simt(ns_dtype dtype, int64_t m, int64_t n, std::initializer_list<const void*> ptrs) {
+  DevCtx* dc = nullptr;
+  if (dev_ctx(&dc) != NS_OK) return true;
+  if (g_path == 1 || dtype != NS_BF16 || dc->cc_major != 10) return true;
+  if (m % 8 || n % 8) return true;
+  for (const void* p : ptrs)
+    if (reinterpret_cast<uintptr_t>(p) & 15) return true;
+  return false;
+}
+
+static void finish_tiles(GemmJob& J, SimtJob& S) {
+  if (J.sym) {
+    const int nb = (J.P + kSymBlock - 1) / kSymBlock;
+    J.tiles = nb * (nb + 1);
+    J.tiles_q = nb;
+  } else {
+    J.tiles_q = (J.Q + kBN - 1) / kBN;
+    J.tiles = ((J.P + kBM - 1) / kBM) * J.tiles_q;
+  }
+  S.tiles_q = (S.Q + kSimtTile - 1) / kSimtTile;
+  S.tiles = ((S.P + kSimtTile - 1) / kSimtTile) * S.tiles_q;
+}
+
+ns_status nsx_gram(const void* X, int64_t m, int64_t n, void* A, ns_dtype dtype, void* stream) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  ns_status st;
+  if ((st = validate_mat(X, m, n, dtype)) != NS_OK) return st;
+  if (!A) return fail(NS_ERR_INVALID_VALUE, "A is NULL");
+  const bool wide = m < n;
+  const int64_t M = wide ? n : m, N = wide ? m : n;
+  GemmJob J; SimtJob S;
+  std::memset(&J, 0, sizeof(J)); std::memset(&S, 0, sizeof(S));
+  J.mode = S.mode = MODE_GRAM;
+  J.sym = 1; J.P = J.Q = S.P = S.Q = (int)N; J.K = S.K = (int)M;
+  J.a_mn = J.b_mn = wide ? 0 : 1;
+  J.out = S.out = A; J.ld = S.ld = N;
+  S.A = S.B = X;
+  if (!wide) { S.sa_p = S.sb_q = 1; S.sa_k = S.sb_k = n; } else { S.sa_p = S.sb_q = n; S.sa_k = S.sb_k = 1; }
+  finish_tiles(J, S);
+  const bool simt = step_simt(dtype, m, n, {X, A});
+  return one_gemm(J, (int)m, (int)n, X, (int)m, (int)n, X, S, simt, dtype, reinterpret_cast<cudaStream_t>(stream));
+}
+
+ns_status nsx_poly(const void* A, int64_t N, float b, float c, const float* s, void* B, ns_dtype dtype,
+                   void* stream) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  ns_status st;
+  if ((st = validate_mat(A, N, N, dtype)) != NS_OK) return st;
+  if (!B) return fail(NS_ERR_INVALID_VALUE, "B is NULL");
+  GemmJob J; SimtJob S;
+  std::memset(&J, 0, sizeof(J)); std::memset(&S, 0, sizeof(S));
+  J.mode = S.mode = MODE_POLY;
+  J.sym = 1; J.P = J.Q = J.K = S.P = S.Q = S.K = (int)N;
+  J.out = S.out = B; J.aux = S.aux = A; J.ld = S.ld = N;
+  J.s = S.s = s; J.b = S.b = b; J.c = S.c = c;
+  S.A = S.B = A; S.sa_p = S.sb_q = N; S.sa_k = S.sb_k = 1;
+  finish_tiles(J, S);
+  const bool simt = step_simt(dtype, N, N, {A, B});
+  return one_gemm(J, (int)N, (int)N, A, (int)N, (int)N, A, S, simt, dtype, reinterpret_cast<cudaStream_t>(stream));
+}
+
+ns_status nsx_update(const void* X, int64_t m, int64_t n, const void* B, float a, const float* s, void* Out,
+                     ns_dtype dtype, void* stream) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  ns_status st;
+  if ((st = validate_mat(X, m, n, dtype)) != NS_OK) return st;
+  if (!B || !Out) return fail(NS_ERR_INVALID_VALUE, "B/Out is NULL");
+  const bool wide = m < n;
+  const int64_t M = wide ? n : m, N = wide ? m : n;
+  GemmJob J; SimtJob S;
+  std::memset(&J, 0, sizeof(J)); std::memset(&S, 0, sizeof(S));
+  J.mode = S.mode = MODE_XB;
+  J.sym = 0; J.K = S.K = (int)N;
+  J.out = S.out = Out; J.aux = S.aux = X; J.ld = S.ld = n;
+  J.s = S.s = s; J.a = S.a = a;
+  int ta_r, ta_c, tb_r, tb_c; const void *ta, *tb;
+  if (!wide) {
+    J.a_mn = 0; J.b_mn = 0; J.P = S.P = (int)M; J.Q = S.Q = (int)N; J.s_by_row = S.s_by_row = 0;
+    ta = X; ta_r = (int)m; ta_c = (int)n; tb = B; tb_r = (int)N; tb_c = (int)N;
+    S.A = X; S.sa_p = n; S.sa_k = 1; S.B = B; S.sb_q = N; S.sb_k = 1;
+  } else {
+    J.a_mn = 0; J.b_mn = 1; J.P = S.P = (int)N; J.Q = S.Q = (int)M; J.s_by_row = S.s_by_row = 1;
+    ta = B; ta_r = (int)N; ta_c = (int)N; tb = X; tb_r = (int)m; tb_c = (int)n;
+    S.A = B; S.sa_p = N; S.sa_k = 1; S.B = X; S.sb_q = 1; S.sb_k = n;
+  }
+  finish_tiles(J, S);
+  const bool simt = step_simt(dtype, m, n, {X, B, Out});
+  return one_gemm(J, ta_r, ta_c, ta, tb_r, tb_c, tb, S, simt, dtype, reinterpret_cast<cudaStream_t>(stream));
+}
+
+ns_status nsx_precondition(void* A, int64_t N, ns_precond precond, float* s, ns_dtype dtype, void* stream) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  ns_status st;
+  if ((st = validate_mat(A, N, N, dtype)) != NS_OK) return st;
+  if (!s) return fail(NS_ERR_INVALID_VALUE, "s is NULL");
+  if (precond != NS_PRECOND_FROBENIUS && precond != NS_PRECOND_AOL)
+    return fail(NS_ERR_INVALID_VALUE, "precond must be FROBENIUS or AOL");
+  DevCtx* dc = nullptr;
+  if ((st = dev_ctx(&dc)) != NS_OK) return st;
+  cudaStream_t strm = reinterpret_cast<cudaStream_t>(stream);
+  const bool vec8 = dtype == NS_BF16 && N % 8 == 0 && !(reinterpret_cast<uintptr_t>(A) & 15);
+  PrecondJob J;
+  std::memset(&J, 0, sizeof(J));
+  J.A = A; J.s = s; J.N = (int)N; J.precond = (int)precond;
+  void* dmem = nullptr;
+  CU_TRY(cudaMalloc(&dmem, 256 + sizeof(J)));
+  CU_TRY(cudaMemcpy(reinterpret_cast<uint8_t*>(dmem) + 256, &J, sizeof(J), cudaMemcpyHostToDevice));
+  cudaError_t e = launch_precondition(reinterpret_cast<const PrecondJob*>(reinterpret_cast<uint8_t*>(dmem) + 256), 1,
+                                      N, vec8 ? N * N / 8 : N * N, vec8, dtype == NS_BF16,
+                                      reinterpret_cast<unsigned*>(dmem), dc->flags, strm);
+  ++g_launches;
+  cudaError_t e2 = cudaStreamSynchronize(strm);
+  cudaFree(dmem);
+  if (e != cudaSuccess) return fail(NS_ERR_CUDA, std::string("precond launch: ") + cudaGetErrorString(e));
+  if (e2 != cudaSuccess) return fail(NS_ERR_CUDA, std::string("precond exec: ") + cudaGetErrorString(e2));
+  return NS_OK;
+}
+
+}  // extern "C"

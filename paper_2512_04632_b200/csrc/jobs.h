@@ -1,0 +1,73 @@
+// Work descriptors shared by the host planner (api.cu) and the kernels.
+// One GemmJob = one matrix's share of one NS step launch; a launch walks a device
+// array of jobs (grouped/batched launch).
+#pragma once
+#include <cstdint>
+
+namespace tns {
+
+enum GemmMode : int32_t {
+  MODE_GRAM = 0,  // out = Xh^T Xh                          (Eq. 3 / Eq. 7)
+  MODE_POLY = 1,  // out = (b aux + c acc) * s[col]         (Eq. 4; aux = A)
+  MODE_XB = 2     // out = acc + a * aux * s[row|col]       (Eq. 5; aux = X_k)
+};
+
+// Tile geometry of the tcgen05 kernel (one CTA = one 128 x 256 output tile at a time).
+constexpr int kBM = 128;  // UMMA M
+constexpr int kBN = 256;  // UMMA N
+constexpr int kBK = 64;   // K elements per pipeline stage = one 128-byte swizzle atom
+constexpr int kSymBlock = 256;  // symmetric phases tile the lower triangle in 256 x 256 blocks
+constexpr int kGroupP = 16;     // XB raster: tiles grouped 16 row-blocks deep for L2 reuse
+
+struct GemmJob {
+  // Operand sources: D[p][q] = sum_k Aop[p][k] * Bop[q][k].
+  const void* tmA;  // CUtensorMap (global memory) of the tensor holding Aop
+  const void* tmB;  // CUtensorMap of the tensor holding Bop
+  int32_t a_mn;     // 1: Aop stored [k][p] (MN-major), 0: stored [p][k] (K-major)
+  int32_t b_mn;
+  int32_t mode;     // GemmMode
+  int32_t sym;      // 1: lower-triangle 256-blocks, mirrored store (P == Q)
+  int32_t P, Q, K;  // output rows/cols, contraction length
+  int32_t tiles_q;  // number of 256-wide column tiles (rect jobs)
+  int32_t tiles;    // tiles in this job
+  int64_t tile_start;  // exclusive prefix over jobs of `tiles`
+  void* out;           // output matrix, row-major, ld = ld
+  const void* aux;     // POLY: A ; XB: X_k  (same [p][q] indexing, ld = ld)
+  int64_t ld;
+  const float* s;      // scaling vector or nullptr
+  int32_t s_by_row;    // XB: scale a*aux by s[p] (1) or s[q] (0)
+  float a, b, c;
+};
+
+// CUDA-core (SIMT) variant of a GemmJob: operands by pointer + strides (elements),
+// Aop[p][k] = A[p*sa_p + k*sa_k], Bop[q][k] = B[q*sb_q + k*sb_k].  Full (non-triangular)
+// 64 x 64 tiles.  Used for the fp32 "exact" mode and for bf16 shapes TMA cannot address.
+struct SimtJob {
+  const void* A;
+  const void* B;
+  int64_t sa_p, sa_k, sb_q, sb_k;
+  int32_t mode;
+  int32_t P, Q, K;
+  int32_t tiles_q;
+  int32_t tiles;
+  int64_t tile_start;
+  void* out;
+  const void* aux;
+  int64_t ld;
+  const float* s;
+  int32_t s_by_row;
+  float a, b, c;
+};
+constexpr int kSimtTile = 64;
+
+// Per-matrix descriptor for the preconditioning kernel (AOL / Frobenius).
+struct PrecondJob {
+  void* A;          // N x N symmetric Gram, in place -> A1
+  float* s;         // N
+  int32_t N;
+  int32_t precond;  // 1 Frobenius, 2 AOL
+  int64_t row_start;  // prefix over jobs of N (AOL: one warp per row)
+  int64_t vec_start;  // prefix over jobs of ceil(N*N / 8) (rescale: 16-byte vectors)
+};
+
+}  // namespace tns

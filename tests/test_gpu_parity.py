@@ -1,0 +1,196 @@
+"""End-to-end parity of the CUDA path (through the C ABI) against the fp64 oracle (GPU).
+
+Gates (BASELINE.json north_star): relative Frobenius difference <= 2e-2 in bf16 and
+<= 1e-4 in fp32 mode; the GPU polar error no worse than the oracle's by more than 5%.
+Both sides consume the same bf16-representable inputs from synth/ and the same
+coefficient arrays.
+"""
+import numpy as np
+import pytest
+import torch
+
+from oracle import ns_oracle as O
+from synth import coeffs as C
+from synth import inputs as I
+from tests.helpers import oracle_run, polar_excess, relF
+
+pytestmark = pytest.mark.gpu
+
+ns = pytest.importorskip("paper_2512_04632_b200")
+
+BF16_TOL = 2e-2
+FP32_TOL = 1e-4
+POLAR_SLACK = 1.05
+
+
+def _run(x32: np.ndarray, coeffs, precond: str, dtype=torch.bfloat16) -> np.ndarray:
+    t = torch.from_numpy(np.ascontiguousarray(x32, dtype=np.float32)).to(dtype).cuda()
+    ns.orthogonalize(t, iters=len(coeffs), precond=precond, coeffs=coeffs)
+    torch.cuda.synchronize()
+    return t.float().cpu().numpy().astype(np.float64)
+
+
+CASES = [
+    # (m, n, dist) -- square, tall, wide, ragged tiles, CIFAR, GPT-2 shapes, unaligned (SIMT)
+    (256, 256, "gaussian"),
+    (768, 768, "gaussian"),
+    (3072, 768, "gaussian"),
+    (768, 3072, "gaussian"),
+    (520, 136, "gaussian"),
+    (64, 216, "gaussian"),
+    (256, 2304, "lowrank"),
+    (512, 512, "levy1.0"),
+    (1000, 600, "levy1.5"),
+    (100, 37, "gaussian"),
+]
+
+
+@pytest.mark.parametrize("m,n,dist", CASES)
+def test_turbo_muon_aol4(m, n, dist):
+    x = I.make_matrix(m, n, seed=I.matrix_seed(1, m + n), dist=dist)
+    coeffs = C.turbo(4)
+    out = _run(x, coeffs, "aol")
+    ref = oracle_run(x, coeffs, "aol")
+    assert np.all(np.isfinite(out))
+    r = relF(out, ref)
+    assert r <= BF16_TOL, r
+    eg, eo = polar_excess(out, ref, x)
+    assert eg <= POLAR_SLACK * eo, (eg, eo)
+
+
+@pytest.mark.parametrize("m,n", [(768, 768), (3072, 768), (64, 576)])
+def test_muon_plus_frobenius5(m, n):
+    x = I.gaussian(m, n, seed=21)
+    coeffs = C.muon_plus(5)
+    out = _run(x, coeffs, "frobenius")
+    ref = oracle_run(x, coeffs, "frobenius")
+    assert relF(out, ref) <= BF16_TOL
+    eg, eo = polar_excess(out, ref, x)
+    assert eg <= POLAR_SLACK * eo, (eg, eo)
+
+
+def test_precond_none_closed_form():
+    """precond=none on a matrix with ||X||_2 < 1."""
+    x = I.round_bf16(I.gaussian(384, 256, seed=22, bf16=False) / np.float32(40.0))
+    coeffs = C.turbo(4)
+    assert relF(_run(x, coeffs, "none"), oracle_run(x, coeffs, "none")) <= BF16_TOL
+
+
+@pytest.mark.parametrize("m,n,dist", [(128, 128, "gaussian"), (128, 128, "levy1.5"), (96, 200, "gaussian")])
+def test_fp32_exact_mode(m, n, dist):
+    """Config 1: 128 x 128 fp32, relF <= 1e-4 vs the fp64 oracle."""
+    x = I.make_matrix(m, n, seed=31, dist=dist, bf16=False)
+    coeffs = C.turbo(4)
+    out = _run(x, coeffs, "aol", dtype=torch.float32)
+    ref = oracle_run(x, coeffs, "aol")
+    assert relF(out, ref) <= FP32_TOL
+    eg, eo = polar_excess(out, ref, x)
+    assert eg <= POLAR_SLACK * eo
+
+
+def test_batched_equals_single_bitwise():
+    shapes = [(768, 768), (3072, 768), (768, 3072), (64, 216), (520, 136)]
+    xs = [I.gaussian(m, n, seed=40 + i) for i, (m, n) in enumerate(shapes)]
+    singles = [_run(x, C.turbo(4), "aol") for x in xs]
+    ts = [torch.from_numpy(x).to(torch.bfloat16).cuda() for x in xs]
+    outs = [torch.empty_like(t) for t in ts]
+    ns.orthogonalize_list(ts, out=outs, iters=4)
+    for o, s in zip(outs, singles):
+        assert np.array_equal(o.float().cpu().numpy().astype(np.float64), s)
+    # batch-strided entry point
+    xb = np.stack([I.gaussian(256, 128, seed=50 + i) for i in range(3)])
+    tb = torch.from_numpy(xb).to(torch.bfloat16).cuda()
+    ns.orthogonalize(tb, iters=4)
+    for i in range(3):
+        assert np.array_equal(tb[i].float().cpu().numpy(), _run(xb[i], C.turbo(4), "aol").astype(np.float32))
+
+
+def test_odd_iters_in_place_and_out_of_place():
+    x = I.gaussian(512, 256, seed=60)
+    coeffs = C.muon_plus(5)
+    a = _run(x, coeffs, "aol")
+    t = torch.from_numpy(x).to(torch.bfloat16).cuda()
+    o = torch.empty_like(t)
+    ns.orthogonalize_list([t], out=[o], iters=5, precond="aol", coeffs=coeffs)
+    assert np.array_equal(o.float().cpu().numpy().astype(np.float64), a)
+    assert np.array_equal(t.float().cpu().numpy(), x)  # input untouched
+
+
+def test_scale_invariance_bitwise():
+    """NS(AOL(4^k X)) == NS(AOL(X)) bitwise: exponent-exact scaling (reading R4)."""
+    x = I.gaussian(768, 512, seed=61)
+    a = _run(x, C.turbo(4), "aol")
+    b = _run(x * np.float32(16.0), C.turbo(4), "aol")
+    assert np.array_equal(a, b)
+
+
+def test_transpose_symmetry():
+    x = I.gaussian(1024, 384, seed=62)
+    a = _run(x, C.turbo(4), "aol")
+    b = _run(np.ascontiguousarray(x.T), C.turbo(4), "aol")
+    assert relF(b.T, a) <= 1e-2
+
+
+def test_singular_value_band_tall():
+    """Tall Gaussian (aspect 4): sigma_min(X1) >= 0.05, so sigma(out) in [0.97, 1.04]."""
+    x = I.gaussian(3072, 768, seed=63)
+    out = _run(x, C.turbo(4), "aol")
+    sv = np.linalg.svd(out, compute_uv=False)
+    assert sv.min() >= 0.97 and sv.max() <= 1.04, (sv.min(), sv.max())
+
+
+def test_descent_alignment_and_determinism():
+    x = I.levy(512, 384, seed=64, alpha=1.0)
+    a = _run(x, C.turbo(4), "aol")
+    b = _run(x, C.turbo(4), "aol")
+    assert np.array_equal(a, b)
+    assert O.descent_alignment(x, a) > 0
+
+
+def test_zero_column_flag():
+    x = I.gaussian(256, 128, seed=65)
+    x[:, 5] = 0
+    ns.read_flags()
+    out = _run(x, C.turbo(4), "aol")
+    assert ns.read_flags() & 1
+    assert np.all(np.isfinite(out)) and np.all(out[:, 5] == 0)
+    assert relF(out, oracle_run(x, C.turbo(4), "aol")) <= BF16_TOL
+
+
+def test_launch_count_grouped():
+    shapes = [(768, 768)] * 4 + [(3072, 768), (768, 3072)]
+    ts = [torch.from_numpy(I.gaussian(m, n, seed=70 + i)).to(torch.bfloat16).cuda() for i, (m, n) in enumerate(shapes)]
+    ns.orthogonalize_list(ts, iters=4)  # builds the plan
+    c0 = ns.launch_count()
+    ns.orthogonalize_list(ts, iters=4)
+    torch.cuda.synchronize()
+    assert ns.launch_count() - c0 == 3 * 4 + 1
+
+
+@pytest.mark.parametrize("n", [8192])
+def test_full_size_properties(n):
+    """8192^2 (BASELINE config 4): properties that hold at any size -- finite output,
+    bitwise determinism, exact scale invariance, descent alignment, bounded spectrum."""
+    x = I.gaussian(n, n, seed=80)
+    t1 = torch.from_numpy(x).to(torch.bfloat16).cuda()
+    t2 = (t1 * 4).contiguous()
+    ns.orthogonalize(t1)
+    ns.orthogonalize(t2)
+    torch.cuda.synchronize()
+    assert torch.isfinite(t1.float()).all()
+    assert torch.equal(t1, t2)
+    xf = torch.from_numpy(x).cuda()
+    assert float((xf * t1.float()).sum()) > 0
+    # spectral norm by power iteration (fp32): AOL keeps ||X1||_2 <= 1, so every output
+    # singular value is at most max_{s in [0,1]} P(s) of the schedule (Eq. 2 acts per
+    # singular value); allow 2% for bf16 rounding.
+    grid = np.linspace(0.0, 1.0, 200001)
+    for a, b, c in C.turbo(4):
+        grid = a * grid + b * grid ** 3 + c * grid ** 5
+    bound = 1.02 * grid.max()
+    v = torch.randn(n, 1, device="cuda", generator=None)
+    o = t1.float()
+    for _ in range(30):
+        v = o.T @ (o @ v)
+        v = v / v.norm()
+    assert float((o @ v).norm()) <= bound
