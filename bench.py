@@ -1,0 +1,485 @@
+#!/usr/bin/env python
+"""Benchmark: Turbo-Muon Newton-Schulz orthogonalisation of a GPT-2 Muon parameter set.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl own|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...      (N > 1: one rank per GPU, NCCL)
+
+One step = one pass of the whole hot path over one batch of synthetic input: AOL-
+preconditioned NS, T = 4 (Alg. 2, Eqs. 3-5) on every hidden matrix of the
+GPT-2-medium Muon parameter set (BASELINE.json configs[4]: 96 x 1024^2, 24 x 4096x1024,
+24 x 1024x4096; 604 MB bf16 -- larger than the 126 MB L2, so no flush is needed), sharded
+by whole-matrix ownership (LPT) across the N ranks with one NCCL all-gather of the
+results.  Metric: ms per orthogonalisation of the full set (time-like, strong scaling:
+the total work is fixed as N grows).  At N = 1 the line also carries the other two
+workloads the metric names: 8192^2 (config 4, with the plain Frobenius T=5 comparator
+and a cuBLAS dense-GEMM comparator of the same algorithm) and the GPT-2-small set
+(config 2).
+
+--impl reference times the fp64 CPU oracle (oracle/, as it stands) on the host cores on a
+bounded sample of the same workload, extrapolated to the metric by algorithmic FLOPs.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+from synth import coeffs as C  # noqa: E402
+from synth import inputs as I  # noqa: E402
+
+METRIC = "ms per NS orthogonalization (GPT-2-medium Muon hidden-matrix set; Turbo-Muon AOL, 4 iters)"
+WORKLOAD = "gpt2-medium"
+
+
+def ns_flops(m: int, n: int, iters: int) -> int:
+    """Algorithmic FLOPs: iters * (MN(N+1) + N^2(N+1) + 2MN^2)."""
+    M, N = max(m, n), min(m, n)
+    return iters * (M * N * (N + 1) + N * N * (N + 1) + 2 * M * N * N)
+
+
+def kernel_units(shapes, iters):
+    """Per-launch algorithmic work of each kernel kind over the given matrices (one launch
+    covers all of them): FLOPs for the GEMMs, bytes for the preconditioner."""
+    g = p = u = pre = 0
+    for m, n in shapes:
+        M, N = max(m, n), min(m, n)
+        g += M * N * (N + 1)
+        p += N * N * (N + 1)
+        u += 2 * M * N * N
+        pre += 4 * N * N + 4 * N  # read A0 + write A1 (bf16) + write s (fp32)
+    return {"gram": g, "poly": p, "update": u, "precondition": pre}
+
+
+def load_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        d = json.load(open(path))
+        return {"hbm": float(d["hbm_gbs"]), "bf16": float(d["bf16_tflops"]),
+                "bf16_sustained": float(d.get("bf16_tflops_sustained", d["bf16_tflops"])),
+                "source": "measured"}
+    except Exception:
+        return {"hbm": 6650.0, "bf16": 1590.0, "bf16_sustained": 1400.0, "source": "fallback"}
+
+
+# ------------------------------------------------------------------------------ clocks
+class ClockSampler:
+    REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+               0x2: "applications_clocks_setting", 0x10: "sync_boost"}
+
+    def __init__(self, index: int):
+        self.ok = False
+        self.samples = []
+        self.reasons = 0
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # pragma: no cover
+            self.err = str(e)
+
+    def _loop(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                self.reasons |= int(nv.nvmlDeviceGetCurrentClocksEventReasons(self.h))
+            except Exception:
+                pass
+            time.sleep(0.005)
+
+    def start(self):
+        if not self.ok:
+            return
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._loop, daemon=True)
+        self._t.start()
+
+    def stop(self):
+        if not self.ok:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable"]}
+        self._stop.set()
+        self._t.join()
+        names = [v for k, v in self.REASONS.items() if self.reasons & k]
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": names, "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------------------------ helpers
+def blas_threads() -> int:
+    try:
+        from threadpoolctl import threadpool_info
+        return max(int(i.get("num_threads", 1)) for i in threadpool_info() if i.get("user_api") == "blas")
+    except Exception:
+        return len(os.sched_getaffinity(0))
+
+
+def make_inputs(shapes, config_id: int):
+    return [I.gaussian(m, n, seed=I.matrix_seed(config_id, i)) for i, (m, n) in enumerate(shapes)]
+
+
+def oracle_sample_ms(shapes, iters, budget_s: float, precond="aol", start: int = 0):
+    """Time the fp64 oracle on whole matrices of the workload (one per distinct shape,
+    cycling) until `budget_s` is spent; extrapolate to the full set by FLOPs."""
+    from oracle import ns_oracle as O
+    coeffs = C.turbo(iters) if precond == "aol" else C.muon_plus(iters)
+    distinct = []
+    for s in shapes:
+        if s not in distinct:
+            distinct.append(s)
+    t_tot = 0.0
+    f_tot = 0
+    done = []
+    k = start
+    while True:
+        m, n = distinct[k % len(distinct)]
+        x = I.gaussian(m, n, seed=I.matrix_seed(99, k)).astype(np.float64)
+        t0 = time.perf_counter()
+        O.newton_schulz(x, coeffs, precond)
+        t_tot += time.perf_counter() - t0
+        f_tot += ns_flops(m, n, iters)
+        done.append(f"{m}x{n}")
+        k += 1
+        if t_tot >= budget_s or len(done) >= 64:
+            break
+    total = sum(ns_flops(m, n, iters) for m, n in shapes)
+    ms = t_tot * 1e3 * total / f_tot
+    return ms, done, t_tot
+
+
+# ------------------------------------------------------------------------------ reference arm
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    shapes = I.shape_set(args.workload)
+    vals = []
+    for w in range(args.warmup):
+        oracle_sample_ms(shapes, args.iters, 0.0, start=w)
+    samples = []
+    for k in range(args.steps):
+        ms, done, secs = oracle_sample_ms(shapes, args.iters, 0.0, start=k)
+        vals.append(ms)
+        samples += done
+    v = float(np.mean(vals))
+    cores = blas_threads()
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(v, 3), "unit": "ms", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(v, 3), "higher_is_better": False,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": args.workload, "matrices": len(shapes), "iters": args.iters, "precond": "aol"},
+        "cpu_baseline": {"value": round(v, 3), "unit": "ms", "cores": cores, "kind": "oracle",
+                         "sample": f"one whole matrix per step ({', '.join(sorted(set(samples)))}), "
+                                   f"numpy fp64 + OpenBLAS, extrapolated to the {len(shapes)}-matrix set by algorithmic FLOPs"},
+        "e2e": {"value": round(v, 3), "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------------------ own arm
+def time_calls(fn, reps: int, flush=None):
+    import torch
+    ts = []
+    for _ in range(reps):
+        if flush is not None:
+            flush()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        fn()
+        e1.record()
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    return statistics.median(ts)
+
+
+def torch_dense_ns(x, coeffs):
+    """In-run context comparator ONLY (never in the library): the same AOL-NS algorithm
+    with torch.matmul (cuBLAS dense bf16 GEMMs), SURVEY §8(d)."""
+    import torch
+    A = x.T @ x
+    s = A.float().abs().sum(1).rsqrt()
+    A = (s[:, None] * A.float() * s[None, :]).to(x.dtype)
+    x = (x.float() * s[None, :]).to(x.dtype)
+    for k, (a, b, c) in enumerate(coeffs):
+        if k:
+            A = x.T @ x
+        B = b * A + c * (A @ A)
+        x = a * x + x @ B
+    return x
+
+
+def run_own(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2512_04632_b200 as ns
+    from paper_2512_04632_b200.parallel import make_plan, orthogonalize_sharded
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    peaks = load_peaks()
+
+    shapes = I.shape_set(args.workload)
+    iters = args.iters
+    xs_np = make_inputs(shapes, 5)
+    xs = [torch.from_numpy(x).to(torch.bfloat16).to(dev) for x in xs_np]
+    del xs_np
+    plan = make_plan(shapes, world, iters)
+    mine = plan.mine(rank)
+
+    def step():
+        return orthogonalize_sharded(xs, None, iters=iters, precond="aol")
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    sampler = ClockSampler(local)
+    c0 = ns.launch_count()
+    ns.profile_enable(True)
+    sampler.start()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(args.steps):
+        step()
+    e1.record()
+    torch.cuda.synchronize()
+    clocks = sampler.stop()
+    prof = ns.profile_read()
+    ns.profile_enable(False)
+    launches = ns.launch_count() - c0
+    if world > 1:
+        dist.barrier()
+    ms = e0.elapsed_time(e1) / args.steps
+    t = torch.tensor([ms], device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    total_flops = sum(ns_flops(m, n, iters) for m, n in shapes)
+
+    # ---- roofline of the dominant kernel (per-launch algorithmic work / avg launch time)
+    units = kernel_units([shapes[i] for i in mine], iters)
+    kinds = [k for k in ("gram", "poly", "update", "precondition") if prof[k][1] > 0]
+    dom = max(kinds, key=lambda k: prof[k][0]) if kinds else None
+    region_ms = ms * args.steps
+    sustained = region_ms >= 1000.0
+    roof = None
+    if dom is not None:
+        avg_ms = prof[dom][0] / prof[dom][1]
+        if dom == "precondition":
+            ach = units[dom] / (avg_ms * 1e-3) / 1e9
+            roof = {"kernel": dom, "bound": "hbm", "achieved": round(ach, 1), "peak": peaks["hbm"], "unit": "GB/s"}
+        else:
+            ach = units[dom] / (avg_ms * 1e-3) / 1e12
+            pk = peaks["bf16_sustained"] if sustained else peaks["bf16"]
+            roof = {"kernel": dom, "bound": "tensor", "achieved": round(ach, 1), "peak": pk, "unit": "TFLOP/s"}
+        roof["frac"] = round(roof["achieved"] / roof["peak"], 4)
+        roof["traffic"] = lookup_traffic(args.workload, dom)
+        roof["peak_source"] = f"{peaks['source']} MEASURED_PEAKS.json " + (
+            "hbm_gbs" if roof["bound"] == "hbm" else ("bf16_tflops_sustained" if sustained else "bf16_tflops (burst)"))
+        roof["avg_launch_ms"] = round(avg_ms, 4)
+        roof["share_of_step"] = round(prof[dom][0] / max(region_ms, 1e-9), 4)
+        roof["kernel_ms_per_step"] = {k: round(v[0] / args.steps, 4) for k, v in prof.items() if v[1]}
+
+    # ---- e2e through the public API with host buffers (pinned), copies inside the region
+    e2e = run_e2e(args, xs, shapes, plan, mine, rank, world, dev, iters)
+
+    line = {
+        "metric": METRIC, "value": round(ms, 4), "unit": "ms", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": False,
+        "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic (seeded Gaussian N(0,1) matrices, bf16-rounded, GPT-2-medium hidden-matrix shapes)",
+        "config": {"workload": WORKLOAD if args.workload == "gpt2-medium" else args.workload,
+                   "matrices": len(shapes), "iters": iters, "precond": "aol", "coeffs": "Muon+ last 4 (App. D)",
+                   "sharding": f"LPT whole-matrix ownership over {world} rank(s) + NCCL all-gather" if world > 1
+                   else "1 rank, grouped launch (13 launches / step)",
+                   "l2": f"inputs {sum(m * n for m, n in shapes) * 2 / 1e6:.0f} MB > 126 MB L2, no flush",
+                   "parallelism": f"dp{world} (matrix ownership)"},
+        "tflops_alg": round(total_flops / (ms * 1e-3) / 1e12, 1),
+        "e2e": e2e,
+        "gpu_launches": int(launches),
+        "roofline": roof,
+        "clocks": clocks,
+    }
+    if world == 1 and rank == 0 and not args.quick:
+        line["extras"] = run_extras(args, peaks)
+        cpu_ms, done, secs = oracle_sample_ms(shapes, iters, args.cpu_budget)
+        line["cpu_baseline"] = {"value": round(cpu_ms, 1), "unit": "ms", "cores": blas_threads(), "kind": "oracle",
+                                "sample": f"{len(done)} whole matrices ({summarize(done)}) in {secs:.1f} s, numpy fp64 "
+                                          f"+ OpenBLAS; extrapolated to the {len(shapes)}-matrix set by algorithmic FLOPs"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def summarize(done):
+    from collections import Counter
+    return ", ".join(f"{v} x {k}" for k, v in Counter(done).items())
+
+
+def lookup_traffic(workload, kernel):
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
+        return d.get(workload, {}).get(kernel)
+    except Exception:
+        return None
+
+
+def run_e2e(args, xs, shapes, plan, mine, rank, world, dev, iters):
+    import torch
+
+    from paper_2512_04632_b200.parallel import orthogonalize_sharded
+    host_in = {i: xs[i].cpu().pin_memory() for i in mine}
+    gathered = orthogonalize_sharded(xs, None, iters=iters)
+    buf = gathered[0]._base if gathered[0]._base is not None else gathered[0]
+    host_out = torch.empty(buf.numel(), dtype=buf.dtype).pin_memory()
+    h2d = sum(host_in[i].numel() * 2 for i in mine)
+    d2h = host_out.numel() * 2
+
+    def step():
+        for i in mine:
+            xs[i].copy_(host_in[i], non_blocking=True)
+        g = orthogonalize_sharded(xs, None, iters=iters)
+        b = g[0]._base if g[0]._base is not None else g[0]
+        host_out.copy_(b, non_blocking=True)
+
+    step()
+    torch.cuda.synchronize()
+    k = max(1, min(args.steps, args.e2e_steps))
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(k):
+        step()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / k
+    t = torch.tensor([ms], device=dev)
+    if world > 1:
+        import torch.distributed as dist
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return {"value": round(float(t.item()), 3), "unit": "ms", "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": int(d2h), "steps": k,
+            "path": "pinned host -> H2D -> orthogonalize_sharded (C ABI) -> all-gather -> D2H pinned host"}
+
+
+def run_extras(args, peaks):
+    """The other workloads the metric names (N = 1 only)."""
+    import torch
+
+    import paper_2512_04632_b200 as ns
+    out = {}
+    flush_buf = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+
+    def flush():
+        flush_buf.fill_(1.0)
+
+    # --- 8192^2 (config 4): Turbo-Muon AOL T=4 vs plain Frobenius T=5 vs cuBLAS dense
+    n = 8192
+    x0 = torch.from_numpy(I.gaussian(n, n, seed=I.matrix_seed(4, 0))).to(torch.bfloat16).cuda()
+    out_t = torch.empty_like(x0)
+    reps = args.extra_reps
+    ns.orthogonalize_list([x0], out=[out_t], iters=4, precond="aol")
+    ns.orthogonalize_list([x0], out=[out_t], iters=5, precond="frobenius")
+    ns.profile_enable(True)
+    ms_turbo = time_calls(lambda: ns.orthogonalize_list([x0], out=[out_t], iters=4, precond="aol"), reps, flush)
+    prof = ns.profile_read()
+    ms_frob = time_calls(lambda: ns.orthogonalize_list([x0], out=[out_t], iters=5, precond="frobenius"), reps, flush)
+    ns.profile_read()
+    ns.profile_enable(False)
+    ms_dense = time_calls(lambda: torch_dense_ns(x0, C.turbo(4)), max(3, reps // 2), flush)
+    f4 = ns_flops(n, n, 4)
+    units = kernel_units([(n, n)], 4)
+    kern = {}
+    for k in ("gram", "poly", "update"):
+        tot, cnt = prof[k]
+        if cnt:
+            avg = tot / cnt
+            kern[k] = {"avg_ms": round(avg, 4), "tflops_alg": round(units[k] / (avg * 1e-3) / 1e12, 1),
+                       "frac_of_burst_peak": round(units[k] / (avg * 1e-3) / 1e12 / peaks["bf16"], 4)}
+    if prof["precondition"][1]:
+        avg = prof["precondition"][0] / prof["precondition"][1]
+        kern["precondition"] = {"avg_ms": round(avg, 4),
+                                "gbs_alg": round(units["precondition"] / (avg * 1e-3) / 1e9, 1),
+                                "frac_of_hbm": round(units["precondition"] / (avg * 1e-3) / 1e9 / peaks["hbm"], 4)}
+    out["square_8192"] = {
+        "turbo_aol_t4_ms": round(ms_turbo, 3),
+        "tflops_alg": round(f4 / (ms_turbo * 1e-3) / 1e12, 1),
+        "frac_of_bf16_peak": round(f4 / (ms_turbo * 1e-3) / 1e12 / peaks["bf16"], 4),
+        "target_ms_at_60pct": round(f4 / (0.6 * peaks["bf16"] * 1e12) * 1e3, 3),
+        "frobenius_t5_ms": round(ms_frob, 3),
+        "cublas_dense_turbo_t4_ms": round(ms_dense, 3),
+        "speedup_vs_frobenius_t5": round(ms_frob / ms_turbo, 3),
+        "speedup_vs_cublas_dense": round(ms_dense / ms_turbo, 3),
+        "kernels": kern,
+        "timing": f"median of {reps} calls, L2 flushed (256 MB write) before each",
+    }
+    del x0, out_t
+    # --- GPT-2 small set (config 2)
+    shapes = I.shape_set("gpt2-small")
+    xs = [torch.from_numpy(x).to(torch.bfloat16).cuda() for x in make_inputs(shapes, 2)]
+    outs = [torch.empty_like(t) for t in xs]
+    ns.orthogonalize_list(xs, out=outs, iters=4)
+    ms_s = time_calls(lambda: ns.orthogonalize_list(xs, out=outs, iters=4), reps, flush)
+    fs = sum(ns_flops(m, n, 4) for m, n in shapes)
+    out["gpt2_small"] = {"ms": round(ms_s, 4), "tflops_alg": round(fs / (ms_s * 1e-3) / 1e12, 1),
+                         "matrices": len(shapes)}
+    # --- CIFAR conv set (config 3), latency-bound
+    shapes = I.shape_set("cifar")
+    xs = [torch.from_numpy(x).to(torch.bfloat16).cuda() for x in make_inputs(shapes, 3)]
+    outs = [torch.empty_like(t) for t in xs]
+    ns.orthogonalize_list(xs, out=outs, iters=4)
+    ms_c = time_calls(lambda: ns.orthogonalize_list(xs, out=outs, iters=4), reps, None)
+    out["cifar"] = {"us": round(ms_c * 1e3, 1), "launches": 13, "matrices": len(shapes)}
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["own", "reference"], default="own")
+    ap.add_argument("--workload", default="gpt2-medium")
+    ap.add_argument("--iters", type=int, default=4)
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--extra-reps", type=int, default=10)
+    ap.add_argument("--cpu-budget", type=float, default=12.0, help="seconds of oracle CPU work")
+    ap.add_argument("--quick", action="store_true", help="skip extras and cpu_baseline (profiling runs)")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_own(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

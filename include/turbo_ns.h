@@ -103,6 +103,14 @@ uint64_t ns_launch_count(void);
  * 1 = force the SIMT (CUDA-core) kernels.  Returns the previous value. */
 int ns_set_path(int path);
 
+/* Per-kernel event timing (measurement support for bench.py; off by default).
+ * When enabled, every launch the library enqueues is bracketed by CUDA events recorded
+ * on the SAME stream.  ns_profile_read SYNCHRONISES on the last event, writes for each
+ * kind k (0 GRAM, 1 PRECOND, 2 POLY, 3 XB, 4 SIMT, 5 COPY; nkinds <= 6) the summed
+ * device milliseconds ms[k] and the launch count counts[k], then clears the records. */
+void ns_profile_enable(int on);
+ns_status ns_profile_read(double* ms, uint64_t* counts, int nkinds);
+
 const char* ns_status_string(ns_status s);
 const char* ns_last_error(void); /* detail of the last non-OK status (thread-local) */
 int ns_abi_version(void);

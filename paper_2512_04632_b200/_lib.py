@@ -19,7 +19,7 @@ FLAG_ZERO_SCALE, FLAG_NONFINITE = 1, 2
 EXPORTS = [
     "ns_orthogonalize", "ns_orthogonalize_batched", "ns_workspace_size", "ns_read_flags",
     "ns_launch_count", "ns_set_path", "ns_status_string", "ns_last_error", "ns_abi_version",
-    "ns_shutdown", "nsx_gram", "nsx_precondition", "nsx_poly", "nsx_update",
+    "ns_shutdown", "ns_profile_enable", "ns_profile_read", "nsx_gram", "nsx_precondition", "nsx_poly", "nsx_update",
 ]
 
 
@@ -30,7 +30,7 @@ class NSError(RuntimeError):
 def _load() -> ctypes.CDLL:
     if not os.path.exists(LIB_PATH):
         raise ImportError(
-            f"{LIB_PATH} not found: build it with `python -m paper_2512_04632_b200.build` "
+            f"{LIB_PATH} not found: build it with `python paper_2512_04632_b200/build.py` "
             "(or __graft_entry__.build()); there is no CPU fallback")
     lib = ctypes.CDLL(LIB_PATH)
     c_i64, c_int, c_vp, c_float = ctypes.c_int64, ctypes.c_int, ctypes.c_void_p, ctypes.c_float
@@ -53,13 +53,16 @@ def _load() -> ctypes.CDLL:
     lib.ns_abi_version.restype = c_int
     lib.ns_shutdown.argtypes = []
     lib.ns_shutdown.restype = None
+    lib.ns_profile_enable.argtypes = [c_int]
+    lib.ns_profile_enable.restype = None
+    lib.ns_profile_read.argtypes = [ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_uint64), c_int]
     lib.nsx_gram.argtypes = [c_vp, c_i64, c_i64, c_vp, c_int, c_vp]
     lib.nsx_precondition.argtypes = [c_vp, c_i64, c_int, c_vp, c_int, c_vp]
     lib.nsx_poly.argtypes = [c_vp, c_i64, c_float, c_float, c_vp, c_vp, c_int, c_vp]
     lib.nsx_update.argtypes = [c_vp, c_i64, c_i64, c_vp, c_float, c_vp, c_vp, c_int, c_vp]
     for name in EXPORTS:
         if name not in ("ns_launch_count", "ns_set_path", "ns_status_string", "ns_last_error",
-                        "ns_abi_version", "ns_shutdown"):
+                        "ns_abi_version", "ns_shutdown", "ns_profile_enable"):
             getattr(lib, name).restype = c_int
     return lib
 

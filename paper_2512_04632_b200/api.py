@@ -16,7 +16,7 @@ from ._lib import DTYPE_BF16, DTYPE_FP32, PRECOND, check, lib
 
 __all__ = [
     "orthogonalize", "orthogonalize_list", "workspace_size", "read_flags", "launch_count",
-    "set_path", "shutdown", "gram", "precondition", "poly", "update", "default_coeffs",
+    "set_path", "shutdown", "profile_enable", "profile_read", "gram", "precondition", "poly", "update", "default_coeffs",
 ]
 
 
@@ -131,6 +131,22 @@ def launch_count() -> int:
 def set_path(path: int) -> int:
     """0 = auto (tcgen05 for aligned bf16), 1 = force the CUDA-core kernels."""
     return int(lib.ns_set_path(int(path)))
+
+
+KERNEL_KINDS = ("gram", "precondition", "poly", "update", "simt", "copy")
+
+
+def profile_enable(on: bool = True) -> None:
+    """Bracket every library launch with CUDA events on its stream (measurement)."""
+    lib.ns_profile_enable(1 if on else 0)
+
+
+def profile_read() -> dict:
+    """Synchronise and return {kind: (total_ms, launches)}; clears the records."""
+    ms = (ctypes.c_double * 6)()
+    cnt = (ctypes.c_uint64 * 6)()
+    check(lib.ns_profile_read(ms, cnt, 6), "ns_profile_read")
+    return {k: (float(ms[i]), int(cnt[i])) for i, k in enumerate(KERNEL_KINDS)}
 
 
 def shutdown() -> None:

@@ -1,6 +1,6 @@
 """Build libturbons.so in-tree with nvcc for sm_100a (no JIT cache, no torch extension).
 
-    python -m paper_2512_04632_b200.build [--force]
+    python paper_2512_04632_b200/build.py [--force]     (or __graft_entry__.build())
 """
 from __future__ import annotations
 

@@ -32,6 +32,27 @@ static uint64_t g_launches = 0;
 static int g_path = 0;
 static thread_local std::string g_err;
 
+// ---- optional per-launch event timing (ns_profile_*)
+struct ProfRec { int kind; cudaEvent_t a, b; };
+static bool g_prof = false;
+static std::vector<ProfRec> g_prof_recs;
+static std::vector<cudaEvent_t> g_ev_pool;
+static cudaEvent_t ev_get() {
+  if (!g_ev_pool.empty()) { cudaEvent_t e = g_ev_pool.back(); g_ev_pool.pop_back(); return e; }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+struct ProfScope {
+  bool on; int kind; cudaStream_t s; cudaEvent_t a = nullptr, b = nullptr;
+  ProfScope(int k, cudaStream_t st) : on(g_prof), kind(k), s(st) {
+    if (on) { a = ev_get(); cudaEventRecord(a, s); }
+  }
+  ~ProfScope() {
+    if (on) { b = ev_get(); cudaEventRecord(b, s); g_prof_recs.push_back({kind, a, b}); }
+  }
+};
+
 static ns_status fail(ns_status s, const std::string& msg) {
   g_err = msg;
   return s;
@@ -115,6 +136,7 @@ struct Phase {
   int64_t total;    // tiles (GEMM/SIMT) or items (PRECOND)
   int64_t total_rows;
   bool vec8;
+  int gemm_kind;  // profiling kind: 0 GRAM, 2 POLY, 3 XB
   // copies (PH_COPY)
   std::vector<std::pair<std::pair<void*, const void*>, size_t>> copies;
 };
@@ -300,6 +322,7 @@ static ns_status build_plan(Plan& P, HostTables& H, DevCtx* dc, const float* coe
           tmi.push_back({ta, tb});
         }
         Phase ph{PH_GEMM};
+        ph.gemm_kind = mode == MODE_GRAM ? 0 : (mode == MODE_POLY ? 2 : 3);
         ph.dev_off = H.push(jobs.data(), jobs.size() * sizeof(GemmJob), 64);
         ph.njobs = (int)jobs.size();
         ph.total = total;
@@ -404,26 +427,34 @@ static ns_status enqueue_plan(Plan& P, DevCtx* dc, cudaStream_t stream) {
   uint8_t* dbase = reinterpret_cast<uint8_t*>(P.dtab);
   for (const Phase& ph : P.phases) {
     switch (ph.kind) {
-      case PH_COPY:
+      case PH_COPY: {
+        ProfScope ps(5, stream);
         for (auto& c : ph.copies)
           CU_TRY(cudaMemcpyAsync(c.first.first, c.first.second, c.second, cudaMemcpyDeviceToDevice, stream));
         break;
-      case PH_GEMM:
+      }
+      case PH_GEMM: {
+        ProfScope ps(ph.gemm_kind, stream);
         CU_TRY(launch_umma_gemm(reinterpret_cast<const GemmJob*>(dbase + ph.dev_off), ph.njobs, ph.total,
                                 dc->sms, dc->flags, stream));
         ++g_launches;
         break;
-      case PH_SIMT:
+      }
+      case PH_SIMT: {
+        ProfScope ps(4, stream);
         CU_TRY(launch_simt_gemm(reinterpret_cast<const SimtJob*>(dbase + ph.dev_off), ph.njobs, ph.total,
                                 dc->sms, P.dtype == NS_BF16, dc->flags, stream));
         ++g_launches;
         break;
-      case PH_PRECOND:
+      }
+      case PH_PRECOND: {
+        ProfScope ps(1, stream);
         CU_TRY(launch_precondition(reinterpret_cast<const PrecondJob*>(dbase + ph.dev_off), ph.njobs,
                                    ph.total_rows, ph.total, ph.vec8, P.dtype == NS_BF16, P.barrier,
                                    dc->flags, stream));
         ++g_launches;
         break;
+      }
     }
   }
   return NS_OK;
@@ -532,6 +563,27 @@ const char* ns_last_error(void) { return g_err.c_str(); }
 uint64_t ns_launch_count(void) {
   std::lock_guard<std::mutex> lk(g_mu);
   return g_launches;
+}
+
+void ns_profile_enable(int on) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  g_prof = on != 0;
+}
+
+ns_status ns_profile_read(double* ms, uint64_t* counts, int nkinds) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (!ms || !counts || nkinds < 1 || nkinds > 6) return fail(NS_ERR_INVALID_VALUE, "bad arguments");
+  for (int k = 0; k < nkinds; ++k) { ms[k] = 0.0; counts[k] = 0; }
+  if (!g_prof_recs.empty()) CU_TRY(cudaEventSynchronize(g_prof_recs.back().b));
+  for (const ProfRec& r : g_prof_recs) {
+    float t = 0.f;
+    CU_TRY(cudaEventElapsedTime(&t, r.a, r.b));
+    if (r.kind < nkinds) { ms[r.kind] += t; counts[r.kind] += 1; }
+    g_ev_pool.push_back(r.a);
+    g_ev_pool.push_back(r.b);
+  }
+  g_prof_recs.clear();
+  return NS_OK;
 }
 
 int ns_set_path(int path) {
