@@ -99,8 +99,9 @@ ns_status ns_read_flags(void* stream, uint32_t* flags);
 /* Number of kernels the library launched on this process since load (host counter). */
 uint64_t ns_launch_count(void);
 
-/* Execution-path override for testing: 0 = auto (tcgen05 for aligned bf16),
- * 1 = force the SIMT (CUDA-core) kernels.  Returns the previous value. */
+/* Execution-path override for testing: 0 = auto (tcgen05, 256x256 tiles on CTA pairs,
+ * for aligned bf16), 1 = force the SIMT (CUDA-core) kernels, 2 = tcgen05 with single-CTA
+ * 128x256 tiles.  Returns the previous value. */
 int ns_set_path(int path);
 
 /* Per-kernel event timing (measurement support for bench.py; off by default).

@@ -129,7 +129,7 @@ def launch_count() -> int:
 
 
 def set_path(path: int) -> int:
-    """0 = auto (tcgen05 for aligned bf16), 1 = force the CUDA-core kernels."""
+    """0 = auto (tcgen05 CTA-pair 256x256 tiles), 1 = CUDA-core kernels, 2 = tcgen05 1-CTA tiles."""
     return int(lib.ns_set_path(int(path)))
 
 

@@ -145,6 +145,7 @@ struct Plan {
   int device = 0;
   ns_dtype dtype = NS_BF16;
   bool simt = false;
+  int cg = 2;  // tcgen05 CTA group (2: 256x256 tiles on CTA pairs)
   int iters = 0;
   ns_precond precond = NS_PRECOND_AOL;
   std::vector<Mat> mats;
@@ -308,14 +309,8 @@ static ns_status build_plan(Plan& P, HostTables& H, DevCtx* dc, const float* coe
             J.s = scaled ? Sv(mt) : nullptr;
             J.a = a;
           }
-          if (J.sym) {
-            const int nb = (J.P + kSymBlock - 1) / kSymBlock;
-            J.tiles = nb * (nb + 1);  // two halves per lower-triangle block
-            J.tiles_q = nb;
-          } else {
-            J.tiles_q = (J.Q + kBN - 1) / kBN;
-            J.tiles = ((J.P + kBM - 1) / kBM) * J.tiles_q;
-          }
+          J.tiles_q = J.sym ? (J.P + kSymBlock - 1) / kSymBlock : (J.Q + kBN - 1) / kBN;
+          J.tiles = umma_tiles(J.sym, J.P, J.Q, P.cg);
           J.tile_start = total;
           total += J.tiles;
           jobs.push_back(J);
@@ -436,7 +431,7 @@ static ns_status enqueue_plan(Plan& P, DevCtx* dc, cudaStream_t stream) {
       case PH_GEMM: {
         ProfScope ps(ph.gemm_kind, stream);
         CU_TRY(launch_umma_gemm(reinterpret_cast<const GemmJob*>(dbase + ph.dev_off), ph.njobs, ph.total,
-                                dc->sms, dc->flags, stream));
+                                P.cg, dc->sms, dc->flags, stream));
         ++g_launches;
         break;
       }
@@ -496,7 +491,9 @@ static ns_status run(const std::vector<Mat>& mats_in, int iters, const float* co
   // plan key
   std::vector<uint64_t> key;
   key.reserve(mats_in.size() * 4 + 8 + 3 * iters);
+  const int cg = (g_path == 2) ? 1 : 2;
   key.push_back((uint64_t)dev); key.push_back((uint64_t)dtype); key.push_back(simt ? 1 : 0);
+  key.push_back((uint64_t)cg);
   key.push_back((uint64_t)iters); key.push_back((uint64_t)precond);
   for (int i = 0; i < 3 * iters; ++i) { uint32_t u; std::memcpy(&u, &coeffs[i], 4); key.push_back(u); }
   for (const Mat& mt : mats_in) {
@@ -514,7 +511,7 @@ static ns_status run(const std::vector<Mat>& mats_in, int iters, const float* co
       g_plans.erase(victim);
     }
     std::unique_ptr<Plan> np(new Plan());
-    np->device = dev; np->dtype = dtype; np->simt = simt; np->iters = iters; np->precond = precond;
+    np->device = dev; np->dtype = dtype; np->simt = simt; np->cg = cg; np->iters = iters; np->precond = precond;
     np->mats = mats_in;
     HostTables H;
     st = build_plan(*np, H, dc, coeffs);
@@ -684,7 +681,7 @@ static ns_status one_gemm(GemmJob J, int ta_rows, int ta_cols, const void* ta_pt
     std::memcpy(h.data() + 2 * sizeof(CUtensorMap), &J, sizeof(J));
     CU_TRY(cudaMemcpy(dmem, h.data(), bytes, cudaMemcpyHostToDevice));
     cudaError_t e = launch_umma_gemm(reinterpret_cast<const GemmJob*>(d + 2 * sizeof(CUtensorMap)), 1,
-                                      J.tiles, dc->sms, dc->flags, stream);
+                                      J.tiles, g_path == 2 ? 1 : 2, dc->sms, dc->flags, stream);
     ++g_launches;
     cudaError_t e2 = cudaStreamSynchronize(stream);
     cudaFree(dmem);
@@ -715,14 +712,8 @@ static bool step_simt(ns_dtype dtype, int64_t m, int64_t n, std::initializer_lis
 }
 
 static void finish_tiles(GemmJob& J, SimtJob& S) {
-  if (J.sym) {
-    const int nb = (J.P + kSymBlock - 1) / kSymBlock;
-    J.tiles = nb * (nb + 1);
-    J.tiles_q = nb;
-  } else {
-    J.tiles_q = (J.Q + kBN - 1) / kBN;
-    J.tiles = ((J.P + kBM - 1) / kBM) * J.tiles_q;
-  }
+  J.tiles_q = J.sym ? (J.P + kSymBlock - 1) / kSymBlock : (J.Q + kBN - 1) / kBN;
+  J.tiles = umma_tiles(J.sym, J.P, J.Q, g_path == 2 ? 1 : 2);
   S.tiles_q = (S.Q + kSimtTile - 1) / kSimtTile;
   S.tiles = ((S.P + kSimtTile - 1) / kSimtTile) * S.tiles_q;
 }

@@ -7,8 +7,11 @@
 namespace tns {
 
 // tcgen05 bf16 engine (umma_gemm.cu).  One persistent launch over all jobs' tiles.
-cudaError_t launch_umma_gemm(const GemmJob* d_jobs, int njobs, int64_t total_tiles, int num_sms,
-                             uint32_t* d_flags, cudaStream_t stream);
+// cg = 1: 128 x 256 tiles per CTA; cg = 2: 256 x 256 tiles per CTA pair (cta_group::2).
+cudaError_t launch_umma_gemm(const GemmJob* d_jobs, int njobs, int64_t total_tiles, int cg,
+                             int num_sms, uint32_t* d_flags, cudaStream_t stream);
+// Number of tiles of one job for the given cta group (host side).
+int umma_tiles(int sym, int P, int Q, int cg);
 
 // CUDA-core engine (simt.cu); is_bf16 selects the storage type.
 cudaError_t launch_simt_gemm(const SimtJob* d_jobs, int njobs, int64_t total_tiles, int num_sms,

@@ -42,7 +42,7 @@ def _assert_close(gpu, ref, absmag, rel=2.0 ** -8, k=1.0):
 
 
 @pytest.mark.parametrize("shape", SHAPES)
-@pytest.mark.parametrize("path", [0, 1])
+@pytest.mark.parametrize("path", [0, 1, 2])
 def test_gram(shape, path):
     m, n = shape
     x = I.gaussian(m, n, seed=1)
@@ -85,7 +85,7 @@ def test_precondition(N, precond):
 
 @pytest.mark.parametrize("N", [136, 256, 520, 768])
 @pytest.mark.parametrize("scaled", [False, True])
-@pytest.mark.parametrize("path", [0, 1])
+@pytest.mark.parametrize("path", [0, 1, 2])
 def test_poly(N, scaled, path):
     x = I.gaussian(N + 40, N, seed=4).astype(np.float64)
     y1, a1 = O.precondition(x, "aol")
@@ -106,7 +106,7 @@ def test_poly(N, scaled, path):
 
 @pytest.mark.parametrize("shape", SHAPES)
 @pytest.mark.parametrize("scaled", [False, True])
-@pytest.mark.parametrize("path", [0, 1])
+@pytest.mark.parametrize("path", [0, 1, 2])
 def test_update(shape, scaled, path):
     m, n = shape
     N = min(m, n)
