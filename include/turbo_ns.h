@@ -111,6 +111,10 @@ int ns_set_path(int path);
  * device milliseconds ms[k] and the launch count counts[k], then clears the records. */
 void ns_profile_enable(int on);
 ns_status ns_profile_read(double* ms, uint64_t* counts, int nkinds);
+/* Measurement only: epilogue clock counters collected when the environment variable
+ * TNS_DBG has bit 8 set (tiles, cycles waiting for the accumulator, TMEM load, aux wait,
+ * math, staging wait, store issue, -).  SYNCHRONISES the device; reset != 0 zeroes them. */
+ns_status nsx_epilogue_counters(uint64_t* out8, int reset);
 
 const char* ns_status_string(ns_status s);
 const char* ns_last_error(void); /* detail of the last non-OK status (thread-local) */

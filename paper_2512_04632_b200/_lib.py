@@ -19,7 +19,7 @@ FLAG_ZERO_SCALE, FLAG_NONFINITE = 1, 2
 EXPORTS = [
     "ns_orthogonalize", "ns_orthogonalize_batched", "ns_workspace_size", "ns_read_flags",
     "ns_launch_count", "ns_set_path", "ns_status_string", "ns_last_error", "ns_abi_version",
-    "ns_shutdown", "ns_profile_enable", "ns_profile_read", "nsx_gram", "nsx_precondition", "nsx_poly", "nsx_update",
+    "ns_shutdown", "ns_profile_enable", "ns_profile_read", "nsx_epilogue_counters", "nsx_gram", "nsx_precondition", "nsx_poly", "nsx_update",
 ]
 
 
@@ -56,6 +56,7 @@ def _load() -> ctypes.CDLL:
     lib.ns_profile_enable.argtypes = [c_int]
     lib.ns_profile_enable.restype = None
     lib.ns_profile_read.argtypes = [ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_uint64), c_int]
+    lib.nsx_epilogue_counters.argtypes = [ctypes.POINTER(ctypes.c_uint64), c_int]
     lib.nsx_gram.argtypes = [c_vp, c_i64, c_i64, c_vp, c_int, c_vp]
     lib.nsx_precondition.argtypes = [c_vp, c_i64, c_int, c_vp, c_int, c_vp]
     lib.nsx_poly.argtypes = [c_vp, c_i64, c_float, c_float, c_vp, c_vp, c_int, c_vp]

@@ -11,6 +11,7 @@
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 
+#include <array>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -100,18 +101,30 @@ static ns_status dev_ctx(DevCtx** out) {
 
 static inline size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
-// Row-major R x C bf16 matrix, 64 x 64 boxes, 128-byte swizzle, zero OOB fill.
-static ns_status encode_tmap(CUtensorMap* tm, const void* base, int64_t rows, int64_t cols) {
+// Row-major R x C bf16 matrix, zero OOB fill.  box = 64: 64 x 64 boxes with 128-byte
+// swizzle (GEMM operands); box = 32: 32 x 32 boxes with 64-byte swizzle (epilogue).
+static ns_status encode_tmap(CUtensorMap* tm, const void* base, int64_t rows, int64_t cols, int box_dim = 64) {
   cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
   cuuint64_t strides[1] = {(cuuint64_t)cols * 2};
-  cuuint32_t box[2] = {64, 64};
+  cuuint32_t box[2] = {(cuuint32_t)box_dim, (cuuint32_t)box_dim};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = g_encode(tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims,
                         strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                        box_dim == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS)
     return fail(NS_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+  return NS_OK;
+}
+// Both maps of one buffer, consecutively: [64-box operand map, 32-box epilogue map].
+static ns_status encode_pair(std::vector<CUtensorMap>& v, const void* base, int64_t rows, int64_t cols, int* idx) {
+  CUtensorMap tm[2];
+  ns_status st;
+  if ((st = encode_tmap(&tm[0], base, rows, cols, 64)) != NS_OK) return st;
+  if ((st = encode_tmap(&tm[1], base, rows, cols, 32)) != NS_OK) return st;
+  *idx = (int)v.size();
+  v.push_back(tm[0]);
+  v.push_back(tm[1]);
   return NS_OK;
 }
 
@@ -137,6 +150,7 @@ struct Phase {
   int64_t total_rows;
   bool vec8;
   int gemm_kind;  // profiling kind: 0 GRAM, 2 POLY, 3 XB
+  size_t tiles_off = 0;  // offset of the packed tile list (PH_GEMM)
   // copies (PH_COPY)
   std::vector<std::pair<std::pair<void*, const void*>, size_t>> copies;
 };
@@ -176,6 +190,10 @@ static bool tma_ok(const Mat& mt, ns_dtype dt) {
   return true;
 }
 
+// s is padded with zeros to a multiple of the 256-wide tile (+32): the epilogue reads
+// s[q .. q+32) and s[p] for whole tiles without bounds checks.
+static size_t s_floats(int64_t N) { return (size_t)((N + 255) / 256 * 256 + 32); }
+
 static size_t workspace_bytes_for(const std::vector<Mat>& mats, ns_dtype dt) {
   size_t off = 256;  // [0,256): barrier counter
   const size_t es = elem_size(dt);
@@ -183,7 +201,7 @@ static size_t workspace_bytes_for(const std::vector<Mat>& mats, ns_dtype dt) {
     off = align_up(off, 256) + (size_t)mt.M * mt.N * es;
     off = align_up(off, 256) + (size_t)mt.N * mt.N * es;
     off = align_up(off, 256) + (size_t)mt.N * mt.N * es;
-    off = align_up(off, 256) + (size_t)mt.N * 4;
+    off = align_up(off, 256) + s_floats(mt.N) * 4;
   }
   return align_up(off, 256);
 }
@@ -209,7 +227,7 @@ static ns_status build_plan(Plan& P, HostTables& H, DevCtx* dc, const float* coe
     off = align_up(off, 256); mt.w_off = off; off += (size_t)mt.M * mt.N * es;
     off = align_up(off, 256); mt.a_off = off; off += (size_t)mt.N * mt.N * es;
     off = align_up(off, 256); mt.b_off = off; off += (size_t)mt.N * mt.N * es;
-    off = align_up(off, 256); mt.s_off = off; off += (size_t)mt.N * 4;
+    off = align_up(off, 256); mt.s_off = off; off += s_floats(mt.N) * 4;
   }
   P.ws_bytes = align_up(off, 256);
   cudaError_t e = cudaMalloc(&P.ws, P.ws_bytes);
@@ -219,6 +237,7 @@ static ns_status build_plan(Plan& P, HostTables& H, DevCtx* dc, const float* coe
   }
   uint8_t* ws = reinterpret_cast<uint8_t*>(P.ws);
   P.barrier = reinterpret_cast<unsigned*>(ws);
+  CU_TRY(cudaMemset(P.ws, 0, P.ws_bytes));  // zero padding of s (and everything else) once
   auto W = [&](const Mat& mt) { return (void*)(ws + mt.w_off); };
   auto Am = [&](const Mat& mt) { return (void*)(ws + mt.a_off); };
   auto Bm = [&](const Mat& mt) { return (void*)(ws + mt.b_off); };
@@ -228,22 +247,16 @@ static ns_status build_plan(Plan& P, HostTables& H, DevCtx* dc, const float* coe
   std::vector<CUtensorMap> tmaps;
   if (!P.simt) {
     for (Mat& mt : P.mats) {
-      CUtensorMap tm;
       ns_status st;
-      if ((st = encode_tmap(&tm, mt.x, mt.m, mt.n)) != NS_OK) return st;
-      mt.tm_x = (int)tmaps.size(); tmaps.push_back(tm);
+      if ((st = encode_pair(tmaps, mt.x, mt.m, mt.n, &mt.tm_x)) != NS_OK) return st;
       if (mt.out != mt.x) {
-        if ((st = encode_tmap(&tm, mt.out, mt.m, mt.n)) != NS_OK) return st;
-        mt.tm_out = (int)tmaps.size(); tmaps.push_back(tm);
+        if ((st = encode_pair(tmaps, mt.out, mt.m, mt.n, &mt.tm_out)) != NS_OK) return st;
       } else {
         mt.tm_out = mt.tm_x;
       }
-      if ((st = encode_tmap(&tm, W(mt), mt.m, mt.n)) != NS_OK) return st;
-      mt.tm_w = (int)tmaps.size(); tmaps.push_back(tm);
-      if ((st = encode_tmap(&tm, Am(mt), mt.N, mt.N)) != NS_OK) return st;
-      mt.tm_a = (int)tmaps.size(); tmaps.push_back(tm);
-      if ((st = encode_tmap(&tm, Bm(mt), mt.N, mt.N)) != NS_OK) return st;
-      mt.tm_b = (int)tmaps.size(); tmaps.push_back(tm);
+      if ((st = encode_pair(tmaps, W(mt), mt.m, mt.n, &mt.tm_w)) != NS_OK) return st;
+      if ((st = encode_pair(tmaps, Am(mt), mt.N, mt.N, &mt.tm_a)) != NS_OK) return st;
+      if ((st = encode_pair(tmaps, Bm(mt), mt.N, mt.N, &mt.tm_b)) != NS_OK) return st;
     }
   }
   size_t tm_off = tmaps.empty() ? 0 : H.push(tmaps.data(), tmaps.size() * sizeof(CUtensorMap), 128);
@@ -251,7 +264,7 @@ static ns_status build_plan(Plan& P, HostTables& H, DevCtx* dc, const float* coe
   // Device addresses of tensormaps are known only after allocation: record indices now,
   // patch pointers after cudaMalloc of the table (two-pass).  We first compute the final
   // table size by building jobs with placeholder bases, then fix them up.
-  struct Fix { size_t job_off; int ta, tb; };
+  struct Fix { size_t job_off; int ta, tb, tout, taux; };
   std::vector<Fix> fixes;
 
   // -- phases
@@ -277,20 +290,21 @@ static ns_status build_plan(Plan& P, HostTables& H, DevCtx* dc, const float* coe
       const int mode = step;  // GRAM, POLY, XB
       if (!P.simt) {
         std::vector<GemmJob> jobs;
-        std::vector<std::pair<int, int>> tmi;
-        int64_t total = 0;
+        std::vector<std::array<int, 4>> tmi;
         for (Mat& mt : P.mats) {
           GemmJob J;
           std::memset(&J, 0, sizeof(J));
           J.mode = mode;
-          int ta = 0, tb = 0;
+          int ta = 0, tb = 0, tout = -1, taux = -1;
           if (mode == MODE_GRAM) {
             ta = tb = cur_tm(mt, k);
+            tout = mt.tm_a;
             J.a_mn = J.b_mn = mt.wide ? 0 : 1;
             J.sym = 1; J.P = J.Q = (int)mt.N; J.K = (int)mt.M;
             J.out = Am(mt); J.aux = nullptr; J.ld = mt.N;
           } else if (mode == MODE_POLY) {
             ta = tb = mt.tm_a;
+            tout = mt.tm_b; taux = mt.tm_a;
             J.a_mn = J.b_mn = 0;
             J.sym = 1; J.P = J.Q = J.K = (int)mt.N;
             J.out = Bm(mt); J.aux = Am(mt); J.ld = mt.N;
@@ -306,23 +320,25 @@ static ns_status build_plan(Plan& P, HostTables& H, DevCtx* dc, const float* coe
             }
             J.sym = 0; J.K = (int)mt.N;
             J.out = cur_ptr(mt, k + 1); J.aux = cur_ptr(mt, k); J.ld = mt.n;
+            tout = ((T - k) % 2 == 0) ? mt.tm_out : mt.tm_w;
+            taux = cur_tm(mt, k);
             J.s = scaled ? Sv(mt) : nullptr;
             J.a = a;
           }
           J.tiles_q = J.sym ? (J.P + kSymBlock - 1) / kSymBlock : (J.Q + kBN - 1) / kBN;
-          J.tiles = umma_tiles(J.sym, J.P, J.Q, P.cg);
-          J.tile_start = total;
-          total += J.tiles;
           jobs.push_back(J);
-          tmi.push_back({ta, tb});
+          tmi.push_back({ta, tb, tout, taux});
         }
         Phase ph{PH_GEMM};
         ph.gemm_kind = mode == MODE_GRAM ? 0 : (mode == MODE_POLY ? 2 : 3);
         ph.dev_off = H.push(jobs.data(), jobs.size() * sizeof(GemmJob), 64);
         ph.njobs = (int)jobs.size();
-        ph.total = total;
+        std::vector<uint64_t> tl;
+        for (size_t j = 0; j < jobs.size(); ++j) umma_tile_list(jobs[j], (uint32_t)j, P.cg, tl);
+        ph.tiles_off = H.push(tl.data(), tl.size() * sizeof(uint64_t), 64);
+        ph.total = (int64_t)tl.size();
         for (size_t j = 0; j < jobs.size(); ++j)
-          fixes.push_back({ph.dev_off + j * sizeof(GemmJob), tmi[j].first, tmi[j].second});
+          fixes.push_back({ph.dev_off + j * sizeof(GemmJob), tmi[j][0], tmi[j][1], tmi[j][2], tmi[j][3]});
         P.phases.push_back(ph);
       } else {
         std::vector<SimtJob> jobs;
@@ -411,6 +427,8 @@ static ns_status build_plan(Plan& P, HostTables& H, DevCtx* dc, const float* coe
       GemmJob* J = reinterpret_cast<GemmJob*>(H.bytes.data() + f.job_off);
       J->tmA = dbase + tm_off + (size_t)f.ta * sizeof(CUtensorMap);
       J->tmB = dbase + tm_off + (size_t)f.tb * sizeof(CUtensorMap);
+      J->tmOut = dbase + tm_off + (size_t)(f.tout + 1) * sizeof(CUtensorMap);
+      J->tmAux = f.taux >= 0 ? dbase + tm_off + (size_t)(f.taux + 1) * sizeof(CUtensorMap) : nullptr;
     }
     CU_TRY(cudaMemcpy(P.dtab, H.bytes.data(), H.bytes.size(), cudaMemcpyHostToDevice));
   }
@@ -430,7 +448,8 @@ static ns_status enqueue_plan(Plan& P, DevCtx* dc, cudaStream_t stream) {
       }
       case PH_GEMM: {
         ProfScope ps(ph.gemm_kind, stream);
-        CU_TRY(launch_umma_gemm(reinterpret_cast<const GemmJob*>(dbase + ph.dev_off), ph.njobs, ph.total,
+        CU_TRY(launch_umma_gemm(reinterpret_cast<const GemmJob*>(dbase + ph.dev_off),
+                                reinterpret_cast<const uint64_t*>(dbase + ph.tiles_off), ph.total,
                                 P.cg, dc->sms, dc->flags, stream));
         ++g_launches;
         break;
@@ -583,6 +602,14 @@ ns_status ns_profile_read(double* ms, uint64_t* counts, int nkinds) {
   return NS_OK;
 }
 
+ns_status nsx_epilogue_counters(uint64_t* out8, int reset) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (!out8) return fail(NS_ERR_INVALID_VALUE, "NULL");
+  CU_TRY(cudaDeviceSynchronize());
+  CU_TRY(umma_epi_prof(reinterpret_cast<unsigned long long*>(out8), reset != 0));
+  return NS_OK;
+}
+
 int ns_set_path(int path) {
   std::lock_guard<std::mutex> lk(g_mu);
   int old = g_path;
@@ -661,27 +688,46 @@ void ns_shutdown(void) {
 
 // ------------------------------------------------------------------------------ single steps
 // These build a one-off job table, launch one kernel and synchronise (test entry points).
-static ns_status one_gemm(GemmJob J, int ta_rows, int ta_cols, const void* ta_ptr, int tb_rows, int tb_cols,
-                          const void* tb_ptr, SimtJob S, bool simt, ns_dtype dtype, cudaStream_t stream) {
+struct TDesc { const void* ptr; int rows, cols; };
+static ns_status one_gemm(GemmJob J, TDesc ta, TDesc tb, TDesc tout, TDesc taux, SimtJob S, bool simt,
+                          ns_dtype dtype, cudaStream_t stream, int64_t s_len = 0) {
   DevCtx* dc = nullptr;
   ns_status st = dev_ctx(&dc);
   if (st != NS_OK) return st;
   void* dmem = nullptr;
   if (!simt) {
-    CUtensorMap tm[2];
-    if ((st = encode_tmap(&tm[0], ta_ptr, ta_rows, ta_cols)) != NS_OK) return st;
-    if ((st = encode_tmap(&tm[1], tb_ptr, tb_rows, tb_cols)) != NS_OK) return st;
-    const size_t bytes = 2 * sizeof(CUtensorMap) + sizeof(GemmJob);
+    float* spad = nullptr;  // the tcgen05 epilogue reads s in whole tiles: pad with zeros
+    if (J.s) {
+      CU_TRY(cudaMalloc(&spad, s_floats(s_len) * 4));
+      CU_TRY(cudaMemsetAsync(spad, 0, s_floats(s_len) * 4, stream));
+      CU_TRY(cudaMemcpyAsync(spad, J.s, s_len * 4, cudaMemcpyDeviceToDevice, stream));
+      J.s = spad;
+    }
+    struct FreeS { float* p; ~FreeS() { if (p) { cudaDeviceSynchronize(); cudaFree(p); } } } free_s{spad};
+    std::vector<CUtensorMap> tm;
+    int ia, ib, io, ix = -1;
+    if ((st = encode_pair(tm, ta.ptr, ta.rows, ta.cols, &ia)) != NS_OK) return st;
+    if ((st = encode_pair(tm, tb.ptr, tb.rows, tb.cols, &ib)) != NS_OK) return st;
+    if ((st = encode_pair(tm, tout.ptr, tout.rows, tout.cols, &io)) != NS_OK) return st;
+    if (taux.ptr && (st = encode_pair(tm, taux.ptr, taux.rows, taux.cols, &ix)) != NS_OK) return st;
+    const int cg = g_path == 2 ? 1 : 2;
+    std::vector<uint64_t> tl;
+    umma_tile_list(J, 0, cg, tl);
+    const size_t jo = tm.size() * sizeof(CUtensorMap), to = jo + align_up(sizeof(GemmJob), 64);
+    const size_t bytes = to + tl.size() * sizeof(uint64_t);
     CU_TRY(cudaMalloc(&dmem, bytes));
     uint8_t* d = reinterpret_cast<uint8_t*>(dmem);
-    J.tmA = d;
-    J.tmB = d + sizeof(CUtensorMap);
+    J.tmA = d + ia * sizeof(CUtensorMap);
+    J.tmB = d + ib * sizeof(CUtensorMap);
+    J.tmOut = d + (io + 1) * sizeof(CUtensorMap);
+    J.tmAux = ix >= 0 ? d + (ix + 1) * sizeof(CUtensorMap) : nullptr;
     std::vector<uint8_t> h(bytes);
-    std::memcpy(h.data(), tm, sizeof(tm));
-    std::memcpy(h.data() + 2 * sizeof(CUtensorMap), &J, sizeof(J));
+    std::memcpy(h.data(), tm.data(), jo);
+    std::memcpy(h.data() + jo, &J, sizeof(J));
+    std::memcpy(h.data() + to, tl.data(), tl.size() * sizeof(uint64_t));
     CU_TRY(cudaMemcpy(dmem, h.data(), bytes, cudaMemcpyHostToDevice));
-    cudaError_t e = launch_umma_gemm(reinterpret_cast<const GemmJob*>(d + 2 * sizeof(CUtensorMap)), 1,
-                                      J.tiles, g_path == 2 ? 1 : 2, dc->sms, dc->flags, stream);
+    cudaError_t e = launch_umma_gemm(reinterpret_cast<const GemmJob*>(d + jo), reinterpret_cast<const uint64_t*>(d + to),
+                                     (int64_t)tl.size(), cg, dc->sms, dc->flags, stream);
     ++g_launches;
     cudaError_t e2 = cudaStreamSynchronize(stream);
     cudaFree(dmem);
@@ -713,7 +759,6 @@ static bool step_simt(ns_dtype dtype, int64_t m, int64_t n, std::initializer_lis
 
 static void finish_tiles(GemmJob& J, SimtJob& S) {
   J.tiles_q = J.sym ? (J.P + kSymBlock - 1) / kSymBlock : (J.Q + kBN - 1) / kBN;
-  J.tiles = umma_tiles(J.sym, J.P, J.Q, g_path == 2 ? 1 : 2);
   S.tiles_q = (S.Q + kSimtTile - 1) / kSimtTile;
   S.tiles = ((S.P + kSimtTile - 1) / kSimtTile) * S.tiles_q;
 }
@@ -735,7 +780,8 @@ ns_status nsx_gram(const void* X, int64_t m, int64_t n, void* A, ns_dtype dtype,
   if (!wide) { S.sa_p = S.sb_q = 1; S.sa_k = S.sb_k = n; } else { S.sa_p = S.sb_q = n; S.sa_k = S.sb_k = 1; }
   finish_tiles(J, S);
   const bool simt = step_simt(dtype, m, n, {X, A});
-  return one_gemm(J, (int)m, (int)n, X, (int)m, (int)n, X, S, simt, dtype, reinterpret_cast<cudaStream_t>(stream));
+  return one_gemm(J, {X, (int)m, (int)n}, {X, (int)m, (int)n}, {A, (int)N, (int)N}, {nullptr, 0, 0}, S, simt, dtype,
+                  reinterpret_cast<cudaStream_t>(stream));
 }
 
 ns_status nsx_poly(const void* A, int64_t N, float b, float c, const float* s, void* B, ns_dtype dtype,
@@ -753,7 +799,8 @@ ns_status nsx_poly(const void* A, int64_t N, float b, float c, const float* s, v
   S.A = S.B = A; S.sa_p = S.sb_q = N; S.sa_k = S.sb_k = 1;
   finish_tiles(J, S);
   const bool simt = step_simt(dtype, N, N, {A, B});
-  return one_gemm(J, (int)N, (int)N, A, (int)N, (int)N, A, S, simt, dtype, reinterpret_cast<cudaStream_t>(stream));
+  return one_gemm(J, {A, (int)N, (int)N}, {A, (int)N, (int)N}, {B, (int)N, (int)N}, {A, (int)N, (int)N}, S, simt,
+                  dtype, reinterpret_cast<cudaStream_t>(stream), N);
 }
 
 ns_status nsx_update(const void* X, int64_t m, int64_t n, const void* B, float a, const float* s, void* Out,
@@ -782,7 +829,8 @@ ns_status nsx_update(const void* X, int64_t m, int64_t n, const void* B, float a
   }
   finish_tiles(J, S);
   const bool simt = step_simt(dtype, m, n, {X, B, Out});
-  return one_gemm(J, ta_r, ta_c, ta, tb_r, tb_c, tb, S, simt, dtype, reinterpret_cast<cudaStream_t>(stream));
+  return one_gemm(J, {ta, ta_r, ta_c}, {tb, tb_r, tb_c}, {Out, (int)m, (int)n}, {X, (int)m, (int)n}, S, simt, dtype,
+                  reinterpret_cast<cudaStream_t>(stream), N);
 }
 
 ns_status nsx_precondition(void* A, int64_t N, ns_precond precond, float* s, ns_dtype dtype, void* stream) {

@@ -19,10 +19,19 @@ constexpr int kBK = 64;   // K elements per pipeline stage = one 128-byte swizzl
 constexpr int kSymBlock = 256;  // symmetric phases tile the lower triangle in 256 x 256 blocks
 constexpr int kGroupP = 16;     // XB raster: tiles grouped 16 row-blocks deep for L2 reuse
 
+// One entry of a launch's tile list (built on the host in execution order):
+//   bits [0,20) job index | [20,40) p0 / 128 | [40,60) q0 / 256 | bit 63 mirrored store.
+__host__ __device__ inline uint64_t pack_tile(uint32_t job, uint32_t p0, uint32_t q0, bool mirror) {
+  return (uint64_t)job | ((uint64_t)(p0 / 128) << 20) | ((uint64_t)(q0 / 256) << 40) |
+         ((uint64_t)(mirror ? 1 : 0) << 63);
+}
+
 struct GemmJob {
   // Operand sources: D[p][q] = sum_k Aop[p][k] * Bop[q][k].
   const void* tmA;  // CUtensorMap (global memory) of the tensor holding Aop
   const void* tmB;  // CUtensorMap of the tensor holding Bop
+  const void* tmOut;  // CUtensorMap of `out`, 32 x 32 boxes, 64-byte swizzle (epilogue stores)
+  const void* tmAux;  // CUtensorMap of `aux`, 32 x 32 boxes, 64-byte swizzle (epilogue loads)
   int32_t a_mn;     // 1: Aop stored [k][p] (MN-major), 0: stored [p][k] (K-major)
   int32_t b_mn;
   int32_t mode;     // GemmMode

@@ -2,16 +2,21 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <vector>
+
 #include "jobs.h"
 
 namespace tns {
 
 // tcgen05 bf16 engine (umma_gemm.cu).  One persistent launch over all jobs' tiles.
 // cg = 1: 128 x 256 tiles per CTA; cg = 2: 256 x 256 tiles per CTA pair (cta_group::2).
-cudaError_t launch_umma_gemm(const GemmJob* d_jobs, int njobs, int64_t total_tiles, int cg,
+// d_tiles: packed tile list (pack_tile) in execution order, total_tiles entries.
+cudaError_t launch_umma_gemm(const GemmJob* d_jobs, const uint64_t* d_tiles, int64_t total_tiles, int cg,
                              int num_sms, uint32_t* d_flags, cudaStream_t stream);
-// Number of tiles of one job for the given cta group (host side).
-int umma_tiles(int sym, int P, int Q, int cg);
+// Read (and optionally reset) the epilogue clock counters (TNS_DBG bit 8 measurement).
+cudaError_t umma_epi_prof(unsigned long long* out, bool reset);
+// Append the tiles of job `job` (host side).
+void umma_tile_list(const GemmJob& J, uint32_t job, int cg, std::vector<uint64_t>& out);
 
 // CUDA-core engine (simt.cu); is_bf16 selects the storage type.
 cudaError_t launch_simt_gemm(const SimtJob* d_jobs, int njobs, int64_t total_tiles, int num_sms,

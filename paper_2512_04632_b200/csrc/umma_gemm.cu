@@ -15,16 +15,25 @@
 //                                        the accumulator in the epilogue, so X is not
 //                                        re-read by a second kernel.
 //
-// Structure (persistent, warp-specialised, one CTA per SM):
-//   warp 0      : TMA producer (one thread) -> 4-stage smem ring (48 KB / stage)
-//   warp 1      : TMEM allocator + single-thread tcgen05.mma issuer
-//   warps 4..11 : epilogue, TMEM -> registers -> global (two 128-column halves x four
-//                 32-lane TMEM quadrants); the accumulator is double-buffered in TMEM
-//                 (2 x 256 columns) so the epilogue of tile i overlaps the MMAs of tile i+1.
+// Structure (persistent, warp-specialised, one CTA per SM, CTA pairs = clusters of 2):
+//   warp 0      : TMA producer (one thread): 64x64 bf16 boxes, 128-byte swizzle, 5-stage
+//                 smem ring (32 KB / CTA / stage); 2-CTA loads signal the leader's barrier
+//   warp 1      : TMEM allocator + single-thread tcgen05.mma.cta_group::2 issuer (leader)
+//   warps 4..11 : epilogue; each warp owns 32 TMEM lanes (rows) x 128 columns, in 32-column
+//                 chunks: tcgen05.ld -> fused math in registers -> 64-byte-swizzled smem box
+//                 -> TMA bulk store (mirrored blocks: a second, transposed box).  The aux
+//                 operand (A for POLY, X for XB) arrives by TMA into smem, one chunk ahead.
+//   The accumulator is double-buffered in TMEM (2 x 256 columns), so tile i's epilogue
+//   overlaps tile i+1's MMAs.  Tiles come from a host-built list (one 8-byte word each).
 // Operand tiles are moved as 64 x 64 bf16 boxes with 128-byte swizzle; K-major and
 // MN-major operands use the same boxes (only the coordinate order and the UMMA
 // descriptor differ), so X^T X on a row-major X needs no transpose copy.
+// TNS_DBG (environment, measurement only) bits: 1 skip epilogue math/stores, 2 skip
+// mirrored stores, 4 skip aux loads, 8 collect epilogue clock counters.
 #include <cuda_runtime.h>
+
+#include <cstdlib>
+#include <vector>
 
 #include "jobs.h"
 #include "kernels.h"
@@ -50,60 +59,52 @@ struct Geo {
   static constexpr int kABytes = kARows * kBK * 2;
   static constexpr int kBBytes = kBRows * kBK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
-  static constexpr int kStages = CG == 1 ? 4 : 6;
-  static constexpr size_t kSmemBytes = (size_t)kStages * kStageBytes + 1024 + 256;
+  static constexpr int kStages = CG == 1 ? 3 : 5;
+  static constexpr int kEpiOff = kStages * kStageBytes;          // epilogue staging
+  static constexpr int kEpiBytes = kNumEpiWarps * 3 * 2048;      // aux/out/mirror per warp
+  static constexpr size_t kSmemBytes = (size_t)kEpiOff + kEpiBytes + 1024 + 512;
 };
+
+// Measurement counters (TNS_DBG bit 8): per-epilogue-warp clock64 deltas summed over tiles.
+__device__ unsigned long long g_epi_prof[8];
 
 struct TileInfo {
   int job;
   int p0, q0;
   bool mirror;
-  bool valid;
 };
 
-__device__ __forceinline__ int find_job(const GemmJob* __restrict__ jobs, int njobs, int64_t t) {
-  int lo = 0, hi = njobs - 1;
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (jobs[mid].tile_start <= t) lo = mid; else hi = mid - 1;
-  }
-  return lo;
+__device__ __forceinline__ TileInfo decode_tile(const uint64_t* __restrict__ tiles, int64_t t) {
+  const uint64_t w = __ldg(tiles + t);
+  TileInfo ti;
+  ti.job = (int)(w & 0xFFFFFu);
+  ti.p0 = (int)((w >> 20) & 0xFFFFFu) * 128;
+  ti.q0 = (int)((w >> 40) & 0xFFFFFu) * 256;
+  ti.mirror = (w >> 63) != 0;
+  return ti;
 }
 
-template <int CG>
-__device__ __forceinline__ TileInfo decode_tile(const GemmJob* __restrict__ jobs, int njobs,
-                                                int64_t t) {
-  TileInfo ti;
-  ti.job = find_job(jobs, njobs, t);
-  const GemmJob& J = jobs[ti.job];
-  const int local = (int)(t - J.tile_start);
-  if (J.sym) {
-    // lower-triangle 256 x 256 block L = bi(bi+1)/2 + bj; (2 / CG) row parts per block
-    constexpr int parts = 2 / CG;
-    const int L = local / parts, h = local % parts;
-    int bi = (int)((sqrtf(8.0f * (float)L + 1.0f) - 1.0f) * 0.5f);
-    while ((bi + 1) * (bi + 2) / 2 <= L) ++bi;
-    while (bi * (bi + 1) / 2 > L) --bi;
-    const int bj = L - bi * (bi + 1) / 2;
-    ti.p0 = bi * kSymBlock + h * kBM;
-    ti.q0 = bj * kSymBlock;
-    ti.mirror = (bi != bj);
-    ti.valid = ti.p0 < J.P;
-  } else {
-    // grouped raster: kGroupP row-blocks deep, column-block index slowest within a group
-    constexpr int TM = kBM * CG;
-    const int tiles_p = (J.P + TM - 1) / TM;
-    const int tq = J.tiles_q;
-    const int group = local / (kGroupP * tq);
-    const int first_p = group * kGroupP;
-    const int gsz = min(tiles_p - first_p, kGroupP);
-    const int r = local - group * kGroupP * tq;
-    ti.p0 = (first_p + r % gsz) * TM;
-    ti.q0 = (r / gsz) * kBN;
-    ti.mirror = false;
-    ti.valid = true;
-  }
-  return ti;
+// Epilogue parameters of one job, held in registers for the whole tile.
+struct Epi {
+  const void* tmOut;
+  const void* tmAux;
+  int mode, P, Q, s_by_row;
+  int64_t ld;
+  uint16_t* out;
+  const uint16_t* aux;
+  const float* s;
+  float a, b, c;
+};
+__device__ __forceinline__ Epi load_epi(const GemmJob* __restrict__ J) {
+  Epi e;
+  e.tmOut = J->tmOut; e.tmAux = J->tmAux;
+  e.mode = J->mode; e.P = J->P; e.Q = J->Q; e.s_by_row = J->s_by_row;
+  e.ld = J->ld;
+  e.out = reinterpret_cast<uint16_t*>(J->out);
+  e.aux = reinterpret_cast<const uint16_t*>(J->aux);
+  e.s = J->s;
+  e.a = J->a; e.b = J->b; e.c = J->c;
+  return e;
 }
 
 __device__ __forceinline__ float bf2f(uint16_t h) {
@@ -113,109 +114,116 @@ __device__ __forceinline__ uint16_t f2bf(float f) {
   return __bfloat16_as_ushort(__float2bfloat16_rn(f));
 }
 
-// One 32-column chunk of one output row, values v[0..31] = D[p][q..q+31].
-__device__ __forceinline__ void epilogue_chunk(const GemmJob& J, int p, int q, const uint32_t (&r)[32],
-                                               bool mirror, bool& bad) {
-  const bool rowok = p < J.P;
-  const int64_t ld = J.ld;
-  uint16_t* __restrict__ out = reinterpret_cast<uint16_t*>(J.out);
-  const uint16_t* __restrict__ aux = reinterpret_cast<const uint16_t*>(J.aux);
-  const bool full = (q + 32 <= J.Q);
-  float v[32];
-#pragma unroll
-  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+// Epilogue staging: per warp three 32 x 32 bf16 boxes (2 KB each, 64-byte rows) in the
+// 64-byte-swizzle layout the TMA uses (16-byte chunk c of row r lives at chunk
+// c ^ ((r >> 1) & 3)), so one-row-per-lane and one-column-per-lane smem accesses are both
+// bank-conflict free, and every global access is a coalesced bulk-tensor transfer.
+__device__ __forceinline__ uint32_t sw64(uint32_t row, uint32_t byte) {
+  return row * 64u + (byte ^ (((row >> 1) & 3u) << 4));
+}
 
-  // direct-tile values w[i] (before any per-destination scaling)
-  if (J.mode != MODE_GRAM && rowok) {
-    float x[32];
-    if (full) {
-      const uint4* src = reinterpret_cast<const uint4*>(aux + (int64_t)p * ld + q);
+// Epilogue variants (warp-uniform, chosen once per tile; each is branch-free per element).
+enum EpiVariant : int { V_GRAM = 0, V_POLY = 1, V_POLY_S = 2, V_XB = 3, V_XB_SROW = 4, V_XB_SCOL = 5 };
+__device__ __forceinline__ int epi_variant(const Epi& E) {
+  if (E.mode == MODE_GRAM) return V_GRAM;
+  if (E.mode == MODE_POLY) return E.s ? V_POLY_S : V_POLY;
+  return E.s ? (E.s_by_row ? V_XB_SROW : V_XB_SCOL) : V_XB;
+}
+__device__ __forceinline__ float lo_bf(uint32_t w) { return __uint_as_float(w << 16); }
+__device__ __forceinline__ float hi_bf(uint32_t w) { return __uint_as_float(w & 0xFFFF0000u); }
+__device__ __forceinline__ uint32_t pack_bf2(float a, float b) {
+  uint32_t r;
+  asm("cvt.rn.bf16x2.f32 %0, %2, %1;" : "=r"(r) : "f"(a), "f"(b));
+  return r;
+}
+// any bf16 of the pair is Inf/NaN (exponent all ones)
+__device__ __forceinline__ bool nonfinite2(uint32_t w) {
+  return ((w & 0x7F800000u) == 0x7F800000u) | ((w & 0x7F80u) == 0x7F80u);
+}
+// s[q .. q+32) as fp32 (the same for all lanes: broadcast loads; s is padded with zeros).
+__device__ __forceinline__ void load_s32(const float* s, int q, float (&sv)[32]) {
+  const float4* src = reinterpret_cast<const float4*>(s + q);
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const uint4 u = __ldg(src + j);
-        const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
+  for (int j = 0; j < 8; ++j) {
+    const float4 f = __ldg(src + j);
+    sv[4 * j] = f.x; sv[4 * j + 1] = f.y; sv[4 * j + 2] = f.z; sv[4 * j + 3] = f.w;
+  }
+}
+
+// Math of one 32-column chunk of one output row.  r = fp32 accumulator D[p][q..q+32),
+// x = aux row chunk (bf16 pairs).  o = bf16 pairs for out[p][q..], m = bf16 pairs for the
+// mirrored out[q..][p] (only V_POLY_S differs from o: destination-column scaling).
+__device__ __forceinline__ void epi_math(int var, const Epi& E, int p, int q, const uint32_t (&r)[32],
+                                         const uint32_t (&x)[16], uint32_t (&o)[16], uint32_t (&m)[16],
+                                         bool& bad) {
+  switch (var) {
+    case V_GRAM:
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          x[8 * j + 2 * e] = bf2f((uint16_t)(w4[e] & 0xFFFFu));
-          x[8 * j + 2 * e + 1] = bf2f((uint16_t)(w4[e] >> 16));
-        }
+      for (int i = 0; i < 16; ++i) o[i] = pack_bf2(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1]));
+      break;
+    case V_POLY:
+#pragma unroll
+      for (int i = 0; i < 16; ++i)
+        o[i] = pack_bf2(fmaf(E.c, __uint_as_float(r[2 * i]), E.b * lo_bf(x[i])),
+                        fmaf(E.c, __uint_as_float(r[2 * i + 1]), E.b * hi_bf(x[i])));
+      break;
+    case V_POLY_S: {
+      float sv[32];
+      load_s32(E.s, q, sv);
+      const float sp = __ldg(E.s + p);
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const float w0 = fmaf(E.c, __uint_as_float(r[2 * i]), E.b * lo_bf(x[i]));
+        const float w1 = fmaf(E.c, __uint_as_float(r[2 * i + 1]), E.b * hi_bf(x[i]));
+        o[i] = pack_bf2(w0 * sv[2 * i], w1 * sv[2 * i + 1]);
+        m[i] = pack_bf2(w0 * sp, w1 * sp);
       }
-    } else {
-#pragma unroll
-      for (int i = 0; i < 32; ++i) x[i] = (q + i < J.Q) ? bf2f(aux[(int64_t)p * ld + q + i]) : 0.f;
+      break;
     }
-    if (J.mode == MODE_POLY) {
+    case V_XB:
 #pragma unroll
-      for (int i = 0; i < 32; ++i) v[i] = fmaf(J.c, v[i], J.b * x[i]);
-    } else {  // MODE_XB
-      if (J.s == nullptr) {
+      for (int i = 0; i < 16; ++i)
+        o[i] = pack_bf2(fmaf(E.a, lo_bf(x[i]), __uint_as_float(r[2 * i])),
+                        fmaf(E.a, hi_bf(x[i]), __uint_as_float(r[2 * i + 1])));
+      break;
+    case V_XB_SROW: {
+      const float as = E.a * __ldg(E.s + p);
 #pragma unroll
-        for (int i = 0; i < 32; ++i) v[i] = fmaf(J.a, x[i], v[i]);
-      } else if (J.s_by_row) {
-        const float as = J.a * J.s[p];
+      for (int i = 0; i < 16; ++i)
+        o[i] = pack_bf2(fmaf(as, lo_bf(x[i]), __uint_as_float(r[2 * i])),
+                        fmaf(as, hi_bf(x[i]), __uint_as_float(r[2 * i + 1])));
+      break;
+    }
+    default: {  // V_XB_SCOL
+      float sv[32];
+      load_s32(E.s, q, sv);
 #pragma unroll
-        for (int i = 0; i < 32; ++i) v[i] = fmaf(as, x[i], v[i]);
-      } else {
-#pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          const float sq = (q + i < J.Q) ? J.s[q + i] : 0.f;
-          v[i] = fmaf(J.a * sq, x[i], v[i]);
-        }
-      }
+      for (int i = 0; i < 16; ++i)
+        o[i] = pack_bf2(fmaf(E.a * sv[2 * i], lo_bf(x[i]), __uint_as_float(r[2 * i])),
+                        fmaf(E.a * sv[2 * i + 1], hi_bf(x[i]), __uint_as_float(r[2 * i + 1])));
+      break;
     }
   }
-
-  // direct store: out[p][q + i]
-  if (rowok) {
-    const bool colscale = (J.mode == MODE_POLY && J.s != nullptr);
-    uint16_t o[32];
+  bool nf = false;
 #pragma unroll
-    for (int i = 0; i < 32; ++i) {
-      float w = v[i];
-      if (colscale) w *= (q + i < J.Q) ? J.s[q + i] : 0.f;
-      o[i] = f2bf(w);
-      bad |= !isfinite(w) && (q + i < J.Q);
-    }
-    if (full) {
-      uint4* dst = reinterpret_cast<uint4*>(out + (int64_t)p * ld + q);
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        uint4 u;
-        u.x = (uint32_t)o[8 * j + 0] | ((uint32_t)o[8 * j + 1] << 16);
-        u.y = (uint32_t)o[8 * j + 2] | ((uint32_t)o[8 * j + 3] << 16);
-        u.z = (uint32_t)o[8 * j + 4] | ((uint32_t)o[8 * j + 5] << 16);
-        u.w = (uint32_t)o[8 * j + 6] | ((uint32_t)o[8 * j + 7] << 16);
-        dst[j] = u;
-      }
-    } else {
-#pragma unroll
-      for (int i = 0; i < 32; ++i)
-        if (q + i < J.Q) out[(int64_t)p * ld + q + i] = o[i];
-    }
-    // mirrored store: out[q + i][p]  (coalesced across the warp: consecutive p)
-    if (mirror) {
-      const float sp = (J.mode == MODE_POLY && J.s != nullptr) ? J.s[p] : 1.f;
-#pragma unroll
-      for (int i = 0; i < 32; ++i) {
-        if (q + i < J.Q) out[(int64_t)(q + i) * ld + p] = f2bf(v[i] * sp);
-      }
-    }
-  }
+  for (int i = 0; i < 16; ++i) nf |= nonfinite2(o[i]);
+  bad |= nf;
 }
 
 template <int CG>
 __global__ void __launch_bounds__(kThreads, 1)
-    umma_gemm_kernel(const GemmJob* __restrict__ jobs, int njobs, int64_t total_tiles,
-                     uint32_t* __restrict__ flags) {
+    umma_gemm_kernel(const GemmJob* __restrict__ jobs, const uint64_t* __restrict__ tiles,
+                     int64_t total_tiles, uint32_t* __restrict__ flags, int dbg) {
   using G = Geo<CG>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
-  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + (size_t)G::kStages * G::kStageBytes);
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + (size_t)G::kEpiOff + G::kEpiBytes);
   uint64_t* empty_bar = full_bar + G::kStages;
   uint64_t* tfull_bar = empty_bar + G::kStages;
   uint64_t* tempty_bar = tfull_bar + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+  uint64_t* aux_bar = tempty_bar + 2;  // one per epilogue warp
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aux_bar + kNumEpiWarps);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -232,6 +240,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&tfull_bar[i], 1);
       mbar_init(&tempty_bar[i], kNumEpiWarps * CG);
     }
+    for (int i = 0; i < kNumEpiWarps; ++i) mbar_init(&aux_bar[i], 1);
     fence_mbar_init();
   }
   if (warp == 1) {
@@ -249,17 +258,19 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t stage = 0, phase = 0;
       int last_job = -1;
       for (int64_t t = cid; t < total_tiles; t += ncl) {
-        const TileInfo ti = decode_tile<CG>(jobs, njobs, t);
-        if (!ti.valid) continue;
-        const GemmJob& J = jobs[ti.job];
+        const TileInfo ti = decode_tile(tiles, t);
+        const GemmJob* J = jobs + ti.job;
+        const void* tmA = J->tmA;
+        const void* tmB = J->tmB;
+        const int a_mn = J->a_mn, b_mn = J->b_mn, K = J->K;
         if (ti.job != last_job) {
-          tma_desc_acquire(J.tmA);
-          tma_desc_acquire(J.tmB);
+          tma_desc_acquire(tmA);
+          tma_desc_acquire(tmB);
           last_job = ti.job;
         }
         const int pa = ti.p0 + (int)rank * G::kARows;  // this CTA's A rows
         const int qb = ti.q0 + (int)rank * G::kBRows;  // this CTA's B rows
-        const int nk = (J.K + kBK - 1) / kBK;
+        const int nk = (K + kBK - 1) / kBK;
         for (int kb = 0; kb < nk; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
           uint8_t* sa = smem + (size_t)stage * G::kStageBytes;
@@ -268,15 +279,15 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int k0 = kb * kBK;
 #pragma unroll
           for (int i = 0; i < G::kARows / 64; ++i) {
-            const int c0 = J.a_mn ? pa + 64 * i : k0, c1 = J.a_mn ? k0 : pa + 64 * i;
-            if constexpr (CG == 2) tma_load_2d_cg2(sa + i * kBoxBytes, J.tmA, &full_bar[stage], c0, c1);
-            else tma_load_2d(sa + i * kBoxBytes, J.tmA, &full_bar[stage], c0, c1);
+            const int c0 = a_mn ? pa + 64 * i : k0, c1 = a_mn ? k0 : pa + 64 * i;
+            if constexpr (CG == 2) tma_load_2d_cg2(sa + i * kBoxBytes, tmA, &full_bar[stage], c0, c1);
+            else tma_load_2d(sa + i * kBoxBytes, tmA, &full_bar[stage], c0, c1);
           }
 #pragma unroll
           for (int i = 0; i < G::kBRows / 64; ++i) {
-            const int c0 = J.b_mn ? qb + 64 * i : k0, c1 = J.b_mn ? k0 : qb + 64 * i;
-            if constexpr (CG == 2) tma_load_2d_cg2(sb + i * kBoxBytes, J.tmB, &full_bar[stage], c0, c1);
-            else tma_load_2d(sb + i * kBoxBytes, J.tmB, &full_bar[stage], c0, c1);
+            const int c0 = b_mn ? qb + 64 * i : k0, c1 = b_mn ? k0 : qb + 64 * i;
+            if constexpr (CG == 2) tma_load_2d_cg2(sb + i * kBoxBytes, tmB, &full_bar[stage], c0, c1);
+            else tma_load_2d(sb + i * kBoxBytes, tmB, &full_bar[stage], c0, c1);
           }
           if (++stage == G::kStages) { stage = 0; phase ^= 1; }
         }
@@ -293,16 +304,17 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0 && rank == 0) {
       uint32_t stage = 0, phase = 0, as = 0, aphase = 0;
       for (int64_t t = cid; t < total_tiles; t += ncl) {
-        const TileInfo ti = decode_tile<CG>(jobs, njobs, t);
-        if (!ti.valid) continue;
-        const GemmJob& J = jobs[ti.job];
-        const uint32_t idesc = make_idesc_bf16(kBM * CG, kBN, (uint32_t)J.a_mn, (uint32_t)J.b_mn);
-        const uint32_t a_lbo = J.a_mn ? 8192u : 16u, a_step = J.a_mn ? 2048u : 32u;
-        const uint32_t b_lbo = J.b_mn ? 8192u : 16u, b_step = J.b_mn ? 2048u : 32u;
+        const TileInfo ti = decode_tile(tiles, t);
+        const GemmJob* J = jobs + ti.job;
+        const uint32_t a_mn = (uint32_t)J->a_mn, b_mn = (uint32_t)J->b_mn;
+        const int K = J->K;
+        const uint32_t idesc = make_idesc_bf16(kBM * CG, kBN, a_mn, b_mn);
+        const uint32_t a_lbo = a_mn ? 8192u : 16u, a_step = a_mn ? 2048u : 32u;
+        const uint32_t b_lbo = b_mn ? 8192u : 16u, b_step = b_mn ? 2048u : 32u;
         mbar_wait(&tempty_bar[as], aphase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + as * kBN;
-        const int nk = (J.K + kBK - 1) / kBK;
+        const int nk = (K + kBK - 1) / kBK;
         for (int kb = 0; kb < nk; ++kb) {
           mbar_wait(&full_bar[stage], phase);
           tc_fence_after();
@@ -323,35 +335,112 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp >= 4) {
     // ------------------------------------------------------------------ epilogue
-    const int quad = warp & 3;         // TMEM lanes [32*quad, 32*quad + 32)
-    const int half = (warp - 4) >> 2;  // 128-column half of the 256-wide tile
-    uint32_t as = 0, aphase = 0;
+    const int ew = warp - 4;
+    const int quad = warp & 3;  // TMEM lanes [32*quad, 32*quad + 32)
+    const int half = ew >> 2;   // 128-column half of the 256-wide tile
+    uint8_t* s_aux = smem + G::kEpiOff + ew * 6144;
+    uint8_t* s_out = s_aux + 2048;
+    uint8_t* s_mir = s_aux + 4096;
+    uint64_t* abar = aux_bar + ew;
+    const uint32_t sa_aux = smem_u32(s_aux), sa_out = smem_u32(s_out), sa_mir = smem_u32(s_mir);
+    uint32_t as = 0, aphase = 0, xphase = 0;
     bool bad = false;
+    long long pc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     for (int64_t t = cid; t < total_tiles; t += ncl) {
-      const TileInfo ti = decode_tile<CG>(jobs, njobs, t);
-      if (!ti.valid) continue;
-      const GemmJob& J = jobs[ti.job];
+      const TileInfo ti = decode_tile(tiles, t);
+      const Epi E = load_epi(jobs + ti.job);
+      const int var = epi_variant(E);
+      const bool has_aux = (E.mode != MODE_GRAM) && !(dbg & 4);
+      const int prow = ti.p0 + (int)rank * kBM + quad * 32;  // first of this warp's 32 rows
+      const int p = prow + lane;
+      const int qh = ti.q0 + half * 128;
+      if (has_aux && lane == 0) {  // prefetch the aux chunk 0 before the accumulator is ready
+        mbar_arrive_expect_tx(abar, 2048);
+        tma_load_2d(s_aux, E.tmAux, abar, qh, prow);
+      }
+      const bool prof = (dbg & 8) && lane == 0;
+      long long t0 = prof ? clock64() : 0, t1;
       mbar_wait(&tfull_bar[as], aphase);
       tc_fence_after();
-      const int p = ti.p0 + (int)rank * kBM + quad * 32 + lane;
+      if (prof) { t1 = clock64(); pc[1] += t1 - t0; t0 = t1; pc[0] += 1; }
 #pragma unroll 1
       for (int c = 0; c < 4; ++c) {
-        const int cl = half * 128 + c * 32;
+        const int q = qh + c * 32;
         uint32_t r[32];
-        tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(quad * 32) << 16) + as * kBN + (uint32_t)cl, r);
+        tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(quad * 32) << 16) + as * kBN + (uint32_t)(q - ti.q0), r);
+        uint32_t x[16];
+        if (has_aux) {
+          mbar_wait(abar, xphase);
+          if (prof) { t1 = clock64(); pc[3] += t1 - t0; t0 = t1; }
+          xphase ^= 1;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            uint4 u;
+            asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];"
+                         : "=r"(u.x), "=r"(u.y), "=r"(u.z), "=r"(u.w)
+                         : "r"(sa_aux + sw64((uint32_t)lane, 16u * j)));
+            x[4 * j] = u.x; x[4 * j + 1] = u.y; x[4 * j + 2] = u.z; x[4 * j + 3] = u.w;
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) x[j] = 0u;
+        }
         tmem_ld_wait();
+        if (prof) { t1 = clock64(); pc[2] += t1 - t0; t0 = t1; }
         if (c == 3) {
           tc_fence_before();
           __syncwarp();
           if (lane == 0) {
             if constexpr (CG == 2) mbar_arrive_cluster(&tempty_bar[as], 0);
-            else mbar_arrive(&tempty_bar[as]);
+            else mbar_arrive_relaxed(&tempty_bar[as]);
           }
         }
-        epilogue_chunk(J, p, ti.q0 + cl, r, ti.mirror, bad);
+        if (has_aux && c < 3) {  // refill the aux buffer with the next chunk
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            mbar_arrive_expect_tx(abar, 2048);
+            tma_load_2d(s_aux, E.tmAux, abar, q + 32, prow);
+          }
+        }
+        if (dbg & 1) continue;
+        const bool mir = ti.mirror && !(dbg & 2);
+        uint32_t o[16], m[16];
+        epi_math(var, E, p, q, r, x, o, m, bad);
+        if (prof) { t1 = clock64(); pc[4] += t1 - t0; t0 = t1; }
+        // the previous chunk's bulk stores must have finished reading the staging boxes
+        if (lane == 0) bulk_wait_read<0>();
+        __syncwarp();
+        if (prof) { t1 = clock64(); pc[5] += t1 - t0; t0 = t1; }
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(sa_out + sw64((uint32_t)lane, 16u * j)),
+                       "r"(o[4 * j]), "r"(o[4 * j + 1]), "r"(o[4 * j + 2]), "r"(o[4 * j + 3])
+                       : "memory");
+        if (mir) {
+          const bool sep = (var == V_POLY_S);
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            const uint32_t w = sep ? m[i >> 1] : o[i >> 1];
+            const uint16_t h = (uint16_t)(i & 1 ? (w >> 16) : (w & 0xFFFFu));
+            asm volatile("st.shared.u16 [%0], %1;" ::"r"(sa_mir + sw64((uint32_t)i, 2u * lane)), "h"(h)
+                         : "memory");
+          }
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          tma_store_2d(E.tmOut, s_out, q, prow);          // rows prow.., cols q..
+          if (mir) tma_store_2d(E.tmOut, s_mir, prow, q);  // rows q.., cols prow..
+          bulk_commit();
+        }
+        if (prof) { t1 = clock64(); pc[6] += t1 - t0; t0 = t1; }
       }
       if (++as == 2) { as = 0; aphase ^= 1; }
     }
+    if (lane == 0) bulk_wait<0>();
+    if ((dbg & 8) && lane == 0)
+      for (int i = 0; i < 8; ++i) atomicAdd(&g_epi_prof[i], (unsigned long long)pc[i]);
     if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(flags, 2u);
   }
 
@@ -364,7 +453,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 template <int CG>
-static cudaError_t launch_cg(const GemmJob* d_jobs, int njobs, int64_t total_tiles, int num_sms,
+static cudaError_t launch_cg(const GemmJob* d_jobs, const uint64_t* d_tiles, int64_t total_tiles, int num_sms,
                              uint32_t* d_flags, cudaStream_t stream) {
   static bool attr_set[64] = {};
   int dev = 0;
@@ -394,23 +483,51 @@ static cudaError_t launch_cg(const GemmJob* d_jobs, int njobs, int64_t total_til
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kern, d_jobs, njobs, total_tiles, d_flags);
+  static int dbg = -1;
+  if (dbg < 0) {  // measurement knob (never set in production): TNS_DBG bits 1 skip epilogue,
+    const char* e = getenv("TNS_DBG");  // 2 skip mirrored stores, 4 skip aux prefetch
+    dbg = e ? atoi(e) : 0;
+  }
+  return cudaLaunchKernelEx(&cfg, kern, d_jobs, d_tiles, total_tiles, d_flags, dbg);
 }
 
-cudaError_t launch_umma_gemm(const GemmJob* d_jobs, int njobs, int64_t total_tiles, int cg, int num_sms,
-                             uint32_t* d_flags, cudaStream_t stream) {
+cudaError_t launch_umma_gemm(const GemmJob* d_jobs, const uint64_t* d_tiles, int64_t total_tiles, int cg,
+                             int num_sms, uint32_t* d_flags, cudaStream_t stream) {
   if (total_tiles <= 0) return cudaSuccess;
-  return cg == 2 ? launch_cg<2>(d_jobs, njobs, total_tiles, num_sms, d_flags, stream)
-                 : launch_cg<1>(d_jobs, njobs, total_tiles, num_sms, d_flags, stream);
+  return cg == 2 ? launch_cg<2>(d_jobs, d_tiles, total_tiles, num_sms, d_flags, stream)
+                 : launch_cg<1>(d_jobs, d_tiles, total_tiles, num_sms, d_flags, stream);
 }
 
-int umma_tiles(int sym, int P, int Q, int cg) {
-  if (sym) {
-    const int nb = (P + kSymBlock - 1) / kSymBlock;
-    return nb * (nb + 1) / 2 * (2 / cg);
+cudaError_t umma_epi_prof(unsigned long long* out, bool reset) {
+  cudaError_t e = cudaMemcpyFromSymbol(out, g_epi_prof, sizeof(g_epi_prof));
+  if (e == cudaSuccess && reset) {
+    unsigned long long z[8] = {};
+    e = cudaMemcpyToSymbol(g_epi_prof, z, sizeof(z));
+  }
+  return e;
+}
+
+// Tiles of one job in execution order (host).  Symmetric jobs: lower-triangle 256 x 256
+// blocks row by row, (2 / cg) row parts each.  Rectangular jobs: grouped raster, kGroupP
+// tile-rows deep, so concurrently running tiles share operand rows/columns in L2.
+void umma_tile_list(const GemmJob& J, uint32_t job, int cg, std::vector<uint64_t>& out) {
+  if (J.sym) {
+    const int nb = (J.P + kSymBlock - 1) / kSymBlock;
+    for (int bi = 0; bi < nb; ++bi)
+      for (int bj = 0; bj <= bi; ++bj)
+        for (int h = 0; h < 2 / cg; ++h) {
+          const int p0 = bi * kSymBlock + h * kBM;
+          if (p0 < J.P) out.push_back(pack_tile(job, p0, bj * kSymBlock, bi != bj));
+        }
+    return;
   }
   const int tm = kBM * cg;
-  return ((P + tm - 1) / tm) * ((Q + kBN - 1) / kBN);
+  const int tp = (J.P + tm - 1) / tm, tq = (J.Q + kBN - 1) / kBN;
+  for (int g0 = 0; g0 < tp; g0 += kGroupP) {
+    const int gsz = tp - g0 < kGroupP ? tp - g0 : kGroupP;
+    for (int qb = 0; qb < tq; ++qb)
+      for (int i = 0; i < gsz; ++i) out.push_back(pack_tile(job, (g0 + i) * tm, qb * kBN, false));
+  }
 }
 
 }  // namespace tns

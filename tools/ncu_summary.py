@@ -8,10 +8,12 @@ import json
 import subprocess
 import sys
 
+UNIT = {"ns": 1e-3, "us": 1.0, "usecond": 1.0, "msecond": 1e3, "ms": 1e3, "nsecond": 1e-3,
+        "byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3, "Tbyte": 1e6}
 KEYS = {
-    "time_us": ("gpu__time_duration.sum", 1e-3),
-    "dram_read_MB": ("dram__bytes_read.sum", 1e-6),
-    "dram_write_MB": ("dram__bytes_write.sum", 1e-6),
+    "time_us": ("gpu__time_duration.sum", None),
+    "dram_read_MB": ("dram__bytes_read.sum", None),
+    "dram_write_MB": ("dram__bytes_write.sum", None),
     "dram_pct": ("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", 1),
     "tensor_pct": ("sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed", 1),
     "tensor_hmma_pct": ("sm__ops_path_tensor_op_hmma_src_bf16_dst_fp32_sparsity_off.avg.pct_of_peak_sustained_elapsed", 1),
@@ -27,6 +29,7 @@ def load(path):
     out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     hdr = rows[0]
+    units = rows[1]
     res = []
     for r in rows[2:]:
         d = {"kernel": r[hdr.index("Kernel Name")][:60]}
@@ -35,6 +38,8 @@ def load(path):
             if cands:
                 v = r[cands[0]].replace(",", "")
                 try:
+                    if sc is None:
+                        sc = UNIT.get(units[cands[0]], 1.0)
                     d[k] = round(float(v) * sc, 3)
                 except ValueError:
                     d[k] = v
