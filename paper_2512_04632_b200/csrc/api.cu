@@ -136,7 +136,8 @@ struct Mat {
   bool wide;
   bool copy_in;
   // workspace byte offsets
-  size_t w_off, a_off, b_off, s_off;
+  size_t w_off, a_off, b_off, s_off, part_off;
+  int part_ld;
   // tensormap indices (tcgen05 path)
   int tm_x, tm_out, tm_w, tm_a, tm_b;
 };
@@ -193,6 +194,8 @@ static bool tma_ok(const Mat& mt, ns_dtype dt) {
 // s is padded with zeros to a multiple of the 256-wide tile (+32): the epilogue reads
 // s[q .. q+32) and s[p] for whole tiles without bounds checks.
 static size_t s_floats(int64_t N) { return (size_t)((N + 255) / 256 * 256 + 32); }
+// AOL row-sum partial slots per row (see GemmJob::part).
+static int part_ld_for(int64_t N) { return (int)((N + 127) / 128 + (N + 31) / 32); }
 
 static size_t workspace_bytes_for(const std::vector<Mat>& mats, ns_dtype dt) {
   size_t off = 256;  // [0,256): barrier counter
@@ -202,6 +205,7 @@ static size_t workspace_bytes_for(const std::vector<Mat>& mats, ns_dtype dt) {
     off = align_up(off, 256) + (size_t)mt.N * mt.N * es;
     off = align_up(off, 256) + (size_t)mt.N * mt.N * es;
     off = align_up(off, 256) + s_floats(mt.N) * 4;
+    off = align_up(off, 256) + (size_t)mt.N * part_ld_for(mt.N) * 4;
   }
   return align_up(off, 256);
 }
@@ -228,6 +232,9 @@ static ns_status build_plan(Plan& P, HostTables& H, DevCtx* dc, const float* coe
     off = align_up(off, 256); mt.a_off = off; off += (size_t)mt.N * mt.N * es;
     off = align_up(off, 256); mt.b_off = off; off += (size_t)mt.N * mt.N * es;
     off = align_up(off, 256); mt.s_off = off; off += s_floats(mt.N) * 4;
+    mt.part_ld = part_ld_for(mt.N);
+    off = align_up(off, 256); mt.part_off = off;
+    if (P.precond == NS_PRECOND_AOL && !P.simt) off += (size_t)mt.N * mt.part_ld * 4;
   }
   P.ws_bytes = align_up(off, 256);
   cudaError_t e = cudaMalloc(&P.ws, P.ws_bytes);
@@ -242,6 +249,8 @@ static ns_status build_plan(Plan& P, HostTables& H, DevCtx* dc, const float* coe
   auto Am = [&](const Mat& mt) { return (void*)(ws + mt.a_off); };
   auto Bm = [&](const Mat& mt) { return (void*)(ws + mt.b_off); };
   auto Sv = [&](const Mat& mt) { return (float*)(ws + mt.s_off); };
+  auto Part = [&](const Mat& mt) { return (float*)(ws + mt.part_off); };
+  const bool use_part = (P.precond == NS_PRECOND_AOL) && !P.simt;
 
   // -- tensormaps (tcgen05 path)
   std::vector<CUtensorMap> tmaps;
@@ -302,6 +311,7 @@ static ns_status build_plan(Plan& P, HostTables& H, DevCtx* dc, const float* coe
             J.a_mn = J.b_mn = mt.wide ? 0 : 1;
             J.sym = 1; J.P = J.Q = (int)mt.N; J.K = (int)mt.M;
             J.out = Am(mt); J.aux = nullptr; J.ld = mt.N;
+            if (k == 1 && use_part) { J.part = Part(mt); J.part_ld = mt.part_ld; }
           } else if (mode == MODE_POLY) {
             ta = tb = mt.tm_a;
             tout = mt.tm_b; taux = mt.tm_a;
@@ -398,6 +408,7 @@ static ns_status build_plan(Plan& P, HostTables& H, DevCtx* dc, const float* coe
           PrecondJob J;
           std::memset(&J, 0, sizeof(J));
           J.A = Am(mt); J.s = Sv(mt); J.N = (int)mt.N; J.precond = (int)P.precond;
+          if (use_part) { J.part = Part(mt); J.part_ld = mt.part_ld; }
           J.row_start = rows; J.vec_start = items;
           rows += mt.N;
           items += vec8 ? (mt.N * mt.N) / 8 : mt.N * mt.N;

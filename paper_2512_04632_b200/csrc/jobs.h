@@ -46,6 +46,11 @@ struct GemmJob {
   const float* s;      // scaling vector or nullptr
   int32_t s_by_row;    // XB: scale a*aux by s[p] (1) or s[q] (0)
   float a, b, c;
+  // GRAM with AOL (iteration 1): per-tile |A0| row-sum partials, written once each (no
+  // atomics): part[i * part_ld + slot]; slots [0, ceil(N/128)) = direct 128-column blocks,
+  // [ceil(N/128), + ceil(N/32)) = mirrored 32-row blocks.  nullptr = not collected.
+  float* part;
+  int32_t part_ld;
 };
 
 // CUDA-core (SIMT) variant of a GemmJob: operands by pointer + strides (elements),
@@ -73,6 +78,8 @@ constexpr int kSimtTile = 64;
 struct PrecondJob {
   void* A;          // N x N symmetric Gram, in place -> A1
   float* s;         // N
+  const float* part;  // row-sum partials from the Gram epilogue (GemmJob::part) or nullptr
+  int32_t part_ld;
   int32_t N;
   int32_t precond;  // 1 Frobenius, 2 AOL
   int64_t row_start;  // prefix over jobs of N (AOL: one warp per row)

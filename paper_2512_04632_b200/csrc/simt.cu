@@ -151,13 +151,30 @@ __global__ void __launch_bounds__(256)
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   uint32_t fl = 0;
 
+  (void)total_items;
   // ---- phase 1: scaling vector s (Eq. 8 / Eq. 10)
   for (int64_t row = gwarp; row < total_rows; row += nwarps) {
     const PrecondJob& J = jobs[find_pjob(jobs, njobs, row, true)];
     const int i = (int)(row - J.row_start);
     const T* __restrict__ A = reinterpret_cast<const T*>(J.A);
     const int N = J.N;
-    if (J.precond == 2) {  // AOL: s_i = (sum_j |A0_ij|)^(-1/2)
+    if (J.precond == 2 && J.part != nullptr) {
+      // AOL from the Gram epilogue's partials: direct 128-column slots of blocks <= bi,
+      // mirrored 32-row slots of blocks > bi (each |A0_ij| counted exactly once)
+      const int bi = i / 256;
+      const int n1 = (N + 127) / 128, n2 = (N + 31) / 32;
+      const float* pr = J.part + (int64_t)i * J.part_ld;
+      const int d_end = min(2 * (bi + 1), n1), m_beg = min(8 * (bi + 1), n2);
+      float acc = 0.f;
+      for (int k = lane; k < d_end; k += 32) acc += pr[k];
+      for (int k = m_beg + lane; k < n2; k += 32) acc += pr[n1 + k];
+      const float r = warp_sum(acc);
+      if (lane == 0) {
+        J.s[i] = r > 0.f ? rsqrtf(r) : 0.f;
+        if (!(r > 0.f)) fl |= 1u;
+        if (!isfinite(r)) fl |= 2u;
+      }
+    } else if (J.precond == 2) {  // AOL: s_i = (sum_j |A0_ij|)^(-1/2)
       float acc = 0.f;
       const T* Ai = A + (int64_t)i * N;
       if (VEC8 && sizeof(T) == 2) {
@@ -192,30 +209,33 @@ __global__ void __launch_bounds__(256)
 
   grid_barrier(barrier);
 
-  // ---- phase 2: A1 = diag(s) A0 diag(s)  (Alg. 2 l.4)
-  const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t v = gtid; v < total_items; v += nthreads) {
-    const PrecondJob& J = jobs[find_pjob(jobs, njobs, v, false)];
-    const int64_t e0 = (v - J.vec_start) * (VEC8 ? 8 : 1);
+  // ---- phase 2: A1 = diag(s) A0 diag(s)  (Alg. 2 l.4), one warp per row: s_i once,
+  // 16-byte vectors of A and float4 pairs of s along the row (coalesced, no divisions)
+  for (int64_t row = gwarp; row < total_rows; row += nwarps) {
+    const PrecondJob& J = jobs[find_pjob(jobs, njobs, row, true)];
+    const int i = (int)(row - J.row_start);
     const int N = J.N;
-    const int i = (int)(e0 / N), j0 = (int)(e0 % N);
     const float si = J.s[i];
-    T* A = reinterpret_cast<T*>(J.A);
+    T* Ai = reinterpret_cast<T*>(J.A) + (int64_t)i * N;
     if (VEC8 && sizeof(T) == 2) {
-      uint4* p = reinterpret_cast<uint4*>(A + e0);
-      uint4 u = *p;
-      uint32_t w[4] = {u.x, u.y, u.z, u.w};
+      for (int j = lane * 8; j < N; j += 256) {
+        uint4* pv = reinterpret_cast<uint4*>(Ai + j);
+        uint4 u = *pv;
+        const float4 s0 = *reinterpret_cast<const float4*>(J.s + j);
+        const float4 s1 = *reinterpret_cast<const float4*>(J.s + j + 4);
+        const float sj[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
+        uint32_t w[4] = {u.x, u.y, u.z, u.w};
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const float lo = (si * __uint_as_float(w[e] << 16)) * J.s[j0 + 2 * e];
-        const float hi = (si * __uint_as_float(w[e] & 0xFFFF0000u)) * J.s[j0 + 2 * e + 1];
-        w[e] = (uint32_t)st_conv<uint16_t>(lo) | ((uint32_t)st_conv<uint16_t>(hi) << 16);
+        for (int e = 0; e < 4; ++e) {
+          const float lo = (si * __uint_as_float(w[e] << 16)) * sj[2 * e];
+          const float hi = (si * __uint_as_float(w[e] & 0xFFFF0000u)) * sj[2 * e + 1];
+          w[e] = (uint32_t)st_conv<uint16_t>(lo) | ((uint32_t)st_conv<uint16_t>(hi) << 16);
+        }
+        u.x = w[0]; u.y = w[1]; u.z = w[2]; u.w = w[3];
+        *pv = u;
       }
-      u.x = w[0]; u.y = w[1]; u.z = w[2]; u.w = w[3];
-      *p = u;
     } else {
-      A[e0] = st_conv<T>((si * ld_val<T>(A + e0)) * J.s[j0]);
+      for (int j = lane; j < N; j += 32) Ai[j] = st_conv<T>((si * ld_val<T>(Ai + j)) * J.s[j]);
     }
   }
   if (fl) atomicOr(flags, fl);
@@ -231,9 +251,7 @@ static cudaError_t launch_precond_t(const PrecondJob* d_jobs, int njobs, int64_t
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, 0);
   if (occ < 1) occ = 1;
-  int64_t want = (total_items + 255) / 256;
-  const int64_t want_rows = (total_rows * 32 + 255) / 256;
-  if (want_rows > want) want = want_rows;
+  const int64_t want = (total_rows * 32 + 255) / 256;  // one warp per row
   int64_t cap = (int64_t)sms * occ;
   int grid = (int)(want < cap ? (want < 1 ? 1 : want) : cap);
   cudaError_t e = cudaMemsetAsync(d_barrier, 0, sizeof(unsigned), stream);

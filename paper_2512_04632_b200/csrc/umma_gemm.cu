@@ -94,6 +94,8 @@ struct Epi {
   const uint16_t* aux;
   const float* s;
   float a, b, c;
+  float* part;
+  int part_ld;
 };
 __device__ __forceinline__ Epi load_epi(const GemmJob* __restrict__ J) {
   Epi e;
@@ -104,6 +106,7 @@ __device__ __forceinline__ Epi load_epi(const GemmJob* __restrict__ J) {
   e.aux = reinterpret_cast<const uint16_t*>(J->aux);
   e.s = J->s;
   e.a = J->a; e.b = J->b; e.c = J->c;
+  e.part = J->part; e.part_ld = J->part_ld;
   return e;
 }
 
@@ -354,6 +357,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int prow = ti.p0 + (int)rank * kBM + quad * 32;  // first of this warp's 32 rows
       const int p = prow + lane;
       const int qh = ti.q0 + half * 128;
+      float rsum = 0.f;
       if (has_aux && lane == 0) {  // prefetch the aux chunk 0 before the accumulator is ready
         mbar_arrive_expect_tx(abar, 2048);
         tma_load_2d(s_aux, E.tmAux, abar, qh, prow);
@@ -407,6 +411,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         const bool mir = ti.mirror && !(dbg & 2);
         uint32_t o[16], m[16];
         epi_math(var, E, p, q, r, x, o, m, bad);
+        if (E.part != nullptr) {  // AOL row sums of |A0| over this warp's 128 columns (Eq. 8)
+#pragma unroll
+          for (int i = 0; i < 16; ++i) rsum += fabsf(lo_bf(o[i])) + fabsf(hi_bf(o[i]));
+        }
         if (prof) { t1 = clock64(); pc[4] += t1 - t0; t0 = t1; }
         // the previous chunk's bulk stores must have finished reading the staging boxes
         if (lane == 0) bulk_wait_read<0>();
@@ -434,8 +442,25 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (mir) tma_store_2d(E.tmOut, s_mir, prow, q);  // rows q.., cols prow..
           bulk_commit();
         }
+        if (E.part != nullptr && mir) {
+          // mirrored block: row q+lane of A0 gets the |.| sum over this warp's 32 rows,
+          // read back from the transposed staging box (row `lane` of it)
+          float cs = 0.f;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            uint4 u;
+            asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];"
+                         : "=r"(u.x), "=r"(u.y), "=r"(u.z), "=r"(u.w)
+                         : "r"(sa_mir + sw64((uint32_t)lane, 16u * j)));
+            cs += fabsf(lo_bf(u.x)) + fabsf(hi_bf(u.x)) + fabsf(lo_bf(u.y)) + fabsf(hi_bf(u.y)) +
+                  fabsf(lo_bf(u.z)) + fabsf(hi_bf(u.z)) + fabsf(lo_bf(u.w)) + fabsf(hi_bf(u.w));
+          }
+          if (q + lane < E.Q && prow < E.P)
+            E.part[(int64_t)(q + lane) * E.part_ld + (E.Q + 127) / 128 + prow / 32] = cs;
+        }
         if (prof) { t1 = clock64(); pc[6] += t1 - t0; t0 = t1; }
       }
+      if (E.part != nullptr && p < E.P && qh < E.Q) E.part[(int64_t)p * E.part_ld + qh / 128] = rsum;
       if (++as == 2) { as = 0; aphase ^= 1; }
     }
     if (lane == 0) bulk_wait<0>();
