@@ -11,6 +11,7 @@
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <array>
 #include <cmath>
 #include <cstdio>
@@ -343,8 +344,12 @@ static ns_status build_plan(Plan& P, HostTables& H, DevCtx* dc, const float* coe
         ph.gemm_kind = mode == MODE_GRAM ? 0 : (mode == MODE_POLY ? 2 : 3);
         ph.dev_off = H.push(jobs.data(), jobs.size() * sizeof(GemmJob), 64);
         ph.njobs = (int)jobs.size();
+        // longest-K jobs first (LPT-like): long tiles do not end up in the last wave
+        std::vector<size_t> order(jobs.size());
+        for (size_t j = 0; j < jobs.size(); ++j) order[j] = j;
+        std::stable_sort(order.begin(), order.end(), [&](size_t x, size_t y) { return jobs[x].K > jobs[y].K; });
         std::vector<uint64_t> tl;
-        for (size_t j = 0; j < jobs.size(); ++j) umma_tile_list(jobs[j], (uint32_t)j, P.cg, tl);
+        for (size_t j : order) umma_tile_list(jobs[j], (uint32_t)j, P.cg, tl);
         ph.tiles_off = H.push(tl.data(), tl.size() * sizeof(uint64_t), 64);
         ph.total = (int64_t)tl.size();
         for (size_t j = 0; j < jobs.size(); ++j)
@@ -860,6 +865,7 @@ ns_status nsx_precondition(void* A, int64_t N, ns_precond precond, float* s, ns_
   J.A = A; J.s = s; J.N = (int)N; J.precond = (int)precond;
   void* dmem = nullptr;
   CU_TRY(cudaMalloc(&dmem, 256 + sizeof(J)));
+  CU_TRY(cudaMemset(dmem, 0, 256));  // grid-barrier words
   CU_TRY(cudaMemcpy(reinterpret_cast<uint8_t*>(dmem) + 256, &J, sizeof(J), cudaMemcpyHostToDevice));
   cudaError_t e = launch_precondition(reinterpret_cast<const PrecondJob*>(reinterpret_cast<uint8_t*>(dmem) + 256), 1,
                                       N, vec8 ? N * N / 8 : N * N, vec8, dtype == NS_BF16,

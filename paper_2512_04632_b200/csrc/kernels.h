@@ -23,8 +23,8 @@ cudaError_t launch_simt_gemm(const SimtJob* d_jobs, int njobs, int64_t total_til
                              bool is_bf16, uint32_t* d_flags, cudaStream_t stream);
 
 // Fused AOL / Frobenius preconditioner (simt.cu): row-abs-sum (or trace) + rsqrt, grid
-// barrier, then A <- diag(s) A diag(s).  `barrier` must point at a zeroed uint32 (the
-// wrapper zeroes it on `stream`).  vec8 = all N are multiples of 8 (16-byte vectors).
+// barrier, then A <- diag(s) A diag(s).  `barrier` points at two zero-initialised uint32
+// words (arrival count, generation) owned by the caller; the barrier resets itself.  vec8 = all N are multiples of 8 (16-byte vectors).
 cudaError_t launch_precondition(const PrecondJob* d_jobs, int njobs, int64_t total_rows,
                                 int64_t total_elems_or_vecs, bool vec8, bool is_bf16,
                                 unsigned* d_barrier, uint32_t* d_flags, cudaStream_t stream);

@@ -113,6 +113,14 @@ __device__ __forceinline__ void tma_load_2d_cg2(void* smem_dst, const void* tmap
       : "memory");
 }
 
+// ----------------------------------------------------------------------------- PDL
+// Programmatic dependent launch: wait until the preceding grid in the stream has completed
+// (and its writes are visible); allow the next grid to be scheduled early.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 // ----------------------------------------------------------------------------- clusters
 __device__ __forceinline__ uint32_t cluster_ctarank() {
   uint32_t r;

@@ -131,12 +131,23 @@ __device__ __forceinline__ float warp_sum(float v) {
   return v;
 }
 
-__device__ __forceinline__ void grid_barrier(unsigned* counter) {
+// Self-resetting grid barrier (all CTAs co-resident: cooperative launch).  bar[0] counts
+// arrivals, bar[1] is a generation number; the last arriver resets the count and bumps the
+// generation, so no host-side reset (memset) is needed between launches.
+__device__ __forceinline__ void grid_barrier(unsigned* bar) {
   __syncthreads();
   if (threadIdx.x == 0) {
+    volatile unsigned* gen = bar + 1;
+    const unsigned g0 = *gen;
     __threadfence();
-    atomicAdd(counter, 1u);
-    while (*((volatile unsigned*)counter) < gridDim.x) __nanosleep(32);
+    const unsigned old = atomicAdd(bar, 1u);
+    if (old == gridDim.x - 1) {
+      bar[0] = 0;
+      __threadfence();
+      atomicAdd(bar + 1, 1u);
+    } else {
+      while (*gen == g0) __nanosleep(32);
+    }
     __threadfence();
   }
   __syncthreads();
@@ -146,6 +157,8 @@ template <typename T, bool VEC8>
 __global__ void __launch_bounds__(256)
     precondition_kernel(const PrecondJob* __restrict__ jobs, int njobs, int64_t total_rows,
                         int64_t total_items, unsigned* barrier, uint32_t* __restrict__ flags) {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // A0 comes from the preceding Gram launch
   const int lane = threadIdx.x & 31;
   const int64_t gwarp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -254,13 +267,18 @@ static cudaError_t launch_precond_t(const PrecondJob* d_jobs, int njobs, int64_t
   const int64_t want = (total_rows * 32 + 255) / 256;  // one warp per row
   int64_t cap = (int64_t)sms * occ;
   int grid = (int)(want < cap ? (want < 1 ? 1 : want) : cap);
-  cudaError_t e = cudaMemsetAsync(d_barrier, 0, sizeof(unsigned), stream);
-  if (e != cudaSuccess) return e;
-  void* args[] = {(void*)&d_jobs, (void*)&njobs, (void*)&total_rows, (void*)&total_items,
-                  (void*)&d_barrier, (void*)&d_flags};
-  e = cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(256), args, 0, stream);
-  if (e != cudaSuccess) return e;
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(256);
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
+  return cudaLaunchKernelEx(&cfg, kern, d_jobs, njobs, total_rows, total_items, d_barrier, d_flags);
 }
 
 cudaError_t launch_precondition(const PrecondJob* d_jobs, int njobs, int64_t total_rows,

@@ -254,6 +254,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   if constexpr (CG == 2) cluster_sync(); else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // everything above overlaps the previous kernel's tail (PDL); data buffers are touched
+  // only after it has completed
+  pdl_trigger();
+  pdl_wait();
 
   if (warp == 0) {
     // ------------------------------------------------------------------ TMA producer
@@ -501,13 +505,15 @@ static cudaError_t launch_cg(const GemmJob* d_jobs, const uint64_t* d_tiles, int
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = Geo<CG>::kSmemBytes;
   cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = CG;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   static int dbg = -1;
   if (dbg < 0) {  // measurement knob (never set in production): TNS_DBG bits 1 skip epilogue,
     const char* e = getenv("TNS_DBG");  // 2 skip mirrored stores, 4 skip aux prefetch
