@@ -100,8 +100,9 @@ ns_status ns_read_flags(void* stream, uint32_t* flags);
 uint64_t ns_launch_count(void);
 
 /* Execution-path override for testing: 0 = auto (tcgen05, 256x256 tiles on CTA pairs,
- * for aligned bf16), 1 = force the SIMT (CUDA-core) kernels, 2 = tcgen05 with single-CTA
- * 128x256 tiles.  Returns the previous value. */
+ * for aligned bf16; one PDL-chained launch per step), 1 = force the SIMT (CUDA-core)
+ * kernels, 2 = tcgen05 with single-CTA 128x256 tiles, 3 = all 3T+1 steps in ONE fused
+ * launch with device-side step barriers, 4 = per-step launches.  Returns the previous value. */
 int ns_set_path(int path);
 
 /* Per-kernel event timing (measurement support for bench.py; off by default).

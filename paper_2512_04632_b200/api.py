@@ -129,11 +129,12 @@ def launch_count() -> int:
 
 
 def set_path(path: int) -> int:
-    """0 = auto (tcgen05 CTA-pair 256x256 tiles), 1 = CUDA-core kernels, 2 = tcgen05 1-CTA tiles."""
+    """0 auto, 1 CUDA-core kernels, 2 tcgen05 1-CTA tiles, 3 force fused single launch,
+    4 never fuse (one launch per step)."""
     return int(lib.ns_set_path(int(path)))
 
 
-KERNEL_KINDS = ("gram", "precondition", "poly", "update", "simt", "copy")
+KERNEL_KINDS = ("gram", "precondition", "poly", "update", "simt", "copy", "fused")
 
 
 def profile_enable(on: bool = True) -> None:
@@ -143,9 +144,9 @@ def profile_enable(on: bool = True) -> None:
 
 def profile_read() -> dict:
     """Synchronise and return {kind: (total_ms, launches)}; clears the records."""
-    ms = (ctypes.c_double * 6)()
-    cnt = (ctypes.c_uint64 * 6)()
-    check(lib.ns_profile_read(ms, cnt, 6), "ns_profile_read")
+    ms = (ctypes.c_double * 7)()
+    cnt = (ctypes.c_uint64 * 7)()
+    check(lib.ns_profile_read(ms, cnt, 7), "ns_profile_read")
     return {k: (float(ms[i]), int(cnt[i])) for i, k in enumerate(KERNEL_KINDS)}
 
 

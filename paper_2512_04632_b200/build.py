@@ -13,7 +13,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libturbons.so")
 SOURCES = ["api.cu", "umma_gemm.cu", "simt.cu"]
-HEADERS = ["ptx.cuh", "jobs.h", "kernels.h"]
+HEADERS = ["ptx.cuh", "jobs.h", "kernels.h", "precond_rows.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -143,7 +143,7 @@ struct Mat {
   int tm_x, tm_out, tm_w, tm_a, tm_b;
 };
 
-enum PhaseKind { PH_GEMM = 0, PH_SIMT = 1, PH_PRECOND = 2, PH_COPY = 3 };
+enum PhaseKind { PH_GEMM = 0, PH_SIMT = 1, PH_PRECOND = 2, PH_COPY = 3, PH_FUSED = 4 };
 struct Phase {
   PhaseKind kind;
   size_t dev_off;  // offset of the job array in the device table
@@ -152,7 +152,11 @@ struct Phase {
   int64_t total_rows;
   bool vec8;
   int gemm_kind;  // profiling kind: 0 GRAM, 2 POLY, 3 XB
-  size_t tiles_off = 0;  // offset of the packed tile list (PH_GEMM)
+  size_t tiles_off = 0;   // offset of the packed tile list (PH_GEMM / PH_FUSED)
+  size_t phdesc_off = 0;  // offset of the PhaseDesc array (PH_GEMM / PH_FUSED)
+  size_t jobs_off = 0;    // offset of the GemmJob array (PH_FUSED)
+  int nphases = 1;        // PH_FUSED: number of steps
+  int64_t max_tiles = 0;  // largest GEMM step
   // copies (PH_COPY)
   std::vector<std::pair<std::pair<void*, const void*>, size_t>> copies;
 };
@@ -161,6 +165,7 @@ struct Plan {
   int device = 0;
   ns_dtype dtype = NS_BF16;
   bool simt = false;
+  bool fused = false;  // all 3T+1 steps in one launch (small problems)
   int cg = 2;  // tcgen05 CTA group (2: 256x256 tiles on CTA pairs)
   int iters = 0;
   ns_precond precond = NS_PRECOND_AOL;
@@ -199,7 +204,7 @@ static size_t s_floats(int64_t N) { return (size_t)((N + 255) / 256 * 256 + 32);
 static int part_ld_for(int64_t N) { return (int)((N + 127) / 128 + (N + 31) / 32); }
 
 static size_t workspace_bytes_for(const std::vector<Mat>& mats, ns_dtype dt) {
-  size_t off = 256;  // [0,256): barrier counter
+  size_t off = 1024;  // [0,1024): grid-barrier words and fused-mode phase counters
   const size_t es = elem_size(dt);
   for (const Mat& mt : mats) {
     off = align_up(off, 256) + (size_t)mt.M * mt.N * es;
@@ -227,7 +232,7 @@ static ns_status build_plan(Plan& P, HostTables& H, DevCtx* dc, const float* coe
   const size_t es = elem_size(P.dtype);
   const bool bf16 = P.dtype == NS_BF16;
   // -- workspace layout
-  size_t off = 256;
+  size_t off = 1024;  // [0,16): preconditioner grid barrier; [64, 1024): phase counters
   for (Mat& mt : P.mats) {
     off = align_up(off, 256); mt.w_off = off; off += (size_t)mt.M * mt.N * es;
     off = align_up(off, 256); mt.a_off = off; off += (size_t)mt.N * mt.N * es;
@@ -276,6 +281,19 @@ static ns_status build_plan(Plan& P, HostTables& H, DevCtx* dc, const float* coe
   // table size by building jobs with placeholder bases, then fix them up.
   struct Fix { size_t job_off; int ta, tb, tout, taux; };
   std::vector<Fix> fixes;
+  struct PFix { size_t pd_off, pj_off; };  // PhaseDesc::pjobs pointers (fused mode)
+  std::vector<PFix> pfixes;
+  struct Step {  // one tcgen05-path step before it is laid out as launches
+    int kind = PHK_GEMM;
+    int gemm_kind = 0;
+    std::vector<GemmJob> jobs;
+    std::vector<std::array<int, 4>> tmi;
+    size_t job_base = 0;
+    std::vector<PrecondJob> pj;
+    int64_t rows = 0, items = 0;
+    bool vec8 = false;
+  };
+  std::vector<Step> steps;
 
   // -- phases
   if (P.mats.size() > 0) {
@@ -340,21 +358,12 @@ static ns_status build_plan(Plan& P, HostTables& H, DevCtx* dc, const float* coe
           jobs.push_back(J);
           tmi.push_back({ta, tb, tout, taux});
         }
-        Phase ph{PH_GEMM};
-        ph.gemm_kind = mode == MODE_GRAM ? 0 : (mode == MODE_POLY ? 2 : 3);
-        ph.dev_off = H.push(jobs.data(), jobs.size() * sizeof(GemmJob), 64);
-        ph.njobs = (int)jobs.size();
-        // longest-K jobs first (LPT-like): long tiles do not end up in the last wave
-        std::vector<size_t> order(jobs.size());
-        for (size_t j = 0; j < jobs.size(); ++j) order[j] = j;
-        std::stable_sort(order.begin(), order.end(), [&](size_t x, size_t y) { return jobs[x].K > jobs[y].K; });
-        std::vector<uint64_t> tl;
-        for (size_t j : order) umma_tile_list(jobs[j], (uint32_t)j, P.cg, tl);
-        ph.tiles_off = H.push(tl.data(), tl.size() * sizeof(uint64_t), 64);
-        ph.total = (int64_t)tl.size();
-        for (size_t j = 0; j < jobs.size(); ++j)
-          fixes.push_back({ph.dev_off + j * sizeof(GemmJob), tmi[j][0], tmi[j][1], tmi[j][2], tmi[j][3]});
-        P.phases.push_back(ph);
+        Step stp;
+        stp.kind = PHK_GEMM;
+        stp.gemm_kind = mode == MODE_GRAM ? 0 : (mode == MODE_POLY ? 2 : 3);
+        stp.jobs = std::move(jobs);
+        stp.tmi = std::move(tmi);
+        steps.push_back(std::move(stp));
       } else {
         std::vector<SimtJob> jobs;
         int64_t total = 0;
@@ -419,14 +428,131 @@ static ns_status build_plan(Plan& P, HostTables& H, DevCtx* dc, const float* coe
           items += vec8 ? (mt.N * mt.N) / 8 : mt.N * mt.N;
           pj.push_back(J);
         }
-        Phase ph{PH_PRECOND};
-        ph.dev_off = H.push(pj.data(), pj.size() * sizeof(PrecondJob), 64);
-        ph.njobs = (int)pj.size();
-        ph.total = items;
-        ph.total_rows = rows;
-        ph.vec8 = vec8;
-        P.phases.push_back(ph);
+        if (P.simt) {
+          Phase ph{PH_PRECOND};
+          ph.dev_off = H.push(pj.data(), pj.size() * sizeof(PrecondJob), 64);
+          ph.njobs = (int)pj.size();
+          ph.total = items;
+          ph.total_rows = rows;
+          ph.vec8 = vec8;
+          P.phases.push_back(ph);
+        } else {
+          Step stp;
+          stp.kind = PHK_PRE_S;
+          stp.pj = std::move(pj);
+          stp.rows = rows;
+          stp.items = items;
+          stp.vec8 = vec8;
+          steps.push_back(std::move(stp));
+        }
       }
+    }
+  }
+
+  // -- tcgen05 steps: one launch each (PDL-chained), or all in one fused launch
+  if (!P.simt && !steps.empty()) {
+    const int64_t workers = dc->sms / P.cg;
+    int64_t max_tiles = 0;
+    std::vector<std::vector<uint64_t>> tls(steps.size());
+    size_t job_base = 0;
+    for (size_t si = 0; si < steps.size(); ++si) {
+      Step& st = steps[si];
+      if (st.kind != PHK_GEMM) continue;
+      // longest-K jobs first (LPT-like): long tiles do not end up in the last wave
+      std::vector<size_t> order(st.jobs.size());
+      for (size_t j = 0; j < st.jobs.size(); ++j) order[j] = j;
+      std::stable_sort(order.begin(), order.end(),
+                       [&](size_t x, size_t y) { return st.jobs[x].K > st.jobs[y].K; });
+      for (size_t j : order) umma_tile_list(st.jobs[j], (uint32_t)(job_base + j), P.cg, tls[si]);
+      max_tiles = std::max(max_tiles, (int64_t)tls[si].size());
+      st.job_base = job_base;
+      job_base += st.jobs.size();
+    }
+    // The fused single launch is opt-in (path 3): measured slower than PDL-chained per-step
+    // launches even on the latency-bound CIFAR set (178 vs 166 us), because its grid-wide
+    // step barriers serialise what PDL overlaps (profiles/README.md).
+    P.fused = (g_path == 3);
+    (void)workers;
+    if (!P.fused) {
+      for (size_t si = 0; si < steps.size(); ++si) {
+        Step& st = steps[si];
+        if (st.kind == PHK_GEMM) {
+          // per-step launch: job indices are local to the step
+          std::vector<uint64_t> tl;
+          std::vector<size_t> order(st.jobs.size());
+          for (size_t j = 0; j < st.jobs.size(); ++j) order[j] = j;
+          std::stable_sort(order.begin(), order.end(),
+                           [&](size_t x, size_t y) { return st.jobs[x].K > st.jobs[y].K; });
+          for (size_t j : order) umma_tile_list(st.jobs[j], (uint32_t)j, P.cg, tl);
+          Phase ph{PH_GEMM};
+          ph.gemm_kind = st.gemm_kind;
+          ph.dev_off = H.push(st.jobs.data(), st.jobs.size() * sizeof(GemmJob), 64);
+          ph.njobs = (int)st.jobs.size();
+          ph.tiles_off = H.push(tl.data(), tl.size() * sizeof(uint64_t), 64);
+          ph.total = (int64_t)tl.size();
+          ph.max_tiles = ph.total;
+          PhaseDesc pd;
+          std::memset(&pd, 0, sizeof(pd));
+          pd.kind = PHK_GEMM; pd.tile_begin = 0; pd.tile_end = ph.total;
+          ph.phdesc_off = H.push(&pd, sizeof(pd), 64);
+          for (size_t j = 0; j < st.jobs.size(); ++j)
+            fixes.push_back({ph.dev_off + j * sizeof(GemmJob), st.tmi[j][0], st.tmi[j][1], st.tmi[j][2], st.tmi[j][3]});
+          P.phases.push_back(ph);
+        } else {
+          Phase ph{PH_PRECOND};
+          ph.dev_off = H.push(st.pj.data(), st.pj.size() * sizeof(PrecondJob), 64);
+          ph.njobs = (int)st.pj.size();
+          ph.total = st.items;
+          ph.total_rows = st.rows;
+          ph.vec8 = st.vec8;
+          P.phases.push_back(ph);
+        }
+      }
+    } else {
+      // fused: all jobs in one array (global job indices), one tile list, one PhaseDesc
+      // per step; the preconditioner becomes two steps (row sums -> s, rescale A)
+      std::vector<GemmJob> alljobs;
+      std::vector<std::array<int, 4>> alltmi;
+      std::vector<uint64_t> alltiles;
+      std::vector<PhaseDesc> pds;
+      size_t pj_off = 0;
+      int npj = 0;
+      int64_t prow = 0;
+      for (size_t si = 0; si < steps.size(); ++si) {
+        Step& st = steps[si];
+        PhaseDesc pd;
+        std::memset(&pd, 0, sizeof(pd));
+        if (st.kind == PHK_GEMM) {
+          alljobs.insert(alljobs.end(), st.jobs.begin(), st.jobs.end());
+          alltmi.insert(alltmi.end(), st.tmi.begin(), st.tmi.end());
+          pd.kind = PHK_GEMM;
+          pd.tile_begin = (int64_t)alltiles.size();
+          alltiles.insert(alltiles.end(), tls[si].begin(), tls[si].end());
+          pd.tile_end = (int64_t)alltiles.size();
+          pds.push_back(pd);
+        } else {
+          pj_off = H.push(st.pj.data(), st.pj.size() * sizeof(PrecondJob), 64);
+          npj = (int)st.pj.size();
+          prow = st.rows;
+          pd.npjobs = npj; pd.prow_total = prow;
+          pd.kind = PHK_PRE_S;
+          pds.push_back(pd);
+          pd.kind = PHK_PRE_SCALE;
+          pds.push_back(pd);
+        }
+      }
+      Phase ph{PH_FUSED};
+      ph.jobs_off = H.push(alljobs.data(), alljobs.size() * sizeof(GemmJob), 64);
+      for (size_t j = 0; j < alljobs.size(); ++j)
+        fixes.push_back({ph.jobs_off + j * sizeof(GemmJob), alltmi[j][0], alltmi[j][1], alltmi[j][2], alltmi[j][3]});
+      ph.tiles_off = H.push(alltiles.data(), alltiles.size() * sizeof(uint64_t), 64);
+      ph.phdesc_off = H.push(pds.data(), pds.size() * sizeof(PhaseDesc), 64);
+      for (size_t i = 0; i < pds.size(); ++i)
+        if (pds[i].kind != PHK_GEMM) pfixes.push_back({ph.phdesc_off + i * sizeof(PhaseDesc), pj_off});
+      ph.nphases = (int)pds.size();
+      ph.max_tiles = max_tiles;
+      if (ph.nphases + 1 > (1024 - 64) / 4) return fail(NS_ERR_NOT_SUPPORTED, "too many steps for the fused mode");
+      P.phases.push_back(ph);
     }
   }
 
@@ -445,6 +571,10 @@ static ns_status build_plan(Plan& P, HostTables& H, DevCtx* dc, const float* coe
       J->tmB = dbase + tm_off + (size_t)f.tb * sizeof(CUtensorMap);
       J->tmOut = dbase + tm_off + (size_t)(f.tout + 1) * sizeof(CUtensorMap);
       J->tmAux = f.taux >= 0 ? dbase + tm_off + (size_t)(f.taux + 1) * sizeof(CUtensorMap) : nullptr;
+    }
+    for (const PFix& f : pfixes) {
+      PhaseDesc* pd = reinterpret_cast<PhaseDesc*>(H.bytes.data() + f.pd_off);
+      pd->pjobs = reinterpret_cast<const PrecondJob*>(dbase + f.pj_off);
     }
     CU_TRY(cudaMemcpy(P.dtab, H.bytes.data(), H.bytes.size(), cudaMemcpyHostToDevice));
   }
@@ -465,8 +595,19 @@ static ns_status enqueue_plan(Plan& P, DevCtx* dc, cudaStream_t stream) {
       case PH_GEMM: {
         ProfScope ps(ph.gemm_kind, stream);
         CU_TRY(launch_umma_gemm(reinterpret_cast<const GemmJob*>(dbase + ph.dev_off),
-                                reinterpret_cast<const uint64_t*>(dbase + ph.tiles_off), ph.total,
-                                P.cg, dc->sms, dc->flags, stream));
+                                reinterpret_cast<const uint64_t*>(dbase + ph.tiles_off),
+                                reinterpret_cast<const PhaseDesc*>(dbase + ph.phdesc_off), 1, nullptr,
+                                ph.max_tiles, P.cg, dc->sms, dc->flags, stream));
+        ++g_launches;
+        break;
+      }
+      case PH_FUSED: {
+        ProfScope ps(6, stream);
+        CU_TRY(launch_umma_gemm(reinterpret_cast<const GemmJob*>(dbase + ph.jobs_off),
+                                reinterpret_cast<const uint64_t*>(dbase + ph.tiles_off),
+                                reinterpret_cast<const PhaseDesc*>(dbase + ph.phdesc_off), ph.nphases,
+                                reinterpret_cast<unsigned*>(reinterpret_cast<uint8_t*>(P.ws) + 64),
+                                ph.max_tiles, P.cg, dc->sms, dc->flags, stream));
         ++g_launches;
         break;
       }
@@ -529,6 +670,7 @@ static ns_status run(const std::vector<Mat>& mats_in, int iters, const float* co
   const int cg = (g_path == 2) ? 1 : 2;
   key.push_back((uint64_t)dev); key.push_back((uint64_t)dtype); key.push_back(simt ? 1 : 0);
   key.push_back((uint64_t)cg);
+  key.push_back((uint64_t)g_path);
   key.push_back((uint64_t)iters); key.push_back((uint64_t)precond);
   for (int i = 0; i < 3 * iters; ++i) { uint32_t u; std::memcpy(&u, &coeffs[i], 4); key.push_back(u); }
   for (const Mat& mt : mats_in) {
@@ -604,7 +746,7 @@ void ns_profile_enable(int on) {
 
 ns_status ns_profile_read(double* ms, uint64_t* counts, int nkinds) {
   std::lock_guard<std::mutex> lk(g_mu);
-  if (!ms || !counts || nkinds < 1 || nkinds > 6) return fail(NS_ERR_INVALID_VALUE, "bad arguments");
+  if (!ms || !counts || nkinds < 1 || nkinds > 7) return fail(NS_ERR_INVALID_VALUE, "bad arguments");
   for (int k = 0; k < nkinds; ++k) { ms[k] = 0.0; counts[k] = 0; }
   if (!g_prof_recs.empty()) CU_TRY(cudaEventSynchronize(g_prof_recs.back().b));
   for (const ProfRec& r : g_prof_recs) {
@@ -742,8 +884,20 @@ static ns_status one_gemm(GemmJob J, TDesc ta, TDesc tb, TDesc tout, TDesc taux,
     std::memcpy(h.data() + jo, &J, sizeof(J));
     std::memcpy(h.data() + to, tl.data(), tl.size() * sizeof(uint64_t));
     CU_TRY(cudaMemcpy(dmem, h.data(), bytes, cudaMemcpyHostToDevice));
+    // single GEMM step: its PhaseDesc sits after the tile list
+    PhaseDesc pd;
+    std::memset(&pd, 0, sizeof(pd));
+    pd.kind = PHK_GEMM; pd.tile_begin = 0; pd.tile_end = (int64_t)tl.size();
+    const size_t po = align_up(bytes, 64);
+    void* dpd = nullptr;
+    CU_TRY(cudaMalloc(&dpd, sizeof(pd)));
+    CU_TRY(cudaMemcpy(dpd, &pd, sizeof(pd), cudaMemcpyHostToDevice));
+    (void)po;
     cudaError_t e = launch_umma_gemm(reinterpret_cast<const GemmJob*>(d + jo), reinterpret_cast<const uint64_t*>(d + to),
-                                     (int64_t)tl.size(), cg, dc->sms, dc->flags, stream);
+                                     reinterpret_cast<const PhaseDesc*>(dpd), 1, nullptr, (int64_t)tl.size(), cg,
+                                     dc->sms, dc->flags, stream);
+    cudaStreamSynchronize(stream);
+    cudaFree(dpd);
     ++g_launches;
     cudaError_t e2 = cudaStreamSynchronize(stream);
     cudaFree(dmem);

@@ -86,4 +86,15 @@ struct PrecondJob {
   int64_t vec_start;  // prefix over jobs of ceil(N*N / 8) (rescale: 16-byte vectors)
 };
 
+// One step of a launch.  A per-step launch carries one GEMM phase; the fused single-launch
+// mode (small problems) carries all 3T+1 steps, separated by device-side phase barriers.
+enum PhaseKindDev : int32_t { PHK_GEMM = 0, PHK_PRE_S = 1, PHK_PRE_SCALE = 2 };
+struct PhaseDesc {
+  int32_t kind;
+  int32_t npjobs;
+  int64_t tile_begin, tile_end;  // GEMM: range of the launch's tile list
+  const PrecondJob* pjobs;       // PRE_*: matrices and their row prefix
+  int64_t prow_total;
+};
+
 }  // namespace tns

@@ -12,19 +12,9 @@
 
 #include "jobs.h"
 #include "kernels.h"
+#include "precond_rows.cuh"
 
 namespace tns {
-
-template <typename T> __device__ __forceinline__ float ld_val(const T* p);
-template <> __device__ __forceinline__ float ld_val<float>(const float* p) { return *p; }
-template <> __device__ __forceinline__ float ld_val<uint16_t>(const uint16_t* p) {
-  return __uint_as_float(((uint32_t)*p) << 16);
-}
-template <typename T> __device__ __forceinline__ T st_conv(float f);
-template <> __device__ __forceinline__ float st_conv<float>(float f) { return f; }
-template <> __device__ __forceinline__ uint16_t st_conv<uint16_t>(float f) {
-  return __bfloat16_as_ushort(__float2bfloat16_rn(f));
-}
 
 // ------------------------------------------------------------------------------ SIMT GEMM
 template <typename T>
@@ -114,23 +104,6 @@ cudaError_t launch_simt_gemm(const SimtJob* d_jobs, int njobs, int64_t total_til
 }
 
 // ------------------------------------------------------------------------------ preconditioner
-__device__ __forceinline__ int find_pjob(const PrecondJob* __restrict__ jobs, int njobs,
-                                         int64_t v, bool by_row) {
-  int lo = 0, hi = njobs - 1;
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    const int64_t st = by_row ? jobs[mid].row_start : jobs[mid].vec_start;
-    if (st <= v) lo = mid; else hi = mid - 1;
-  }
-  return lo;
-}
-
-__device__ __forceinline__ float warp_sum(float v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
-}
-
 // Self-resetting grid barrier (all CTAs co-resident: cooperative launch).  bar[0] counts
 // arrivals, bar[1] is a generation number; the last arriver resets the count and bumps the
 // generation, so no host-side reset (memset) is needed between launches.
@@ -159,97 +132,21 @@ __global__ void __launch_bounds__(256)
                         int64_t total_items, unsigned* barrier, uint32_t* __restrict__ flags) {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   asm volatile("griddepcontrol.wait;" ::: "memory");  // A0 comes from the preceding Gram launch
+  (void)total_items;
   const int lane = threadIdx.x & 31;
   const int64_t gwarp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   uint32_t fl = 0;
-
-  (void)total_items;
   // ---- phase 1: scaling vector s (Eq. 8 / Eq. 10)
   for (int64_t row = gwarp; row < total_rows; row += nwarps) {
-    const PrecondJob& J = jobs[find_pjob(jobs, njobs, row, true)];
-    const int i = (int)(row - J.row_start);
-    const T* __restrict__ A = reinterpret_cast<const T*>(J.A);
-    const int N = J.N;
-    if (J.precond == 2 && J.part != nullptr) {
-      // AOL from the Gram epilogue's partials: direct 128-column slots of blocks <= bi,
-      // mirrored 32-row slots of blocks > bi (each |A0_ij| counted exactly once)
-      const int bi = i / 256;
-      const int n1 = (N + 127) / 128, n2 = (N + 31) / 32;
-      const float* pr = J.part + (int64_t)i * J.part_ld;
-      const int d_end = min(2 * (bi + 1), n1), m_beg = min(8 * (bi + 1), n2);
-      float acc = 0.f;
-      for (int k = lane; k < d_end; k += 32) acc += pr[k];
-      for (int k = m_beg + lane; k < n2; k += 32) acc += pr[n1 + k];
-      const float r = warp_sum(acc);
-      if (lane == 0) {
-        J.s[i] = r > 0.f ? rsqrtf(r) : 0.f;
-        if (!(r > 0.f)) fl |= 1u;
-        if (!isfinite(r)) fl |= 2u;
-      }
-    } else if (J.precond == 2) {  // AOL: s_i = (sum_j |A0_ij|)^(-1/2)
-      float acc = 0.f;
-      const T* Ai = A + (int64_t)i * N;
-      if (VEC8 && sizeof(T) == 2) {
-        for (int j = lane * 8; j < N; j += 256) {
-          const uint4 u = __ldg(reinterpret_cast<const uint4*>(Ai + j));
-          const uint32_t w[4] = {u.x, u.y, u.z, u.w};
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            acc += fabsf(__uint_as_float(w[e] << 16));
-            acc += fabsf(__uint_as_float(w[e] & 0xFFFF0000u));
-          }
-        }
-      } else {
-        for (int j = lane; j < N; j += 32) acc += fabsf(ld_val<T>(Ai + j));
-      }
-      const float r = warp_sum(acc);
-      if (lane == 0) {
-        J.s[i] = r > 0.f ? rsqrtf(r) : 0.f;
-        if (!(r > 0.f)) fl |= 1u;
-        if (!isfinite(r)) fl |= 2u;
-      }
-    } else if (i == 0) {  // Frobenius: s = 1/sqrt(trace A0) = 1/||X||_F, one warp per matrix
-      float acc = 0.f;
-      for (int j = lane; j < N; j += 32) acc += ld_val<T>(A + (int64_t)j * N + j);
-      const float tr = warp_sum(acc);
-      const float sv = tr > 0.f ? rsqrtf(tr) : 0.f;
-      for (int j = lane; j < N; j += 32) J.s[j] = sv;
-      if (lane == 0 && !(tr > 0.f)) fl |= 1u;
-      if (lane == 0 && !isfinite(tr)) fl |= 2u;
-    }
+    const PrecondJob& J = jobs[find_pjob(jobs, njobs, row)];
+    precond_row_s<T, VEC8>(J, (int)(row - J.row_start), lane, fl);
   }
-
   grid_barrier(barrier);
-
-  // ---- phase 2: A1 = diag(s) A0 diag(s)  (Alg. 2 l.4), one warp per row: s_i once,
-  // 16-byte vectors of A and float4 pairs of s along the row (coalesced, no divisions)
+  // ---- phase 2: A1 = diag(s) A0 diag(s)  (Alg. 2 l.4)
   for (int64_t row = gwarp; row < total_rows; row += nwarps) {
-    const PrecondJob& J = jobs[find_pjob(jobs, njobs, row, true)];
-    const int i = (int)(row - J.row_start);
-    const int N = J.N;
-    const float si = J.s[i];
-    T* Ai = reinterpret_cast<T*>(J.A) + (int64_t)i * N;
-    if (VEC8 && sizeof(T) == 2) {
-      for (int j = lane * 8; j < N; j += 256) {
-        uint4* pv = reinterpret_cast<uint4*>(Ai + j);
-        uint4 u = *pv;
-        const float4 s0 = *reinterpret_cast<const float4*>(J.s + j);
-        const float4 s1 = *reinterpret_cast<const float4*>(J.s + j + 4);
-        const float sj[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
-        uint32_t w[4] = {u.x, u.y, u.z, u.w};
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const float lo = (si * __uint_as_float(w[e] << 16)) * sj[2 * e];
-          const float hi = (si * __uint_as_float(w[e] & 0xFFFF0000u)) * sj[2 * e + 1];
-          w[e] = (uint32_t)st_conv<uint16_t>(lo) | ((uint32_t)st_conv<uint16_t>(hi) << 16);
-        }
-        u.x = w[0]; u.y = w[1]; u.z = w[2]; u.w = w[3];
-        *pv = u;
-      }
-    } else {
-      for (int j = lane; j < N; j += 32) Ai[j] = st_conv<T>((si * ld_val<T>(Ai + j)) * J.s[j]);
-    }
+    const PrecondJob& J = jobs[find_pjob(jobs, njobs, row)];
+    precond_row_scale<T, VEC8>(J, (int)(row - J.row_start), lane);
   }
   if (fl) atomicOr(flags, fl);
 }

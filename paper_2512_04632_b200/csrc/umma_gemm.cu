@@ -37,6 +37,7 @@
 
 #include "jobs.h"
 #include "kernels.h"
+#include "precond_rows.cuh"
 #include "ptx.cuh"
 
 namespace tns {
@@ -64,6 +65,23 @@ struct Geo {
   static constexpr int kEpiBytes = kNumEpiWarps * 3 * 2048;      // aux/out/mirror per warp
   static constexpr size_t kSmemBytes = (size_t)kEpiOff + kEpiBytes + 1024 + 512;
 };
+
+// Fused mode: spin until `target` arrivals were counted for a phase, then order later
+// async-proxy (TMA) reads after it.
+__device__ __forceinline__ void wait_phase(const unsigned* cnt, unsigned target) {
+  while (true) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(cnt) : "memory");
+    if (v >= target) break;
+    __nanosleep(64);
+  }
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+__device__ __forceinline__ void arrive_phase(unsigned* cnt) {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+  __threadfence();
+  atomicAdd(cnt, 1u);
+}
 
 // Measurement counters (TNS_DBG bit 8): per-epilogue-warp clock64 deltas summed over tiles.
 __device__ unsigned long long g_epi_prof[8];
@@ -216,7 +234,8 @@ __device__ __forceinline__ void epi_math(int var, const Epi& E, int p, int q, co
 template <int CG>
 __global__ void __launch_bounds__(kThreads, 1)
     umma_gemm_kernel(const GemmJob* __restrict__ jobs, const uint64_t* __restrict__ tiles,
-                     int64_t total_tiles, uint32_t* __restrict__ flags, int dbg) {
+                     const PhaseDesc* __restrict__ phases, int nphases, unsigned* sync,
+                     uint32_t* __restrict__ flags, int dbg) {
   using G = Geo<CG>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
@@ -264,7 +283,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       uint32_t stage = 0, phase = 0;
       int last_job = -1;
-      for (int64_t t = cid; t < total_tiles; t += ncl) {
+      const unsigned arrivals = kNumEpiWarps * gridDim.x;
+      for (int ph = 0; ph < nphases; ++ph) {
+      const PhaseDesc PD = phases[ph];
+      if (PD.kind != PHK_GEMM) continue;
+      if (ph > 0) wait_phase(sync + ph - 1, arrivals);  // fused mode: previous step complete
+      for (int64_t t = PD.tile_begin + cid; t < PD.tile_end; t += ncl) {
         const TileInfo ti = decode_tile(tiles, t);
         const GemmJob* J = jobs + ti.job;
         const void* tmA = J->tmA;
@@ -299,6 +323,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (++stage == G::kStages) { stage = 0; phase ^= 1; }
         }
       }
+      }
       // tail: wait until the MMA released every stage, so no commit-arrive is still in
       // flight towards this CTA's barriers when it exits
       for (int i = 0; i < G::kStages; ++i) {
@@ -310,7 +335,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ------------------------------------------------------------------ MMA issuer (leader)
     if (lane == 0 && rank == 0) {
       uint32_t stage = 0, phase = 0, as = 0, aphase = 0;
-      for (int64_t t = cid; t < total_tiles; t += ncl) {
+      for (int ph = 0; ph < nphases; ++ph) {
+      const PhaseDesc PD = phases[ph];
+      if (PD.kind != PHK_GEMM) continue;
+      for (int64_t t = PD.tile_begin + cid; t < PD.tile_end; t += ncl) {
         const TileInfo ti = decode_tile(tiles, t);
         const GemmJob* J = jobs + ti.job;
         const uint32_t a_mn = (uint32_t)J->a_mn, b_mn = (uint32_t)J->b_mn;
@@ -339,6 +367,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         umma_commit<CG>(&tfull_bar[as]);
         if (++as == 2) { as = 0; aphase ^= 1; }
       }
+      }
     }
   } else if (warp >= 4) {
     // ------------------------------------------------------------------ epilogue
@@ -353,7 +382,30 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t as = 0, aphase = 0, xphase = 0;
     bool bad = false;
     long long pc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    for (int64_t t = cid; t < total_tiles; t += ncl) {
+    uint32_t pfl = 0;
+    const unsigned arrivals = kNumEpiWarps * gridDim.x;
+    for (int ph = 0; ph < nphases; ++ph) {
+    const PhaseDesc PD = phases[ph];
+    if (PD.kind != PHK_GEMM) {
+      // fused mode, preconditioner step: one warp per matrix row across the whole grid
+      if (lane == 0) wait_phase(sync + ph - 1, arrivals);
+      __syncwarp();
+      const int64_t gw = (int64_t)blockIdx.x * kNumEpiWarps + ew, nw = (int64_t)gridDim.x * kNumEpiWarps;
+      for (int64_t row = gw; row < PD.prow_total; row += nw) {
+        const PrecondJob& PJ = PD.pjobs[find_pjob(PD.pjobs, PD.npjobs, row)];
+        const int i = (int)(row - PJ.row_start);
+        if (PD.kind == PHK_PRE_S) precond_row_s<uint16_t, true>(PJ, i, lane, pfl);
+        else precond_row_scale<uint16_t, true>(PJ, i, lane);
+      }
+      __syncwarp();
+      if (lane == 0) arrive_phase(sync + ph);
+      continue;
+    }
+    if (ph > 0) {  // fused mode: the aux prefetch below reads the previous step's output
+      if (lane == 0) wait_phase(sync + ph - 1, arrivals);
+      __syncwarp();
+    }
+    for (int64_t t = PD.tile_begin + cid; t < PD.tile_end; t += ncl) {
       const TileInfo ti = decode_tile(tiles, t);
       const Epi E = load_epi(jobs + ti.job);
       const int var = epi_variant(E);
@@ -467,6 +519,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (E.part != nullptr && p < E.P && qh < E.Q) E.part[(int64_t)p * E.part_ld + qh / 128] = rsum;
       if (++as == 2) { as = 0; aphase ^= 1; }
     }
+    if (nphases > 1) {  // fused mode: this warp's part of the step is written and visible
+      if (lane == 0) bulk_wait<0>();
+      __syncwarp();
+      if (lane == 0) arrive_phase(sync + ph);
+    }
+    }
+    if (pfl && lane == 0) atomicOr(flags, pfl);
     if (lane == 0) bulk_wait<0>();
     if ((dbg & 8) && lane == 0)
       for (int i = 0; i < 8; ++i) atomicAdd(&g_epi_prof[i], (unsigned long long)pc[i]);
@@ -479,11 +538,19 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_after();
     tmem_dealloc<CG>(tmem_base, kTmemCols);
   }
+  if (nphases > 1 && threadIdx.x == 0) {  // last CTA out resets the phase counters
+    __threadfence();
+    if (atomicAdd(sync + nphases, 1u) == gridDim.x - 1) {
+      for (int k = 0; k <= nphases; ++k) sync[k] = 0;
+      __threadfence();
+    }
+  }
 }
 
 template <int CG>
-static cudaError_t launch_cg(const GemmJob* d_jobs, const uint64_t* d_tiles, int64_t total_tiles, int num_sms,
-                             uint32_t* d_flags, cudaStream_t stream) {
+static cudaError_t launch_cg(const GemmJob* d_jobs, const uint64_t* d_tiles, const PhaseDesc* d_phases,
+                             int nphases, unsigned* d_sync, int64_t max_tiles, int num_sms, uint32_t* d_flags,
+                             cudaStream_t stream) {
   static bool attr_set[64] = {};
   int dev = 0;
   cudaGetDevice(&dev);
@@ -498,8 +565,10 @@ static cudaError_t launch_cg(const GemmJob* d_jobs, const uint64_t* d_tiles, int
     }
     attr_set[dev & 63] = true;
   }
-  const int64_t workers = num_sms / CG;  // persistent: one CTA (pair) per SM (pair)
-  const int64_t nclusters = total_tiles < workers ? total_tiles : workers;
+  // persistent: one CTA (pair) per SM (pair); the fused mode uses every SM (its phase
+  // barriers need all CTAs co-resident, which one CTA per SM guarantees)
+  const int64_t workers = num_sms / CG;
+  const int64_t nclusters = (nphases > 1 || max_tiles > workers) ? workers : max_tiles;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(nclusters * CG));
   cfg.blockDim = dim3(kThreads);
@@ -516,17 +585,18 @@ static cudaError_t launch_cg(const GemmJob* d_jobs, const uint64_t* d_tiles, int
   cfg.numAttrs = 2;
   static int dbg = -1;
   if (dbg < 0) {  // measurement knob (never set in production): TNS_DBG bits 1 skip epilogue,
-    const char* e = getenv("TNS_DBG");  // 2 skip mirrored stores, 4 skip aux prefetch
+    const char* e = getenv("TNS_DBG");  // 2 skip mirrored stores, 4 skip aux prefetch, 8 counters
     dbg = e ? atoi(e) : 0;
   }
-  return cudaLaunchKernelEx(&cfg, kern, d_jobs, d_tiles, total_tiles, d_flags, dbg);
+  return cudaLaunchKernelEx(&cfg, kern, d_jobs, d_tiles, d_phases, nphases, d_sync, d_flags, dbg);
 }
 
-cudaError_t launch_umma_gemm(const GemmJob* d_jobs, const uint64_t* d_tiles, int64_t total_tiles, int cg,
-                             int num_sms, uint32_t* d_flags, cudaStream_t stream) {
-  if (total_tiles <= 0) return cudaSuccess;
-  return cg == 2 ? launch_cg<2>(d_jobs, d_tiles, total_tiles, num_sms, d_flags, stream)
-                 : launch_cg<1>(d_jobs, d_tiles, total_tiles, num_sms, d_flags, stream);
+cudaError_t launch_umma_gemm(const GemmJob* d_jobs, const uint64_t* d_tiles, const PhaseDesc* d_phases,
+                             int nphases, unsigned* d_sync, int64_t max_tiles, int cg, int num_sms,
+                             uint32_t* d_flags, cudaStream_t stream) {
+  if (max_tiles <= 0) return cudaSuccess;
+  return cg == 2 ? launch_cg<2>(d_jobs, d_tiles, d_phases, nphases, d_sync, max_tiles, num_sms, d_flags, stream)
+                 : launch_cg<1>(d_jobs, d_tiles, d_phases, nphases, d_sync, max_tiles, num_sms, d_flags, stream);
 }
 
 cudaError_t umma_epi_prof(unsigned long long* out, bool reset) {

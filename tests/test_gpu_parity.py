@@ -45,8 +45,16 @@ CASES = [
 ]
 
 
+@pytest.fixture(params=[0, 3, 4], ids=["auto", "fused", "per-step"])
+def launch_mode(request):
+    """0 auto, 3 all steps in one fused launch, 4 one launch per step."""
+    old = ns.set_path(request.param)
+    yield request.param
+    ns.set_path(old)
+
+
 @pytest.mark.parametrize("m,n,dist", CASES)
-def test_turbo_muon_aol4(m, n, dist):
+def test_turbo_muon_aol4(m, n, dist, launch_mode):
     x = I.make_matrix(m, n, seed=I.matrix_seed(1, m + n), dist=dist)
     coeffs = C.turbo(4)
     out = _run(x, coeffs, "aol")
@@ -59,7 +67,7 @@ def test_turbo_muon_aol4(m, n, dist):
 
 
 @pytest.mark.parametrize("m,n", [(768, 768), (3072, 768), (64, 576)])
-def test_muon_plus_frobenius5(m, n):
+def test_muon_plus_frobenius5(m, n, launch_mode):
     x = I.gaussian(m, n, seed=21)
     coeffs = C.muon_plus(5)
     out = _run(x, coeffs, "frobenius")
@@ -88,7 +96,7 @@ def test_fp32_exact_mode(m, n, dist):
     assert eg <= POLAR_SLACK * eo
 
 
-def test_batched_equals_single_bitwise():
+def test_batched_equals_single_bitwise(launch_mode):
     shapes = [(768, 768), (3072, 768), (768, 3072), (64, 216), (520, 136)]
     xs = [I.gaussian(m, n, seed=40 + i) for i, (m, n) in enumerate(shapes)]
     singles = [_run(x, C.turbo(4), "aol") for x in xs]
@@ -147,6 +155,25 @@ def test_descent_alignment_and_determinism():
     assert O.descent_alignment(x, a) > 0
 
 
+def test_fused_equals_per_step_bitwise():
+    """The fused single launch and the per-step launches run the same kernels on the same
+    tiles: outputs are bitwise equal."""
+    shapes = [(256, 2304), (64, 216), (768, 768), (520, 136)]
+    xs = [I.gaussian(m, n, seed=90 + i) for i, (m, n) in enumerate(shapes)]
+    res = {}
+    for path in (3, 4):
+        old = ns.set_path(path)
+        try:
+            ts = [torch.from_numpy(x).to(torch.bfloat16).cuda() for x in xs]
+            ns.orthogonalize_list(ts, iters=4)
+            torch.cuda.synchronize()
+            res[path] = [t.float().cpu().numpy() for t in ts]
+        finally:
+            ns.set_path(old)
+    for a, b in zip(res[3], res[4]):
+        assert np.array_equal(a, b)
+
+
 def test_zero_column_flag():
     x = I.gaussian(256, 128, seed=65)
     x[:, 5] = 0
@@ -158,6 +185,7 @@ def test_zero_column_flag():
 
 
 def test_launch_count_grouped():
+    """One launch per step over all matrices: 3T + 1 launches (path 0/4)."""
     shapes = [(768, 768)] * 4 + [(3072, 768), (768, 3072)]
     ts = [torch.from_numpy(I.gaussian(m, n, seed=70 + i)).to(torch.bfloat16).cuda() for i, (m, n) in enumerate(shapes)]
     ns.orthogonalize_list(ts, iters=4)  # builds the plan

@@ -18,6 +18,8 @@ ap.add_argument("--workload", default="gpt2-medium")
 ap.add_argument("--reps", type=int, default=10)
 ap.add_argument("--iters", type=int, default=4)
 a = ap.parse_args()
+if os.environ.get("TNS_PATH"):
+    ns.set_path(int(os.environ["TNS_PATH"]))
 shapes = I.shape_set(a.workload)
 xs = [torch.from_numpy(I.gaussian(m, n, seed=i)).to(torch.bfloat16).cuda() for i, (m, n) in enumerate(shapes)]
 outs = [torch.empty_like(t) for t in xs]
@@ -44,7 +46,7 @@ e1.record()
 torch.cuda.synchronize()
 prof = ns.profile_read()
 clk = cs.stop()
-print(json.dumps({"workload": a.workload, "dbg": os.environ.get("TNS_DBG", "0"), "sm_mhz": clk["sm_mhz"],
+print(json.dumps({"workload": a.workload, "dbg": os.environ.get("TNS_DBG", "0"), "path": os.environ.get("TNS_PATH", "0"), "sm_mhz": clk["sm_mhz"],
                   "reasons": clk["reasons"], "ms_per_call_no_events": round(ms_clean, 4),
                   "ms_per_call": round(e0.elapsed_time(e1) / a.reps, 4),
                   "kernel_ms_per_call": {k: round(v[0] / a.reps, 4) for k, v in prof.items() if v[1]}}))
