@@ -233,9 +233,10 @@ def run_own(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    distributed = "WORLD_SIZE" in os.environ  # launched by torchrun (also at N = 1)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
+    if distributed:
         dist.init_process_group("nccl", device_id=dev)
     peaks = load_peaks()
 
@@ -247,13 +248,15 @@ def run_own(args):
     plan = make_plan(shapes, world, iters)
     mine = plan.mine(rank)
 
+    buckets = 1 if world == 1 else args.buckets
+
     def step():
-        return orthogonalize_sharded(xs, None, iters=iters, precond="aol")
+        return orthogonalize_sharded(xs, None, iters=iters, precond="aol", buckets=buckets)
 
     for _ in range(max(args.warmup, 3)):
         step()
     torch.cuda.synchronize()
-    if world > 1:
+    if distributed:
         dist.barrier()
     sampler = ClockSampler(local)
     c0 = ns.launch_count()
@@ -268,7 +271,7 @@ def run_own(args):
     torch.cuda.synchronize()
     clocks = sampler.stop()
     launches = ns.launch_count() - c0
-    if world > 1:
+    if distributed:
         dist.barrier()
     ms = e0.elapsed_time(e1) / args.steps
     # per-kernel durations: the same K steps again with library-side CUDA events around
@@ -286,7 +289,7 @@ def run_own(args):
     ns.profile_enable(False)
     ms_prof = p0.elapsed_time(p1) / args.steps
     t = torch.tensor([ms], device=dev)
-    if world > 1:
+    if distributed:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
     total_flops = sum(ns_flops(m, n, iters) for m, n in shapes)
@@ -327,7 +330,8 @@ def run_own(args):
         "data": "synthetic (seeded Gaussian N(0,1) matrices, bf16-rounded, GPT-2-medium hidden-matrix shapes)",
         "config": {"workload": WORKLOAD if args.workload == "gpt2-medium" else args.workload,
                    "matrices": len(shapes), "iters": iters, "precond": "aol", "coeffs": "Muon+ last 4 (App. D)",
-                   "sharding": f"LPT whole-matrix ownership over {world} rank(s) + NCCL all-gather" if world > 1
+                   "sharding": f"LPT whole-matrix ownership over {world} ranks + {buckets} bucketed NCCL "
+                               "all-gathers overlapped with the NS launches" if world > 1
                    else "1 rank, grouped launch (13 launches / step)",
                    "l2": f"inputs {sum(m * n for m, n in shapes) * 2 / 1e6:.0f} MB > 126 MB L2, no flush",
                    "parallelism": f"dp{world} (matrix ownership)"},
@@ -345,7 +349,7 @@ def run_own(args):
                                           f"+ OpenBLAS; extrapolated to the {len(shapes)}-matrix set by algorithmic FLOPs"}
     if rank == 0:
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if distributed:
         dist.barrier()
         dist.destroy_process_group()
     return 0
@@ -365,44 +369,39 @@ def lookup_traffic(workload, kernel):
 
 
 def run_e2e(args, xs, shapes, plan, mine, rank, world, dev, iters):
+    """Same metric through the public host-resident API: pinned host inputs in, pinned host
+    results out, host<->device copies inside the timed region (overlapped with the NS
+    launches and the all-gather by `orthogonalize_host`'s bucket pipeline)."""
     import torch
+    import torch.distributed as dist
 
-    from paper_2512_04632_b200.parallel import orthogonalize_sharded
-    host_in = {i: xs[i].cpu().pin_memory() for i in mine}
-    gathered = orthogonalize_sharded(xs, None, iters=iters)
-    buf = gathered[0]._base if gathered[0]._base is not None else gathered[0]
-    host_out = torch.empty(buf.numel(), dtype=buf.dtype).pin_memory()
-    h2d = sum(host_in[i].numel() * 2 for i in mine)
-    d2h = host_out.numel() * 2
-
-    def step():
-        for i in mine:
-            xs[i].copy_(host_in[i], non_blocking=True)
-        g = orthogonalize_sharded(xs, None, iters=iters)
-        b = g[0]._base if g[0]._base is not None else g[0]
-        host_out.copy_(b, non_blocking=True)
-
-    step()
+    from paper_2512_04632_b200.parallel import make_plan as _mk
+    from paper_2512_04632_b200.parallel import orthogonalize_host
+    host_in = [x.cpu().pin_memory() for x in xs]
+    nb = args.e2e_buckets
+    orthogonalize_host(host_in, iters=iters, buckets=nb)
     torch.cuda.synchronize()
+    hp = _mk(shapes, world, iters, nb)
+    h2d = sum(host_in[i].numel() * 2 for i in hp.mine(rank))
+    d2h = hp.total * 2
     k = max(1, min(args.steps, args.e2e_steps))
-    if world > 1:
-        import torch.distributed as dist
+    if dist.is_initialized():
         dist.barrier()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record()
     for _ in range(k):
-        step()
+        orthogonalize_host(host_in, iters=iters, buckets=nb)
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / k
     t = torch.tensor([ms], device=dev)
-    if world > 1:
-        import torch.distributed as dist
+    if dist.is_initialized():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return {"value": round(float(t.item()), 3), "unit": "ms", "h2d_bytes_per_step": int(h2d),
-            "d2h_bytes_per_step": int(d2h), "steps": k,
-            "path": "pinned host -> H2D -> orthogonalize_sharded (C ABI) -> all-gather -> D2H pinned host"}
+            "d2h_bytes_per_step": int(d2h), "steps": k, "buckets": nb,
+            "path": "pinned host -> H2D -> NS (C ABI) -> all-gather -> D2H pinned host, "
+                    f"{nb}-bucket pipeline on separate copy/compute/comm streams (orthogonalize_host)"}
 
 
 def run_extras(args, peaks):
@@ -485,6 +484,8 @@ def main():
     ap.add_argument("--workload", default="gpt2-medium")
     ap.add_argument("--iters", type=int, default=4)
     ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--e2e-buckets", type=int, default=6)
+    ap.add_argument("--buckets", type=int, default=4, help="all-gather buckets at N > 1")
     ap.add_argument("--extra-reps", type=int, default=10)
     ap.add_argument("--cpu-budget", type=float, default=12.0, help="seconds of oracle CPU work")
     ap.add_argument("--quick", action="store_true", help="skip extras and cpu_baseline (profiling runs)")

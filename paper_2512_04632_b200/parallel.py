@@ -1,24 +1,29 @@
-"""Multi-GPU orthogonalisation of a Muon parameter set: whole-matrix ownership + all-gather.
+"""Multi-GPU orthogonalisation of a Muon parameter set: whole-matrix ownership + all-gather,
+and the host-resident (offload) pipeline.
 
 Matrices are independent units (the paper orthogonalises every 2-D update separately,
 P:L97, "batches of 32 matrices" P:L247), so the path shards by matrix: each rank runs the
-grouped NS launch on the matrices it owns, writing straight into its segment of a packed
-buffer, and one collective (NCCL all-gather over NVLink) gives every rank every result --
-the exchange a data-parallel optimizer step needs.  No matrix is split across ranks
-(splitting one would need a Gram all-reduce every step, the bottleneck P:L100/L313 name).
+grouped NS launches on the matrices it owns, writing straight into its segment of a packed
+buffer, and NCCL all-gathers over NVLink give every rank every result -- the exchange a
+data-parallel optimizer step needs.  No matrix is split across ranks (splitting one would
+need a Gram all-reduce every step, the bottleneck P:L100/L313 name).
 
-Ownership is LPT (longest-processing-time-first) on the algorithmic FLOPs of §8(a):
-deterministic and identical on every rank (no communication to agree on it).
+Ownership is LPT (longest-processing-time-first) on the algorithmic FLOPs of SURVEY §8(a):
+deterministic and identical on every rank (no communication to agree on it).  The owned
+matrices are further cut into `buckets`; the packed buffer is laid out bucket-major,
+rank-minor, so bucket b's all-gather (on a communication stream) overlaps the NS launches
+of bucket b+1 (SURVEY §8(e) "Overlap").
 """
 from __future__ import annotations
 
-from dataclasses import dataclass
+from dataclasses import dataclass, field
 from typing import Callable, Sequence
 
 import torch
 import torch.distributed as dist
 
-__all__ = ["ns_flops", "lpt_owners", "ShardPlan", "make_plan", "orthogonalize_sharded"]
+__all__ = ["ns_flops", "lpt_owners", "ShardPlan", "make_plan", "orthogonalize_sharded",
+           "orthogonalize_host"]
 
 _ALIGN = 64  # elements; keeps every packed matrix 128-byte aligned in bf16
 
@@ -42,81 +47,190 @@ def lpt_owners(shapes: Sequence[tuple[int, int]], world: int, iters: int = 4) ->
     return owner
 
 
+def _aligned(n: int) -> int:
+    return -(-n // _ALIGN) * _ALIGN
+
+
 @dataclass
 class ShardPlan:
     world: int
     owners: list[int]
-    offsets: list[int]       # element offset of matrix i inside the gathered buffer
-    seg_elems: int           # elements per rank segment (equal for all ranks)
-    load: list[int]          # FLOPs per rank
+    offsets: list[int]          # element offset of matrix i inside the packed buffer
+    load: list[int]             # FLOPs per rank
+    buckets: list[list[list[int]]] = field(default_factory=list)  # [bucket][rank] -> matrices
+    bucket_base: list[int] = field(default_factory=list)          # element offset of bucket b
+    bucket_seg: list[int] = field(default_factory=list)           # per-rank segment of bucket b
+    total: int = 0              # elements of the packed buffer
 
     def mine(self, rank: int) -> list[int]:
-        return [i for i, r in enumerate(self.owners) if r == rank]
+        return [i for b in self.buckets for i in b[rank]]
+
+    @property
+    def seg_elems(self) -> int:  # single-bucket plans: per-rank segment
+        return self.bucket_seg[0]
 
 
-def make_plan(shapes: Sequence[tuple[int, int]], world: int, iters: int = 4) -> ShardPlan:
+def make_plan(shapes: Sequence[tuple[int, int]], world: int, iters: int = 4, buckets: int = 1) -> ShardPlan:
     owners = lpt_owners(shapes, world, iters)
-    seg_fill = [0] * world
-    local = [0] * len(shapes)
-    for i, (m, n) in enumerate(shapes):
-        r = owners[i]
-        local[i] = seg_fill[r]
-        seg_fill[r] += -(-(m * n) // _ALIGN) * _ALIGN
-    seg = max(max(seg_fill), _ALIGN)
-    offsets = [owners[i] * seg + local[i] for i in range(len(shapes))]
     load = [0] * world
     for i, s in enumerate(shapes):
         load[owners[i]] += ns_flops(*s, iters)
-    return ShardPlan(world, owners, offsets, seg, load)
+    # per rank: owned matrices in index order, cut into `buckets` runs of ~equal FLOPs
+    per_rank = [[i for i in range(len(shapes)) if owners[i] == r] for r in range(world)]
+    nb = max(1, int(buckets))
+    bk: list[list[list[int]]] = [[[] for _ in range(world)] for _ in range(nb)]
+    for r in range(world):
+        tot = sum(ns_flops(*shapes[i], iters) for i in per_rank[r])
+        acc = 0
+        for i in per_rank[r]:
+            b = min(nb - 1, (acc * nb) // tot) if tot else 0
+            bk[b][r].append(i)
+            acc += ns_flops(*shapes[i], iters)
+    bk = [b for b in bk if any(b)] or [[[] for _ in range(world)]]
+    offsets = [0] * len(shapes)
+    bases, segs = [], []
+    base = 0
+    for b in bk:
+        seg = max(max((sum(_aligned(shapes[i][0] * shapes[i][1]) for i in b[r]) for r in range(world)),
+                      default=0), _ALIGN)
+        for r in range(world):
+            off = base + r * seg
+            for i in b[r]:
+                offsets[i] = off
+                off += _aligned(shapes[i][0] * shapes[i][1])
+        bases.append(base)
+        segs.append(seg)
+        base += world * seg
+    return ShardPlan(world, owners, offsets, load, bk, bases, segs, base)
 
 
 _BUFFERS: dict = {}
+_STREAMS: dict = {}
 
 
-def _gather_buffer(key, numel, dtype, device) -> torch.Tensor:
-    buf = _BUFFERS.get(key)
-    if buf is None or buf.numel() != numel:
-        buf = torch.empty(numel, dtype=dtype, device=device)
-        _BUFFERS[key] = buf
-    return buf
+def _cached(key, make):
+    v = _BUFFERS.get(key)
+    if v is None:
+        v = make()
+        _BUFFERS[key] = v
+    return v
+
+
+def _stream(device, name):
+    k = (str(device), name)
+    if k not in _STREAMS:
+        _STREAMS[k] = torch.cuda.Stream(device=device)
+    return _STREAMS[k]
+
+
+def _gather(buf, plan, b, rank, group):
+    lo = plan.bucket_base[b]
+    seg = plan.bucket_seg[b]
+    region = buf[lo:lo + plan.world * seg]
+    mine = region[rank * seg:(rank + 1) * seg]
+    if dist.get_backend(group) == "nccl":
+        dist.all_gather_into_tensor(region, mine, group=group)
+    else:
+        chunks = list(region.split(seg))
+        dist.all_gather(chunks, mine.clone(), group=group)
 
 
 def orthogonalize_sharded(xs: Sequence[torch.Tensor], group=None, iters: int = 4,
                           precond: str = "aol", coeffs=None, inplace: bool = False,
-                          compute: Callable | None = None) -> list[torch.Tensor]:
+                          compute: Callable | None = None, buckets: int = 1) -> list[torch.Tensor]:
     """Every rank passes the same list (the post-all-reduce gradients / momenta).
-    Returns the orthogonalised matrices (views into one gathered buffer); with
+    Returns the orthogonalised matrices (views into one packed, gathered buffer); with
     inplace=True they are also copied back into `xs`.
 
-    `compute(inputs, outputs)` runs NS on this rank's matrices; it defaults to the
-    grouped CUDA call.  (The CPU multi-process tests inject a CPU function here.)
+    `compute(inputs, outputs)` runs NS on this rank's matrices; it defaults to the grouped
+    CUDA call.  (The CPU multi-process tests inject a CPU function here.)
     """
     xs = list(xs)
-    world = dist.get_world_size(group) if dist.is_initialized() else 1
-    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    on = dist.is_initialized()
+    world = dist.get_world_size(group) if on else 1
+    rank = dist.get_rank(group) if on else 0
     shapes = [tuple(t.shape) for t in xs]
-    plan = make_plan(shapes, world, iters)
+    plan = make_plan(shapes, world, iters, buckets)
     dtype, device = xs[0].dtype, xs[0].device
-    key = (tuple(shapes), world, dtype, str(device), id(group))
-    buf = _gather_buffer(key, plan.seg_elems * world, dtype, device)
+    key = ("gather", tuple(shapes), world, buckets, dtype, str(device), id(group))
+    buf = _cached(key, lambda: torch.empty(plan.total, dtype=dtype, device=device))
     views = [buf[o:o + m * n].view(m, n) for o, (m, n) in zip(plan.offsets, shapes)]
-    mine = plan.mine(rank)
-    if mine:
-        ins = [xs[i] for i in mine]
-        outs = [views[i] for i in mine]
-        if compute is None:
-            from .api import orthogonalize_list
-            orthogonalize_list(ins, out=outs, iters=iters, precond=precond, coeffs=coeffs)
-        else:
-            compute(ins, outs)
-    if world > 1:
-        seg = buf[rank * plan.seg_elems:(rank + 1) * plan.seg_elems]
-        if dist.get_backend(group) == "nccl":
-            dist.all_gather_into_tensor(buf, seg, group=group)
-        else:
-            chunks = list(buf.split(plan.seg_elems))
-            dist.all_gather(chunks, seg.clone(), group=group)
+    cuda = device.type == "cuda"
+    overlap = on and cuda and len(plan.buckets) > 1
+    comm = _stream(device, "comm") if overlap else None
+    for b, per_rank in enumerate(plan.buckets):
+        mine = per_rank[rank]
+        if mine:
+            ins = [xs[i] for i in mine]
+            outs = [views[i] for i in mine]
+            if compute is None:
+                from .api import orthogonalize_list
+                orthogonalize_list(ins, out=outs, iters=iters, precond=precond, coeffs=coeffs)
+            else:
+                compute(ins, outs)
+        if on:
+            if overlap:  # bucket b's exchange overlaps bucket b+1's compute
+                comm.wait_stream(torch.cuda.current_stream(device))
+                with torch.cuda.stream(comm):
+                    _gather(buf, plan, b, rank, group)
+            else:
+                _gather(buf, plan, b, rank, group)
+    if overlap:
+        torch.cuda.current_stream(device).wait_stream(comm)
     if inplace:
         for t, v in zip(xs, views):
             t.copy_(v)
     return views
+
+
+def orthogonalize_host(host_xs: Sequence[torch.Tensor], group=None, iters: int = 4,
+                       precond: str = "aol", coeffs=None, buckets: int = 4,
+                       device=None) -> list[torch.Tensor]:
+    """Host-resident (offload) entry point: inputs are pinned CPU tensors, results come back
+    as views into one pinned CPU buffer.  Each rank copies in only the matrices it owns;
+    per bucket, the host->device copies, the NS launches, the all-gather and the
+    device->host copies run on separate streams, so the PCIe transfers overlap the compute.
+    """
+    host_xs = list(host_xs)
+    device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+    on = dist.is_initialized()
+    world = dist.get_world_size(group) if on else 1
+    rank = dist.get_rank(group) if on else 0
+    shapes = [tuple(t.shape) for t in host_xs]
+    dtype = host_xs[0].dtype
+    plan = make_plan(shapes, world, iters, buckets)
+    key = ("host", tuple(shapes), world, buckets, dtype, str(device), id(group))
+    dev_in = _cached(key + ("in",), lambda: [torch.empty(s, dtype=dtype, device=device) for s in shapes])
+    buf = _cached(key + ("gather",), lambda: torch.empty(plan.total, dtype=dtype, device=device))
+    hout = _cached(key + ("hout",), lambda: torch.empty(plan.total, dtype=dtype).pin_memory())
+    views = [buf[o:o + m * n].view(m, n) for o, (m, n) in zip(plan.offsets, shapes)]
+    cur = torch.cuda.current_stream(device)
+    h2d, d2h = _stream(device, "h2d"), _stream(device, "d2h")
+    comm = _stream(device, "comm") if on else None
+    h2d.wait_stream(cur)
+    d2h.wait_stream(cur)
+    for b, per_rank in enumerate(plan.buckets):
+        mine = per_rank[rank]
+        with torch.cuda.stream(h2d):
+            for i in mine:
+                dev_in[i].copy_(host_xs[i], non_blocking=True)
+        cur.wait_stream(h2d)
+        if mine:
+            from .api import orthogonalize_list
+            orthogonalize_list([dev_in[i] for i in mine], out=[views[i] for i in mine],
+                               iters=iters, precond=precond, coeffs=coeffs)
+        src = cur
+        if on:
+            comm.wait_stream(cur)
+            with torch.cuda.stream(comm):
+                _gather(buf, plan, b, rank, group)
+            src = comm
+        d2h.wait_stream(src)
+        lo, hi = plan.bucket_base[b], plan.bucket_base[b] + plan.world * plan.bucket_seg[b]
+        with torch.cuda.stream(d2h):
+            hout[lo:hi].copy_(buf[lo:hi], non_blocking=True)
+        # keep the device input slots alive until their copies are consumed
+    cur.wait_stream(d2h)
+    if on:
+        cur.wait_stream(comm)
+    return [hout[o:o + m * n].view(m, n) for o, (m, n) in zip(plan.offsets, shapes)]

@@ -222,3 +222,43 @@ def test_full_size_properties(n):
         v = o.T @ (o @ v)
         v = v / v.norm()
     assert float((o @ v).norm()) <= bound
+
+
+def test_host_pipeline_matches_device_path():
+    """orthogonalize_host (pinned host in/out, bucketed copy/compute overlap) returns the
+    same bits as the device-resident grouped call."""
+    from paper_2512_04632_b200.parallel import orthogonalize_host
+    shapes = [(768, 768)] * 3 + [(3072, 768), (768, 3072), (64, 216)]
+    xs = [I.gaussian(m, n, seed=110 + i) for i, (m, n) in enumerate(shapes)]
+    host = [torch.from_numpy(x).to(torch.bfloat16).pin_memory() for x in xs]
+    outs = orthogonalize_host(host, iters=4, buckets=3)
+    torch.cuda.synchronize()
+    for x, o in zip(xs, outs):
+        t = torch.from_numpy(x).to(torch.bfloat16).cuda()
+        ns.orthogonalize(t, iters=4)
+        assert torch.equal(o, t.cpu())
+
+
+def test_sharded_nccl_world1():
+    """The NCCL code path of the sharder (init, in-place all_gather_into_tensor, bucketed
+    overlap on a comm stream) at world size 1 -- the only size one GPU can run."""
+    import os
+    import torch.distributed as dist
+    from paper_2512_04632_b200.parallel import orthogonalize_sharded
+    if dist.is_initialized():
+        pytest.skip("process group already initialised")
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29531")
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        shapes = [(1024, 1024)] * 4 + [(4096, 1024), (1024, 4096)]
+        xs = [torch.from_numpy(I.gaussian(m, n, seed=120 + i)).to(torch.bfloat16).cuda()
+              for i, (m, n) in enumerate(shapes)]
+        outs = orthogonalize_sharded(xs, iters=4, buckets=3)
+        torch.cuda.synchronize()
+        for x, o in zip(xs, outs):
+            t = x.clone()
+            ns.orthogonalize(t, iters=4)
+            assert torch.equal(o, t)
+    finally:
+        dist.destroy_process_group()

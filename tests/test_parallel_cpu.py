@@ -56,12 +56,29 @@ def _oracle_compute(ins, outs):
         o.copy_(torch.from_numpy(y).to(o.dtype))
 
 
-def _worker(rank, world, port, shapes, q):
+def test_bucketed_layout():
+    shapes = I.gpt2_shapes("small")
+    for world in (1, 2, 4):
+        for nb in (1, 3, 4):
+            plan = make_plan(shapes, world, buckets=nb)
+            spans = sorted((o, o + m * n) for o, (m, n) in zip(plan.offsets, shapes))
+            for (a0, a1), (b0, b1) in zip(spans, spans[1:]):
+                assert a1 <= b0
+            assert spans[-1][1] <= plan.total
+            assert sorted(plan.mine(0) + [i for r in range(1, world) for i in plan.mine(r)]) == list(range(len(shapes)))
+            for b, per_rank in enumerate(plan.buckets):  # each rank's matrices sit in its segment
+                for r, mats in enumerate(per_rank):
+                    lo = plan.bucket_base[b] + r * plan.bucket_seg[b]
+                    for i in mats:
+                        assert lo <= plan.offsets[i] and plan.offsets[i] + shapes[i][0] * shapes[i][1] <= lo + plan.bucket_seg[b]
+
+
+def _worker(rank, world, port, shapes, q, buckets=1):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     xs = [torch.from_numpy(I.gaussian(m, n, seed=100 + i)) for i, (m, n) in enumerate(shapes)]
-    outs = orthogonalize_sharded(xs, iters=4, compute=_oracle_compute)
+    outs = orthogonalize_sharded(xs, iters=4, compute=_oracle_compute, buckets=buckets)
     q.put((rank, [o.clone().numpy() for o in outs]))
     dist.barrier()
     dist.destroy_process_group()
@@ -75,15 +92,15 @@ def _free_port():
     return p
 
 
-@pytest.mark.parametrize("world", [2, 4])
-def test_sharded_gloo_matches_single(world):
+@pytest.mark.parametrize("world,buckets", [(2, 1), (4, 1), (2, 3)])
+def test_sharded_gloo_matches_single(world, buckets):
     shapes = [(96, 64), (64, 160), (128, 128), (40, 24), (200, 56), (64, 64), (32, 96)]
     xs = [torch.from_numpy(I.gaussian(m, n, seed=100 + i)) for i, (m, n) in enumerate(shapes)]
     single = orthogonalize_sharded(xs, iters=4, compute=_oracle_compute)
     ctx = mp.get_context("spawn")
     q = ctx.SimpleQueue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, shapes, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, shapes, q, buckets)) for r in range(world)]
     for p in procs:
         p.start()
     results = [q.get() for _ in range(world)]
