@@ -472,6 +472,12 @@ def run_extras(args, peaks):
     ns.orthogonalize_list(xs, out=outs, iters=4)
     ms_c = time_calls(lambda: ns.orthogonalize_list(xs, out=outs, iters=4), reps, None)
     out["cifar"] = {"us": round(ms_c * 1e3, 1), "launches": 13, "matrices": len(shapes)}
+    # --- config 1: one 128 x 128 fp32 matrix, fp32 "exact" mode
+    x1 = torch.from_numpy(I.gaussian(128, 128, seed=I.matrix_seed(1, 0), bf16=False)).cuda()
+    o1 = torch.empty_like(x1)
+    ns.orthogonalize_list([x1], out=[o1], iters=4)
+    ms_1 = time_calls(lambda: ns.orthogonalize_list([x1], out=[o1], iters=4), reps, None)
+    out["fp32_128"] = {"us": round(ms_1 * 1e3, 1), "tflops_alg": round(ns_flops(128, 128, 4) / (ms_1 * 1e-3) / 1e12, 3)}
     return out
 
 

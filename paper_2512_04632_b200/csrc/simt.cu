@@ -21,11 +21,14 @@ template <typename T>
 __global__ void __launch_bounds__(256)
     simt_gemm_kernel(const SimtJob* __restrict__ jobs, int njobs, int64_t total_tiles,
                      uint32_t* __restrict__ flags) {
-  constexpr int TILE = kSimtTile, KT = 16;
+  // KT = 64: one global round trip per 64 k (the fp32 path is latency-bound at small sizes)
+  constexpr int TILE = kSimtTile, KT = 64;
   __shared__ float As[KT][TILE + 4];
   __shared__ float Bs[KT][TILE + 4];
   const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
   bool bad = false;
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // operands come from the previous step
   for (int64_t t = blockIdx.x; t < total_tiles; t += gridDim.x) {
     int lo = 0, hi = njobs - 1;
     while (lo < hi) {
@@ -39,17 +42,24 @@ __global__ void __launch_bounds__(256)
     const T* __restrict__ B = reinterpret_cast<const T*>(J.B);
     float acc[4][4] = {};
     for (int k0 = 0; k0 < J.K; k0 += KT) {
+      float ra[16], rb[16];  // issue all 32 loads before any smem store (one round trip)
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
+      for (int e = 0; e < 16; ++e) {
         const int idx = tid + e * 256;
         int pp, kk;
-        if (J.sa_p == 1) { pp = idx & 63; kk = idx >> 6; } else { kk = idx & 15; pp = idx >> 4; }
+        if (J.sa_p == 1) { pp = idx & 63; kk = idx >> 6; } else { kk = idx & 63; pp = idx >> 6; }
         const int gp = p0 + pp, gk = k0 + kk;
-        As[kk][pp] = (gp < J.P && gk < J.K) ? ld_val<T>(A + gp * J.sa_p + gk * J.sa_k) : 0.f;
+        ra[e] = (gp < J.P && gk < J.K) ? ld_val<T>(A + gp * J.sa_p + gk * J.sa_k) : 0.f;
         int qq, kq;
-        if (J.sb_q == 1) { qq = idx & 63; kq = idx >> 6; } else { kq = idx & 15; qq = idx >> 4; }
+        if (J.sb_q == 1) { qq = idx & 63; kq = idx >> 6; } else { kq = idx & 63; qq = idx >> 6; }
         const int gq = q0 + qq, gk2 = k0 + kq;
-        Bs[kq][qq] = (gq < J.Q && gk2 < J.K) ? ld_val<T>(B + gq * J.sb_q + gk2 * J.sb_k) : 0.f;
+        rb[e] = (gq < J.Q && gk2 < J.K) ? ld_val<T>(B + gq * J.sb_q + gk2 * J.sb_k) : 0.f;
+      }
+#pragma unroll
+      for (int e = 0; e < 16; ++e) {
+        const int idx = tid + e * 256;
+        if (J.sa_p == 1) As[idx >> 6][idx & 63] = ra[e]; else As[idx & 63][idx >> 6] = ra[e];
+        if (J.sb_q == 1) Bs[idx >> 6][idx & 63] = rb[e]; else Bs[idx & 63][idx >> 6] = rb[e];
       }
       __syncthreads();
 #pragma unroll
@@ -96,11 +106,17 @@ cudaError_t launch_simt_gemm(const SimtJob* d_jobs, int njobs, int64_t total_til
   if (total_tiles <= 0) return cudaSuccess;
   const int64_t cap = (int64_t)num_sms * 8;
   const int grid = (int)(total_tiles < cap ? total_tiles : cap);
-  if (is_bf16)
-    simt_gemm_kernel<uint16_t><<<grid, 256, 0, stream>>>(d_jobs, njobs, total_tiles, d_flags);
-  else
-    simt_gemm_kernel<float><<<grid, 256, 0, stream>>>(d_jobs, njobs, total_tiles, d_flags);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(256);
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // PDL
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (is_bf16) return cudaLaunchKernelEx(&cfg, simt_gemm_kernel<uint16_t>, d_jobs, njobs, total_tiles, d_flags);
+  return cudaLaunchKernelEx(&cfg, simt_gemm_kernel<float>, d_jobs, njobs, total_tiles, d_flags);
 }
 
 // ------------------------------------------------------------------------------ preconditioner
