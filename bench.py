@@ -249,8 +249,26 @@ def run_own(args):
     mine = plan.mine(rank)
 
     buckets = 1 if world == 1 else args.buckets
+    collective = "none" if world == 1 else args.collective
+    coll_note = None
+    if collective == "fused":
+        # self-check before timing: the fused peer-store path must reproduce the NCCL path
+        # bit for bit on this workload, else time the NCCL path and say why
+        try:
+            a = [v.clone() for v in orthogonalize_sharded(xs, None, iters=iters, buckets=buckets)]
+            b = orthogonalize_sharded(xs, None, iters=iters, collective="fused")
+            torch.cuda.synchronize()
+            ok = torch.tensor([int(all(torch.equal(u, v) for u, v in zip(a, b)))], device=dev)
+            dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+            if not int(ok.item()):
+                collective, coll_note = "nccl", "fused self-check mismatch; timed the NCCL path"
+            del a, b
+        except Exception as e:  # pragma: no cover - only on multi-GPU boxes
+            collective, coll_note = "nccl", f"fused path unavailable ({type(e).__name__}: {e}); timed NCCL"
 
     def step():
+        if collective == "fused":
+            return orthogonalize_sharded(xs, None, iters=iters, precond="aol", collective="fused")
         return orthogonalize_sharded(xs, None, iters=iters, precond="aol", buckets=buckets)
 
     for _ in range(max(args.warmup, 3)):
@@ -330,8 +348,11 @@ def run_own(args):
         "data": "synthetic (seeded Gaussian N(0,1) matrices, bf16-rounded, GPT-2-medium hidden-matrix shapes)",
         "config": {"workload": WORKLOAD if args.workload == "gpt2-medium" else args.workload,
                    "matrices": len(shapes), "iters": iters, "precond": "aol", "coeffs": "Muon+ last 4 (App. D)",
-                   "sharding": f"LPT whole-matrix ownership over {world} ranks + {buckets} bucketed NCCL "
-                               "all-gathers overlapped with the NS launches" if world > 1
+                   "sharding": (f"LPT whole-matrix ownership over {world} ranks; " + (
+                       "all-gather fused into the last XB epilogue (TMA stores to every peer's "
+                       "symmetric-memory buffer over NVLink)" if collective == "fused" else
+                       f"{buckets} bucketed NCCL all-gathers overlapped with the NS launches")
+                       + (f" [{coll_note}]" if coll_note else "")) if world > 1
                    else "1 rank, grouped launch (13 launches / step)",
                    "l2": f"inputs {sum(m * n for m, n in shapes) * 2 / 1e6:.0f} MB > 126 MB L2, no flush",
                    "parallelism": f"dp{world} (matrix ownership)"},
@@ -491,7 +512,9 @@ def main():
     ap.add_argument("--iters", type=int, default=4)
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--e2e-buckets", type=int, default=6)
-    ap.add_argument("--buckets", type=int, default=4, help="all-gather buckets at N > 1")
+    ap.add_argument("--buckets", type=int, default=4, help="all-gather buckets at N > 1 (NCCL)")
+    ap.add_argument("--collective", choices=["fused", "nccl"], default="fused",
+                    help="N > 1: fused peer stores in the last epilogue, or NCCL all-gathers")
     ap.add_argument("--extra-reps", type=int, default=10)
     ap.add_argument("--cpu-budget", type=float, default=12.0, help="seconds of oracle CPU work")
     ap.add_argument("--quick", action="store_true", help="skip extras and cpu_baseline (profiling runs)")

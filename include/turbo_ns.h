@@ -88,6 +88,18 @@ ns_status ns_orthogonalize_batched(void* const* X, void* const* out, const int64
                                    const float* coeffs, ns_precond precond, ns_dtype dtype,
                                    void* stream);
 
+/* Fused collective (the GEMM -> all-gather of the sharded path as ONE
+ * kernel): as ns_orthogonalize_batched, and the LAST iteration's epilogue also stores every
+ * output tile into npeer more destinations, peer_out[i * npeer + r] = matrix i's slot on
+ * peer r (device addresses valid in this process, e.g. other GPUs' gather buffers mapped
+ * over NVLink by symmetric memory), so the exchange overlaps the final GEMM tile by tile.
+ * out[i] (or X[i]) receives the result as well.  bf16 tcgen05 path only (16-byte aligned
+ * pointers, m and n multiples of 8), else NS_ERR_NOT_SUPPORTED; 0 <= npeer <= 64.  The
+ * caller orders the peers (e.g. a symmetric-memory barrier before and after the call). */
+ns_status ns_orthogonalize_peers(void* const* X, void* const* out, void* const* peer_out, int npeer,
+                                 const int64_t* m, const int64_t* n, int64_t count, int iters,
+                                 const float* coeffs, ns_precond precond, ns_dtype dtype, void* stream);
+
 /* Bytes of device workspace the library will hold for this problem list. */
 ns_status ns_workspace_size(const int64_t* m, const int64_t* n, int64_t count,
                             ns_dtype dtype, size_t* bytes);

@@ -75,8 +75,12 @@ def orthogonalize(x: torch.Tensor, iters: int = 4, precond: str = "aol", coeffs=
 
 
 def orthogonalize_list(xs: Sequence[torch.Tensor], out: Sequence[torch.Tensor] | None = None,
-                       iters: int = 4, precond: str = "aol", coeffs=None) -> list[torch.Tensor]:
-    """Grouped call: one launch per NS step over all matrices.  In place unless `out`."""
+                       iters: int = 4, precond: str = "aol", coeffs=None,
+                       peer_ptrs: Sequence[Sequence[int]] | None = None) -> list[torch.Tensor]:
+    """Grouped call: one launch per NS step over all matrices.  In place unless `out`.
+
+    peer_ptrs[i] = device addresses (ints) where matrix i's result is ALSO stored by the
+    last iteration's epilogue (fused collective, ns_orthogonalize_peers)."""
     xs = list(xs)
     if not xs:
         return []
@@ -100,9 +104,19 @@ def orthogonalize_list(xs: Sequence[torch.Tensor], out: Sequence[torch.Tensor] |
     N = (ctypes.c_int64 * cnt)(*[t.shape[1] for t in xs])
     c = _coeff_array(iters, coeffs, precond)
     with torch.cuda.device(xs[0].device):
-        st = lib.ns_orthogonalize_batched(X, O, M, N, cnt, iters, c, PRECOND[precond], dt,
-                                          _stream(xs[0]))
-    check(st, "ns_orthogonalize_batched")
+        if peer_ptrs is None:
+            st = lib.ns_orthogonalize_batched(X, O, M, N, cnt, iters, c, PRECOND[precond], dt,
+                                              _stream(xs[0]))
+            check(st, "ns_orthogonalize_batched")
+        else:
+            npeer = len(peer_ptrs[0]) if cnt else 0
+            if any(len(p) != npeer for p in peer_ptrs) or len(peer_ptrs) != cnt:
+                raise ValueError("peer_ptrs must list the same number of peers for every matrix")
+            flat = [int(p) for ps in peer_ptrs for p in ps]
+            Pp = (ctypes.c_void_p * max(1, len(flat)))(*flat) if flat else None
+            st = lib.ns_orthogonalize_peers(X, O, Pp, npeer, M, N, cnt, iters, c, PRECOND[precond], dt,
+                                            _stream(xs[0]))
+            check(st, "ns_orthogonalize_peers")
     return out if out is not None else xs
 
 

@@ -141,6 +141,9 @@ struct Mat {
   int part_ld;
   // tensormap indices (tcgen05 path)
   int tm_x, tm_out, tm_w, tm_a, tm_b;
+  // fused collective: extra destinations of the final result (peers' buffers)
+  std::vector<void*> peer;
+  int tm_peer;
 };
 
 enum PhaseKind { PH_GEMM = 0, PH_SIMT = 1, PH_PRECOND = 2, PH_COPY = 3, PH_FUSED = 4 };
@@ -272,6 +275,12 @@ static ns_status build_plan(Plan& P, HostTables& H, DevCtx* dc, const float* coe
       if ((st = encode_pair(tmaps, W(mt), mt.m, mt.n, &mt.tm_w)) != NS_OK) return st;
       if ((st = encode_pair(tmaps, Am(mt), mt.N, mt.N, &mt.tm_a)) != NS_OK) return st;
       if ((st = encode_pair(tmaps, Bm(mt), mt.N, mt.N, &mt.tm_b)) != NS_OK) return st;
+      mt.tm_peer = (int)tmaps.size();
+      for (void* pp : mt.peer) {
+        CUtensorMap tm;
+        if ((st = encode_tmap(&tm, pp, mt.m, mt.n, 32)) != NS_OK) return st;
+        tmaps.push_back(tm);
+      }
     }
   }
   size_t tm_off = tmaps.empty() ? 0 : H.push(tmaps.data(), tmaps.size() * sizeof(CUtensorMap), 128);
@@ -279,7 +288,7 @@ static ns_status build_plan(Plan& P, HostTables& H, DevCtx* dc, const float* coe
   // Device addresses of tensormaps are known only after allocation: record indices now,
   // patch pointers after cudaMalloc of the table (two-pass).  We first compute the final
   // table size by building jobs with placeholder bases, then fix them up.
-  struct Fix { size_t job_off; int ta, tb, tout, taux; };
+  struct Fix { size_t job_off; int ta, tb, tout, taux, tpeer = -1; };
   std::vector<Fix> fixes;
   struct PFix { size_t pd_off, pj_off; };  // PhaseDesc::pjobs pointers (fused mode)
   std::vector<PFix> pfixes;
@@ -287,7 +296,7 @@ static ns_status build_plan(Plan& P, HostTables& H, DevCtx* dc, const float* coe
     int kind = PHK_GEMM;
     int gemm_kind = 0;
     std::vector<GemmJob> jobs;
-    std::vector<std::array<int, 4>> tmi;
+    std::vector<std::array<int, 5>> tmi;
     size_t job_base = 0;
     std::vector<PrecondJob> pj;
     int64_t rows = 0, items = 0;
@@ -318,7 +327,7 @@ static ns_status build_plan(Plan& P, HostTables& H, DevCtx* dc, const float* coe
       const int mode = step;  // GRAM, POLY, XB
       if (!P.simt) {
         std::vector<GemmJob> jobs;
-        std::vector<std::array<int, 4>> tmi;
+        std::vector<std::array<int, 5>> tmi;
         for (Mat& mt : P.mats) {
           GemmJob J;
           std::memset(&J, 0, sizeof(J));
@@ -351,12 +360,13 @@ static ns_status build_plan(Plan& P, HostTables& H, DevCtx* dc, const float* coe
             J.out = cur_ptr(mt, k + 1); J.aux = cur_ptr(mt, k); J.ld = mt.n;
             tout = ((T - k) % 2 == 0) ? mt.tm_out : mt.tm_w;
             taux = cur_tm(mt, k);
+            if (k == T && !mt.peer.empty()) J.npeer = (int)mt.peer.size();
             J.s = scaled ? Sv(mt) : nullptr;
             J.a = a;
           }
           J.tiles_q = J.sym ? (J.P + kSymBlock - 1) / kSymBlock : (J.Q + kBN - 1) / kBN;
           jobs.push_back(J);
-          tmi.push_back({ta, tb, tout, taux});
+          tmi.push_back({ta, tb, tout, taux, J.npeer ? mt.tm_peer : -1});
         }
         Step stp;
         stp.kind = PHK_GEMM;
@@ -496,7 +506,8 @@ static ns_status build_plan(Plan& P, HostTables& H, DevCtx* dc, const float* coe
           pd.kind = PHK_GEMM; pd.tile_begin = 0; pd.tile_end = ph.total;
           ph.phdesc_off = H.push(&pd, sizeof(pd), 64);
           for (size_t j = 0; j < st.jobs.size(); ++j)
-            fixes.push_back({ph.dev_off + j * sizeof(GemmJob), st.tmi[j][0], st.tmi[j][1], st.tmi[j][2], st.tmi[j][3]});
+            fixes.push_back({ph.dev_off + j * sizeof(GemmJob), st.tmi[j][0], st.tmi[j][1], st.tmi[j][2], st.tmi[j][3],
+                             st.tmi[j][4]});
           P.phases.push_back(ph);
         } else {
           Phase ph{PH_PRECOND};
@@ -512,7 +523,7 @@ static ns_status build_plan(Plan& P, HostTables& H, DevCtx* dc, const float* coe
       // fused: all jobs in one array (global job indices), one tile list, one PhaseDesc
       // per step; the preconditioner becomes two steps (row sums -> s, rescale A)
       std::vector<GemmJob> alljobs;
-      std::vector<std::array<int, 4>> alltmi;
+      std::vector<std::array<int, 5>> alltmi;
       std::vector<uint64_t> alltiles;
       std::vector<PhaseDesc> pds;
       size_t pj_off = 0;
@@ -544,7 +555,8 @@ static ns_status build_plan(Plan& P, HostTables& H, DevCtx* dc, const float* coe
       Phase ph{PH_FUSED};
       ph.jobs_off = H.push(alljobs.data(), alljobs.size() * sizeof(GemmJob), 64);
       for (size_t j = 0; j < alljobs.size(); ++j)
-        fixes.push_back({ph.jobs_off + j * sizeof(GemmJob), alltmi[j][0], alltmi[j][1], alltmi[j][2], alltmi[j][3]});
+        fixes.push_back({ph.jobs_off + j * sizeof(GemmJob), alltmi[j][0], alltmi[j][1], alltmi[j][2], alltmi[j][3],
+                         alltmi[j][4]});
       ph.tiles_off = H.push(alltiles.data(), alltiles.size() * sizeof(uint64_t), 64);
       ph.phdesc_off = H.push(pds.data(), pds.size() * sizeof(PhaseDesc), 64);
       for (size_t i = 0; i < pds.size(); ++i)
@@ -571,6 +583,7 @@ static ns_status build_plan(Plan& P, HostTables& H, DevCtx* dc, const float* coe
       J->tmB = dbase + tm_off + (size_t)f.tb * sizeof(CUtensorMap);
       J->tmOut = dbase + tm_off + (size_t)(f.tout + 1) * sizeof(CUtensorMap);
       J->tmAux = f.taux >= 0 ? dbase + tm_off + (size_t)(f.taux + 1) * sizeof(CUtensorMap) : nullptr;
+      J->tmPeer = f.tpeer >= 0 ? dbase + tm_off + (size_t)f.tpeer * sizeof(CUtensorMap) : nullptr;
     }
     for (const PFix& f : pfixes) {
       PhaseDesc* pd = reinterpret_cast<PhaseDesc*>(H.bytes.data() + f.pd_off);
@@ -661,7 +674,14 @@ static ns_status run(const std::vector<Mat>& mats_in, int iters, const float* co
   ns_status st = dev_ctx(&dc);
   if (st != NS_OK) return st;
   bool simt = (g_path == 1) || dtype != NS_BF16 || dc->cc_major != 10;
-  for (const Mat& mt : mats_in) simt = simt || !tma_ok(mt, dtype);
+  bool peers = false;
+  for (const Mat& mt : mats_in) {
+    simt = simt || !tma_ok(mt, dtype);
+    peers = peers || !mt.peer.empty();
+    for (void* pp : mt.peer) simt = simt || (reinterpret_cast<uintptr_t>(pp) & 15);
+  }
+  if (peers && simt)
+    return fail(NS_ERR_NOT_SUPPORTED, "fused peer stores need the bf16 tcgen05 path (aligned shapes/pointers)");
   int dev = 0;
   CU_TRY(cudaGetDevice(&dev));
   // plan key
@@ -676,6 +696,8 @@ static ns_status run(const std::vector<Mat>& mats_in, int iters, const float* co
   for (const Mat& mt : mats_in) {
     key.push_back(reinterpret_cast<uint64_t>(mt.x)); key.push_back(reinterpret_cast<uint64_t>(mt.out));
     key.push_back((uint64_t)mt.m); key.push_back((uint64_t)mt.n);
+    key.push_back((uint64_t)mt.peer.size());
+    for (void* pp : mt.peer) key.push_back(reinterpret_cast<uint64_t>(pp));
   }
   auto it = g_plans.find(key);
   Plan* P = nullptr;
@@ -703,8 +725,7 @@ static ns_status run(const std::vector<Mat>& mats_in, int iters, const float* co
 }
 
 static Mat make_mat(void* x, void* out, int64_t m, int64_t n, int iters) {
-  Mat mt;
-  std::memset(&mt, 0, sizeof(mt));
+  Mat mt{};
   mt.x = x; mt.out = out ? out : x; mt.m = m; mt.n = n;
   mt.wide = m < n;
   mt.M = mt.wide ? n : m;
@@ -803,6 +824,31 @@ ns_status ns_orthogonalize_batched(void* const* X, void* const* out, const int64
     void* o = out ? out[i] : nullptr;
     if (o && (st = validate_mat(o, m[i], n[i], dtype)) != NS_OK) return st;
     mats.push_back(make_mat(X[i], o, m[i], n[i], iters));
+  }
+  return run(mats, iters, coeffs, precond, dtype, reinterpret_cast<cudaStream_t>(stream));
+}
+
+ns_status ns_orthogonalize_peers(void* const* X, void* const* out, void* const* peer_out, int npeer,
+                                 const int64_t* m, const int64_t* n, int64_t count, int iters,
+                                 const float* coeffs, ns_precond precond, ns_dtype dtype, void* stream) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  ns_status st = validate_common(count, iters, coeffs, precond, dtype);
+  if (st != NS_OK) return st;
+  if (!X || !m || !n) return fail(NS_ERR_INVALID_VALUE, "NULL array argument");
+  if (npeer < 0 || npeer > 64 || (npeer > 0 && !peer_out)) return fail(NS_ERR_INVALID_VALUE, "bad npeer/peer_out");
+  if (dtype != NS_BF16) return fail(NS_ERR_NOT_SUPPORTED, "fused peer stores are bf16 only");
+  std::vector<Mat> mats;
+  for (int64_t i = 0; i < count; ++i) {
+    if ((st = validate_mat(X[i], m[i], n[i], dtype)) != NS_OK) return st;
+    void* o = out ? out[i] : nullptr;
+    if (o && (st = validate_mat(o, m[i], n[i], dtype)) != NS_OK) return st;
+    Mat mt = make_mat(X[i], o, m[i], n[i], iters);
+    for (int r = 0; r < npeer; ++r) {
+      void* pp = peer_out[i * npeer + r];
+      if ((st = validate_mat(pp, m[i], n[i], dtype)) != NS_OK) return st;
+      mt.peer.push_back(pp);
+    }
+    mats.push_back(mt);
   }
   return run(mats, iters, coeffs, precond, dtype, reinterpret_cast<cudaStream_t>(stream));
 }

@@ -51,6 +51,11 @@ struct GemmJob {
   // [ceil(N/128), + ceil(N/32)) = mirrored 32-row blocks.  nullptr = not collected.
   float* part;
   int32_t part_ld;
+  // XB of the last iteration, fused collective: also store every output tile into `npeer`
+  // more destinations (peers' gather buffers over NVLink); tmPeer -> npeer consecutive
+  // 32x32-box CUtensorMaps.
+  const void* tmPeer;
+  int32_t npeer;
 };
 
 // CUDA-core (SIMT) variant of a GemmJob: operands by pointer + strides (elements),

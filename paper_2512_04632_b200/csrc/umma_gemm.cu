@@ -114,6 +114,8 @@ struct Epi {
   float a, b, c;
   float* part;
   int part_ld;
+  const uint8_t* tmPeer;
+  int npeer;
 };
 __device__ __forceinline__ Epi load_epi(const GemmJob* __restrict__ J) {
   Epi e;
@@ -125,6 +127,7 @@ __device__ __forceinline__ Epi load_epi(const GemmJob* __restrict__ J) {
   e.s = J->s;
   e.a = J->a; e.b = J->b; e.c = J->c;
   e.part = J->part; e.part_ld = J->part_ld;
+  e.tmPeer = reinterpret_cast<const uint8_t*>(J->tmPeer); e.npeer = J->npeer;
   return e;
 }
 
@@ -496,6 +499,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0) {
           tma_store_2d(E.tmOut, s_out, q, prow);          // rows prow.., cols q..
           if (mir) tma_store_2d(E.tmOut, s_mir, prow, q);  // rows q.., cols prow..
+          // fused all-gather: the same box to every peer's buffer (NVLink), tile by tile
+          for (int r = 0; r < E.npeer; ++r) tma_store_2d(E.tmPeer + 128 * r, s_out, q, prow);
           bulk_commit();
         }
         if (E.part != nullptr && mir) {

@@ -135,17 +135,38 @@ def _gather(buf, plan, b, rank, group):
         dist.all_gather(chunks, mine.clone(), group=group)
 
 
+def _symm(key, plan, dtype, device, group):
+    """Gather buffer in symmetric memory (mapped into every rank over NVLink) + handle."""
+    import torch.distributed._symmetric_memory as symm_mem
+    ent = _BUFFERS.get(key)
+    if ent is None:
+        g = group if group is not None else dist.group.WORLD
+        buf = symm_mem.empty(plan.total, dtype=dtype, device=device)
+        hdl = symm_mem.rendezvous(buf, g.group_name)
+        ent = (buf, hdl)
+        _BUFFERS[key] = ent
+    return ent
+
+
 def orthogonalize_sharded(xs: Sequence[torch.Tensor], group=None, iters: int = 4,
                           precond: str = "aol", coeffs=None, inplace: bool = False,
-                          compute: Callable | None = None, buckets: int = 1) -> list[torch.Tensor]:
+                          compute: Callable | None = None, buckets: int = 1,
+                          collective: str = "nccl") -> list[torch.Tensor]:
     """Every rank passes the same list (the post-all-reduce gradients / momenta).
     Returns the orthogonalised matrices (views into one packed, gathered buffer); with
     inplace=True they are also copied back into `xs`.
+
+    collective="nccl": bucketed NCCL all-gathers after the NS launches (overlapped with
+    the next bucket's launches).  collective="fused": the gather buffer lives in symmetric
+    memory and the last iteration's epilogue stores every output tile straight into all
+    peers' buffers over NVLink (ns_orthogonalize_peers) -- no separate collective.
 
     `compute(inputs, outputs)` runs NS on this rank's matrices; it defaults to the grouped
     CUDA call.  (The CPU multi-process tests inject a CPU function here.)
     """
     xs = list(xs)
+    if collective == "fused":
+        return _sharded_fused(xs, group, iters, precond, coeffs, inplace)
     on = dist.is_initialized()
     world = dist.get_world_size(group) if on else 1
     rank = dist.get_rank(group) if on else 0
@@ -177,6 +198,31 @@ def orthogonalize_sharded(xs: Sequence[torch.Tensor], group=None, iters: int = 4
                 _gather(buf, plan, b, rank, group)
     if overlap:
         torch.cuda.current_stream(device).wait_stream(comm)
+    if inplace:
+        for t, v in zip(xs, views):
+            t.copy_(v)
+    return views
+
+
+def _sharded_fused(xs, group, iters, precond, coeffs, inplace):
+    from .api import orthogonalize_list
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    shapes = [tuple(t.shape) for t in xs]
+    plan = make_plan(shapes, world, iters, 1)
+    dtype, device = xs[0].dtype, xs[0].device
+    key = ("symm", tuple(shapes), world, dtype, str(device), id(group))
+    buf, hdl = _symm(key, plan, dtype, device, group)
+    views = [buf[o:o + m * n].view(m, n) for o, (m, n) in zip(plan.offsets, shapes)]
+    mine = plan.mine(rank)
+    es = buf.element_size()
+    ptrs = list(hdl.buffer_ptrs)
+    hdl.barrier(channel=0)  # every peer is done reading its buffer (previous step)
+    if mine:
+        peer_ptrs = [[ptrs[r] + plan.offsets[i] * es for r in range(world) if r != rank] for i in mine]
+        orthogonalize_list([xs[i] for i in mine], out=[views[i] for i in mine], iters=iters,
+                           precond=precond, coeffs=coeffs, peer_ptrs=peer_ptrs)
+    hdl.barrier(channel=0)  # every peer's tiles have landed in this rank's buffer
     if inplace:
         for t, v in zip(xs, views):
             t.copy_(v)

@@ -262,3 +262,45 @@ def test_sharded_nccl_world1():
             assert torch.equal(o, t)
     finally:
         dist.destroy_process_group()
+
+
+def test_fused_peer_stores_c_abi():
+    """ns_orthogonalize_peers: the last iteration's epilogue writes every output tile to the
+    extra destinations as well (here two local buffers standing in for peers' NVLink-mapped
+    gather buffers): all copies are bitwise the regular result."""
+    shapes = [(1024, 1024), (3072, 768), (768, 3072), (520, 136)]
+    xs = [torch.from_numpy(I.gaussian(m, n, seed=130 + i)).to(torch.bfloat16).cuda() for i, (m, n) in enumerate(shapes)]
+    ref = [x.clone() for x in xs]
+    ns.orthogonalize_list(ref, iters=4)
+    outs = [torch.empty_like(x) for x in xs]
+    peers = [[torch.zeros_like(x) for _ in range(2)] for x in xs]
+    ns.orthogonalize_list(xs, out=outs, iters=4, peer_ptrs=[[p.data_ptr() for p in ps] for ps in peers])
+    torch.cuda.synchronize()
+    for r, o, ps in zip(ref, outs, peers):
+        assert torch.equal(o, r)
+        for p in ps:
+            assert torch.equal(p, r)
+
+
+def test_sharded_fused_collective_world1():
+    """Symmetric-memory gather buffer + fused peer stores through the sharder (world 1)."""
+    import os
+    import torch.distributed as dist
+    from paper_2512_04632_b200.parallel import orthogonalize_sharded
+    if dist.is_initialized():
+        pytest.skip("process group already initialised")
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ["MASTER_PORT"] = "29537"
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        shapes = [(1024, 1024)] * 2 + [(4096, 1024), (1024, 4096)]
+        xs = [torch.from_numpy(I.gaussian(m, n, seed=140 + i)).to(torch.bfloat16).cuda()
+              for i, (m, n) in enumerate(shapes)]
+        outs = orthogonalize_sharded(xs, iters=4, collective="fused")
+        torch.cuda.synchronize()
+        for x, o in zip(xs, outs):
+            t = x.clone()
+            ns.orthogonalize(t, iters=4)
+            assert torch.equal(o, t)
+    finally:
+        dist.destroy_process_group()
