@@ -304,3 +304,27 @@ def test_sharded_fused_collective_world1():
             assert torch.equal(o, t)
     finally:
         dist.destroy_process_group()
+
+
+def test_cuda_graph_capture_replay():
+    """After the first (plan-building) call, a call only enqueues kernel launches: it can be
+    captured in a CUDA graph and replayed, with bitwise-identical results."""
+    shapes = [(768, 768), (3072, 768), (768, 3072)]
+    xs = [torch.from_numpy(I.gaussian(m, n, seed=150 + i)).to(torch.bfloat16).cuda() for i, (m, n) in enumerate(shapes)]
+    outs = [torch.empty_like(x) for x in xs]
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        ns.orthogonalize_list(xs, out=outs, iters=4)  # builds the plan (not capturable)
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    ref = [o.clone() for o in outs]
+    for o in outs:
+        o.zero_()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        ns.orthogonalize_list(xs, out=outs, iters=4)
+    g.replay()
+    torch.cuda.synchronize()
+    for r, o in zip(ref, outs):
+        assert torch.equal(r, o)
