@@ -348,6 +348,7 @@ static ns_status build_plan(Plan& P, HostTables& H, DevCtx* dc, const float* coe
             J.out = Bm(mt); J.aux = Am(mt); J.ld = mt.N;
             J.s = scaled ? Sv(mt) : nullptr;
             J.b = b; J.c = c;
+            J.diag_add = a;  // B' = bA + cA^2 + aI: Eq. 5 becomes the single product X B'
           } else {
             if (!mt.wide) {
               ta = cur_tm(mt, k); tb = mt.tm_b; J.a_mn = 0; J.b_mn = 0;
@@ -357,12 +358,12 @@ static ns_status build_plan(Plan& P, HostTables& H, DevCtx* dc, const float* coe
               J.P = (int)mt.N; J.Q = (int)mt.M; J.s_by_row = 1;
             }
             J.sym = 0; J.K = (int)mt.N;
-            J.out = cur_ptr(mt, k + 1); J.aux = cur_ptr(mt, k); J.ld = mt.n;
+            J.out = cur_ptr(mt, k + 1); J.aux = nullptr; J.ld = mt.n;
             tout = ((T - k) % 2 == 0) ? mt.tm_out : mt.tm_w;
-            taux = cur_tm(mt, k);
             if (k == T && !mt.peer.empty()) J.npeer = (int)mt.peer.size();
-            J.s = scaled ? Sv(mt) : nullptr;
-            J.a = a;
+            // a_k and diag(s) are folded into B' by the POLY epilogue: no aux, plain store
+            J.s = nullptr;
+            J.a = 0.f;
           }
           J.tiles_q = J.sym ? (J.P + kSymBlock - 1) / kSymBlock : (J.Q + kBN - 1) / kBN;
           jobs.push_back(J);

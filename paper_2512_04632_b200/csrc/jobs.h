@@ -56,6 +56,9 @@ struct GemmJob {
   // 32x32-box CUtensorMaps.
   const void* tmPeer;
   int32_t npeer;
+  // POLY: added to diagonal elements before the column scaling, B' = bA + cA^2 + dI.  With
+  // d = a_k the next XB needs no a*X term: X(aI + B) = aX + XB (Eq. 5 as one product).
+  float diag_add;
 };
 
 // CUDA-core (SIMT) variant of a GemmJob: operands by pointer + strides (elements),

@@ -116,6 +116,7 @@ struct Epi {
   int part_ld;
   const uint8_t* tmPeer;
   int npeer;
+  float diag_add;
 };
 __device__ __forceinline__ Epi load_epi(const GemmJob* __restrict__ J) {
   Epi e;
@@ -128,6 +129,7 @@ __device__ __forceinline__ Epi load_epi(const GemmJob* __restrict__ J) {
   e.a = J->a; e.b = J->b; e.c = J->c;
   e.part = J->part; e.part_ld = J->part_ld;
   e.tmPeer = reinterpret_cast<const uint8_t*>(J->tmPeer); e.npeer = J->npeer;
+  e.diag_add = J->diag_add;
   return e;
 }
 
@@ -151,7 +153,11 @@ enum EpiVariant : int { V_GRAM = 0, V_POLY = 1, V_POLY_S = 2, V_XB = 3, V_XB_SRO
 __device__ __forceinline__ int epi_variant(const Epi& E) {
   if (E.mode == MODE_GRAM) return V_GRAM;
   if (E.mode == MODE_POLY) return E.s ? V_POLY_S : V_POLY;
+  if (E.s == nullptr && E.a == 0.f) return V_GRAM;  // a folded into B: plain store of X B'^T
   return E.s ? (E.s_by_row ? V_XB_SROW : V_XB_SCOL) : V_XB;
+}
+__device__ __forceinline__ bool epi_needs_aux(const Epi& E) {
+  return E.mode == MODE_POLY || (E.mode == MODE_XB && (E.s != nullptr || E.a != 0.f));
 }
 __device__ __forceinline__ float lo_bf(uint32_t w) { return __uint_as_float(w << 16); }
 __device__ __forceinline__ float hi_bf(uint32_t w) { return __uint_as_float(w & 0xFFFF0000u); }
@@ -177,28 +183,36 @@ __device__ __forceinline__ void load_s32(const float* s, int q, float (&sv)[32])
 // Math of one 32-column chunk of one output row.  r = fp32 accumulator D[p][q..q+32),
 // x = aux row chunk (bf16 pairs).  o = bf16 pairs for out[p][q..], m = bf16 pairs for the
 // mirrored out[q..][p] (only V_POLY_S differs from o: destination-column scaling).
+// dg: warp-uniform, this chunk intersects the matrix diagonal and diag_add != 0.
 __device__ __forceinline__ void epi_math(int var, const Epi& E, int p, int q, const uint32_t (&r)[32],
                                          const uint32_t (&x)[16], uint32_t (&o)[16], uint32_t (&m)[16],
-                                         bool& bad) {
+                                         bool dg, bool& bad) {
   switch (var) {
     case V_GRAM:
 #pragma unroll
       for (int i = 0; i < 16; ++i) o[i] = pack_bf2(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1]));
       break;
-    case V_POLY:
+    case V_POLY: {
+      const int d = p - q;  // this lane's diagonal element sits at column index d (if 0..31)
 #pragma unroll
-      for (int i = 0; i < 16; ++i)
-        o[i] = pack_bf2(fmaf(E.c, __uint_as_float(r[2 * i]), E.b * lo_bf(x[i])),
-                        fmaf(E.c, __uint_as_float(r[2 * i + 1]), E.b * hi_bf(x[i])));
+      for (int i = 0; i < 16; ++i) {
+        float w0 = fmaf(E.c, __uint_as_float(r[2 * i]), E.b * lo_bf(x[i]));
+        float w1 = fmaf(E.c, __uint_as_float(r[2 * i + 1]), E.b * hi_bf(x[i]));
+        if (dg) { w0 += (d == 2 * i) ? E.diag_add : 0.f; w1 += (d == 2 * i + 1) ? E.diag_add : 0.f; }
+        o[i] = pack_bf2(w0, w1);
+      }
       break;
+    }
     case V_POLY_S: {
       float sv[32];
       load_s32(E.s, q, sv);
       const float sp = __ldg(E.s + p);
+      const int d = p - q;
 #pragma unroll
       for (int i = 0; i < 16; ++i) {
-        const float w0 = fmaf(E.c, __uint_as_float(r[2 * i]), E.b * lo_bf(x[i]));
-        const float w1 = fmaf(E.c, __uint_as_float(r[2 * i + 1]), E.b * hi_bf(x[i]));
+        float w0 = fmaf(E.c, __uint_as_float(r[2 * i]), E.b * lo_bf(x[i]));
+        float w1 = fmaf(E.c, __uint_as_float(r[2 * i + 1]), E.b * hi_bf(x[i]));
+        if (dg) { w0 += (d == 2 * i) ? E.diag_add : 0.f; w1 += (d == 2 * i + 1) ? E.diag_add : 0.f; }
         o[i] = pack_bf2(w0 * sv[2 * i], w1 * sv[2 * i + 1]);
         m[i] = pack_bf2(w0 * sp, w1 * sp);
       }
@@ -412,7 +426,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const TileInfo ti = decode_tile(tiles, t);
       const Epi E = load_epi(jobs + ti.job);
       const int var = epi_variant(E);
-      const bool has_aux = (E.mode != MODE_GRAM) && !(dbg & 4);
+      const bool has_aux = epi_needs_aux(E) && !(dbg & 4);
       const int prow = ti.p0 + (int)rank * kBM + quad * 32;  // first of this warp's 32 rows
       const int p = prow + lane;
       const int qh = ti.q0 + half * 128;
@@ -469,7 +483,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (dbg & 1) continue;
         const bool mir = ti.mirror && !(dbg & 2);
         uint32_t o[16], m[16];
-        epi_math(var, E, p, q, r, x, o, m, bad);
+        // chunk rows [prow, prow+32) x cols [q, q+32) contain diagonal elements iff they overlap
+        const bool dg = (E.diag_add != 0.f) && !ti.mirror && (q < prow + 32) && (prow < q + 32);
+        epi_math(var, E, p, q, r, x, o, m, dg, bad);
         if (E.part != nullptr) {  // AOL row sums of |A0| over this warp's 128 columns (Eq. 8)
 #pragma unroll
           for (int i = 0; i < 16; ++i) rsum += fabsf(lo_bf(o[i])) + fabsf(hi_bf(o[i]));
