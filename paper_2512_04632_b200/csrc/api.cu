@@ -854,6 +854,64 @@ ns_status ns_orthogonalize_peers(void* const* X, void* const* out, void* const* 
   return run(mats, iters, coeffs, precond, dtype, reinterpret_cast<cudaStream_t>(stream));
 }
 
+// Muon step: cached device job tables, keyed by the pointer lists.
+static std::map<std::vector<uint64_t>, void*> g_muon_tabs;
+
+ns_status ns_muon_step(void* const* W, const void* const* G, float* const* M, void* const* U,
+                       const int64_t* m, const int64_t* n, int64_t count, ns_dtype w_dtype, ns_dtype g_dtype,
+                       float lr, float beta, float weight_decay, int nesterov, int iters, const float* coeffs,
+                       ns_precond precond, void* stream) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  ns_status st = validate_common(count, iters, coeffs, precond, NS_BF16);
+  if (st != NS_OK) return st;
+  if (!W || !G || !M || !U || !m || !n) return fail(NS_ERR_INVALID_VALUE, "NULL array argument");
+  if ((w_dtype != NS_BF16 && w_dtype != NS_FP32) || (g_dtype != NS_BF16 && g_dtype != NS_FP32))
+    return fail(NS_ERR_INVALID_VALUE, "bad dtype");
+  if (!std::isfinite(lr) || !std::isfinite(beta) || !std::isfinite(weight_decay) || beta < 0.f || beta >= 1.f)
+    return fail(NS_ERR_INVALID_VALUE, "lr / beta / weight_decay out of range");
+  std::vector<Mat> mats;
+  std::vector<MuonJob> jobs;
+  std::vector<uint64_t> key;
+  int64_t max_numel = 0;
+  for (int64_t i = 0; i < count; ++i) {
+    if ((st = validate_mat(U[i], m[i], n[i], NS_BF16)) != NS_OK) return st;
+    if ((st = validate_mat(W[i], m[i], n[i], w_dtype)) != NS_OK) return st;
+    if ((st = validate_mat(G[i], m[i], n[i], g_dtype)) != NS_OK) return st;
+    if ((st = validate_mat(M[i], m[i], n[i], NS_FP32)) != NS_OK) return st;
+    mats.push_back(make_mat(U[i], U[i], m[i], n[i], iters));
+    MuonJob J;
+    J.M = M[i]; J.G = G[i]; J.U = U[i]; J.W = W[i];
+    J.numel = m[i] * n[i];
+    J.scale = (float)std::sqrt(std::max(1.0, (double)m[i] / (double)n[i]));
+    jobs.push_back(J);
+    max_numel = std::max(max_numel, J.numel);
+    for (const void* p : {(const void*)W[i], G[i], (const void*)M[i], (const void*)U[i]})
+      key.push_back(reinterpret_cast<uint64_t>(p));
+    key.push_back((uint64_t)m[i]); key.push_back((uint64_t)n[i]);
+  }
+  if (count > 65535) return fail(NS_ERR_NOT_SUPPORTED, "more than 65535 matrices in one Muon step");
+  DevCtx* dc = nullptr;
+  if ((st = dev_ctx(&dc)) != NS_OK) return st;
+  auto it = g_muon_tabs.find(key);
+  void* dtab = nullptr;
+  if (it == g_muon_tabs.end()) {
+    CU_TRY(cudaMalloc(&dtab, jobs.size() * sizeof(MuonJob)));
+    CU_TRY(cudaMemcpy(dtab, jobs.data(), jobs.size() * sizeof(MuonJob), cudaMemcpyHostToDevice));
+    g_muon_tabs[key] = dtab;
+  } else {
+    dtab = it->second;
+  }
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  CU_TRY(launch_muon_momentum(reinterpret_cast<const MuonJob*>(dtab), (int)count, max_numel, g_dtype == NS_BF16,
+                              beta, nesterov, dc->sms, s));
+  ++g_launches;
+  if ((st = run(mats, iters, coeffs, precond, NS_BF16, s)) != NS_OK) return st;
+  CU_TRY(launch_muon_apply(reinterpret_cast<const MuonJob*>(dtab), (int)count, max_numel, w_dtype == NS_BF16, lr,
+                           weight_decay, dc->sms, s));
+  ++g_launches;
+  return NS_OK;
+}
+
 ns_status ns_workspace_size(const int64_t* m, const int64_t* n, int64_t count, ns_dtype dtype, size_t* bytes) {
   if (!m || !n || !bytes || count < 1) return fail(NS_ERR_INVALID_VALUE, "bad arguments");
   if (dtype != NS_BF16 && dtype != NS_FP32) return fail(NS_ERR_INVALID_VALUE, "bad dtype");
@@ -885,6 +943,8 @@ void ns_shutdown(void) {
   std::lock_guard<std::mutex> lk(g_mu);
   cudaDeviceSynchronize();
   g_plans.clear();
+  for (auto& kv : g_muon_tabs) cudaFree(kv.second);
+  g_muon_tabs.clear();
   for (auto& d : g_dev) {
     if (d.init && d.flags) cudaFree(d.flags);
     d = DevCtx();

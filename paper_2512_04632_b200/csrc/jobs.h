@@ -94,6 +94,16 @@ struct PrecondJob {
   int64_t vec_start;  // prefix over jobs of ceil(N*N / 8) (rescale: 16-byte vectors)
 };
 
+// One matrix of a Muon optimizer step (muon.cu).
+struct MuonJob {
+  float* M;        // momentum, fp32, numel
+  const void* G;   // gradient (fp32 or bf16)
+  void* U;         // bf16 staging: NS input, orthogonalised in place
+  void* W;         // weight (fp32 or bf16)
+  int64_t numel;
+  float scale;     // max(1, m/n)^(1/2)
+};
+
 // One step of a launch.  A per-step launch carries one GEMM phase; the fused single-launch
 // mode (small problems) carries all 3T+1 steps, separated by device-side phase barriers.
 enum PhaseKindDev : int32_t { PHK_GEMM = 0, PHK_PRE_S = 1, PHK_PRE_SCALE = 2 };

@@ -32,4 +32,10 @@ cudaError_t launch_precondition(const PrecondJob* d_jobs, int njobs, int64_t tot
                                 int64_t total_elems_or_vecs, bool vec8, bool is_bf16,
                                 unsigned* d_barrier, uint32_t* d_flags, cudaStream_t stream);
 
+// Muon step around the path (muon.cu): momentum + nesterov -> bf16 U; W update from U.
+cudaError_t launch_muon_momentum(const MuonJob* d_jobs, int count, int64_t max_numel, bool g_bf16, float beta,
+                                 int nesterov, int sms, cudaStream_t stream);
+cudaError_t launch_muon_apply(const MuonJob* d_jobs, int count, int64_t max_numel, bool w_bf16, float lr, float wd,
+                              int sms, cudaStream_t stream);
+
 }  // namespace tns
