@@ -14,6 +14,7 @@
 #include <algorithm>
 #include <array>
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <map>
@@ -230,7 +231,19 @@ struct HostTables {
   }
 };
 
+// Measurement knob (A/B of the half-storage symmetric matrices): TNS_NOHALF=1 stores A
+// and B' whole (mirrored) and reads them K-major only.
+static bool half_storage_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("TNS_NOHALF");
+    v = (e && atoi(e)) ? 0 : 1;
+  }
+  return v == 1;
+}
+
 static ns_status build_plan(Plan& P, HostTables& H, DevCtx* dc, const float* coeffs) {
+  const int hs = half_storage_enabled() ? 1 : 0;
   const int T = P.iters;
   const size_t es = elem_size(P.dtype);
   const bool bf16 = P.dtype == NS_BF16;
@@ -339,6 +352,7 @@ static ns_status build_plan(Plan& P, HostTables& H, DevCtx* dc, const float* coe
             J.a_mn = J.b_mn = mt.wide ? 0 : 1;
             J.sym = 1; J.P = J.Q = (int)mt.N; J.K = (int)mt.M;
             J.out = Am(mt); J.aux = nullptr; J.ld = mt.N;
+            J.half = hs;  // A: lower-triangle blocks only (readers take the upper transposed)
             if (k == 1 && use_part) { J.part = Part(mt); J.part_ld = mt.part_ld; }
           } else if (mode == MODE_POLY) {
             ta = tb = mt.tm_a;
@@ -349,13 +363,17 @@ static ns_status build_plan(Plan& P, HostTables& H, DevCtx* dc, const float* coe
             J.s = scaled ? Sv(mt) : nullptr;
             J.b = b; J.c = c;
             J.diag_add = a;  // B' = bA + cA^2 + aI: Eq. 5 becomes the single product X B'
+            J.a_sym = J.b_sym = hs;       // A is half-stored
+            J.half = scaled ? 0 : hs;     // B1' = sym * diag(s) is not symmetric: store it whole
           } else {
             if (!mt.wide) {
               ta = cur_tm(mt, k); tb = mt.tm_b; J.a_mn = 0; J.b_mn = 0;
               J.P = (int)mt.M; J.Q = (int)mt.N; J.s_by_row = 0;
+              J.b_sym = scaled ? 0 : hs;  // B' half-stored except the scaled iteration 1
             } else {
               ta = mt.tm_b; tb = cur_tm(mt, k); J.a_mn = 0; J.b_mn = 1;
               J.P = (int)mt.N; J.Q = (int)mt.M; J.s_by_row = 1;
+              J.a_sym = scaled ? 0 : hs;
             }
             J.sym = 0; J.K = (int)mt.N;
             J.out = cur_ptr(mt, k + 1); J.aux = nullptr; J.ld = mt.n;
@@ -434,6 +452,7 @@ static ns_status build_plan(Plan& P, HostTables& H, DevCtx* dc, const float* coe
           std::memset(&J, 0, sizeof(J));
           J.A = Am(mt); J.s = Sv(mt); J.N = (int)mt.N; J.precond = (int)P.precond;
           if (use_part) { J.part = Part(mt); J.part_ld = mt.part_ld; }
+          J.half = P.simt ? 0 : hs;
           J.row_start = rows; J.vec_start = items;
           rows += mt.N;
           items += vec8 ? (mt.N * mt.N) / 8 : mt.N * mt.N;

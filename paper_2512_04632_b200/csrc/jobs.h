@@ -56,6 +56,11 @@ struct GemmJob {
   // 32x32-box CUtensorMaps.
   const void* tmPeer;
   int32_t npeer;
+  // Half-storage symmetric matrices: a_sym / b_sym = the operand is symmetric and stored
+  // as its lower-triangle 256-blocks only (diagonal blocks whole); k-blocks in the upper
+  // triangle are read transposed from the mirrored block (TMA coordinates swapped, UMMA
+  // major bit flipped).  half = sym job stores only its lower-triangle tiles (no mirror).
+  int32_t a_sym, b_sym, half;
   // POLY: added to diagonal elements before the column scaling, B' = bA + cA^2 + dI.  With
   // d = a_k the next XB needs no a*X term: X(aI + B) = aX + XB (Eq. 5 as one product).
   float diag_add;
@@ -88,6 +93,7 @@ struct PrecondJob {
   float* s;         // N
   const float* part;  // row-sum partials from the Gram epilogue (GemmJob::part) or nullptr
   int32_t part_ld;
+  int32_t half;       // A stored as lower-triangle 256-blocks: rescale only those
   int32_t N;
   int32_t precond;  // 1 Frobenius, 2 AOL
   int64_t row_start;  // prefix over jobs of N (AOL: one warp per row)

@@ -92,9 +92,10 @@ __device__ __forceinline__ void precond_row_s(const PrecondJob& J, int i, int la
 // Phase 2 for row i: A1[i][:] = s_i A0[i][:] s_:  (Alg. 2 l.4), 16-byte vectors along the row.
 template <typename T, bool VEC8>
 __device__ __forceinline__ void precond_row_scale(const PrecondJob& J, int i, int lane) {
-  const int N = J.N;
+  // half storage: row i holds blocks 0..bi only (the rest is never read)
+  const int N = J.half ? min(J.N, (i / 256 + 1) * 256) : J.N;
   const float si = J.s[i];
-  T* Ai = reinterpret_cast<T*>(J.A) + (int64_t)i * N;
+  T* Ai = reinterpret_cast<T*>(J.A) + (int64_t)i * J.N;
   if (VEC8 && sizeof(T) == 2) {
     for (int j = lane * 8; j < N; j += 256) {
       uint4* pv = reinterpret_cast<uint4*>(Ai + j);

@@ -117,6 +117,7 @@ struct Epi {
   const uint8_t* tmPeer;
   int npeer;
   float diag_add;
+  int half;
 };
 __device__ __forceinline__ Epi load_epi(const GemmJob* __restrict__ J) {
   Epi e;
@@ -130,6 +131,7 @@ __device__ __forceinline__ Epi load_epi(const GemmJob* __restrict__ J) {
   e.part = J->part; e.part_ld = J->part_ld;
   e.tmPeer = reinterpret_cast<const uint8_t*>(J->tmPeer); e.npeer = J->npeer;
   e.diag_add = J->diag_add;
+  e.half = J->half;
   return e;
 }
 
@@ -311,6 +313,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const void* tmA = J->tmA;
         const void* tmB = J->tmB;
         const int a_mn = J->a_mn, b_mn = J->b_mn, K = J->K;
+        const int a_sym = J->a_sym, b_sym = J->b_sym;
         if (ti.job != last_job) {
           tma_desc_acquire(tmA);
           tma_desc_acquire(tmB);
@@ -325,15 +328,18 @@ __global__ void __launch_bounds__(kThreads, 1)
           uint8_t* sb = sa + G::kABytes;
           if (rank == 0) mbar_arrive_expect_tx(&full_bar[stage], G::kStageBytes * CG);
           const int k0 = kb * kBK;
+          // half-storage symmetric operand: an upper-triangle block is read transposed
+          const int a_e = a_mn ^ (a_sym && (k0 >> 8) > (pa >> 8));
+          const int b_e = b_mn ^ (b_sym && (k0 >> 8) > (qb >> 8));
 #pragma unroll
           for (int i = 0; i < G::kARows / 64; ++i) {
-            const int c0 = a_mn ? pa + 64 * i : k0, c1 = a_mn ? k0 : pa + 64 * i;
+            const int c0 = a_e ? pa + 64 * i : k0, c1 = a_e ? k0 : pa + 64 * i;
             if constexpr (CG == 2) tma_load_2d_cg2(sa + i * kBoxBytes, tmA, &full_bar[stage], c0, c1);
             else tma_load_2d(sa + i * kBoxBytes, tmA, &full_bar[stage], c0, c1);
           }
 #pragma unroll
           for (int i = 0; i < G::kBRows / 64; ++i) {
-            const int c0 = b_mn ? qb + 64 * i : k0, c1 = b_mn ? k0 : qb + 64 * i;
+            const int c0 = b_e ? qb + 64 * i : k0, c1 = b_e ? k0 : qb + 64 * i;
             if constexpr (CG == 2) tma_load_2d_cg2(sb + i * kBoxBytes, tmB, &full_bar[stage], c0, c1);
             else tma_load_2d(sb + i * kBoxBytes, tmB, &full_bar[stage], c0, c1);
           }
@@ -360,9 +366,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         const GemmJob* J = jobs + ti.job;
         const uint32_t a_mn = (uint32_t)J->a_mn, b_mn = (uint32_t)J->b_mn;
         const int K = J->K;
-        const uint32_t idesc = make_idesc_bf16(kBM * CG, kBN, a_mn, b_mn);
-        const uint32_t a_lbo = a_mn ? 8192u : 16u, a_step = a_mn ? 2048u : 32u;
-        const uint32_t b_lbo = b_mn ? 8192u : 16u, b_step = b_mn ? 2048u : 32u;
+        const int a_sym = J->a_sym, b_sym = J->b_sym;
+        const int pblk = ti.p0 >> 8, qblk = ti.q0 >> 8;  // both CTAs' rows share the block
         mbar_wait(&tempty_bar[as], aphase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + as * kBN;
@@ -372,6 +377,12 @@ __global__ void __launch_bounds__(kThreads, 1)
           tc_fence_after();
           const uint32_t sa = smem_u32(smem + (size_t)stage * G::kStageBytes);
           const uint32_t sb = sa + G::kABytes;
+          const int kblk = (kb * kBK) >> 8;
+          const uint32_t a_e = a_mn ^ (uint32_t)(a_sym && kblk > pblk);
+          const uint32_t b_e = b_mn ^ (uint32_t)(b_sym && kblk > qblk);
+          const uint32_t idesc = make_idesc_bf16(kBM * CG, kBN, a_e, b_e);
+          const uint32_t a_lbo = a_e ? 8192u : 16u, a_step = a_e ? 2048u : 32u;
+          const uint32_t b_lbo = b_e ? 8192u : 16u, b_step = b_e ? 2048u : 32u;
 #pragma unroll
           for (int kk = 0; kk < kBK / 16; ++kk) {
             const uint64_t adesc = make_sdesc(sa + kk * a_step, a_lbo, 1024u);
@@ -481,7 +492,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
         if (dbg & 1) continue;
-        const bool mir = ti.mirror && !(dbg & 2);
+        // mirrored block: transposed box in smem for the mirrored store (full storage) and/or
+        // the AOL column sums (iteration-1 Gram); half storage skips the store
+        const bool mir_store = ti.mirror && !E.half && !(dbg & 2);
+        const bool mir = mir_store || (ti.mirror && E.part != nullptr);
         uint32_t o[16], m[16];
         // chunk rows [prow, prow+32) x cols [q, q+32) contain diagonal elements iff they overlap
         const bool dg = (E.diag_add != 0.f) && !ti.mirror && (q < prow + 32) && (prow < q + 32);
@@ -514,7 +528,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         __syncwarp();
         if (lane == 0) {
           tma_store_2d(E.tmOut, s_out, q, prow);          // rows prow.., cols q..
-          if (mir) tma_store_2d(E.tmOut, s_mir, prow, q);  // rows q.., cols prow..
+          if (mir_store) tma_store_2d(E.tmOut, s_mir, prow, q);  // rows q.., cols prow..
           // fused all-gather: the same box to every peer's buffer (NVLink), tile by tile
           for (int r = 0; r < E.npeer; ++r) tma_store_2d(E.tmPeer + 128 * r, s_out, q, prow);
           bulk_commit();
