@@ -156,10 +156,12 @@ struct Phase {
   int64_t total_rows;
   bool vec8;
   int gemm_kind;  // profiling kind: 0 GRAM, 2 POLY, 3 XB
-  size_t tiles_off = 0;   // offset of the packed tile list (PH_GEMM / PH_FUSED)
-  size_t phdesc_off = 0;  // offset of the PhaseDesc array (PH_GEMM / PH_FUSED)
+  size_t tiles_off = 0;   // offset of the TaskDesc list (PH_GEMM / PH_FUSED)
   size_t jobs_off = 0;    // offset of the GemmJob array (PH_FUSED)
-  int nphases = 1;        // PH_FUSED: number of steps
+  size_t pjobs_off = 0;   // offset of the PrecondJob array (PH_FUSED)
+  bool has_pjobs = false;
+  size_t done_off = 0;    // offset of the dependency counters (PH_FUSED)
+  int nslots = 0;         // PH_FUSED: dependency counters
   int64_t max_tiles = 0;  // largest GEMM step
   // copies (PH_COPY)
   std::vector<std::pair<std::pair<void*, const void*>, size_t>> copies;
@@ -303,8 +305,6 @@ static ns_status build_plan(Plan& P, HostTables& H, DevCtx* dc, const float* coe
   // table size by building jobs with placeholder bases, then fix them up.
   struct Fix { size_t job_off; int ta, tb, tout, taux, tpeer = -1; };
   std::vector<Fix> fixes;
-  struct PFix { size_t pd_off, pj_off; };  // PhaseDesc::pjobs pointers (fused mode)
-  std::vector<PFix> pfixes;
   struct Step {  // one tcgen05-path step before it is laid out as launches
     int kind = PHK_GEMM;
     int gemm_kind = 0;
@@ -481,50 +481,39 @@ static ns_status build_plan(Plan& P, HostTables& H, DevCtx* dc, const float* coe
 
   // -- tcgen05 steps: one launch each (PDL-chained), or all in one fused launch
   if (!P.simt && !steps.empty()) {
-    const int64_t workers = dc->sms / P.cg;
+    const int nm = (int)P.mats.size();
     int64_t max_tiles = 0;
-    std::vector<std::vector<uint64_t>> tls(steps.size());
-    size_t job_base = 0;
-    for (size_t si = 0; si < steps.size(); ++si) {
-      Step& st = steps[si];
-      if (st.kind != PHK_GEMM) continue;
+    auto tile_list = [&](const Step& st, size_t job_base) {
       // longest-K jobs first (LPT-like): long tiles do not end up in the last wave
       std::vector<size_t> order(st.jobs.size());
       for (size_t j = 0; j < st.jobs.size(); ++j) order[j] = j;
-      std::stable_sort(order.begin(), order.end(),
-                       [&](size_t x, size_t y) { return st.jobs[x].K > st.jobs[y].K; });
-      for (size_t j : order) umma_tile_list(st.jobs[j], (uint32_t)(job_base + j), P.cg, tls[si]);
-      max_tiles = std::max(max_tiles, (int64_t)tls[si].size());
-      st.job_base = job_base;
-      job_base += st.jobs.size();
-    }
-    // The fused single launch is opt-in (path 3): measured slower than PDL-chained per-step
-    // launches even on the latency-bound CIFAR set (178 vs 166 us), because its grid-wide
-    // step barriers serialise what PDL overlaps (profiles/README.md).
+      std::stable_sort(order.begin(), order.end(), [&](size_t x, size_t y) { return st.jobs[x].K > st.jobs[y].K; });
+      std::vector<uint64_t> tl;
+      for (size_t j : order) umma_tile_list(st.jobs[j], (uint32_t)(job_base + j), P.cg, tl);
+      return tl;
+    };
+    auto mk_task = [](uint64_t w) {
+      TaskDesc td;
+      std::memset(&td, 0, sizeof(td));
+      td.tile = w; td.kind = TK_TILE; td.dep_slot = kNoSlot; td.my_slot = kNoSlot;
+      return td;
+    };
+    // The fused single launch is opt-in (path 3): measured against PDL-chained per-step
+    // launches in profiles/README.md.
     P.fused = (g_path == 3);
-    (void)workers;
     if (!P.fused) {
-      for (size_t si = 0; si < steps.size(); ++si) {
-        Step& st = steps[si];
+      for (Step& st : steps) {
         if (st.kind == PHK_GEMM) {
-          // per-step launch: job indices are local to the step
-          std::vector<uint64_t> tl;
-          std::vector<size_t> order(st.jobs.size());
-          for (size_t j = 0; j < st.jobs.size(); ++j) order[j] = j;
-          std::stable_sort(order.begin(), order.end(),
-                           [&](size_t x, size_t y) { return st.jobs[x].K > st.jobs[y].K; });
-          for (size_t j : order) umma_tile_list(st.jobs[j], (uint32_t)j, P.cg, tl);
+          std::vector<uint64_t> tl = tile_list(st, 0);
+          std::vector<TaskDesc> tasks;
+          for (uint64_t w : tl) tasks.push_back(mk_task(w));
           Phase ph{PH_GEMM};
           ph.gemm_kind = st.gemm_kind;
           ph.dev_off = H.push(st.jobs.data(), st.jobs.size() * sizeof(GemmJob), 64);
           ph.njobs = (int)st.jobs.size();
-          ph.tiles_off = H.push(tl.data(), tl.size() * sizeof(uint64_t), 64);
-          ph.total = (int64_t)tl.size();
+          ph.tiles_off = H.push(tasks.data(), tasks.size() * sizeof(TaskDesc), 64);
+          ph.total = (int64_t)tasks.size();
           ph.max_tiles = ph.total;
-          PhaseDesc pd;
-          std::memset(&pd, 0, sizeof(pd));
-          pd.kind = PHK_GEMM; pd.tile_begin = 0; pd.tile_end = ph.total;
-          ph.phdesc_off = H.push(&pd, sizeof(pd), 64);
           for (size_t j = 0; j < st.jobs.size(); ++j)
             fixes.push_back({ph.dev_off + j * sizeof(GemmJob), st.tmi[j][0], st.tmi[j][1], st.tmi[j][2], st.tmi[j][3],
                              st.tmi[j][4]});
@@ -540,36 +529,52 @@ static ns_status build_plan(Plan& P, HostTables& H, DevCtx* dc, const float* coe
         }
       }
     } else {
-      // fused: all jobs in one array (global job indices), one tile list, one PhaseDesc
-      // per step; the preconditioner becomes two steps (row sums -> s, rescale A)
+      // fused: expand the preconditioner into its two row steps; slot (step, matrix)
+      // counts the epilogue-warp arrivals of that step's tasks for that matrix
+      const uint32_t per_task = (uint32_t)(8 * P.cg);  // kNumEpiWarps * CTAs per task
       std::vector<GemmJob> alljobs;
       std::vector<std::array<int, 5>> alltmi;
-      std::vector<uint64_t> alltiles;
-      std::vector<PhaseDesc> pds;
-      size_t pj_off = 0;
-      int npj = 0;
-      int64_t prow = 0;
-      for (size_t si = 0; si < steps.size(); ++si) {
-        Step& st = steps[si];
-        PhaseDesc pd;
-        std::memset(&pd, 0, sizeof(pd));
-        if (st.kind == PHK_GEMM) {
-          alljobs.insert(alljobs.end(), st.jobs.begin(), st.jobs.end());
-          alltmi.insert(alltmi.end(), st.tmi.begin(), st.tmi.end());
-          pd.kind = PHK_GEMM;
-          pd.tile_begin = (int64_t)alltiles.size();
-          alltiles.insert(alltiles.end(), tls[si].begin(), tls[si].end());
-          pd.tile_end = (int64_t)alltiles.size();
-          pds.push_back(pd);
-        } else {
-          pj_off = H.push(st.pj.data(), st.pj.size() * sizeof(PrecondJob), 64);
-          npj = (int)st.pj.size();
-          prow = st.rows;
-          pd.npjobs = npj; pd.prow_total = prow;
-          pd.kind = PHK_PRE_S;
-          pds.push_back(pd);
-          pd.kind = PHK_PRE_SCALE;
-          pds.push_back(pd);
+      std::vector<TaskDesc> tasks;
+      std::vector<uint32_t> count;  // arrivals per slot
+      std::vector<PrecondJob> pjs;
+      int si = 0;  // expanded step index
+      for (Step& st : steps) {
+        const int nsub = (st.kind == PHK_GEMM) ? 1 : 2;
+        for (int sub = 0; sub < nsub; ++sub, ++si) {
+          count.resize((size_t)(si + 1) * nm, 0);
+          auto dep_of = [&](int j, TaskDesc& td) {
+            if (si == 0) return;
+            td.dep_slot = (uint32_t)((si - 1) * nm + j);
+            td.dep_target = count[(size_t)(si - 1) * nm + j];
+          };
+          if (st.kind == PHK_GEMM) {
+            const size_t base = alljobs.size();
+            alljobs.insert(alljobs.end(), st.jobs.begin(), st.jobs.end());
+            alltmi.insert(alltmi.end(), st.tmi.begin(), st.tmi.end());
+            std::vector<uint64_t> tl = tile_list(st, base);
+            for (uint64_t w : tl) {
+              TaskDesc td = mk_task(w);
+              const int j = (int)((w & 0xFFFFFu) - base);  // job index within the step = matrix
+              dep_of(j, td);
+              td.my_slot = (uint32_t)(si * nm + j);
+              count[(size_t)si * nm + j] += per_task;
+              tasks.push_back(td);
+            }
+            max_tiles = std::max(max_tiles, (int64_t)tl.size());
+          } else {
+            if (pjs.empty()) pjs = st.pj;
+            for (int j = 0; j < nm; ++j)
+              for (int r0 = 0; r0 < pjs[j].N; r0 += kPreRows) {
+                TaskDesc td = mk_task(0);
+                td.kind = sub == 0 ? TK_PRE_S : TK_PRE_SCALE;
+                td.pjob = (uint32_t)j;
+                td.row0 = (uint32_t)r0;
+                dep_of(j, td);
+                td.my_slot = (uint32_t)(si * nm + j);
+                count[(size_t)si * nm + j] += per_task;
+                tasks.push_back(td);
+              }
+          }
         }
       }
       Phase ph{PH_FUSED};
@@ -577,13 +582,14 @@ static ns_status build_plan(Plan& P, HostTables& H, DevCtx* dc, const float* coe
       for (size_t j = 0; j < alljobs.size(); ++j)
         fixes.push_back({ph.jobs_off + j * sizeof(GemmJob), alltmi[j][0], alltmi[j][1], alltmi[j][2], alltmi[j][3],
                          alltmi[j][4]});
-      ph.tiles_off = H.push(alltiles.data(), alltiles.size() * sizeof(uint64_t), 64);
-      ph.phdesc_off = H.push(pds.data(), pds.size() * sizeof(PhaseDesc), 64);
-      for (size_t i = 0; i < pds.size(); ++i)
-        if (pds[i].kind != PHK_GEMM) pfixes.push_back({ph.phdesc_off + i * sizeof(PhaseDesc), pj_off});
-      ph.nphases = (int)pds.size();
+      ph.tiles_off = H.push(tasks.data(), tasks.size() * sizeof(TaskDesc), 64);
+      ph.total = (int64_t)tasks.size();
+      ph.pjobs_off = pjs.empty() ? 0 : H.push(pjs.data(), pjs.size() * sizeof(PrecondJob), 64);
+      ph.has_pjobs = !pjs.empty();
+      ph.nslots = (int)count.size();
+      std::vector<unsigned> zeros(count.size() + 1, 0u);  // done counters (+1 exit counter)
+      ph.done_off = H.push(zeros.data(), zeros.size() * sizeof(unsigned), 64);
       ph.max_tiles = max_tiles;
-      if (ph.nphases + 1 > (1024 - 64) / 4) return fail(NS_ERR_NOT_SUPPORTED, "too many steps for the fused mode");
       P.phases.push_back(ph);
     }
   }
@@ -605,10 +611,6 @@ static ns_status build_plan(Plan& P, HostTables& H, DevCtx* dc, const float* coe
       J->tmAux = f.taux >= 0 ? dbase + tm_off + (size_t)(f.taux + 1) * sizeof(CUtensorMap) : nullptr;
       J->tmPeer = f.tpeer >= 0 ? dbase + tm_off + (size_t)f.tpeer * sizeof(CUtensorMap) : nullptr;
     }
-    for (const PFix& f : pfixes) {
-      PhaseDesc* pd = reinterpret_cast<PhaseDesc*>(H.bytes.data() + f.pd_off);
-      pd->pjobs = reinterpret_cast<const PrecondJob*>(dbase + f.pj_off);
-    }
     CU_TRY(cudaMemcpy(P.dtab, H.bytes.data(), H.bytes.size(), cudaMemcpyHostToDevice));
   }
   (void)dc;
@@ -628,19 +630,18 @@ static ns_status enqueue_plan(Plan& P, DevCtx* dc, cudaStream_t stream) {
       case PH_GEMM: {
         ProfScope ps(ph.gemm_kind, stream);
         CU_TRY(launch_umma_gemm(reinterpret_cast<const GemmJob*>(dbase + ph.dev_off),
-                                reinterpret_cast<const uint64_t*>(dbase + ph.tiles_off),
-                                reinterpret_cast<const PhaseDesc*>(dbase + ph.phdesc_off), 1, nullptr,
-                                ph.max_tiles, P.cg, dc->sms, dc->flags, stream));
+                                reinterpret_cast<const TaskDesc*>(dbase + ph.tiles_off), ph.total, nullptr, nullptr,
+                                0, ph.max_tiles, P.cg, dc->sms, dc->flags, stream));
         ++g_launches;
         break;
       }
       case PH_FUSED: {
         ProfScope ps(6, stream);
         CU_TRY(launch_umma_gemm(reinterpret_cast<const GemmJob*>(dbase + ph.jobs_off),
-                                reinterpret_cast<const uint64_t*>(dbase + ph.tiles_off),
-                                reinterpret_cast<const PhaseDesc*>(dbase + ph.phdesc_off), ph.nphases,
-                                reinterpret_cast<unsigned*>(reinterpret_cast<uint8_t*>(P.ws) + 64),
-                                ph.max_tiles, P.cg, dc->sms, dc->flags, stream));
+                                reinterpret_cast<const TaskDesc*>(dbase + ph.tiles_off), ph.total,
+                                ph.has_pjobs ? reinterpret_cast<const PrecondJob*>(dbase + ph.pjobs_off) : nullptr,
+                                reinterpret_cast<unsigned*>(dbase + ph.done_off), ph.nslots, ph.max_tiles, P.cg,
+                                dc->sms, dc->flags, stream));
         ++g_launches;
         break;
       }
@@ -997,8 +998,13 @@ static ns_status one_gemm(GemmJob J, TDesc ta, TDesc tb, TDesc tout, TDesc taux,
     const int cg = g_path == 2 ? 1 : 2;
     std::vector<uint64_t> tl;
     umma_tile_list(J, 0, cg, tl);
+    std::vector<TaskDesc> tasks(tl.size());
+    for (size_t i = 0; i < tl.size(); ++i) {
+      std::memset(&tasks[i], 0, sizeof(TaskDesc));
+      tasks[i].tile = tl[i]; tasks[i].kind = TK_TILE; tasks[i].dep_slot = kNoSlot; tasks[i].my_slot = kNoSlot;
+    }
     const size_t jo = tm.size() * sizeof(CUtensorMap), to = jo + align_up(sizeof(GemmJob), 64);
-    const size_t bytes = to + tl.size() * sizeof(uint64_t);
+    const size_t bytes = to + tasks.size() * sizeof(TaskDesc);
     CU_TRY(cudaMalloc(&dmem, bytes));
     uint8_t* d = reinterpret_cast<uint8_t*>(dmem);
     J.tmA = d + ia * sizeof(CUtensorMap);
@@ -1008,22 +1014,11 @@ static ns_status one_gemm(GemmJob J, TDesc ta, TDesc tb, TDesc tout, TDesc taux,
     std::vector<uint8_t> h(bytes);
     std::memcpy(h.data(), tm.data(), jo);
     std::memcpy(h.data() + jo, &J, sizeof(J));
-    std::memcpy(h.data() + to, tl.data(), tl.size() * sizeof(uint64_t));
+    std::memcpy(h.data() + to, tasks.data(), tasks.size() * sizeof(TaskDesc));
     CU_TRY(cudaMemcpy(dmem, h.data(), bytes, cudaMemcpyHostToDevice));
-    // single GEMM step: its PhaseDesc sits after the tile list
-    PhaseDesc pd;
-    std::memset(&pd, 0, sizeof(pd));
-    pd.kind = PHK_GEMM; pd.tile_begin = 0; pd.tile_end = (int64_t)tl.size();
-    const size_t po = align_up(bytes, 64);
-    void* dpd = nullptr;
-    CU_TRY(cudaMalloc(&dpd, sizeof(pd)));
-    CU_TRY(cudaMemcpy(dpd, &pd, sizeof(pd), cudaMemcpyHostToDevice));
-    (void)po;
-    cudaError_t e = launch_umma_gemm(reinterpret_cast<const GemmJob*>(d + jo), reinterpret_cast<const uint64_t*>(d + to),
-                                     reinterpret_cast<const PhaseDesc*>(dpd), 1, nullptr, (int64_t)tl.size(), cg,
-                                     dc->sms, dc->flags, stream);
-    cudaStreamSynchronize(stream);
-    cudaFree(dpd);
+    cudaError_t e = launch_umma_gemm(reinterpret_cast<const GemmJob*>(d + jo), reinterpret_cast<const TaskDesc*>(d + to),
+                                     (int64_t)tasks.size(), nullptr, nullptr, 0, (int64_t)tasks.size(), cg, dc->sms,
+                                     dc->flags, stream);
     ++g_launches;
     cudaError_t e2 = cudaStreamSynchronize(stream);
     cudaFree(dmem);

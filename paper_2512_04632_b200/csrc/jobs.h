@@ -110,15 +110,25 @@ struct MuonJob {
   float scale;     // max(1, m/n)^(1/2)
 };
 
-// One step of a launch.  A per-step launch carries one GEMM phase; the fused single-launch
-// mode (small problems) carries all 3T+1 steps, separated by device-side phase barriers.
-enum PhaseKindDev : int32_t { PHK_GEMM = 0, PHK_PRE_S = 1, PHK_PRE_SCALE = 2 };
-struct PhaseDesc {
-  int32_t kind;
-  int32_t npjobs;
-  int64_t tile_begin, tile_end;  // GEMM: range of the launch's tile list
-  const PrecondJob* pjobs;       // PRE_*: matrices and their row prefix
-  int64_t prow_total;
+// One unit of work of a launch (umma_gemm_kernel).  A per-step launch is a list of
+// TK_TILE tasks without dependencies.  The fused single launch (ns_set_path(3)) carries all
+// 3T+1 steps of every matrix as one list in topological order: each task waits until its
+// matrix's previous step is complete (device counter `done[dep_slot] >= dep_target`) and,
+// once its outputs are visible, arrives on `done[my_slot]` (one arrival per epilogue warp
+// of the CTA pair).  Matrices therefore pipeline through the steps independently, with no
+// grid-wide barrier.
+constexpr uint32_t kNoSlot = 0xFFFFFFFFu;
+enum TaskKind : uint32_t { TK_TILE = 0, TK_PRE_S = 1, TK_PRE_SCALE = 2 };
+constexpr int kPreRows = 64;  // rows of one preconditioner task
+enum StepKind : int32_t { PHK_GEMM = 0, PHK_PRE_S = 1 };  // host-side step kinds (api.cu)
+struct TaskDesc {
+  uint64_t tile;        // TK_TILE: pack_tile(job, p0, q0, mirror)
+  uint32_t kind;        // TaskKind
+  uint32_t dep_slot;    // kNoSlot: no dependency
+  uint32_t dep_target;  // arrivals that complete the dependency
+  uint32_t my_slot;     // kNoSlot: no arrival
+  uint32_t pjob;        // TK_PRE_*: matrix index into the launch's PrecondJob array
+  uint32_t row0;        // TK_PRE_*: first row of the chunk
 };
 
 }  // namespace tns

@@ -10,12 +10,13 @@ namespace tns {
 
 // tcgen05 bf16 engine (umma_gemm.cu).  One persistent launch over all jobs' tiles.
 // cg = 1: 128 x 256 tiles per CTA; cg = 2: 256 x 256 tiles per CTA pair (cta_group::2).
-// d_tiles: packed tile list (pack_tile) in execution order.  d_phases: nphases step
-// descriptors (device memory); nphases > 1 = fused single-launch mode, which needs d_sync:
-// nphases + 1 zero-initialised counters (self-resetting).  max_tiles = largest GEMM step.
-cudaError_t launch_umma_gemm(const GemmJob* d_jobs, const uint64_t* d_tiles, const PhaseDesc* d_phases,
-                             int nphases, unsigned* d_sync, int64_t max_tiles, int cg, int num_sms,
-                             uint32_t* d_flags, cudaStream_t stream);
+// d_tasks: the launch's task list (TaskDesc) in execution order.  Per-step launches:
+// TK_TILE tasks without dependencies, d_pjobs = d_done = nullptr, nslots = 0.  Fused
+// launches: all steps, d_done = nslots + 1 zero-initialised counters (self-resetting).
+// max_tiles = largest GEMM step (grid sizing of per-step launches).
+cudaError_t launch_umma_gemm(const GemmJob* d_jobs, const TaskDesc* d_tasks, int64_t ntasks, const PrecondJob* d_pjobs,
+                             unsigned* d_done, int nslots, int64_t max_tiles, int cg, int num_sms, uint32_t* d_flags,
+                             cudaStream_t stream);
 // Read (and optionally reset) the epilogue clock counters (TNS_DBG bit 8 measurement).
 cudaError_t umma_epi_prof(unsigned long long* out, bool reset);
 // Append the tiles of job `job` (host side).

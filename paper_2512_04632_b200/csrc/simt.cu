@@ -153,16 +153,25 @@ __global__ void __launch_bounds__(256)
   const int64_t gwarp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   uint32_t fl = 0;
+  // each warp owns a contiguous run of rows: one job lookup per run, not per row
+  const int64_t per = (total_rows + nwarps - 1) / nwarps;
+  const int64_t r_beg = gwarp * per, r_end = min(total_rows, r_beg + per);
   // ---- phase 1: scaling vector s (Eq. 8 / Eq. 10)
-  for (int64_t row = gwarp; row < total_rows; row += nwarps) {
-    const PrecondJob& J = jobs[find_pjob(jobs, njobs, row)];
-    precond_row_s<T, VEC8>(J, (int)(row - J.row_start), lane, fl);
+  if (r_beg < r_end) {
+    int jb = find_pjob(jobs, njobs, r_beg);
+    for (int64_t row = r_beg; row < r_end; ++row) {
+      while (jb + 1 < njobs && jobs[jb + 1].row_start <= row) ++jb;
+      precond_row_s<T, VEC8>(jobs[jb], (int)(row - jobs[jb].row_start), lane, fl);
+    }
   }
   grid_barrier(barrier);
   // ---- phase 2: A1 = diag(s) A0 diag(s)  (Alg. 2 l.4)
-  for (int64_t row = gwarp; row < total_rows; row += nwarps) {
-    const PrecondJob& J = jobs[find_pjob(jobs, njobs, row)];
-    precond_row_scale<T, VEC8>(J, (int)(row - J.row_start), lane);
+  if (r_beg < r_end) {
+    int jb = find_pjob(jobs, njobs, r_beg);
+    for (int64_t row = r_beg; row < r_end; ++row) {
+      while (jb + 1 < njobs && jobs[jb + 1].row_start <= row) ++jb;
+      precond_row_scale<T, VEC8>(jobs[jb], (int)(row - jobs[jb].row_start), lane);
+    }
   }
   if (fl) atomicOr(flags, fl);
 }
