@@ -66,8 +66,8 @@ struct Geo {
   static constexpr size_t kSmemBytes = (size_t)kEpiOff + kEpiBytes + 1024 + 512;
 };
 
-// Fused mode: spin until `target` arrivals were counted for a phase, then order later
-// async-proxy (TMA) reads after it.
+// Fused mode: spin until `target` arrivals were counted on a dependency slot, then order
+// later async-proxy (TMA) reads after it.
 __device__ __forceinline__ void wait_phase(const unsigned* cnt, unsigned target) {
   while (true) {
     unsigned v;
@@ -92,8 +92,7 @@ struct TileInfo {
   bool mirror;
 };
 
-__device__ __forceinline__ TileInfo decode_tile(const uint64_t* __restrict__ tiles, int64_t t) {
-  const uint64_t w = __ldg(tiles + t);
+__device__ __forceinline__ TileInfo decode_word(uint64_t w) {
   TileInfo ti;
   ti.job = (int)(w & 0xFFFFFu);
   ti.p0 = (int)((w >> 20) & 0xFFFFFu) * 128;
@@ -252,8 +251,8 @@ __device__ __forceinline__ void epi_math(int var, const Epi& E, int p, int q, co
 
 template <int CG>
 __global__ void __launch_bounds__(kThreads, 1)
-    umma_gemm_kernel(const GemmJob* __restrict__ jobs, const uint64_t* __restrict__ tiles,
-                     const PhaseDesc* __restrict__ phases, int nphases, unsigned* sync,
+    umma_gemm_kernel(const GemmJob* __restrict__ jobs, const TaskDesc* __restrict__ tasks, int64_t ntasks,
+                     const PrecondJob* __restrict__ pjobs, unsigned* done, int nslots,
                      uint32_t* __restrict__ flags, int dbg) {
   using G = Geo<CG>;
   extern __shared__ uint8_t smem_raw[];
@@ -302,13 +301,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       uint32_t stage = 0, phase = 0;
       int last_job = -1;
-      const unsigned arrivals = kNumEpiWarps * gridDim.x;
-      for (int ph = 0; ph < nphases; ++ph) {
-      const PhaseDesc PD = phases[ph];
-      if (PD.kind != PHK_GEMM) continue;
-      if (ph > 0) wait_phase(sync + ph - 1, arrivals);  // fused mode: previous step complete
-      for (int64_t t = PD.tile_begin + cid; t < PD.tile_end; t += ncl) {
-        const TileInfo ti = decode_tile(tiles, t);
+      for (int64_t t = cid; t < ntasks; t += ncl) {
+        const TaskDesc TD = tasks[t];
+        if (TD.kind != TK_TILE) continue;
+        if (TD.dep_slot != kNoSlot) wait_phase(done + TD.dep_slot, TD.dep_target);
+        const TileInfo ti = decode_word(TD.tile);
         const GemmJob* J = jobs + ti.job;
         const void* tmA = J->tmA;
         const void* tmB = J->tmB;
@@ -346,7 +343,6 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (++stage == G::kStages) { stage = 0; phase ^= 1; }
         }
       }
-      }
       // tail: wait until the MMA released every stage, so no commit-arrive is still in
       // flight towards this CTA's barriers when it exits
       for (int i = 0; i < G::kStages; ++i) {
@@ -358,11 +354,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ------------------------------------------------------------------ MMA issuer (leader)
     if (lane == 0 && rank == 0) {
       uint32_t stage = 0, phase = 0, as = 0, aphase = 0;
-      for (int ph = 0; ph < nphases; ++ph) {
-      const PhaseDesc PD = phases[ph];
-      if (PD.kind != PHK_GEMM) continue;
-      for (int64_t t = PD.tile_begin + cid; t < PD.tile_end; t += ncl) {
-        const TileInfo ti = decode_tile(tiles, t);
+      for (int64_t t = cid; t < ntasks; t += ncl) {
+        const TaskDesc TD = tasks[t];
+        if (TD.kind != TK_TILE) continue;
+        const TileInfo ti = decode_word(TD.tile);
         const GemmJob* J = jobs + ti.job;
         const uint32_t a_mn = (uint32_t)J->a_mn, b_mn = (uint32_t)J->b_mn;
         const int K = J->K;
@@ -395,7 +390,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         umma_commit<CG>(&tfull_bar[as]);
         if (++as == 2) { as = 0; aphase ^= 1; }
       }
-      }
     }
   } else if (warp >= 4) {
     // ------------------------------------------------------------------ epilogue
@@ -411,30 +405,26 @@ __global__ void __launch_bounds__(kThreads, 1)
     bool bad = false;
     long long pc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     uint32_t pfl = 0;
-    const unsigned arrivals = kNumEpiWarps * gridDim.x;
-    for (int ph = 0; ph < nphases; ++ph) {
-    const PhaseDesc PD = phases[ph];
-    if (PD.kind != PHK_GEMM) {
-      // fused mode, preconditioner step: one warp per matrix row across the whole grid
-      if (lane == 0) wait_phase(sync + ph - 1, arrivals);
-      __syncwarp();
-      const int64_t gw = (int64_t)blockIdx.x * kNumEpiWarps + ew, nw = (int64_t)gridDim.x * kNumEpiWarps;
-      for (int64_t row = gw; row < PD.prow_total; row += nw) {
-        const PrecondJob& PJ = PD.pjobs[find_pjob(PD.pjobs, PD.npjobs, row)];
-        const int i = (int)(row - PJ.row_start);
-        if (PD.kind == PHK_PRE_S) precond_row_s<uint16_t, true>(PJ, i, lane, pfl);
-        else precond_row_scale<uint16_t, true>(PJ, i, lane);
+    for (int64_t t = cid; t < ntasks; t += ncl) {
+      const TaskDesc TD = tasks[t];
+      if (TD.dep_slot != kNoSlot) {  // the aux prefetch / preconditioner rows read that step
+        if (lane == 0) wait_phase(done + TD.dep_slot, TD.dep_target);
+        __syncwarp();
       }
-      __syncwarp();
-      if (lane == 0) arrive_phase(sync + ph);
-      continue;
-    }
-    if (ph > 0) {  // fused mode: the aux prefetch below reads the previous step's output
-      if (lane == 0) wait_phase(sync + ph - 1, arrivals);
-      __syncwarp();
-    }
-    for (int64_t t = PD.tile_begin + cid; t < PD.tile_end; t += ncl) {
-      const TileInfo ti = decode_tile(tiles, t);
+      if (TD.kind != TK_TILE) {
+        // preconditioner rows (fused mode): the pair's 8*CG epilogue warps share the chunk
+        const PrecondJob& PJ = pjobs[TD.pjob];
+        const int w = (int)rank * kNumEpiWarps + ew;
+        const int end = min((int)TD.row0 + kPreRows, PJ.N);
+        for (int i = (int)TD.row0 + w; i < end; i += kNumEpiWarps * CG) {
+          if (TD.kind == TK_PRE_S) precond_row_s<uint16_t, true>(PJ, i, lane, pfl);
+          else precond_row_scale<uint16_t, true>(PJ, i, lane);
+        }
+        __syncwarp();
+        if (lane == 0 && TD.my_slot != kNoSlot) arrive_phase(done + TD.my_slot);
+        continue;
+      }
+      const TileInfo ti = decode_word(TD.tile);
       const Epi E = load_epi(jobs + ti.job);
       const int var = epi_variant(E);
       const bool has_aux = epi_needs_aux(E) && !(dbg & 4);
@@ -553,12 +543,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       if (E.part != nullptr && p < E.P && qh < E.Q) E.part[(int64_t)p * E.part_ld + qh / 128] = rsum;
       if (++as == 2) { as = 0; aphase ^= 1; }
-    }
-    if (nphases > 1) {  // fused mode: this warp's part of the step is written and visible
-      if (lane == 0) bulk_wait<0>();
-      __syncwarp();
-      if (lane == 0) arrive_phase(sync + ph);
-    }
+      if (TD.my_slot != kNoSlot) {  // fused mode: this warp's part of the tile is visible
+        __syncwarp();
+        if (lane == 0) {
+          bulk_wait<0>();
+          arrive_phase(done + TD.my_slot);
+        }
+      }
     }
     if (pfl && lane == 0) atomicOr(flags, pfl);
     if (lane == 0) bulk_wait<0>();
@@ -573,18 +564,18 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_after();
     tmem_dealloc<CG>(tmem_base, kTmemCols);
   }
-  if (nphases > 1 && threadIdx.x == 0) {  // last CTA out resets the phase counters
+  if (nslots > 0 && threadIdx.x == 0) {  // fused mode: the last CTA out resets the counters
     __threadfence();
-    if (atomicAdd(sync + nphases, 1u) == gridDim.x - 1) {
-      for (int k = 0; k <= nphases; ++k) sync[k] = 0;
+    if (atomicAdd(done + nslots, 1u) == gridDim.x - 1) {
+      for (int k = 0; k <= nslots; ++k) done[k] = 0;
       __threadfence();
     }
   }
 }
 
 template <int CG>
-static cudaError_t launch_cg(const GemmJob* d_jobs, const uint64_t* d_tiles, const PhaseDesc* d_phases,
-                             int nphases, unsigned* d_sync, int64_t max_tiles, int num_sms, uint32_t* d_flags,
+static cudaError_t launch_cg(const GemmJob* d_jobs, const TaskDesc* d_tasks, int64_t ntasks, const PrecondJob* d_pjobs,
+                             unsigned* d_done, int nslots, int64_t max_tiles, int num_sms, uint32_t* d_flags,
                              cudaStream_t stream) {
   static bool attr_set[64] = {};
   int dev = 0;
@@ -600,10 +591,10 @@ static cudaError_t launch_cg(const GemmJob* d_jobs, const uint64_t* d_tiles, con
     }
     attr_set[dev & 63] = true;
   }
-  // persistent: one CTA (pair) per SM (pair); the fused mode uses every SM (its phase
-  // barriers need all CTAs co-resident, which one CTA per SM guarantees)
+  // persistent: one CTA (pair) per SM (pair); the fused mode uses every SM (its dependency
+  // waits need all CTAs co-resident, which one CTA per SM guarantees)
   const int64_t workers = num_sms / CG;
-  const int64_t nclusters = (nphases > 1 || max_tiles > workers) ? workers : max_tiles;
+  const int64_t nclusters = (nslots > 0 || max_tiles > workers) ? workers : max_tiles;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(nclusters * CG));
   cfg.blockDim = dim3(kThreads);
@@ -623,15 +614,15 @@ static cudaError_t launch_cg(const GemmJob* d_jobs, const uint64_t* d_tiles, con
     const char* e = getenv("TNS_DBG");  // 2 skip mirrored stores, 4 skip aux prefetch, 8 counters
     dbg = e ? atoi(e) : 0;
   }
-  return cudaLaunchKernelEx(&cfg, kern, d_jobs, d_tiles, d_phases, nphases, d_sync, d_flags, dbg);
+  return cudaLaunchKernelEx(&cfg, kern, d_jobs, d_tasks, ntasks, d_pjobs, d_done, nslots, d_flags, dbg);
 }
 
-cudaError_t launch_umma_gemm(const GemmJob* d_jobs, const uint64_t* d_tiles, const PhaseDesc* d_phases,
-                             int nphases, unsigned* d_sync, int64_t max_tiles, int cg, int num_sms,
-                             uint32_t* d_flags, cudaStream_t stream) {
-  if (max_tiles <= 0) return cudaSuccess;
-  return cg == 2 ? launch_cg<2>(d_jobs, d_tiles, d_phases, nphases, d_sync, max_tiles, num_sms, d_flags, stream)
-                 : launch_cg<1>(d_jobs, d_tiles, d_phases, nphases, d_sync, max_tiles, num_sms, d_flags, stream);
+cudaError_t launch_umma_gemm(const GemmJob* d_jobs, const TaskDesc* d_tasks, int64_t ntasks, const PrecondJob* d_pjobs,
+                             unsigned* d_done, int nslots, int64_t max_tiles, int cg, int num_sms, uint32_t* d_flags,
+                             cudaStream_t stream) {
+  if (ntasks <= 0) return cudaSuccess;
+  return cg == 2 ? launch_cg<2>(d_jobs, d_tasks, ntasks, d_pjobs, d_done, nslots, max_tiles, num_sms, d_flags, stream)
+                 : launch_cg<1>(d_jobs, d_tasks, ntasks, d_pjobs, d_done, nslots, max_tiles, num_sms, d_flags, stream);
 }
 
 cudaError_t umma_epi_prof(unsigned long long* out, bool reset) {
