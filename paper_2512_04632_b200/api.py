@@ -74,16 +74,7 @@ def orthogonalize(x: torch.Tensor, iters: int = 4, precond: str = "aol", coeffs=
     return x
 
 
-def orthogonalize_list(xs: Sequence[torch.Tensor], out: Sequence[torch.Tensor] | None = None,
-                       iters: int = 4, precond: str = "aol", coeffs=None,
-                       peer_ptrs: Sequence[Sequence[int]] | None = None) -> list[torch.Tensor]:
-    """Grouped call: one launch per NS step over all matrices.  In place unless `out`.
-
-    peer_ptrs[i] = device addresses (ints) where matrix i's result is ALSO stored by the
-    last iteration's epilogue (fused collective, ns_orthogonalize_peers)."""
-    xs = list(xs)
-    if not xs:
-        return []
+def _check_list(xs, out):
     dt = _dtype_code(xs[0])
     for i, t in enumerate(xs):
         _check_tensor(t, f"xs[{i}]")
@@ -97,6 +88,21 @@ def orthogonalize_list(xs: Sequence[torch.Tensor], out: Sequence[torch.Tensor] |
             _check_tensor(o, f"out[{i}]")
             if o.shape != t.shape or o.dtype != t.dtype:
                 raise ValueError("out[i] must match xs[i] in shape and dtype")
+    return out
+
+
+def orthogonalize_list(xs: Sequence[torch.Tensor], out: Sequence[torch.Tensor] | None = None,
+                       iters: int = 4, precond: str = "aol", coeffs=None,
+                       peer_ptrs: Sequence[Sequence[int]] | None = None) -> list[torch.Tensor]:
+    """Grouped call: one launch per NS step over all matrices.  In place unless `out`.
+
+    peer_ptrs[i] = device addresses (ints) where matrix i's result is ALSO stored by the
+    last iteration's epilogue (fused collective, ns_orthogonalize_peers)."""
+    xs = list(xs)
+    if not xs:
+        return []
+    dt = _dtype_code(xs[0])
+    out = _check_list(xs, out)
     cnt = len(xs)
     X = (ctypes.c_void_p * cnt)(*[t.data_ptr() for t in xs])
     O = (ctypes.c_void_p * cnt)(*[t.data_ptr() for t in out]) if out is not None else None
@@ -118,6 +124,33 @@ def orthogonalize_list(xs: Sequence[torch.Tensor], out: Sequence[torch.Tensor] |
                                             _stream(xs[0]))
             check(st, "ns_orthogonalize_peers")
     return out if out is not None else xs
+
+
+class PreparedCall:
+    """Argument arrays of one grouped call, built once and replayed (an optimizer's steady
+    state calls with the same tensors every step).  `valid()` re-checks the data pointers."""
+
+    def __init__(self, xs, out, iters: int = 4, precond: str = "aol", coeffs=None):
+        _check_list(list(xs), out)
+        self.xs, self.out = list(xs), list(out) if out is not None else None
+        cnt = len(self.xs)
+        self.ptrs = [t.data_ptr() for t in self.xs] + ([t.data_ptr() for t in self.out] if self.out else [])
+        self.X = (ctypes.c_void_p * cnt)(*[t.data_ptr() for t in self.xs])
+        self.O = (ctypes.c_void_p * cnt)(*[t.data_ptr() for t in self.out]) if self.out is not None else None
+        self.M = (ctypes.c_int64 * cnt)(*[t.shape[0] for t in self.xs])
+        self.N = (ctypes.c_int64 * cnt)(*[t.shape[1] for t in self.xs])
+        self.c = _coeff_array(iters, coeffs, precond)
+        self.cnt, self.iters, self.pc, self.dt = cnt, iters, PRECOND[precond], _dtype_code(self.xs[0])
+        self.device = self.xs[0].device
+
+    def valid(self) -> bool:
+        ts = self.xs + (self.out or [])
+        return all(t.data_ptr() == p for t, p in zip(ts, self.ptrs))
+
+    def __call__(self):
+        st = lib.ns_orthogonalize_batched(self.X, self.O, self.M, self.N, self.cnt, self.iters, self.c, self.pc,
+                                          self.dt, ctypes.c_void_p(torch.cuda.current_stream(self.device).cuda_stream))
+        check(st, "ns_orthogonalize_batched")
 
 
 def workspace_size(shapes: Sequence[tuple[int, int]], dtype=torch.bfloat16) -> int:

@@ -16,6 +16,7 @@ of bucket b+1 (SURVEY §8(e) "Overlap").
 """
 from __future__ import annotations
 
+import functools
 from dataclasses import dataclass, field
 from typing import Callable, Sequence
 
@@ -71,6 +72,11 @@ class ShardPlan:
 
 
 def make_plan(shapes: Sequence[tuple[int, int]], world: int, iters: int = 4, buckets: int = 1) -> ShardPlan:
+    return _make_plan(tuple(tuple(s) for s in shapes), world, iters, buckets)
+
+
+@functools.lru_cache(maxsize=64)
+def _make_plan(shapes, world: int, iters: int, buckets: int) -> ShardPlan:
     owners = lpt_owners(shapes, world, iters)
     load = [0] * world
     for i, s in enumerate(shapes):
@@ -170,25 +176,45 @@ def orthogonalize_sharded(xs: Sequence[torch.Tensor], group=None, iters: int = 4
     on = dist.is_initialized()
     world = dist.get_world_size(group) if on else 1
     rank = dist.get_rank(group) if on else 0
-    shapes = [tuple(t.shape) for t in xs]
-    plan = make_plan(shapes, world, iters, buckets)
     dtype, device = xs[0].dtype, xs[0].device
-    key = ("gather", tuple(shapes), world, buckets, dtype, str(device), id(group))
-    buf = _cached(key, lambda: torch.empty(plan.total, dtype=dtype, device=device))
-    views = [buf[o:o + m * n].view(m, n) for o, (m, n) in zip(plan.offsets, shapes)]
+    # steady state: same tensors every step -> packed buffer, views and the prepared
+    # argument arrays of every bucket are built once (host overhead ~tens of us per step)
+    ckey = ("call", tuple(id(t) for t in xs), world, rank, buckets, iters, precond,
+            None if coeffs is None else tuple(map(tuple, coeffs)), id(group), compute is None)
+    ent = _BUFFERS.get(ckey)
+    if ent is None or (ent["calls"] and not all(c.valid() for c in ent["calls"] if c is not None)):
+        shapes = [tuple(t.shape) for t in xs]
+        plan = make_plan(shapes, world, iters, buckets)
+        key = ("gather", tuple(shapes), world, buckets, dtype, str(device), id(group))
+        buf = _cached(key, lambda: torch.empty(plan.total, dtype=dtype, device=device))
+        views = [buf[o:o + m * n].view(m, n) for o, (m, n) in zip(plan.offsets, shapes)]
+        calls = []
+        for per_rank in plan.buckets:
+            mine = per_rank[rank]
+            if mine and compute is None and device.type == "cuda":
+                from .api import PreparedCall
+                calls.append(PreparedCall([xs[i] for i in mine], [views[i] for i in mine], iters, precond, coeffs))
+            else:
+                calls.append(None)
+        ent = {"plan": plan, "buf": buf, "views": views, "calls": calls}
+        _BUFFERS[ckey] = ent
+    plan, buf, views = ent["plan"], ent["buf"], ent["views"]
     cuda = device.type == "cuda"
     overlap = on and cuda and len(plan.buckets) > 1
     comm = _stream(device, "comm") if overlap else None
     for b, per_rank in enumerate(plan.buckets):
         mine = per_rank[rank]
         if mine:
-            ins = [xs[i] for i in mine]
-            outs = [views[i] for i in mine]
-            if compute is None:
-                from .api import orthogonalize_list
-                orthogonalize_list(ins, out=outs, iters=iters, precond=precond, coeffs=coeffs)
+            if ent["calls"][b] is not None:
+                ent["calls"][b]()
             else:
-                compute(ins, outs)
+                ins = [xs[i] for i in mine]
+                outs = [views[i] for i in mine]
+                if compute is None:
+                    from .api import orthogonalize_list
+                    orthogonalize_list(ins, out=outs, iters=iters, precond=precond, coeffs=coeffs)
+                else:
+                    compute(ins, outs)
         if on:
             if overlap:  # bucket b's exchange overlaps bucket b+1's compute
                 comm.wait_stream(torch.cuda.current_stream(device))
