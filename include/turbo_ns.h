@@ -81,7 +81,8 @@ ns_status ns_orthogonalize(void* X, int64_t m, int64_t n, int64_t batch, int ite
  * device pointers (inputs); out is a HOST array of device pointers receiving the
  * results (out may be NULL, or out[i] == X[i], for in place; out[i] must not
  * otherwise overlap any X[j]).  Every NS step runs as ONE launch over all matrices
- * (3*iters + 1 launches in total).  Results are bitwise identical to calling
+ * (3*iters + 1 launches in total), plus ONE cluster launch for all small matrices
+ * (see ns_set_path).  Results are bitwise identical to calling
  * ns_orthogonalize on each matrix alone. */
 ns_status ns_orthogonalize_batched(void* const* X, void* const* out, const int64_t* m,
                                    const int64_t* n, int64_t count, int iters,
@@ -125,16 +126,22 @@ ns_status ns_read_flags(void* stream, uint32_t* flags);
 /* Number of kernels the library launched on this process since load (host counter). */
 uint64_t ns_launch_count(void);
 
-/* Execution-path override for testing: 0 = auto (tcgen05, 256x256 tiles on CTA pairs,
- * for aligned bf16; one PDL-chained launch per step), 1 = force the SIMT (CUDA-core)
- * kernels, 2 = tcgen05 with single-CTA 128x256 tiles, 3 = all 3T+1 steps in ONE fused
- * launch with device-side step barriers, 4 = per-step launches.  Returns the previous value. */
+/* Execution-path override for testing: 0 = auto: matrices with short side N <= 128 whose
+ * fp32 copy fits in shared memory (the "cluster-resident" small-matrix kernel: the whole
+ * NS of one matrix in ONE launch of an 8-CTA thread-block cluster, X, A and B resident in
+ * shared memory, rows exchanged over DSMEM), all
+ * other matrices through the step engine (tcgen05, 256x256 tiles on CTA pairs, for aligned
+ * bf16, else SIMT; one PDL-chained launch per step); when both kinds are present the
+ * cluster launch runs on an internal side stream joined back by events; 1 = force the SIMT
+ * (CUDA-core) step kernels, 2 = tcgen05 with single-CTA 128x256 tiles, 3 = all 3T+1 steps
+ * in ONE fused dataflow launch, 4 = per-step launches for every matrix (no cluster kernel),
+ * 5 = same as 0.  Returns the previous value. */
 int ns_set_path(int path);
 
 /* Per-kernel event timing (measurement support for bench.py; off by default).
  * When enabled, every launch the library enqueues is bracketed by CUDA events recorded
  * on the SAME stream.  ns_profile_read SYNCHRONISES on the last event, writes for each
- * kind k (0 GRAM, 1 PRECOND, 2 POLY, 3 XB, 4 SIMT, 5 COPY; nkinds <= 6) the summed
+ * kind k (0 GRAM, 1 PRECOND, 2 POLY, 3 XB, 4 SIMT, 5 COPY, 6 FUSED, 7 CLUSTER; nkinds <= 8) the summed
  * device milliseconds ms[k] and the launch count counts[k], then clears the records. */
 void ns_profile_enable(int on);
 ns_status ns_profile_read(double* ms, uint64_t* counts, int nkinds);

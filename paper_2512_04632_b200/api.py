@@ -181,7 +181,7 @@ def set_path(path: int) -> int:
     return int(lib.ns_set_path(int(path)))
 
 
-KERNEL_KINDS = ("gram", "precondition", "poly", "update", "simt", "copy", "fused")
+KERNEL_KINDS = ("gram", "precondition", "poly", "update", "simt", "copy", "fused", "cluster")
 
 
 def profile_enable(on: bool = True) -> None:
@@ -191,9 +191,9 @@ def profile_enable(on: bool = True) -> None:
 
 def profile_read() -> dict:
     """Synchronise and return {kind: (total_ms, launches)}; clears the records."""
-    ms = (ctypes.c_double * 7)()
-    cnt = (ctypes.c_uint64 * 7)()
-    check(lib.ns_profile_read(ms, cnt, 7), "ns_profile_read")
+    ms = (ctypes.c_double * 8)()
+    cnt = (ctypes.c_uint64 * 8)()
+    check(lib.ns_profile_read(ms, cnt, 8), "ns_profile_read")
     return {k: (float(ms[i]), int(cnt[i])) for i, k in enumerate(KERNEL_KINDS)}
 
 

@@ -72,6 +72,9 @@ struct DevCtx {
   int sms = 0;
   int cc_major = 0, cc_minor = 0;
   uint32_t* flags = nullptr;  // device word
+  // side stream for the cluster-resident small-matrix launch, joined back by events
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 };
 static DevCtx g_dev[64];
 static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
@@ -87,6 +90,9 @@ static ns_status dev_ctx(DevCtx** out) {
     CU_TRY(cudaDeviceGetAttribute(&d.cc_minor, cudaDevAttrComputeCapabilityMinor, dev));
     CU_TRY(cudaMalloc(&d.flags, sizeof(uint32_t)));
     CU_TRY(cudaMemset(d.flags, 0, sizeof(uint32_t)));
+    CU_TRY(cudaStreamCreateWithFlags(&d.side, cudaStreamNonBlocking));
+    CU_TRY(cudaEventCreateWithFlags(&d.ev_fork, cudaEventDisableTiming));
+    CU_TRY(cudaEventCreateWithFlags(&d.ev_join, cudaEventDisableTiming));
     if (!g_encode) {
       cudaDriverEntryPointQueryResult q;
       void* fn = nullptr;
@@ -147,7 +153,7 @@ struct Mat {
   int tm_peer;
 };
 
-enum PhaseKind { PH_GEMM = 0, PH_SIMT = 1, PH_PRECOND = 2, PH_COPY = 3, PH_FUSED = 4 };
+enum PhaseKind { PH_GEMM = 0, PH_SIMT = 1, PH_PRECOND = 2, PH_COPY = 3, PH_FUSED = 4, PH_CLUSTER = 5 };
 struct Phase {
   PhaseKind kind;
   size_t dev_off;  // offset of the job array in the device table
@@ -163,6 +169,8 @@ struct Phase {
   size_t done_off = 0;    // offset of the dependency counters (PH_FUSED)
   int nslots = 0;         // PH_FUSED: dependency counters
   int64_t max_tiles = 0;  // largest GEMM step
+  size_t coeff_off = 0;   // PH_CLUSTER: 3*iters floats
+  size_t smem = 0;        // PH_CLUSTER: dynamic shared memory per CTA
   // copies (PH_COPY)
   std::vector<std::pair<std::pair<void*, const void*>, size_t>> copies;
 };
@@ -175,7 +183,8 @@ struct Plan {
   int cg = 2;  // tcgen05 CTA group (2: 256x256 tiles on CTA pairs)
   int iters = 0;
   ns_precond precond = NS_PRECOND_AOL;
-  std::vector<Mat> mats;
+  std::vector<Mat> mats;   // tcgen05 / SIMT step engine
+  std::vector<Mat> tiny;   // cluster-resident whole-NS kernel (row a-10)
   void* ws = nullptr;
   size_t ws_bytes = 0;
   void* dtab = nullptr;
@@ -333,7 +342,27 @@ static ns_status build_plan(Plan& P, HostTables& H, DevCtx* dc, const float* coe
     return ((T - (k - 1)) % 2 == 0) ? mt.tm_out : mt.tm_w;
   };
 
-  for (int k = 1; k <= T; ++k) {
+  // -- small matrices: the whole NS in one cluster launch (enqueued first, on a side stream
+  //    when the step engine has work too, so the two overlap)
+  if (!P.tiny.empty()) {
+    std::vector<ClusterJob> cj;
+    size_t smem = 0;
+    for (const Mat& mt : P.tiny) {
+      ClusterJob J;
+      std::memset(&J, 0, sizeof(J));
+      J.x = mt.x; J.out = mt.out;
+      J.m = (int)mt.m; J.n = (int)mt.n; J.M = (int)mt.M; J.N = (int)mt.N; J.wide = mt.wide ? 1 : 0;
+      cj.push_back(J);
+      smem = std::max(smem, cl_layout(J.M, J.N).floats * 4 + kClHdr);
+    }
+    Phase ph{PH_CLUSTER};
+    ph.dev_off = H.push(cj.data(), cj.size() * sizeof(ClusterJob), 64);
+    ph.coeff_off = H.push(coeffs, (size_t)3 * T * sizeof(float), 16);
+    ph.njobs = (int)cj.size();
+    ph.smem = smem;
+    P.phases.push_back(ph);
+  }
+  for (int k = 1; k <= T && !P.mats.empty(); ++k) {
     const float a = coeffs[3 * (k - 1)], b = coeffs[3 * (k - 1) + 1], c = coeffs[3 * (k - 1) + 2];
     const bool scaled = (k == 1 && P.precond != NS_PRECOND_NONE);
     for (int step = 0; step < 3; ++step) {
@@ -619,8 +648,29 @@ static ns_status build_plan(Plan& P, HostTables& H, DevCtx* dc, const float* coe
 
 static ns_status enqueue_plan(Plan& P, DevCtx* dc, cudaStream_t stream) {
   uint8_t* dbase = reinterpret_cast<uint8_t*>(P.dtab);
+  bool joined = true;
   for (const Phase& ph : P.phases) {
     switch (ph.kind) {
+      case PH_CLUSTER: {
+        // alone: on the caller's stream; with step-engine work: forked onto the side stream
+        const bool fork = !P.mats.empty();
+        cudaStream_t s = stream;
+        if (fork) {
+          CU_TRY(cudaEventRecord(dc->ev_fork, stream));
+          CU_TRY(cudaStreamWaitEvent(dc->side, dc->ev_fork, 0));
+          s = dc->side;
+          joined = false;
+        }
+        {
+          ProfScope ps(7, s);
+          CU_TRY(launch_cluster_ns(reinterpret_cast<const ClusterJob*>(dbase + ph.dev_off), ph.njobs,
+                                   reinterpret_cast<const float*>(dbase + ph.coeff_off), P.iters, (int)P.precond,
+                                   P.dtype == NS_BF16, ph.smem, dc->flags, s));
+        }
+        ++g_launches;
+        if (fork) CU_TRY(cudaEventRecord(dc->ev_join, dc->side));
+        break;
+      }
       case PH_COPY: {
         ProfScope ps(5, stream);
         for (auto& c : ph.copies)
@@ -662,6 +712,7 @@ static ns_status enqueue_plan(Plan& P, DevCtx* dc, cudaStream_t stream) {
       }
     }
   }
+  if (!joined) CU_TRY(cudaStreamWaitEvent(stream, dc->ev_join, 0));
   return NS_OK;
 }
 
@@ -694,9 +745,16 @@ static ns_status run(const std::vector<Mat>& mats_in, int iters, const float* co
   DevCtx* dc = nullptr;
   ns_status st = dev_ctx(&dc);
   if (st != NS_OK) return st;
+  // small matrices (short side <= 128, full copy fits in shared memory) run the whole NS
+  // in one cluster launch (paths 0 and 5); the others go through the step engine
+  std::vector<Mat> tiny, big;
+  bool any_peer = false;
+  for (const Mat& mt : mats_in) any_peer = any_peer || !mt.peer.empty();
+  const bool use_cluster = (g_path == 0 || g_path == 5) && !any_peer && dc->cc_major == 10;
+  for (const Mat& mt : mats_in) (use_cluster && cl_fits(mt.M, mt.N) ? tiny : big).push_back(mt);
   bool simt = (g_path == 1) || dtype != NS_BF16 || dc->cc_major != 10;
   bool peers = false;
-  for (const Mat& mt : mats_in) {
+  for (const Mat& mt : big) {
     simt = simt || !tma_ok(mt, dtype);
     peers = peers || !mt.peer.empty();
     for (void* pp : mt.peer) simt = simt || (reinterpret_cast<uintptr_t>(pp) & 15);
@@ -714,6 +772,7 @@ static ns_status run(const std::vector<Mat>& mats_in, int iters, const float* co
   key.push_back((uint64_t)g_path);
   key.push_back((uint64_t)iters); key.push_back((uint64_t)precond);
   for (int i = 0; i < 3 * iters; ++i) { uint32_t u; std::memcpy(&u, &coeffs[i], 4); key.push_back(u); }
+  key.push_back((uint64_t)tiny.size());
   for (const Mat& mt : mats_in) {
     key.push_back(reinterpret_cast<uint64_t>(mt.x)); key.push_back(reinterpret_cast<uint64_t>(mt.out));
     key.push_back((uint64_t)mt.m); key.push_back((uint64_t)mt.n);
@@ -732,7 +791,8 @@ static ns_status run(const std::vector<Mat>& mats_in, int iters, const float* co
     }
     std::unique_ptr<Plan> np(new Plan());
     np->device = dev; np->dtype = dtype; np->simt = simt; np->cg = cg; np->iters = iters; np->precond = precond;
-    np->mats = mats_in;
+    np->mats = big;
+    np->tiny = tiny;
     HostTables H;
     st = build_plan(*np, H, dc, coeffs);
     if (st != NS_OK) return st;
@@ -788,7 +848,7 @@ void ns_profile_enable(int on) {
 
 ns_status ns_profile_read(double* ms, uint64_t* counts, int nkinds) {
   std::lock_guard<std::mutex> lk(g_mu);
-  if (!ms || !counts || nkinds < 1 || nkinds > 7) return fail(NS_ERR_INVALID_VALUE, "bad arguments");
+  if (!ms || !counts || nkinds < 1 || nkinds > 8) return fail(NS_ERR_INVALID_VALUE, "bad arguments");
   for (int k = 0; k < nkinds; ++k) { ms[k] = 0.0; counts[k] = 0; }
   if (!g_prof_recs.empty()) CU_TRY(cudaEventSynchronize(g_prof_recs.back().b));
   for (const ProfRec& r : g_prof_recs) {
@@ -806,6 +866,15 @@ ns_status nsx_epilogue_counters(uint64_t* out8, int reset) {
   std::lock_guard<std::mutex> lk(g_mu);
   if (!out8) return fail(NS_ERR_INVALID_VALUE, "NULL");
   CU_TRY(cudaDeviceSynchronize());
+  const char* dbg = getenv("TNS_DBG");
+  if (dbg && (atoi(dbg) & 128)) {  // cluster-kernel timeline: 7 phase marks averaged per launch + count
+    unsigned long long t[9];
+    CU_TRY(cluster_timeline(t, reset != 0));
+    const unsigned long long n = t[8] ? t[8] : 1;
+    for (int i = 0; i < 7; ++i) out8[i] = t[i] / n;
+    out8[7] = t[8];
+    return NS_OK;
+  }
   CU_TRY(umma_epi_prof(reinterpret_cast<unsigned long long*>(out8), reset != 0));
   return NS_OK;
 }
@@ -967,6 +1036,9 @@ void ns_shutdown(void) {
   g_muon_tabs.clear();
   for (auto& d : g_dev) {
     if (d.init && d.flags) cudaFree(d.flags);
+    if (d.init && d.side) cudaStreamDestroy(d.side);
+    if (d.init && d.ev_fork) cudaEventDestroy(d.ev_fork);
+    if (d.init && d.ev_join) cudaEventDestroy(d.ev_join);
     d = DevCtx();
   }
 }

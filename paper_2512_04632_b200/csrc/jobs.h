@@ -131,4 +131,46 @@ struct TaskDesc {
   uint32_t row0;        // TK_PRE_*: first row of the chunk
 };
 
+// ------------------------------------------------------------------ cluster-resident NS
+// Whole Newton-Schulz of one small matrix (short side N <= 128) inside one cluster of
+// kClCtas CTAs (cluster_ns.cu).  Every CTA holds a full fp32 copy
+// of Xh (M x N), A and B in shared memory; CTA r computes rows [r*Nr, r*Nr+Nr) of A and B
+// and rows [r*Mr, r*Mr+Mr) of X_{k+1} and broadcasts them to its peers over DSMEM.
+constexpr int kClCtas = 8;
+#ifndef TNS_CL_THREADS
+#define TNS_CL_THREADS 512
+#endif
+constexpr int kClThreads = TNS_CL_THREADS;
+constexpr int kClMaxN = 128;
+constexpr size_t kClMaxSmem = 227 * 1024;  // the sm_100 per-block maximum
+constexpr int kClHdr = 64;                  // bytes before the float region (mbarriers)
+struct ClusterJob {
+  const void* x;  // input, caller layout (m x n row-major)
+  void* out;      // output, caller layout (may equal x)
+  int32_t m, n, M, N, wide, pad;
+};
+struct ClLayout {
+  int N4, Nr, Mr, ldx, lda;
+  size_t offA, offB, offX, offXn, floats;  // in floats
+};
+__host__ __device__ inline ClLayout cl_layout(int M, int N) {
+  ClLayout L;
+  L.N4 = (N + 3) & ~3;
+  L.Nr = ((N + kClCtas - 1) / kClCtas + 3) & ~3;
+  L.Mr = ((M + kClCtas - 1) / kClCtas + 3) & ~3;
+  L.ldx = L.N4 + 4;  // X rows are also read with a row stride (XB): pad against bank conflicts
+  L.lda = L.N4 + 4;  // A, B rows: padded too (the k-split lanes read 4 rows at once)
+  size_t o = 0;
+  L.offA = o; o += (size_t)L.N4 * L.lda;
+  L.offB = o; o += (size_t)L.N4 * L.lda;
+  L.offX = o; o += (size_t)kClCtas * L.Mr * L.ldx;
+  L.offXn = o; o += (size_t)L.Mr * L.ldx;
+  o += L.N4;  // s
+  L.floats = o;
+  return L;
+}
+__host__ __device__ inline bool cl_fits(int64_t M, int64_t N) {
+  return N >= 1 && N <= kClMaxN && M <= 4096 && cl_layout((int)M, (int)N).floats * 4 + kClHdr <= kClMaxSmem;
+}
+
 }  // namespace tns

@@ -267,6 +267,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  // TNS_DBG bit 16: latency timeline of CTA 0 (cycles since kernel entry, summed over launches)
+  const bool tl = (dbg & 16) && blockIdx.x == 0 && lane == 0;
+  const long long T0 = tl ? clock64() : 0;
+#define TL(slot) do { if (tl) atomicAdd(&g_epi_prof[slot], (unsigned long long)(clock64() - T0)); } while (0)
   const uint32_t rank = (CG == 2) ? cluster_ctarank() : 0u;  // CTA rank within the pair
   const int64_t cid = blockIdx.x / CG;                       // cluster (tile worker) index
   const int64_t ncl = gridDim.x / CG;
@@ -293,8 +297,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tmem_base = *tmem_slot;
   // everything above overlaps the previous kernel's tail (PDL); data buffers are touched
   // only after it has completed
+  if (warp == 0) TL(0);  // setup done
   pdl_trigger();
   pdl_wait();
+  if (warp == 0) TL(1);  // dependency resolved
 
   if (warp == 0) {
     // ------------------------------------------------------------------ TMA producer
@@ -341,6 +347,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             else tma_load_2d(sb + i * kBoxBytes, tmB, &full_bar[stage], c0, c1);
           }
           if (++stage == G::kStages) { stage = 0; phase ^= 1; }
+          if (kb == 0 && t == cid) TL(2);  // first loads issued
         }
       }
       // tail: wait until the MMA released every stage, so no commit-arrive is still in
@@ -370,6 +377,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int kb = 0; kb < nk; ++kb) {
           mbar_wait(&full_bar[stage], phase);
           tc_fence_after();
+          if (kb == 0 && t == cid) TL(3);  // first operands landed
           const uint32_t sa = smem_u32(smem + (size_t)stage * G::kStageBytes);
           const uint32_t sb = sa + G::kABytes;
           const int kblk = (kb * kBK) >> 8;
@@ -440,6 +448,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       long long t0 = prof ? clock64() : 0, t1;
       mbar_wait(&tfull_bar[as], aphase);
       tc_fence_after();
+      if (ew == 0 && t == cid) TL(4);  // first accumulator ready
       if (prof) { t1 = clock64(); pc[1] += t1 - t0; t0 = t1; pc[0] += 1; }
 #pragma unroll 1
       for (int c = 0; c < 4; ++c) {
@@ -553,6 +562,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     if (pfl && lane == 0) atomicOr(flags, pfl);
     if (lane == 0) bulk_wait<0>();
+    if (ew == 0) TL(5);  // epilogue stores complete
     if ((dbg & 8) && lane == 0)
       for (int i = 0; i < 8; ++i) atomicAdd(&g_epi_prof[i], (unsigned long long)pc[i]);
     if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(flags, 2u);
@@ -563,7 +573,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc<CG>(tmem_base, kTmemCols);
+    TL(6);
+    if (tl) atomicAdd(&g_epi_prof[7], 1ull);
   }
+#undef TL
   if (nslots > 0 && threadIdx.x == 0) {  // fused mode: the last CTA out resets the counters
     __threadfence();
     if (atomicAdd(done + nslots, 1u) == gridDim.x - 1) {
@@ -611,7 +624,7 @@ static cudaError_t launch_cg(const GemmJob* d_jobs, const TaskDesc* d_tasks, int
   cfg.numAttrs = 2;
   static int dbg = -1;
   if (dbg < 0) {  // measurement knob (never set in production): TNS_DBG bits 1 skip epilogue,
-    const char* e = getenv("TNS_DBG");  // 2 skip mirrored stores, 4 skip aux prefetch, 8 counters
+    const char* e = getenv("TNS_DBG");  // 2 skip mirrored stores, 4 skip aux prefetch, 8 counters, 16 timeline
     dbg = e ? atoi(e) : 0;
   }
   return cudaLaunchKernelEx(&cfg, kern, d_jobs, d_tasks, ntasks, d_pjobs, d_done, nslots, d_flags, dbg);
