@@ -135,7 +135,9 @@ uint64_t ns_launch_count(void);
  * cluster launch runs on an internal side stream joined back by events; 1 = force the SIMT
  * (CUDA-core) step kernels, 2 = tcgen05 with single-CTA 128x256 tiles, 3 = all 3T+1 steps
  * in ONE fused dataflow launch, 4 = per-step launches for every matrix (no cluster kernel),
- * 5 = same as 0.  Returns the previous value. */
+ * 5 = same as 0, 6 = per-step launches on 4-CTA clusters: two CTA pairs run tiles sharing
+ * their A operand, loaded once by TMA multicast (bitwise equal to 4; measured slower on
+ * B200 because only 33 4-CTA clusters fit on the 148 SMs).  Returns the previous value. */
 int ns_set_path(int path);
 
 /* Per-kernel event timing (measurement support for bench.py; off by default).

@@ -533,9 +533,22 @@ static ns_status build_plan(Plan& P, HostTables& H, DevCtx* dc, const float* coe
     if (!P.fused) {
       for (Step& st : steps) {
         if (st.kind == PHK_GEMM) {
-          std::vector<uint64_t> tl = tile_list(st, 0);
           std::vector<TaskDesc> tasks;
-          for (uint64_t w : tl) tasks.push_back(mk_task(w));
+          if (P.cg == 4) {  // multicast clusters: tile pairs sharing the A operand
+            std::vector<size_t> order(st.jobs.size());
+            for (size_t j = 0; j < st.jobs.size(); ++j) order[j] = j;
+            std::stable_sort(order.begin(), order.end(), [&](size_t x, size_t y) { return st.jobs[x].K > st.jobs[y].K; });
+            std::vector<std::pair<uint64_t, uint64_t>> pl;
+            for (size_t j : order) umma_pair_list(st.jobs[j], (uint32_t)j, pl);
+            for (auto& pr : pl) {
+              TaskDesc td = mk_task(pr.first);
+              td.tile2 = pr.second;
+              tasks.push_back(td);
+            }
+          } else {
+            std::vector<uint64_t> tl = tile_list(st, 0);
+            for (uint64_t w : tl) tasks.push_back(mk_task(w));
+          }
           Phase ph{PH_GEMM};
           ph.gemm_kind = st.gemm_kind;
           ph.dev_off = H.push(st.jobs.data(), st.jobs.size() * sizeof(GemmJob), 64);
@@ -766,7 +779,7 @@ static ns_status run(const std::vector<Mat>& mats_in, int iters, const float* co
   // plan key
   std::vector<uint64_t> key;
   key.reserve(mats_in.size() * 4 + 8 + 3 * iters);
-  const int cg = (g_path == 2) ? 1 : 2;
+  const int cg = (g_path == 2) ? 1 : (g_path == 6 ? 4 : 2);
   key.push_back((uint64_t)dev); key.push_back((uint64_t)dtype); key.push_back(simt ? 1 : 0);
   key.push_back((uint64_t)cg);
   key.push_back((uint64_t)g_path);

@@ -155,7 +155,7 @@ __global__ void __launch_bounds__(kClThreads, 1)
   const ClusterJob J = jobs[blockIdx.x / kClCtas];
   const uint32_t rank = cluster_ctarank();
   const ClLayout L = cl_layout(J.M, J.N);
-  const int M = J.M, N = J.N, N4 = L.N4, lda = L.lda, ldx = L.ldx, C4 = L.N4 / 4;
+  const int M = J.M, N = J.N, lda = L.lda, ldx = L.ldx, C4 = L.N4 / 4;
   float* A = sm + L.offA;
   float* B = sm + L.offB;
   float* Xf = sm + L.offX;

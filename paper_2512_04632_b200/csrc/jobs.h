@@ -121,8 +121,12 @@ constexpr uint32_t kNoSlot = 0xFFFFFFFFu;
 enum TaskKind : uint32_t { TK_TILE = 0, TK_PRE_S = 1, TK_PRE_SCALE = 2 };
 constexpr int kPreRows = 64;  // rows of one preconditioner task
 enum StepKind : int32_t { PHK_GEMM = 0, PHK_PRE_S = 1 };  // host-side step kinds (api.cu)
+// Bit 62 of a tile word: "shadow" tile -- computed (its operand loads feed the other pair of
+// a multicast cluster) but never stored.
+constexpr uint64_t kTileShadow = 1ull << 62;
 struct TaskDesc {
   uint64_t tile;        // TK_TILE: pack_tile(job, p0, q0, mirror)
+  uint64_t tile2;       // multicast clusters (2 CTA pairs): the second pair's tile, same job/p0/K
   uint32_t kind;        // TaskKind
   uint32_t dep_slot;    // kNoSlot: no dependency
   uint32_t dep_target;  // arrivals that complete the dependency

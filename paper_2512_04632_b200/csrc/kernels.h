@@ -2,6 +2,7 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <utility>
 #include <vector>
 
 #include "jobs.h"
@@ -9,7 +10,8 @@
 namespace tns {
 
 // tcgen05 bf16 engine (umma_gemm.cu).  One persistent launch over all jobs' tiles.
-// cg = 1: 128 x 256 tiles per CTA; cg = 2: 256 x 256 tiles per CTA pair (cta_group::2).
+// cg = 1: 128 x 256 tiles per CTA; cg = 2: 256 x 256 tiles per CTA pair (cta_group::2);
+// cg = 4: two such pairs per 4-CTA cluster sharing the A operand by TMA multicast.
 // d_tasks: the launch's task list (TaskDesc) in execution order.  Per-step launches:
 // TK_TILE tasks without dependencies, d_pjobs = d_done = nullptr, nslots = 0.  Fused
 // launches: all steps, d_done = nslots + 1 zero-initialised counters (self-resetting).
@@ -21,6 +23,8 @@ cudaError_t launch_umma_gemm(const GemmJob* d_jobs, const TaskDesc* d_tasks, int
 cudaError_t umma_epi_prof(unsigned long long* out, bool reset);
 // Append the tiles of job `job` (host side).
 void umma_tile_list(const GemmJob& J, uint32_t job, int cg, std::vector<uint64_t>& out);
+// cg = 4 (two CTA pairs per cluster, A multicast): the job's tiles as pairs sharing p0.
+void umma_pair_list(const GemmJob& J, uint32_t job, std::vector<std::pair<uint64_t, uint64_t>>& out);
 
 // CUDA-core engine (simt.cu); is_bf16 selects the storage type.
 cudaError_t launch_simt_gemm(const SimtJob* d_jobs, int njobs, int64_t total_tiles, int num_sms,

@@ -32,6 +32,7 @@
 // mirrored stores, 4 skip aux loads, 8 collect epilogue clock counters.
 #include <cuda_runtime.h>
 
+#include <cstdio>
 #include <cstdlib>
 #include <vector>
 
@@ -60,7 +61,10 @@ struct Geo {
   static constexpr int kABytes = kARows * kBK * 2;
   static constexpr int kBBytes = kBRows * kBK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
-  static constexpr int kStages = CG == 1 ? 3 : 5;
+#ifndef TNS_STAGES2
+#define TNS_STAGES2 5
+#endif
+  static constexpr int kStages = CG == 1 ? 3 : TNS_STAGES2;
   static constexpr int kEpiOff = kStages * kStageBytes;          // epilogue staging
   static constexpr int kEpiBytes = kNumEpiWarps * 3 * 2048;      // aux/out/mirror per warp
   static constexpr size_t kSmemBytes = (size_t)kEpiOff + kEpiBytes + 1024 + 512;
@@ -249,7 +253,10 @@ __device__ __forceinline__ void epi_math(int var, const Epi& E, int p, int q, co
   bad |= nf;
 }
 
-template <int CG>
+// MC = CTA pairs per cluster (CG == 2 only): with MC == 2 the two pairs of a 4-CTA cluster
+// run tiles that share their A operand rows (same job, p0 and K) and each A box is loaded
+// once and multicast to both pairs: 25% fewer L2->SM bytes per MMA.
+template <int CG, int MC>
 __global__ void __launch_bounds__(kThreads, 1)
     umma_gemm_kernel(const GemmJob* __restrict__ jobs, const TaskDesc* __restrict__ tasks, int64_t ntasks,
                      const PrecondJob* __restrict__ pjobs, unsigned* done, int nslots,
@@ -271,14 +278,19 @@ __global__ void __launch_bounds__(kThreads, 1)
   const bool tl = (dbg & 16) && blockIdx.x == 0 && lane == 0;
   const long long T0 = tl ? clock64() : 0;
 #define TL(slot) do { if (tl) atomicAdd(&g_epi_prof[slot], (unsigned long long)(clock64() - T0)); } while (0)
-  const uint32_t rank = (CG == 2) ? cluster_ctarank() : 0u;  // CTA rank within the pair
-  const int64_t cid = blockIdx.x / CG;                       // cluster (tile worker) index
-  const int64_t ncl = gridDim.x / CG;
+  const uint32_t crank = (CG == 2) ? cluster_ctarank() : 0u;  // CTA rank within the cluster
+  const uint32_t rank = crank & 1u;                            // CTA rank within the pair
+  const uint32_t pair_id = crank >> 1;                         // pair within the cluster (MC == 2)
+  const uint32_t lead = crank & ~1u;                           // cluster rank of this pair's leader
+  const int64_t cid = blockIdx.x / (CG * MC);                  // cluster (tile worker) index
+  const int64_t ncl = gridDim.x / (CG * MC);
+  // MC == 2: this pair's tile of a task
+  auto my_tile = [&](const TaskDesc& TD) -> uint64_t { return (MC == 2 && pair_id) ? TD.tile2 : TD.tile; };
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < G::kStages; ++i) {
       mbar_init(&full_bar[i], 1);
-      mbar_init(&empty_bar[i], 1);
+      mbar_init(&empty_bar[i], MC);  // one commit per pair that reads the stage
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull_bar[i], 1);
@@ -311,7 +323,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const TaskDesc TD = tasks[t];
         if (TD.kind != TK_TILE) continue;
         if (TD.dep_slot != kNoSlot) wait_phase(done + TD.dep_slot, TD.dep_target);
-        const TileInfo ti = decode_word(TD.tile);
+        const TileInfo ti = decode_word(my_tile(TD));
         const GemmJob* J = jobs + ti.job;
         const void* tmA = J->tmA;
         const void* tmB = J->tmB;
@@ -334,11 +346,20 @@ __global__ void __launch_bounds__(kThreads, 1)
           // half-storage symmetric operand: an upper-triangle block is read transposed
           const int a_e = a_mn ^ (a_sym && (k0 >> 8) > (pa >> 8));
           const int b_e = b_mn ^ (b_sym && (k0 >> 8) > (qb >> 8));
-#pragma unroll
-          for (int i = 0; i < G::kARows / 64; ++i) {
+          if constexpr (MC == 2) {
+            // A rows are the same in both pairs: this CTA loads box `pair_id` of its 128 rows
+            // for itself and its counterpart in the other pair
+            const int i = (int)pair_id;
             const int c0 = a_e ? pa + 64 * i : k0, c1 = a_e ? k0 : pa + 64 * i;
-            if constexpr (CG == 2) tma_load_2d_cg2(sa + i * kBoxBytes, tmA, &full_bar[stage], c0, c1);
-            else tma_load_2d(sa + i * kBoxBytes, tmA, &full_bar[stage], c0, c1);
+            tma_load_2d_cg2_mc(sa + i * kBoxBytes, tmA, &full_bar[stage], c0, c1,
+                               (uint16_t)((1u << crank) | (1u << (crank ^ 2u))));
+          } else {
+#pragma unroll
+            for (int i = 0; i < G::kARows / 64; ++i) {
+              const int c0 = a_e ? pa + 64 * i : k0, c1 = a_e ? k0 : pa + 64 * i;
+              if constexpr (CG == 2) tma_load_2d_cg2(sa + i * kBoxBytes, tmA, &full_bar[stage], c0, c1);
+              else tma_load_2d(sa + i * kBoxBytes, tmA, &full_bar[stage], c0, c1);
+            }
           }
 #pragma unroll
           for (int i = 0; i < G::kBRows / 64; ++i) {
@@ -364,7 +385,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int64_t t = cid; t < ntasks; t += ncl) {
         const TaskDesc TD = tasks[t];
         if (TD.kind != TK_TILE) continue;
-        const TileInfo ti = decode_word(TD.tile);
+        const TileInfo ti = decode_word(my_tile(TD));
         const GemmJob* J = jobs + ti.job;
         const uint32_t a_mn = (uint32_t)J->a_mn, b_mn = (uint32_t)J->b_mn;
         const int K = J->K;
@@ -392,10 +413,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint64_t bdesc = make_sdesc(sb + kk * b_step, b_lbo, 1024u);
             umma_bf16<CG>(d_tmem, adesc, bdesc, idesc, (kb | kk) != 0 ? 1u : 0u);
           }
-          umma_commit<CG>(&empty_bar[stage]);
+          if constexpr (MC == 2) umma_commit_mask(&empty_bar[stage], 0xF);  // both pairs' producers
+          else umma_commit<CG>(&empty_bar[stage]);
           if (++stage == G::kStages) { stage = 0; phase ^= 1; }
         }
-        umma_commit<CG>(&tfull_bar[as]);
+        if constexpr (MC == 2) umma_commit_mask(&tfull_bar[as], (uint16_t)(0x3u << lead));
+        else umma_commit<CG>(&tfull_bar[as]);
         if (++as == 2) { as = 0; aphase ^= 1; }
       }
     }
@@ -432,10 +455,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0 && TD.my_slot != kNoSlot) arrive_phase(done + TD.my_slot);
         continue;
       }
-      const TileInfo ti = decode_word(TD.tile);
+      const uint64_t tw = my_tile(TD);
+      const bool shadow = (tw & kTileShadow) != 0;  // computed for the multicast, never stored
+      const TileInfo ti = decode_word(tw);
       const Epi E = load_epi(jobs + ti.job);
       const int var = epi_variant(E);
-      const bool has_aux = epi_needs_aux(E) && !(dbg & 4);
+      const bool has_aux = epi_needs_aux(E) && !(dbg & 4) && !shadow;
       const int prow = ti.p0 + (int)rank * kBM + quad * 32;  // first of this warp's 32 rows
       const int p = prow + lane;
       const int qh = ti.q0 + half * 128;
@@ -478,7 +503,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           tc_fence_before();
           __syncwarp();
           if (lane == 0) {
-            if constexpr (CG == 2) mbar_arrive_cluster(&tempty_bar[as], 0);
+            if constexpr (CG == 2) mbar_arrive_cluster(&tempty_bar[as], lead);
             else mbar_arrive_relaxed(&tempty_bar[as]);
           }
         }
@@ -490,7 +515,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             tma_load_2d(s_aux, E.tmAux, abar, q + 32, prow);
           }
         }
-        if (dbg & 1) continue;
+        if ((dbg & 1) || shadow) continue;
         // mirrored block: transposed box in smem for the mirrored store (full storage) and/or
         // the AOL column sums (iteration-1 Gram); half storage skips the store
         const bool mir_store = ti.mirror && !E.half && !(dbg & 2);
@@ -550,7 +575,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         if (prof) { t1 = clock64(); pc[6] += t1 - t0; t0 = t1; }
       }
-      if (E.part != nullptr && p < E.P && qh < E.Q) E.part[(int64_t)p * E.part_ld + qh / 128] = rsum;
+      if (E.part != nullptr && p < E.P && qh < E.Q && !shadow) E.part[(int64_t)p * E.part_ld + qh / 128] = rsum;
       if (++as == 2) { as = 0; aphase ^= 1; }
       if (TD.my_slot != kNoSlot) {  // fused mode: this warp's part of the tile is visible
         __syncwarp();
@@ -586,14 +611,29 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
-template <int CG>
+template <int CG, int MC>
 static cudaError_t launch_cg(const GemmJob* d_jobs, const TaskDesc* d_tasks, int64_t ntasks, const PrecondJob* d_pjobs,
                              unsigned* d_done, int nslots, int64_t max_tiles, int num_sms, uint32_t* d_flags,
                              cudaStream_t stream) {
   static bool attr_set[64] = {};
+  static int max_clusters[64] = {};
   int dev = 0;
   cudaGetDevice(&dev);
-  auto kern = umma_gemm_kernel<CG>;
+  auto kern = umma_gemm_kernel<CG, MC>;
+  constexpr int kCl = CG * MC;
+  cudaLaunchConfig_t cfg = {};
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = Geo<CG>::kSmemBytes;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = kCl;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
   if (!attr_set[dev & 63]) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)Geo<CG>::kSmemBytes);
@@ -602,26 +642,23 @@ static cudaError_t launch_cg(const GemmJob* d_jobs, const TaskDesc* d_tasks, int
       e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
       if (e != cudaSuccess) return e;
     }
+    // persistent grid: as many clusters as can be co-resident (4-CTA clusters cannot use
+    // every SM of a GPC whose SM count is not a multiple of 4)
+    int nc = 0;
+    cfg.gridDim = dim3((unsigned)(num_sms / kCl * kCl));
+    if (cudaOccupancyMaxActiveClusters(&nc, kern, &cfg) != cudaSuccess || nc <= 0) {
+      cudaGetLastError();
+      nc = num_sms / kCl;
+    }
+    max_clusters[dev & 63] = nc < num_sms / kCl ? nc : num_sms / kCl;
+    if (getenv("TNS_VERBOSE")) fprintf(stderr, "umma_gemm<%d,%d>: %d co-resident clusters of %d CTAs\n", CG, MC, nc, kCl);
     attr_set[dev & 63] = true;
   }
   // persistent: one CTA (pair) per SM (pair); the fused mode uses every SM (its dependency
   // waits need all CTAs co-resident, which one CTA per SM guarantees)
-  const int64_t workers = num_sms / CG;
+  const int64_t workers = MC == 1 ? num_sms / CG : max_clusters[dev & 63];
   const int64_t nclusters = (nslots > 0 || max_tiles > workers) ? workers : max_tiles;
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)(nclusters * CG));
-  cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = Geo<CG>::kSmemBytes;
-  cfg.stream = stream;
-  cudaLaunchAttribute attr[2];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = CG;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[1].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 2;
+  cfg.gridDim = dim3((unsigned)(nclusters * kCl));
   static int dbg = -1;
   if (dbg < 0) {  // measurement knob (never set in production): TNS_DBG bits 1 skip epilogue,
     const char* e = getenv("TNS_DBG");  // 2 skip mirrored stores, 4 skip aux prefetch, 8 counters, 16 timeline
@@ -634,8 +671,10 @@ cudaError_t launch_umma_gemm(const GemmJob* d_jobs, const TaskDesc* d_tasks, int
                              unsigned* d_done, int nslots, int64_t max_tiles, int cg, int num_sms, uint32_t* d_flags,
                              cudaStream_t stream) {
   if (ntasks <= 0) return cudaSuccess;
-  return cg == 2 ? launch_cg<2>(d_jobs, d_tasks, ntasks, d_pjobs, d_done, nslots, max_tiles, num_sms, d_flags, stream)
-                 : launch_cg<1>(d_jobs, d_tasks, ntasks, d_pjobs, d_done, nslots, max_tiles, num_sms, d_flags, stream);
+  if (cg == 4)  // two CTA pairs per cluster, A operand multicast (tasks carry tile pairs)
+    return launch_cg<2, 2>(d_jobs, d_tasks, ntasks, d_pjobs, d_done, nslots, max_tiles, num_sms, d_flags, stream);
+  return cg == 2 ? launch_cg<2, 1>(d_jobs, d_tasks, ntasks, d_pjobs, d_done, nslots, max_tiles, num_sms, d_flags, stream)
+                 : launch_cg<1, 1>(d_jobs, d_tasks, ntasks, d_pjobs, d_done, nslots, max_tiles, num_sms, d_flags, stream);
 }
 
 cudaError_t umma_epi_prof(unsigned long long* out, bool reset) {
@@ -667,6 +706,33 @@ void umma_tile_list(const GemmJob& J, uint32_t job, int cg, std::vector<uint64_t
     const int gsz = tp - g0 < kGroupP ? tp - g0 : kGroupP;
     for (int qb = 0; qb < tq; ++qb)
       for (int i = 0; i < gsz; ++i) out.push_back(pack_tile(job, (g0 + i) * tm, qb * kBN, false));
+  }
+}
+
+// Tiles of job `job` as multicast pairs sharing p0 (A operand rows): (p, q) with the next
+// q of the same p in the same order as umma_tile_list; an odd one out gets a shadow partner.
+void umma_pair_list(const GemmJob& J, uint32_t job, std::vector<std::pair<uint64_t, uint64_t>>& out) {
+  auto emit = [&](uint64_t a, bool has_b, uint64_t b) { out.push_back({a, has_b ? b : (a | kTileShadow)}); };
+  if (J.sym) {
+    const int nb = (J.P + kSymBlock - 1) / kSymBlock;
+    for (int bi = 0; bi < nb; ++bi)
+      for (int bj = 0; bj <= bi; bj += 2) {
+        const bool two = bj + 1 <= bi;
+        emit(pack_tile(job, bi * kSymBlock, bj * kSymBlock, bi != bj), two,
+             two ? pack_tile(job, bi * kSymBlock, (bj + 1) * kSymBlock, bi != bj + 1) : 0);
+      }
+    return;
+  }
+  const int tm = kBM * 2;
+  const int tp = (J.P + tm - 1) / tm, tq = (J.Q + kBN - 1) / kBN;
+  for (int g0 = 0; g0 < tp; g0 += kGroupP) {
+    const int gsz = tp - g0 < kGroupP ? tp - g0 : kGroupP;
+    for (int qb = 0; qb < tq; qb += 2)
+      for (int i = 0; i < gsz; ++i) {
+        const bool two = qb + 1 < tq;
+        emit(pack_tile(job, (g0 + i) * tm, qb * kBN, false), two,
+             two ? pack_tile(job, (g0 + i) * tm, (qb + 1) * kBN, false) : 0);
+      }
   }
 }
 

@@ -45,9 +45,10 @@ CASES = [
 ]
 
 
-@pytest.fixture(params=[0, 3, 4], ids=["auto", "fused", "per-step"])
+@pytest.fixture(params=[0, 3, 4, 6], ids=["auto", "fused", "per-step", "multicast"])
 def launch_mode(request):
-    """0 auto, 3 all steps in one fused launch, 4 one launch per step."""
+    """0 auto, 3 all steps in one fused launch, 4 one launch per step, 6 per-step launches on
+    4-CTA clusters (two CTA pairs sharing the A operand by TMA multicast)."""
     old = ns.set_path(request.param)
     yield request.param
     ns.set_path(old)
@@ -161,7 +162,7 @@ def test_fused_equals_per_step_bitwise():
     shapes = [(256, 2304), (64, 216), (768, 768), (520, 136)]
     xs = [I.gaussian(m, n, seed=90 + i) for i, (m, n) in enumerate(shapes)]
     res = {}
-    for path in (3, 4):
+    for path in (3, 4, 6):
         old = ns.set_path(path)
         try:
             ts = [torch.from_numpy(x).to(torch.bfloat16).cuda() for x in xs]
@@ -170,8 +171,9 @@ def test_fused_equals_per_step_bitwise():
             res[path] = [t.float().cpu().numpy() for t in ts]
         finally:
             ns.set_path(old)
-    for a, b in zip(res[3], res[4]):
+    for a, b, c in zip(res[3], res[4], res[6]):
         assert np.array_equal(a, b)
+        assert np.array_equal(a, c)
 
 
 def test_zero_column_flag():
