@@ -486,19 +486,47 @@ def run_extras(args, peaks):
     fs = sum(ns_flops(m, n, 4) for m, n in shapes)
     out["gpt2_small"] = {"ms": round(ms_s, 4), "tflops_alg": round(fs / (ms_s * 1e-3) / 1e12, 1),
                          "matrices": len(shapes)}
-    # --- CIFAR conv set (config 3), latency-bound
+    def small(fn):
+        """Latency of one call (events around it, median) and of a CUDA-graph replay of it
+        (the launch-bound configs: host enqueue time excluded), plus launches per call."""
+        fn()
+        torch.cuda.synchronize()
+        c0 = ns.launch_count()
+        fn()
+        torch.cuda.synchronize()
+        nl = ns.launch_count() - c0
+        us = time_calls(fn, reps, None) * 1e3
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            fn()
+        torch.cuda.current_stream().wait_stream(s)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            fn()
+        g.replay()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(50):
+            g.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        return us, e0.elapsed_time(e1) / 50 * 1e3, nl
+
+    # --- CIFAR conv set (config 3), latency-bound: the two N = 64 matrices run in the
+    #     cluster-resident kernel on a side stream, the four N = 256 ones in the step engine
     shapes = I.shape_set("cifar")
     xs = [torch.from_numpy(x).to(torch.bfloat16).cuda() for x in make_inputs(shapes, 3)]
     outs = [torch.empty_like(t) for t in xs]
-    ns.orthogonalize_list(xs, out=outs, iters=4)
-    ms_c = time_calls(lambda: ns.orthogonalize_list(xs, out=outs, iters=4), reps, None)
-    out["cifar"] = {"us": round(ms_c * 1e3, 1), "launches": 13, "matrices": len(shapes)}
-    # --- config 1: one 128 x 128 fp32 matrix, fp32 "exact" mode
+    us, gus, nl = small(lambda: ns.orthogonalize_list(xs, out=outs, iters=4))
+    out["cifar"] = {"us": round(us, 1), "us_graph_replay": round(gus, 1), "launches": nl, "matrices": len(shapes)}
+    # --- config 1: one 128 x 128 fp32 matrix, fp32 "exact" mode (cluster-resident kernel)
     x1 = torch.from_numpy(I.gaussian(128, 128, seed=I.matrix_seed(1, 0), bf16=False)).cuda()
     o1 = torch.empty_like(x1)
-    ns.orthogonalize_list([x1], out=[o1], iters=4)
-    ms_1 = time_calls(lambda: ns.orthogonalize_list([x1], out=[o1], iters=4), reps, None)
-    out["fp32_128"] = {"us": round(ms_1 * 1e3, 1), "tflops_alg": round(ns_flops(128, 128, 4) / (ms_1 * 1e-3) / 1e12, 3)}
+    us, gus, nl = small(lambda: ns.orthogonalize_list([x1], out=[o1], iters=4))
+    out["fp32_128"] = {"us": round(us, 1), "us_graph_replay": round(gus, 1), "launches": nl,
+                       "tflops_alg": round(ns_flops(128, 128, 4) / (us * 1e-6) / 1e12, 3)}
     return out
 
 
