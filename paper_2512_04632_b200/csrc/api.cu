@@ -161,6 +161,7 @@ struct Phase {
   int64_t total;    // tiles (GEMM/SIMT) or items (PRECOND)
   int64_t total_rows;
   bool vec8;
+  bool lane_rows = false;  // PH_PRECOND: AOL partials, every part_ld <= kSeqPartials
   int gemm_kind;  // profiling kind: 0 GRAM, 2 POLY, 3 XB
   size_t tiles_off = 0;   // offset of the TaskDesc list (PH_GEMM / PH_FUSED)
   size_t jobs_off = 0;    // offset of the GemmJob array (PH_FUSED)
@@ -567,6 +568,9 @@ static ns_status build_plan(Plan& P, HostTables& H, DevCtx* dc, const float* coe
           ph.total = st.items;
           ph.total_rows = st.rows;
           ph.vec8 = st.vec8;
+          ph.lane_rows = true;
+          for (const PrecondJob& pj : st.pj)
+            ph.lane_rows = ph.lane_rows && pj.precond == 2 && pj.part != nullptr && pj.part_ld <= kSeqPartials;
           P.phases.push_back(ph);
         }
       }
@@ -719,7 +723,7 @@ static ns_status enqueue_plan(Plan& P, DevCtx* dc, cudaStream_t stream) {
         ProfScope ps(1, stream);
         CU_TRY(launch_precondition(reinterpret_cast<const PrecondJob*>(dbase + ph.dev_off), ph.njobs,
                                    ph.total_rows, ph.total, ph.vec8, P.dtype == NS_BF16, P.barrier,
-                                   dc->flags, stream));
+                                   dc->flags, ph.lane_rows, stream));
         ++g_launches;
         break;
       }
@@ -1229,7 +1233,7 @@ ns_status nsx_precondition(void* A, int64_t N, ns_precond precond, float* s, ns_
   CU_TRY(cudaMemcpy(reinterpret_cast<uint8_t*>(dmem) + 256, &J, sizeof(J), cudaMemcpyHostToDevice));
   cudaError_t e = launch_precondition(reinterpret_cast<const PrecondJob*>(reinterpret_cast<uint8_t*>(dmem) + 256), 1,
                                       N, vec8 ? N * N / 8 : N * N, vec8, dtype == NS_BF16,
-                                      reinterpret_cast<unsigned*>(dmem), dc->flags, strm);
+                                      reinterpret_cast<unsigned*>(dmem), dc->flags, false, strm);
   ++g_launches;
   cudaError_t e2 = cudaStreamSynchronize(strm);
   cudaFree(dmem);

@@ -88,6 +88,9 @@ struct SimtJob {
 constexpr int kSimtTile = 64;
 
 // Per-matrix descriptor for the preconditioning kernel (AOL / Frobenius).
+// AOL rows with at most this many Gram-epilogue partial slots (N <= 1536) are summed by
+// one lane in slot order; larger ones by a warp tree (precond_rows.cuh).
+constexpr int kSeqPartials = 64;
 struct PrecondJob {
   void* A;          // N x N symmetric Gram, in place -> A1
   float* s;         // N

@@ -33,9 +33,11 @@ cudaError_t launch_simt_gemm(const SimtJob* d_jobs, int njobs, int64_t total_til
 // Fused AOL / Frobenius preconditioner (simt.cu): row-abs-sum (or trace) + rsqrt, grid
 // barrier, then A <- diag(s) A diag(s).  `barrier` points at two zero-initialised uint32
 // words (arrival count, generation) owned by the caller; the barrier resets itself.  vec8 = all N are multiples of 8 (16-byte vectors).
+// lane_rows: AOL from Gram partials with part_ld <= kSeqPartials for every job -> phase 1
+// runs one lane per row (precond_rows.cuh, same summation order as the fused mode).
 cudaError_t launch_precondition(const PrecondJob* d_jobs, int njobs, int64_t total_rows,
                                 int64_t total_elems_or_vecs, bool vec8, bool is_bf16,
-                                unsigned* d_barrier, uint32_t* d_flags, cudaStream_t stream);
+                                unsigned* d_barrier, uint32_t* d_flags, bool lane_rows, cudaStream_t stream);
 
 // Whole NS of `njobs` small matrices, one cluster of kClCtas CTAs each (cluster_ns.cu).
 // d_coeffs: 3*iters floats in device memory; smem_bytes: max cl_layout(..).floats * 4.

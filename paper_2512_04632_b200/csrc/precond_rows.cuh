@@ -34,17 +34,39 @@ __device__ __forceinline__ float warp_sum(float v) {
   return v;
 }
 
+// AOL row sum of |A0| for row i from the Gram epilogue's partials: direct 128-column slots
+// of the blocks <= bi, mirrored 32-row slots of the blocks > bi (each |A0_ij| counted once),
+// summed sequentially in slot order (independent loads, fixed order: deterministic).
+__device__ __forceinline__ float aol_rowsum_partials(const PrecondJob& J, int i) {
+  const int N = J.N, bi = i / 256;
+  const int n1 = (N + 127) / 128, n2 = (N + 31) / 32;
+  const float* pr = J.part + (int64_t)i * J.part_ld;
+  const int d_end = min(2 * (bi + 1), n1), m_beg = min(8 * (bi + 1), n2);
+  float acc = 0.f;
+  for (int k = 0; k < d_end; ++k) acc += pr[k];
+  for (int k = m_beg; k < n2; ++k) acc += pr[n1 + k];
+  return acc;
+}
+
 // Phase 1 for row i: s_i (AOL, Eq. 8) or, for row 0, the whole Frobenius s (Eq. 10).
 // Fixed-order reductions: deterministic.
 template <typename T, bool VEC8>
 __device__ __forceinline__ void precond_row_s(const PrecondJob& J, int i, int lane, uint32_t& fl) {
   const T* __restrict__ A = reinterpret_cast<const T*>(J.A);
   const int N = J.N;
-  if (J.precond == 2 && J.part != nullptr) {
-    // AOL from the Gram epilogue's partials: direct 128-column slots of blocks <= bi,
-    // mirrored 32-row slots of blocks > bi (each |A0_ij| counted exactly once)
+  if (J.precond == 2 && J.part != nullptr && J.part_ld <= kSeqPartials) {
+    // AOL from the Gram epilogue's partials, few per row: one lane sums them in slot order
+    // (the same order as the standalone kernel's lane-per-row loop: bitwise equal s)
+    if (lane == 0) {
+      const float r = aol_rowsum_partials(J, i);
+      J.s[i] = r > 0.f ? rsqrtf(r) : 0.f;
+      if (!(r > 0.f)) fl |= 1u;
+      if (!isfinite(r)) fl |= 2u;
+    }
+  } else if (J.precond == 2 && J.part != nullptr) {
+    // many partials per row (large N): warp-parallel, fixed-order tree
     const int bi = i / 256;
-    const int n1 = (N + 127) / 128, n2 = (N + 31) / 32;
+    const int n1 = (J.N + 127) / 128, n2 = (J.N + 31) / 32;
     const float* pr = J.part + (int64_t)i * J.part_ld;
     const int d_end = min(2 * (bi + 1), n1), m_beg = min(8 * (bi + 1), n2);
     float acc = 0.f;
@@ -97,21 +119,34 @@ __device__ __forceinline__ void precond_row_scale(const PrecondJob& J, int i, in
   const float si = J.s[i];
   T* Ai = reinterpret_cast<T*>(J.A) + (int64_t)i * J.N;
   if (VEC8 && sizeof(T) == 2) {
-    for (int j = lane * 8; j < N; j += 256) {
-      uint4* pv = reinterpret_cast<uint4*>(Ai + j);
-      uint4 u = *pv;
-      const float4 s0 = *reinterpret_cast<const float4*>(J.s + j);
-      const float4 s1 = *reinterpret_cast<const float4*>(J.s + j + 4);
-      const float sj[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
-      uint32_t w[4] = {u.x, u.y, u.z, u.w};
+    // up to 4 vectors per lane in flight: all loads of a batch before any store
+    for (int j0 = lane * 8; j0 < N; j0 += 4 * 256) {
+      uint4 u[4];
+      float4 s0[4], s1[4];
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const float lo = (si * __uint_as_float(w[e] << 16)) * sj[2 * e];
-        const float hi = (si * __uint_as_float(w[e] & 0xFFFF0000u)) * sj[2 * e + 1];
-        w[e] = (uint32_t)st_conv<uint16_t>(lo) | ((uint32_t)st_conv<uint16_t>(hi) << 16);
+      for (int v = 0; v < 4; ++v) {
+        const int j = j0 + v * 256;
+        if (j < N) {
+          u[v] = *reinterpret_cast<const uint4*>(Ai + j);
+          s0[v] = *reinterpret_cast<const float4*>(J.s + j);
+          s1[v] = *reinterpret_cast<const float4*>(J.s + j + 4);
+        }
       }
-      u.x = w[0]; u.y = w[1]; u.z = w[2]; u.w = w[3];
-      *pv = u;
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        const int j = j0 + v * 256;
+        if (j < N) {
+          const float sj[8] = {s0[v].x, s0[v].y, s0[v].z, s0[v].w, s1[v].x, s1[v].y, s1[v].z, s1[v].w};
+          uint32_t w[4] = {u[v].x, u[v].y, u[v].z, u[v].w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float lo = (si * __uint_as_float(w[e] << 16)) * sj[2 * e];
+            const float hi = (si * __uint_as_float(w[e] & 0xFFFF0000u)) * sj[2 * e + 1];
+            w[e] = (uint32_t)st_conv<uint16_t>(lo) | ((uint32_t)st_conv<uint16_t>(hi) << 16);
+          }
+          *reinterpret_cast<uint4*>(Ai + j) = make_uint4(w[0], w[1], w[2], w[3]);
+        }
+      }
     }
   } else {
     for (int j = lane; j < N; j += 32) Ai[j] = st_conv<T>((si * ld_val<T>(Ai + j)) * J.s[j]);

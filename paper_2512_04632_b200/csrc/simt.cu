@@ -145,7 +145,7 @@ __device__ __forceinline__ void grid_barrier(unsigned* bar) {
 template <typename T, bool VEC8>
 __global__ void __launch_bounds__(256)
     precondition_kernel(const PrecondJob* __restrict__ jobs, int njobs, int64_t total_rows,
-                        int64_t total_items, unsigned* barrier, uint32_t* __restrict__ flags) {
+                        int64_t total_items, unsigned* barrier, uint32_t* __restrict__ flags, int lane_rows) {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   asm volatile("griddepcontrol.wait;" ::: "memory");  // A0 comes from the preceding Gram launch
   (void)total_items;
@@ -157,7 +157,22 @@ __global__ void __launch_bounds__(256)
   const int64_t per = (total_rows + nwarps - 1) / nwarps;
   const int64_t r_beg = gwarp * per, r_end = min(total_rows, r_beg + per);
   // ---- phase 1: scaling vector s (Eq. 8 / Eq. 10)
-  if (r_beg < r_end) {
+  if (lane_rows) {  // AOL from partials, every job with part_ld <= kSeqPartials
+    // AOL from partials: one LANE per row (<= 40 independent loads each), 32 rows per warp
+    // at a time -- the row sums are short, so rows, not columns, carry the parallelism
+    for (int64_t row0 = r_beg; row0 < r_end; row0 += 32) {
+      const int64_t row = row0 + lane;
+      if (row < r_end) {
+        const int jb = find_pjob(jobs, njobs, row);
+        const PrecondJob& J = jobs[jb];
+        const int i = (int)(row - J.row_start);
+        const float r = aol_rowsum_partials(J, i);
+        J.s[i] = r > 0.f ? rsqrtf(r) : 0.f;
+        if (!(r > 0.f)) fl |= 1u;
+        if (!isfinite(r)) fl |= 2u;
+      }
+    }
+  } else if (r_beg < r_end) {
     int jb = find_pjob(jobs, njobs, r_beg);
     for (int64_t row = r_beg; row < r_end; ++row) {
       while (jb + 1 < njobs && jobs[jb + 1].row_start <= row) ++jb;
@@ -179,7 +194,7 @@ __global__ void __launch_bounds__(256)
 template <typename T, bool V>
 static cudaError_t launch_precond_t(const PrecondJob* d_jobs, int njobs, int64_t total_rows,
                                     int64_t total_items, unsigned* d_barrier, uint32_t* d_flags,
-                                    cudaStream_t stream) {
+                                    int lane_rows, cudaStream_t stream) {
   auto kern = precondition_kernel<T, V>;
   int dev = 0, sms = 0, occ = 0;
   cudaGetDevice(&dev);
@@ -200,17 +215,18 @@ static cudaError_t launch_precond_t(const PrecondJob* d_jobs, int njobs, int64_t
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 2;
-  return cudaLaunchKernelEx(&cfg, kern, d_jobs, njobs, total_rows, total_items, d_barrier, d_flags);
+  return cudaLaunchKernelEx(&cfg, kern, d_jobs, njobs, total_rows, total_items, d_barrier, d_flags, lane_rows);
 }
 
 cudaError_t launch_precondition(const PrecondJob* d_jobs, int njobs, int64_t total_rows,
                                 int64_t total_items, bool vec8, bool is_bf16, unsigned* d_barrier,
-                                uint32_t* d_flags, cudaStream_t stream) {
+                                uint32_t* d_flags, bool lane_rows, cudaStream_t stream) {
+  const int lr = lane_rows ? 1 : 0;
   if (is_bf16) {
-    return vec8 ? launch_precond_t<uint16_t, true>(d_jobs, njobs, total_rows, total_items, d_barrier, d_flags, stream)
-                : launch_precond_t<uint16_t, false>(d_jobs, njobs, total_rows, total_items, d_barrier, d_flags, stream);
+    return vec8 ? launch_precond_t<uint16_t, true>(d_jobs, njobs, total_rows, total_items, d_barrier, d_flags, lr, stream)
+                : launch_precond_t<uint16_t, false>(d_jobs, njobs, total_rows, total_items, d_barrier, d_flags, lr, stream);
   }
-  return launch_precond_t<float, false>(d_jobs, njobs, total_rows, total_items, d_barrier, d_flags, stream);
+  return launch_precond_t<float, false>(d_jobs, njobs, total_rows, total_items, d_barrier, d_flags, lr, stream);
 }
 
 }  // namespace tns
