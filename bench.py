@@ -539,7 +539,7 @@ def main():
     ap.add_argument("--workload", default="gpt2-medium")
     ap.add_argument("--iters", type=int, default=4)
     ap.add_argument("--e2e-steps", type=int, default=5)
-    ap.add_argument("--e2e-buckets", type=int, default=6)
+    ap.add_argument("--e2e-buckets", type=int, default=48)
     ap.add_argument("--buckets", type=int, default=4, help="all-gather buckets at N > 1 (NCCL)")
     ap.add_argument("--collective", choices=["fused", "nccl"], default="fused",
                     help="N > 1: fused peer stores in the last epilogue, or NCCL all-gathers")

@@ -201,7 +201,7 @@ struct Plan {
 
 static std::map<std::vector<uint64_t>, std::unique_ptr<Plan>> g_plans;
 static uint64_t g_tick = 0;
-static const size_t kMaxPlans = 32;
+static const size_t kMaxPlans = 256;  // distinct problem lists (e.g. buckets of a pipeline)
 
 static size_t elem_size(ns_dtype d) { return d == NS_BF16 ? 2 : 4; }
 

@@ -268,14 +268,27 @@ def orthogonalize_host(host_xs: Sequence[torch.Tensor], group=None, iters: int =
     on = dist.is_initialized()
     world = dist.get_world_size(group) if on else 1
     rank = dist.get_rank(group) if on else 0
-    shapes = [tuple(t.shape) for t in host_xs]
     dtype = host_xs[0].dtype
-    plan = make_plan(shapes, world, iters, buckets)
-    key = ("host", tuple(shapes), world, buckets, dtype, str(device), id(group))
-    dev_in = _cached(key + ("in",), lambda: [torch.empty(s, dtype=dtype, device=device) for s in shapes])
-    buf = _cached(key + ("gather",), lambda: torch.empty(plan.total, dtype=dtype, device=device))
-    hout = _cached(key + ("hout",), lambda: torch.empty(plan.total, dtype=dtype).pin_memory())
-    views = [buf[o:o + m * n].view(m, n) for o, (m, n) in zip(plan.offsets, shapes)]
+    # steady state (same host tensors every step): buffers, views, per-bucket copy lists and
+    # prepared NS calls are built once, so many small buckets stay cheap on the host
+    ckey = ("hostcall", tuple(id(t) for t in host_xs), world, rank, buckets, iters, precond,
+            None if coeffs is None else tuple(map(tuple, coeffs)), id(group), str(device))
+    ent = _BUFFERS.get(ckey)
+    if ent is None:
+        shapes = [tuple(t.shape) for t in host_xs]
+        plan = make_plan(shapes, world, iters, buckets)
+        key = ("host", tuple(shapes), world, buckets, dtype, str(device), id(group))
+        dev_in = _cached(key + ("in",), lambda: [torch.empty(s, dtype=dtype, device=device) for s in shapes])
+        buf = _cached(key + ("gather",), lambda: torch.empty(plan.total, dtype=dtype, device=device))
+        hout = _cached(key + ("hout",), lambda: torch.empty(plan.total, dtype=dtype).pin_memory())
+        views = [buf[o:o + m * n].view(m, n) for o, (m, n) in zip(plan.offsets, shapes)]
+        from .api import PreparedCall
+        calls = [PreparedCall([dev_in[i] for i in pr[rank]], [views[i] for i in pr[rank]], iters, precond, coeffs)
+                 if pr[rank] and device.type == "cuda" else None for pr in plan.buckets]
+        ent = {"plan": plan, "dev_in": dev_in, "buf": buf, "hout": hout, "calls": calls,
+               "outs": [hout[o:o + m * n].view(m, n) for o, (m, n) in zip(plan.offsets, shapes)]}
+        _BUFFERS[ckey] = ent
+    plan, dev_in, buf, hout = ent["plan"], ent["dev_in"], ent["buf"], ent["hout"]
     cur = torch.cuda.current_stream(device)
     h2d, d2h = _stream(device, "h2d"), _stream(device, "d2h")
     comm = _stream(device, "comm") if on else None
@@ -288,9 +301,7 @@ def orthogonalize_host(host_xs: Sequence[torch.Tensor], group=None, iters: int =
                 dev_in[i].copy_(host_xs[i], non_blocking=True)
         cur.wait_stream(h2d)
         if mine:
-            from .api import orthogonalize_list
-            orthogonalize_list([dev_in[i] for i in mine], out=[views[i] for i in mine],
-                               iters=iters, precond=precond, coeffs=coeffs)
+            ent["calls"][b]()
         src = cur
         if on:
             comm.wait_stream(cur)
@@ -305,4 +316,4 @@ def orthogonalize_host(host_xs: Sequence[torch.Tensor], group=None, iters: int =
     cur.wait_stream(d2h)
     if on:
         cur.wait_stream(comm)
-    return [hout[o:o + m * n].view(m, n) for o, (m, n) in zip(plan.offsets, shapes)]
+    return list(ent["outs"])
