@@ -4,7 +4,7 @@
 //                          (U in bf16 = the NS input, orthogonalised in place afterwards)
 //   muon_apply_kernel    : W <- W (1 - lr wd) - lr * max(1, m/n)^(1/2) * U
 // Both are HBM-bound elementwise passes, grouped over all matrices of a step (blockIdx.y =
-// matrix), 4 elements per thread with vector loads when aligned.  Reading R13.
+// matrix), 8 elements per thread with 16-byte vector accesses when aligned.  Reading R13.
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -22,6 +22,33 @@ template <typename T> __device__ __forceinline__ void stf(T* p, int64_t i, float
 template <> __device__ __forceinline__ void stf<float>(float* p, int64_t i, float v) { p[i] = v; }
 template <> __device__ __forceinline__ void stf<uint16_t>(uint16_t* p, int64_t i, float v) { p[i] = tobf(v); }
 
+// 8 consecutive elements as fp32 (16-byte vector loads / stores; the caller checks alignment)
+__device__ __forceinline__ void ld8(const float* p, float (&v)[8]) {
+  const float4 a = *reinterpret_cast<const float4*>(p), b = *reinterpret_cast<const float4*>(p + 4);
+  v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+}
+__device__ __forceinline__ void ld8(const uint16_t* p, float (&v)[8]) {
+  const uint4 u = *reinterpret_cast<const uint4*>(p);
+  const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    v[2 * e] = __uint_as_float(w[e] << 16);
+    v[2 * e + 1] = __uint_as_float(w[e] & 0xFFFF0000u);
+  }
+}
+__device__ __forceinline__ void st8(float* p, const float (&v)[8]) {
+  *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
+  *reinterpret_cast<float4*>(p + 4) = make_float4(v[4], v[5], v[6], v[7]);
+}
+__device__ __forceinline__ void st8(uint16_t* p, const float (&v)[8]) {
+  uint32_t w[4];
+#pragma unroll
+  for (int e = 0; e < 4; ++e) w[e] = (uint32_t)tobf(v[2 * e]) | ((uint32_t)tobf(v[2 * e + 1]) << 16);
+  *reinterpret_cast<uint4*>(p) = make_uint4(w[0], w[1], w[2], w[3]);
+}
+
+// Grid-stride over 8-element groups (vec: every buffer of the job is 16-byte aligned and
+// numel % 8 == 0; otherwise element by element).  Elementwise, HBM-bound.
 template <typename TG>
 __global__ void __launch_bounds__(256) muon_momentum_kernel(const MuonJob* __restrict__ jobs, float beta,
                                                             int nesterov) {
@@ -29,16 +56,29 @@ __global__ void __launch_bounds__(256) muon_momentum_kernel(const MuonJob* __res
   const TG* G = reinterpret_cast<const TG*>(J.G);
   uint16_t* U = reinterpret_cast<uint16_t*>(J.U);
   const float ob = 1.0f - beta;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x * 4;
-  for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4; i < J.numel; i += stride) {
+  const bool vec = ((J.numel & 7) == 0) && !((reinterpret_cast<uintptr_t>(J.G) | reinterpret_cast<uintptr_t>(J.M) |
+                                               reinterpret_cast<uintptr_t>(J.U)) & 15);
+  const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, nt = (int64_t)gridDim.x * blockDim.x;
+  if (vec) {
+    for (int64_t i = t0 * 8; i < J.numel; i += nt * 8) {
+      float g[8], m[8], u[8];
+      ld8(G + i, g);
+      ld8(J.M + i, m);
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      if (i + e >= J.numel) break;
-      const float g = ldf<TG>(G, i + e);
-      const float m = fmaf(beta, J.M[i + e], ob * g);
-      J.M[i + e] = m;
-      U[i + e] = tobf(nesterov ? fmaf(ob, g, beta * m) : m);
+      for (int e = 0; e < 8; ++e) {
+        m[e] = fmaf(beta, m[e], ob * g[e]);
+        u[e] = nesterov ? fmaf(ob, g[e], beta * m[e]) : m[e];
+      }
+      st8(J.M + i, m);
+      st8(U + i, u);
     }
+    return;
+  }
+  for (int64_t i = t0; i < J.numel; i += nt) {
+    const float g = ldf<TG>(G, i);
+    const float m = fmaf(beta, J.M[i], ob * g);
+    J.M[i] = m;
+    U[i] = tobf(nesterov ? fmaf(ob, g, beta * m) : m);
   }
 }
 
@@ -48,18 +88,24 @@ __global__ void __launch_bounds__(256) muon_apply_kernel(const MuonJob* __restri
   TW* W = reinterpret_cast<TW*>(J.W);
   const uint16_t* O = reinterpret_cast<const uint16_t*>(J.U);
   const float keep = 1.0f - lr * wd, step = lr * J.scale;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x * 4;
-  for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4; i < J.numel; i += stride) {
+  const bool vec = ((J.numel & 7) == 0) && !((reinterpret_cast<uintptr_t>(J.W) | reinterpret_cast<uintptr_t>(J.U)) & 15);
+  const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, nt = (int64_t)gridDim.x * blockDim.x;
+  if (vec) {
+    for (int64_t i = t0 * 8; i < J.numel; i += nt * 8) {
+      float w[8], o[8];
+      ld8(W + i, w);
+      ld8(O + i, o);
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      if (i + e >= J.numel) break;
-      stf<TW>(W, i + e, fmaf(-step, bfv(O[i + e]), ldf<TW>(W, i + e) * keep));
+      for (int e = 0; e < 8; ++e) w[e] = fmaf(-step, o[e], w[e] * keep);
+      st8(W + i, w);
     }
+    return;
   }
+  for (int64_t i = t0; i < J.numel; i += nt) stf<TW>(W, i, fmaf(-step, bfv(O[i]), ldf<TW>(W, i) * keep));
 }
 
 static dim3 muon_grid(int64_t max_numel, int count, int sms) {
-  int64_t want = (max_numel + 1023) / 1024;
+  int64_t want = (max_numel + 2047) / 2048;  // 8 elements per thread
   const int64_t cap = (int64_t)sms * 8 / (count > 0 ? count : 1) + 1;
   if (want > cap) want = cap;
   if (want < 1) want = 1;
