@@ -15,7 +15,8 @@ ns = pytest.importorskip("paper_2512_04632_b200")
 
 @pytest.mark.parametrize("wdt", [torch.float32, torch.bfloat16])
 def test_turbo_muon_two_steps_vs_oracle(wdt):
-    shapes = [(768, 768), (3072, 768), (768, 3072), (64, 576)]
+    # (100, 37): numel % 8 != 0 -> the element-wise fallback of the momentum/update kernels
+    shapes = [(768, 768), (3072, 768), (768, 3072), (64, 576), (100, 37)]
     lr, beta, wd = 0.05, 0.9, 0.01
     ws = [I.gaussian(m, n, seed=200 + i, bf16=(wdt == torch.bfloat16)) for i, (m, n) in enumerate(shapes)]
     params = [torch.nn.Parameter(torch.from_numpy(w).to(wdt).cuda()) for w in ws]
