@@ -21,6 +21,10 @@ FLAGS = [
     "-Xcompiler", "-fPIC,-O2", "-shared",
     "-I", os.path.join(ROOT, "include"),
 ]
+# Measurement build (never the default): TNS_MEASURE=1 compiles in the clock64 epilogue
+# counters / timeline read through nsx_epilogue_counters under TNS_DBG bits 8 and 16.
+if os.environ.get("TNS_MEASURE"):
+    FLAGS += ["-DTNS_MEASURE=1"]
 
 
 def _stale() -> bool:

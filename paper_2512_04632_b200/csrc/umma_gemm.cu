@@ -50,7 +50,15 @@ namespace tns {
 // L2->SM operand traffic per FLOP versus two independent 128 x 256 CTAs.
 constexpr int kBoxBytes = 64 * 64 * 2;  // one 64 x 64 bf16 TMA box
 constexpr int kNumEpiWarps = 8;
-constexpr int kThreads = (4 + kNumEpiWarps) * 32;  // 384
+// Clock64 measurement counters (TNS_DBG bits 8 and 16) cost registers: compiled in only
+// with -DTNS_MEASURE=1 (`TNS_MEASURE=1 python paper_2512_04632_b200/build.py`; tools/time_kernels.py,
+// tools/one_case.py read them).
+#ifndef TNS_MEASURE
+#define TNS_MEASURE 0
+#endif
+constexpr bool kMeasure = TNS_MEASURE != 0;
+constexpr int kEpiWarp0 = 2;                        // epilogue = warps 2..9 (TMEM lane quarter = warp % 4)
+constexpr int kThreads = (kEpiWarp0 + kNumEpiWarps) * 32;  // 320: up to 204 registers per thread
 constexpr uint32_t kTmemCols = 2 * kBN;            // double-buffered accumulator
 
 template <int CG>
@@ -62,11 +70,12 @@ struct Geo {
   static constexpr int kBBytes = kBRows * kBK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
 #ifndef TNS_STAGES2
-#define TNS_STAGES2 5
+#define TNS_STAGES2 4
 #endif
   static constexpr int kStages = CG == 1 ? 3 : TNS_STAGES2;
   static constexpr int kEpiOff = kStages * kStageBytes;          // epilogue staging
-  static constexpr int kEpiBytes = kNumEpiWarps * 3 * 2048;      // aux/out/mirror per warp
+  // per epilogue warp: 2 aux boxes, 2 output boxes (double-buffered), 1 mirror box
+  static constexpr int kEpiBytes = kNumEpiWarps * 5 * 2048;
   static constexpr size_t kSmemBytes = (size_t)kEpiOff + kEpiBytes + 1024 + 512;
 };
 
@@ -269,13 +278,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* empty_bar = full_bar + G::kStages;
   uint64_t* tfull_bar = empty_bar + G::kStages;
   uint64_t* tempty_bar = tfull_bar + 2;
-  uint64_t* aux_bar = tempty_bar + 2;  // one per epilogue warp
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aux_bar + kNumEpiWarps);
+  uint64_t* aux_bar = tempty_bar + 2;  // two per epilogue warp (double-buffered aux box)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aux_bar + 2 * kNumEpiWarps);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   // TNS_DBG bit 16: latency timeline of CTA 0 (cycles since kernel entry, summed over launches)
-  const bool tl = (dbg & 16) && blockIdx.x == 0 && lane == 0;
+  const bool tl = kMeasure && (dbg & 16) && blockIdx.x == 0 && lane == 0;
   const long long T0 = tl ? clock64() : 0;
 #define TL(slot) do { if (tl) atomicAdd(&g_epi_prof[slot], (unsigned long long)(clock64() - T0)); } while (0)
   const uint32_t crank = (CG == 2) ? cluster_ctarank() : 0u;  // CTA rank within the cluster
@@ -296,7 +305,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&tfull_bar[i], 1);
       mbar_init(&tempty_bar[i], kNumEpiWarps * CG);
     }
-    for (int i = 0; i < kNumEpiWarps; ++i) mbar_init(&aux_bar[i], 1);
+    for (int i = 0; i < 2 * kNumEpiWarps; ++i) mbar_init(&aux_bar[i], 1);
     fence_mbar_init();
   }
   if (warp == 1) {
@@ -422,19 +431,22 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (++as == 2) { as = 0; aphase ^= 1; }
       }
     }
-  } else if (warp >= 4) {
+  } else if (warp >= kEpiWarp0) {
     // ------------------------------------------------------------------ epilogue
-    const int ew = warp - 4;
+    const int ew = warp - kEpiWarp0;
     const int quad = warp & 3;  // TMEM lanes [32*quad, 32*quad + 32)
     const int half = ew >> 2;   // 128-column half of the 256-wide tile
-    uint8_t* s_aux = smem + G::kEpiOff + ew * 6144;
-    uint8_t* s_out = s_aux + 2048;
-    uint8_t* s_mir = s_aux + 4096;
-    uint64_t* abar = aux_bar + ew;
+    // staging (2 KB boxes): aux[0..1] @ 0, 2K; out[0..1] @ 4K, 6K; mirror @ 8K
+    uint8_t* s_aux = smem + G::kEpiOff + ew * 10240;
+    uint8_t* s_out = s_aux + 4096;
+    uint8_t* s_mir = s_aux + 8192;
+    uint64_t* abar = aux_bar + 2 * ew;
     const uint32_t sa_aux = smem_u32(s_aux), sa_out = smem_u32(s_out), sa_mir = smem_u32(s_mir);
-    uint32_t as = 0, aphase = 0, xphase = 0;
+    uint32_t as = 0, aphase = 0, xph = 0;  // xph bit b: parity of aux buffer b
     bool bad = false;
-    long long pc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    // measurement counters (TNS_DBG bit 8): accumulated straight into g_epi_prof so that no
+    // register array stays live in production
+#define EPC(i, v) atomicAdd(&g_epi_prof[i], (unsigned long long)(v))
     uint32_t pfl = 0;
     for (int64_t t = cid; t < ntasks; t += ncl) {
       const TaskDesc TD = tasks[t];
@@ -465,32 +477,36 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int p = prow + lane;
       const int qh = ti.q0 + half * 128;
       float rsum = 0.f;
-      if (has_aux && lane == 0) {  // prefetch the aux chunk 0 before the accumulator is ready
-        mbar_arrive_expect_tx(abar, 2048);
-        tma_load_2d(s_aux, E.tmAux, abar, qh, prow);
+      if (has_aux && lane == 0) {  // prefetch aux chunks 0 and 1 before the accumulator is ready
+#pragma unroll
+        for (int b = 0; b < 2; ++b) {
+          mbar_arrive_expect_tx(abar + b, 2048);
+          tma_load_2d(s_aux + b * 2048, E.tmAux, abar + b, qh + 32 * b, prow);
+        }
       }
-      const bool prof = (dbg & 8) && lane == 0;
+      const bool prof = kMeasure && (dbg & 8) && lane == 0;
       long long t0 = prof ? clock64() : 0, t1;
       mbar_wait(&tfull_bar[as], aphase);
       tc_fence_after();
       if (ew == 0 && t == cid) TL(4);  // first accumulator ready
-      if (prof) { t1 = clock64(); pc[1] += t1 - t0; t0 = t1; pc[0] += 1; }
+      if (prof) { t1 = clock64(); EPC(1, t1 - t0); t0 = t1; EPC(0, 1); }
 #pragma unroll 1
       for (int c = 0; c < 4; ++c) {
         const int q = qh + c * 32;
         uint32_t r[32];
         tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(quad * 32) << 16) + as * kBN + (uint32_t)(q - ti.q0), r);
         uint32_t x[16];
+        const int xb = c & 1;  // aux / output buffer of this chunk
         if (has_aux) {
-          mbar_wait(abar, xphase);
-          if (prof) { t1 = clock64(); pc[3] += t1 - t0; t0 = t1; }
-          xphase ^= 1;
+          mbar_wait(abar + xb, (xph >> xb) & 1u);
+          if (prof) { t1 = clock64(); EPC(3, t1 - t0); t0 = t1; }
+          xph ^= 1u << xb;
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
             uint4 u;
             asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];"
                          : "=r"(u.x), "=r"(u.y), "=r"(u.z), "=r"(u.w)
-                         : "r"(sa_aux + sw64((uint32_t)lane, 16u * j)));
+                         : "r"(sa_aux + 2048u * xb + sw64((uint32_t)lane, 16u * j)));
             x[4 * j] = u.x; x[4 * j + 1] = u.y; x[4 * j + 2] = u.z; x[4 * j + 3] = u.w;
           }
         } else {
@@ -498,7 +514,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int j = 0; j < 16; ++j) x[j] = 0u;
         }
         tmem_ld_wait();
-        if (prof) { t1 = clock64(); pc[2] += t1 - t0; t0 = t1; }
+        if (prof) { t1 = clock64(); EPC(2, t1 - t0); t0 = t1; }
         if (c == 3) {
           tc_fence_before();
           __syncwarp();
@@ -507,12 +523,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             else mbar_arrive_relaxed(&tempty_bar[as]);
           }
         }
-        if (has_aux && c < 3) {  // refill the aux buffer with the next chunk
+        if (has_aux && c < 2) {  // refill this aux buffer with chunk c + 2
           fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) {
-            mbar_arrive_expect_tx(abar, 2048);
-            tma_load_2d(s_aux, E.tmAux, abar, q + 32, prow);
+            mbar_arrive_expect_tx(abar + xb, 2048);
+            tma_load_2d(s_aux + 2048 * xb, E.tmAux, abar + xb, q + 64, prow);
           }
         }
         if ((dbg & 1) || shadow) continue;
@@ -528,14 +544,18 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int i = 0; i < 16; ++i) rsum += fabsf(lo_bf(o[i])) + fabsf(hi_bf(o[i]));
         }
-        if (prof) { t1 = clock64(); pc[4] += t1 - t0; t0 = t1; }
-        // the previous chunk's bulk stores must have finished reading the staging boxes
-        if (lane == 0) bulk_wait_read<0>();
+        if (prof) { t1 = clock64(); EPC(4, t1 - t0); t0 = t1; }
+        // the bulk stores that last read these staging boxes must be done with them: the
+        // output box alternates (chunk c - 2's group), the single mirror box does not
+        if (lane == 0) {
+          if (mir) bulk_wait_read<0>();
+          else bulk_wait_read<1>();
+        }
         __syncwarp();
-        if (prof) { t1 = clock64(); pc[5] += t1 - t0; t0 = t1; }
+        if (prof) { t1 = clock64(); EPC(5, t1 - t0); t0 = t1; }
 #pragma unroll
         for (int j = 0; j < 4; ++j)
-          asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(sa_out + sw64((uint32_t)lane, 16u * j)),
+          asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(sa_out + 2048u * xb + sw64((uint32_t)lane, 16u * j)),
                        "r"(o[4 * j]), "r"(o[4 * j + 1]), "r"(o[4 * j + 2]), "r"(o[4 * j + 3])
                        : "memory");
         if (mir) {
@@ -551,10 +571,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) {
-          tma_store_2d(E.tmOut, s_out, q, prow);          // rows prow.., cols q..
+          uint8_t* so = s_out + 2048 * xb;
+          tma_store_2d(E.tmOut, so, q, prow);             // rows prow.., cols q..
           if (mir_store) tma_store_2d(E.tmOut, s_mir, prow, q);  // rows q.., cols prow..
           // fused all-gather: the same box to every peer's buffer (NVLink), tile by tile
-          for (int r = 0; r < E.npeer; ++r) tma_store_2d(E.tmPeer + 128 * r, s_out, q, prow);
+          for (int r = 0; r < E.npeer; ++r) tma_store_2d(E.tmPeer + 128 * r, so, q, prow);
           bulk_commit();
         }
         if (E.part != nullptr && mir) {
@@ -573,7 +594,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (q + lane < E.Q && prow < E.P)
             E.part[(int64_t)(q + lane) * E.part_ld + (E.Q + 127) / 128 + prow / 32] = cs;
         }
-        if (prof) { t1 = clock64(); pc[6] += t1 - t0; t0 = t1; }
+        if (prof) { t1 = clock64(); EPC(6, t1 - t0); t0 = t1; }
       }
       if (E.part != nullptr && p < E.P && qh < E.Q && !shadow) E.part[(int64_t)p * E.part_ld + qh / 128] = rsum;
       if (++as == 2) { as = 0; aphase ^= 1; }
@@ -588,8 +609,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (pfl && lane == 0) atomicOr(flags, pfl);
     if (lane == 0) bulk_wait<0>();
     if (ew == 0) TL(5);  // epilogue stores complete
-    if ((dbg & 8) && lane == 0)
-      for (int i = 0; i < 8; ++i) atomicAdd(&g_epi_prof[i], (unsigned long long)pc[i]);
+#undef EPC
     if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(flags, 2u);
   }
 
