@@ -258,7 +258,10 @@ __global__ void __launch_bounds__(kClThreads, 1)
         if (lane == 0 && !(tr > 0.f)) fl |= 1u;
         if (lane == 0 && !isfinite(tr)) fl |= 2u;
       }
-      __syncthreads();
+      // A0 is rescaled IN PLACE below, including this CTA's own rows, which the bulk copies
+      // of the G phase may still be reading: every CTA has received all of A0 once it
+      // reaches this barrier, so all those copies are complete after it
+      cluster_sync();
       // A1 = diag(s) A0 diag(s) (symmetric product: bitwise symmetric), X1 = X0 diag(s);
       // s is zero beyond N, so the padding stays zero
       if (lane < C4) {
