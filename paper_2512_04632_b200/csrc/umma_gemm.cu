@@ -72,10 +72,10 @@ struct Geo {
 #ifndef TNS_STAGES2
 #define TNS_STAGES2 4
 #endif
-  static constexpr int kStages = CG == 1 ? 3 : TNS_STAGES2;
+  static constexpr int kStages = CG == 1 ? 2 : TNS_STAGES2;
   static constexpr int kEpiOff = kStages * kStageBytes;          // epilogue staging
-  // per epilogue warp: 2 aux boxes, 2 output boxes (double-buffered), 1 mirror box
-  static constexpr int kEpiBytes = kNumEpiWarps * 5 * 2048;
+  // per epilogue warp: 2 aux, 2 output and 2 mirror boxes (all double-buffered)
+  static constexpr int kEpiBytes = kNumEpiWarps * 6 * 2048;
   static constexpr size_t kSmemBytes = (size_t)kEpiOff + kEpiBytes + 1024 + 512;
 };
 
@@ -436,8 +436,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int ew = warp - kEpiWarp0;
     const int quad = warp & 3;  // TMEM lanes [32*quad, 32*quad + 32)
     const int half = ew >> 2;   // 128-column half of the 256-wide tile
-    // staging (2 KB boxes): aux[0..1] @ 0, 2K; out[0..1] @ 4K, 6K; mirror @ 8K
-    uint8_t* s_aux = smem + G::kEpiOff + ew * 10240;
+    // staging (2 KB boxes): aux[0..1] @ 0, 2K; out[0..1] @ 4K, 6K; mirror[0..1] @ 8K, 10K
+    uint8_t* s_aux = smem + G::kEpiOff + ew * 12288;
     uint8_t* s_out = s_aux + 4096;
     uint8_t* s_mir = s_aux + 8192;
     uint64_t* abar = aux_bar + 2 * ew;
@@ -545,12 +545,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int i = 0; i < 16; ++i) rsum += fabsf(lo_bf(o[i])) + fabsf(hi_bf(o[i]));
         }
         if (prof) { t1 = clock64(); EPC(4, t1 - t0); t0 = t1; }
-        // the bulk stores that last read these staging boxes must be done with them: the
-        // output box alternates (chunk c - 2's group), the single mirror box does not
-        if (lane == 0) {
-          if (mir) bulk_wait_read<0>();
-          else bulk_wait_read<1>();
-        }
+        // the bulk stores that last read these staging boxes (chunk c - 2's group) must be
+        // done with them
+        if (lane == 0) bulk_wait_read<1>();
         __syncwarp();
         if (prof) { t1 = clock64(); EPC(5, t1 - t0); t0 = t1; }
 #pragma unroll
@@ -564,7 +561,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int i = 0; i < 32; ++i) {
             const uint32_t w = sep ? m[i >> 1] : o[i >> 1];
             const uint16_t h = (uint16_t)(i & 1 ? (w >> 16) : (w & 0xFFFFu));
-            asm volatile("st.shared.u16 [%0], %1;" ::"r"(sa_mir + sw64((uint32_t)i, 2u * lane)), "h"(h)
+            asm volatile("st.shared.u16 [%0], %1;" ::"r"(sa_mir + 2048u * xb + sw64((uint32_t)i, 2u * lane)), "h"(h)
                          : "memory");
           }
         }
@@ -573,7 +570,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0) {
           uint8_t* so = s_out + 2048 * xb;
           tma_store_2d(E.tmOut, so, q, prow);             // rows prow.., cols q..
-          if (mir_store) tma_store_2d(E.tmOut, s_mir, prow, q);  // rows q.., cols prow..
+          if (mir_store) tma_store_2d(E.tmOut, s_mir + 2048 * xb, prow, q);  // rows q.., cols prow..
           // fused all-gather: the same box to every peer's buffer (NVLink), tile by tile
           for (int r = 0; r < E.npeer; ++r) tma_store_2d(E.tmPeer + 128 * r, so, q, prow);
           bulk_commit();
@@ -587,7 +584,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             uint4 u;
             asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];"
                          : "=r"(u.x), "=r"(u.y), "=r"(u.z), "=r"(u.w)
-                         : "r"(sa_mir + sw64((uint32_t)lane, 16u * j)));
+                         : "r"(sa_mir + 2048u * xb + sw64((uint32_t)lane, 16u * j)));
             cs += fabsf(lo_bf(u.x)) + fabsf(hi_bf(u.x)) + fabsf(lo_bf(u.y)) + fabsf(hi_bf(u.y)) +
                   fabsf(lo_bf(u.z)) + fabsf(hi_bf(u.z)) + fabsf(lo_bf(u.w)) + fabsf(hi_bf(u.w));
           }
