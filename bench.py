@@ -254,17 +254,24 @@ def run_own(args):
     if collective == "fused":
         # self-check before timing: the fused peer-store path must reproduce the NCCL path
         # bit for bit on this workload, else time the NCCL path and say why
+        # (the agreement all-reduce runs on every rank even if this rank's attempt raised,
+        # so one failing rank cannot leave the others waiting in it)
+        a = [v.clone() for v in orthogonalize_sharded(xs, None, iters=iters, buckets=buckets)]
+        local_ok, err = 0, None
         try:
-            a = [v.clone() for v in orthogonalize_sharded(xs, None, iters=iters, buckets=buckets)]
             b = orthogonalize_sharded(xs, None, iters=iters, collective="fused")
             torch.cuda.synchronize()
-            ok = torch.tensor([int(all(torch.equal(u, v) for u, v in zip(a, b)))], device=dev)
-            dist.all_reduce(ok, op=dist.ReduceOp.MIN)
-            if not int(ok.item()):
-                collective, coll_note = "nccl", "fused self-check mismatch; timed the NCCL path"
-            del a, b
+            local_ok = int(all(torch.equal(u, v) for u, v in zip(a, b)))
+            del b
         except Exception as e:  # pragma: no cover - only on multi-GPU boxes
-            collective, coll_note = "nccl", f"fused path unavailable ({type(e).__name__}: {e}); timed NCCL"
+            err = f"{type(e).__name__}: {e}"
+        ok = torch.tensor([local_ok], device=dev)
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        if not int(ok.item()):
+            collective = "nccl"
+            coll_note = (f"fused path unavailable ({err}); timed NCCL" if err else
+                         "fused self-check failed on some rank; timed the NCCL path")
+        del a
 
     def step():
         if collective == "fused":
