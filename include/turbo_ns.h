@@ -115,9 +115,19 @@ ns_status ns_muon_step(void* const* W, const void* const* G, float* const* M, vo
                        float lr, float beta, float weight_decay, int nesterov, int iters, const float* coeffs,
                        ns_precond precond, void* stream);
 
-/* Bytes of device workspace the library will hold for this problem list. */
+/* Bytes of device workspace the library will hold for this problem list (an upper bound:
+ * matrices served by the cluster-resident small-matrix kernel need none). */
 ns_status ns_workspace_size(const int64_t* m, const int64_t* n, int64_t count,
                             ns_dtype dtype, size_t* bytes);
+
+/* Optional caller-owned workspace: `ptr` (device memory of the current
+ * device, 256-byte aligned, `bytes` >= 256) from which every plan built afterwards carves
+ * its workspace (bump allocation; a problem list needs at most ns_workspace_size bytes)
+ * instead of allocating its own.  A call whose new plan does not fit fails with
+ * NS_ERR_WORKSPACE and enqueues nothing.  Synchronises the device and drops the cached
+ * plans that used the previous caller buffer; the caller keeps `ptr` alive until the next
+ * ns_set_workspace or ns_shutdown.  ptr = NULL returns to library-owned workspace. */
+ns_status ns_set_workspace(void* ptr, size_t bytes);
 
 /* SYNCHRONISES `stream`, returns the OR of NS_FLAG_* raised since the last read on
  * the current device, and clears them. */

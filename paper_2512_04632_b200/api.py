@@ -16,7 +16,7 @@ from ._lib import DTYPE_BF16, DTYPE_FP32, PRECOND, check, lib
 
 __all__ = [
     "orthogonalize", "orthogonalize_list", "workspace_size", "read_flags", "launch_count",
-    "set_path", "shutdown", "profile_enable", "profile_read", "gram", "precondition", "poly", "update", "default_coeffs",
+    "set_path", "set_workspace", "shutdown", "profile_enable", "profile_read", "gram", "precondition", "poly", "update", "default_coeffs",
 ]
 
 
@@ -161,6 +161,19 @@ def workspace_size(shapes: Sequence[tuple[int, int]], dtype=torch.bfloat16) -> i
     check(lib.ns_workspace_size(M, N, cnt, DTYPE_BF16 if dtype == torch.bfloat16 else DTYPE_FP32,
                                 ctypes.byref(out)), "ns_workspace_size")
     return out.value
+
+
+def set_workspace(buf: torch.Tensor | None) -> None:
+    """Caller-owned workspace (ns_set_workspace): plans built afterwards carve their
+    workspace from `buf` (a contiguous CUDA tensor, 256-byte aligned); None returns to
+    library-owned workspace.  Keep `buf` alive while it is set."""
+    if buf is None:
+        check(lib.ns_set_workspace(None, 0), "ns_set_workspace")
+        return
+    _check_tensor(buf, "workspace")
+    with torch.cuda.device(buf.device):
+        check(lib.ns_set_workspace(ctypes.c_void_p(buf.data_ptr()), buf.numel() * buf.element_size()),
+              "ns_set_workspace")
 
 
 def read_flags(device=None) -> int:

@@ -193,13 +193,18 @@ struct Plan {
   unsigned* barrier = nullptr;
   std::vector<Phase> phases;
   uint64_t last_use = 0;
+  bool ws_borrowed = false;  // carved from the caller's ns_set_workspace buffer
   ~Plan() {
-    if (ws) cudaFree(ws);
+    if (ws && !ws_borrowed) cudaFree(ws);
     if (dtab) cudaFree(dtab);
   }
 };
 
 static std::map<std::vector<uint64_t>, std::unique_ptr<Plan>> g_plans;
+// Caller-owned workspace (ns_set_workspace): plans built while it is set carve their
+// workspace from it (bump allocation), instead of cudaMalloc.
+struct UserWs { uint8_t* base = nullptr; size_t bytes = 0, used = 0; };
+static UserWs g_uws[64];
 static uint64_t g_tick = 0;
 static const size_t kMaxPlans = 256;  // distinct problem lists (e.g. buckets of a pipeline)
 
@@ -271,10 +276,23 @@ static ns_status build_plan(Plan& P, HostTables& H, DevCtx* dc, const float* coe
     if (P.precond == NS_PRECOND_AOL && !P.simt) off += (size_t)mt.N * mt.part_ld * 4;
   }
   P.ws_bytes = align_up(off, 256);
-  cudaError_t e = cudaMalloc(&P.ws, P.ws_bytes);
-  if (e != cudaSuccess) {
-    cudaGetLastError();
-    return fail(NS_ERR_WORKSPACE, "workspace cudaMalloc(" + std::to_string(P.ws_bytes) + ") failed");
+  cudaError_t e = cudaSuccess;
+  UserWs& uw = g_uws[P.device & 63];
+  if (uw.base) {
+    const size_t at = align_up(uw.used, 256);
+    if (at + P.ws_bytes > uw.bytes)
+      return fail(NS_ERR_WORKSPACE, "caller workspace too small: this problem list needs " +
+                                        std::to_string(P.ws_bytes) + " more bytes, " +
+                                        std::to_string(uw.bytes > at ? uw.bytes - at : 0) + " left");
+    P.ws = uw.base + at;
+    P.ws_borrowed = true;
+    uw.used = at + P.ws_bytes;
+  } else {
+    e = cudaMalloc(&P.ws, P.ws_bytes);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      return fail(NS_ERR_WORKSPACE, "workspace cudaMalloc(" + std::to_string(P.ws_bytes) + ") failed");
+    }
   }
   uint8_t* ws = reinterpret_cast<uint8_t*>(P.ws);
   P.barrier = reinterpret_cast<unsigned*>(ws);
@@ -1027,6 +1045,23 @@ ns_status ns_workspace_size(const int64_t* m, const int64_t* n, int64_t count, n
     mats.push_back(make_mat((void*)16, nullptr, m[i], n[i], 2));
   }
   *bytes = workspace_bytes_for(mats, dtype);
+  return NS_OK;
+}
+
+ns_status ns_set_workspace(void* ptr, size_t bytes) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (ptr && (bytes < 256 || (reinterpret_cast<uintptr_t>(ptr) & 255)))
+    return fail(NS_ERR_INVALID_VALUE, "workspace must be >= 256 bytes and 256-byte aligned");
+  int dev = 0;
+  CU_TRY(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= 64) return fail(NS_ERR_NOT_SUPPORTED, "device index >= 64");
+  CU_TRY(cudaDeviceSynchronize());
+  // drop the cached plans that live in the previous caller buffer
+  for (auto it = g_plans.begin(); it != g_plans.end();) {
+    if (it->second->ws_borrowed && it->second->device == dev) it = g_plans.erase(it);
+    else ++it;
+  }
+  g_uws[dev] = UserWs{reinterpret_cast<uint8_t*>(ptr), ptr ? bytes : 0, 0};
   return NS_OK;
 }
 

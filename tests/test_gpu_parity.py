@@ -358,3 +358,32 @@ def test_many_matrices_one_call_bitwise():
         ns.orthogonalize(t, iters=4)
         torch.cuda.synchronize()
         assert torch.equal(t, outs[k]), (k, shapes[k])
+
+
+def test_caller_owned_workspace():
+    """ns_set_workspace: plans carve their workspace from a caller buffer (results bitwise
+    equal to library-owned workspace); a too-small buffer fails with NS_ERR_WORKSPACE."""
+    shapes = [(768, 768), (3072, 768), (1024, 512)]
+    xs = [torch.from_numpy(I.gaussian(m, n, seed=190 + i)).to(torch.bfloat16).cuda() for i, (m, n) in enumerate(shapes)]
+    ref = [torch.empty_like(x) for x in xs]
+    ns.orthogonalize_list(xs, out=ref, iters=4)
+    need = ns.workspace_size(shapes)
+    buf = torch.empty(need + 4096, dtype=torch.uint8, device="cuda")
+    try:
+        ns.set_workspace(buf)
+        outs = [torch.empty_like(x) for x in xs]
+        ns.orthogonalize_list(xs, out=outs, iters=4)
+        torch.cuda.synchronize()
+        for r, o in zip(ref, outs):
+            assert torch.equal(r, o)
+        small = torch.empty(4096, dtype=torch.uint8, device="cuda")
+        ns.set_workspace(small)
+        with pytest.raises(ns.NSError, match="NS_ERR_WORKSPACE"):
+            ns.orthogonalize_list(xs, out=outs, iters=4)
+    finally:
+        ns.set_workspace(None)
+    outs = [torch.empty_like(x) for x in xs]
+    ns.orthogonalize_list(xs, out=outs, iters=4)
+    torch.cuda.synchronize()
+    for r, o in zip(ref, outs):
+        assert torch.equal(r, o)
