@@ -244,11 +244,17 @@ def _sharded_fused(xs, group, iters, precond, coeffs, inplace):
     es = buf.element_size()
     ptrs = list(hdl.buffer_ptrs)
     hdl.barrier(channel=0)  # every peer is done reading its buffer (previous step)
+    err = None
     if mine:
         peer_ptrs = [[ptrs[r] + plan.offsets[i] * es for r in range(world) if r != rank] for i in mine]
-        orthogonalize_list([xs[i] for i in mine], out=[views[i] for i in mine], iters=iters,
-                           precond=precond, coeffs=coeffs, peer_ptrs=peer_ptrs)
+        try:
+            orthogonalize_list([xs[i] for i in mine], out=[views[i] for i in mine], iters=iters,
+                               precond=precond, coeffs=coeffs, peer_ptrs=peer_ptrs)
+        except Exception as e:  # still reach the barrier below: peers must not wait forever
+            err = e
     hdl.barrier(channel=0)  # every peer's tiles have landed in this rank's buffer
+    if err is not None:
+        raise err
     if inplace:
         for t, v in zip(xs, views):
             t.copy_(v)
