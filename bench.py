@@ -493,6 +493,18 @@ def run_extras(args, peaks):
     fs = sum(ns_flops(m, n, 4) for m, n in shapes)
     out["gpt2_small"] = {"ms": round(ms_s, 4), "tflops_alg": round(fs / (ms_s * 1e-3) / 1e12, 1),
                          "matrices": len(shapes)}
+    # --- GPT-2 large set (config 5's second model: 216 matrices, d = 1280)
+    shapes = I.shape_set("gpt2-large")
+    xs = [torch.from_numpy(x).to(torch.bfloat16).cuda() for x in make_inputs(shapes, 6)]
+    outs = [torch.empty_like(t) for t in xs]
+    ns.orthogonalize_list(xs, out=outs, iters=4)
+    ms_l = time_calls(lambda: ns.orthogonalize_list(xs, out=outs, iters=4), reps, None)
+    fl = sum(ns_flops(m, n, 4) for m, n in shapes)
+    out["gpt2_large"] = {"ms": round(ms_l, 4), "tflops_alg": round(fl / (ms_l * 1e-3) / 1e12, 1),
+                         "matrices": len(shapes), "inputs_gb": round(sum(m * n for m, n in shapes) * 2 / 1e9, 2)}
+    del xs, outs
+    torch.cuda.empty_cache()
+
     def small(fn):
         """Latency of one call (events around it, median) and of a CUDA-graph replay of it
         (the launch-bound configs: host enqueue time excluded), plus launches per call."""

@@ -387,3 +387,25 @@ def test_caller_owned_workspace():
     torch.cuda.synchronize()
     for r, o in zip(ref, outs):
         assert torch.equal(r, o)
+
+
+def test_gpt2_large_set_full_size_sampled():
+    """BASELINE config 5's GPT-2-large hidden-matrix set (216 matrices, 1.4 GB) in one
+    grouped call; one matrix of each shape checked against the oracle, all finite."""
+    shapes = I.shape_set("gpt2-large")
+    xs_np = {}
+    pick = {}
+    for i, s in enumerate(shapes):
+        pick.setdefault(s, i)
+    ts = []
+    for i, (m, n) in enumerate(shapes):
+        x = I.gaussian(m, n, seed=I.matrix_seed(6, i))
+        if i in pick.values():
+            xs_np[i] = x
+        ts.append(torch.from_numpy(x).to(torch.bfloat16).cuda())
+    ns.orthogonalize_list(ts, iters=4)
+    torch.cuda.synchronize()
+    assert all(bool(torch.isfinite(t.float()).all()) for t in ts)
+    for i, x in xs_np.items():
+        out = ts[i].float().cpu().numpy().astype(np.float64)
+        assert relF(out, oracle_run(x, C.turbo(4), "aol")) <= BF16_TOL, (i, shapes[i])
