@@ -259,6 +259,40 @@ static bool half_storage_enabled() {
   return v == 1;
 }
 
+// Persistent workers take tasks t = w, w + nw, w + 2 nw, ...  When a step mixes tile
+// lengths (e.g. a Gram over K = 1024 and K = 4096 matrices), plain round-robin leaves up to
+// ~5 % imbalance; instead assign tiles greedily longest-first to the least-loaded worker
+// (cost = k-blocks + 4 for the epilogue) and lay each worker's list out on its stride,
+// padding with TK_NONE.  Within a worker the original (rasterised) order is kept.
+static void balance_tasks(std::vector<TaskDesc>& tasks, const std::vector<GemmJob>& jobs, int workers) {
+  const int64_t n = (int64_t)tasks.size();
+  if (workers < 2 || n <= workers) return;
+  auto cost = [&](const TaskDesc& td) { return (int64_t)((jobs[td.tile & 0xFFFFFu].K + kBK - 1) / kBK) + 4; };
+  int64_t cmin = INT64_MAX, cmax = 0;
+  for (const TaskDesc& td : tasks) { cmin = std::min(cmin, cost(td)); cmax = std::max(cmax, cost(td)); }
+  if (cmin == cmax) return;  // uniform tiles: round-robin is already balanced
+  std::vector<int64_t> order(n);
+  for (int64_t i = 0; i < n; ++i) order[i] = i;
+  std::stable_sort(order.begin(), order.end(), [&](int64_t a, int64_t b) { return cost(tasks[a]) > cost(tasks[b]); });
+  std::vector<int64_t> load(workers, 0);
+  std::vector<std::vector<int64_t>> lists(workers);
+  for (int64_t i : order) {
+    int w = 0;
+    for (int k = 1; k < workers; ++k) if (load[k] < load[w]) w = k;
+    load[w] += cost(tasks[i]);
+    lists[w].push_back(i);
+  }
+  size_t rounds = 0;
+  for (auto& l : lists) { std::sort(l.begin(), l.end()); rounds = std::max(rounds, l.size()); }
+  TaskDesc pad;
+  std::memset(&pad, 0, sizeof(pad));
+  pad.kind = TK_NONE; pad.dep_slot = kNoSlot; pad.my_slot = kNoSlot;
+  std::vector<TaskDesc> out(rounds * workers, pad);
+  for (int w = 0; w < workers; ++w)
+    for (size_t r = 0; r < lists[w].size(); ++r) out[r * workers + w] = tasks[lists[w][r]];
+  tasks.swap(out);
+}
+
 static ns_status build_plan(Plan& P, HostTables& H, DevCtx* dc, const float* coeffs) {
   const int hs = half_storage_enabled() ? 1 : 0;
   const int T = P.iters;
@@ -567,6 +601,7 @@ static ns_status build_plan(Plan& P, HostTables& H, DevCtx* dc, const float* coe
           } else {
             std::vector<uint64_t> tl = tile_list(st, 0);
             for (uint64_t w : tl) tasks.push_back(mk_task(w));
+            balance_tasks(tasks, st.jobs, dc->sms / P.cg);
           }
           Phase ph{PH_GEMM};
           ph.gemm_kind = st.gemm_kind;

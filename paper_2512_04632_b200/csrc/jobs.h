@@ -121,7 +121,7 @@ struct MuonJob {
 // of the CTA pair).  Matrices therefore pipeline through the steps independently, with no
 // grid-wide barrier.
 constexpr uint32_t kNoSlot = 0xFFFFFFFFu;
-enum TaskKind : uint32_t { TK_TILE = 0, TK_PRE_S = 1, TK_PRE_SCALE = 2 };
+enum TaskKind : uint32_t { TK_TILE = 0, TK_PRE_S = 1, TK_PRE_SCALE = 2, TK_NONE = 3 };  // NONE: schedule padding
 constexpr int kPreRows = 64;  // rows of one preconditioner task
 enum StepKind : int32_t { PHK_GEMM = 0, PHK_PRE_S = 1 };  // host-side step kinds (api.cu)
 // Bit 62 of a tile word: "shadow" tile -- computed (its operand loads feed the other pair of

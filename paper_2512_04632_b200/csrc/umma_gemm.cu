@@ -454,6 +454,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0) wait_phase(done + TD.dep_slot, TD.dep_target);
         __syncwarp();
       }
+      if (TD.kind == TK_NONE) continue;  // schedule padding (balanced per-step task lists)
       if (TD.kind != TK_TILE) {
         // preconditioner rows (fused mode): the pair's 8*CG epilogue warps share the chunk
         const PrecondJob& PJ = pjobs[TD.pjob];
