@@ -3,13 +3,17 @@
 Our launches come in a fixed order per NS call: GRAM, PRECOND, POLY, XB, then (GRAM, POLY,
 XB) x (T-1); this labels each umma_gemm launch by its position in that sequence.
 
-    python tools/launch_shares.py profiles/r01_v4_bench_quick_launches.csv
+    python tools/launch_shares.py profiles/r01_v4_bench_quick_launches.csv [--first N]
+
+--first N keeps the first N launches (bench.py --quick runs the timed workload first --
+warm-up, timed and profiled steps, 13 launches each -- and its e2e pipeline afterwards).
 """
 import collections
 import csv
 import sys
 
 rows = [r for r in csv.reader(open(sys.argv[1])) if len(r) > 10]
+first = int(sys.argv[sys.argv.index("--first") + 1]) if "--first" in sys.argv else None
 hdr = rows[0]
 ki, vi = hdr.index("Kernel Name"), hdr.index("Metric Value")
 seq = []
@@ -18,6 +22,8 @@ for r in rows[1:]:
         seq.append((r[ki], float(r[vi].replace(",", ""))))
     except ValueError:
         pass
+if first is not None:
+    seq = seq[:first]
 agg = collections.defaultdict(lambda: [0, 0.0])
 state = 0  # position within GRAM -> POLY -> XB
 for name, ns in seq:
