@@ -4,6 +4,8 @@ import ctypes
 import os
 import re
 
+import numpy as np
+
 import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -68,3 +70,12 @@ def test_product_does_not_import_oracle():
             if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
                 src = open(os.path.join(dirpath, f)).read()
                 assert not re.search(r"^\s*(import|from)\s+oracle\b|ns_oracle|#include.*oracle", src, re.M), f
+
+
+def test_product_polar_express_matches_test_generator():
+    from paper_2512_04632_b200 import coeffs as P
+    from synth import polar_express as PE
+    for t in (1, 3, 5, 9):
+        for saf in (0.0, 2e-2):
+            a, b = P.polar_express(t, safety=saf), PE.polar_express(t, safety=saf)
+            np.testing.assert_allclose(np.array(a), np.array(b), rtol=1e-12, atol=1e-12)
