@@ -400,12 +400,28 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int K = J->K;
         const int a_sym = J->a_sym, b_sym = J->b_sym;
         const int pblk = ti.p0 >> 8, qblk = ti.q0 >> 8;  // both CTAs' rows share the block
+        // TNS_MEASURE builds, TNS_DBG bit 64: MMA-issuer stall cycles (slot 0 tiles, 1 waiting
+        // for a free accumulator = epilogue-bound, 2 waiting for operands = feed-bound, 3 busy)
+        const bool mprof = kMeasure && (dbg & 64);
+        long long m0 = mprof ? clock64() : 0;
         mbar_wait(&tempty_bar[as], aphase ^ 1);
+        if (mprof) { const long long m1 = clock64(); atomicAdd(&g_epi_prof[1], (unsigned long long)(m1 - m0)); m0 = m1;
+                     atomicAdd(&g_epi_prof[0], 1ull); }
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + as * kBN;
         const int nk = (K + kBK - 1) / kBK;
         for (int kb = 0; kb < nk; ++kb) {
+          if (mprof) {
+            const long long m1 = clock64();
+            atomicAdd(&g_epi_prof[3], (unsigned long long)(m1 - m0));
+            m0 = m1;
+          }
           mbar_wait(&full_bar[stage], phase);
+          if (mprof) {
+            const long long m1 = clock64();
+            atomicAdd(&g_epi_prof[2], (unsigned long long)(m1 - m0));
+            m0 = m1;
+          }
           tc_fence_after();
           if (kb == 0 && t == cid) TL(3);  // first operands landed
           const uint32_t sa = smem_u32(smem + (size_t)stage * G::kStageBytes);
