@@ -115,6 +115,14 @@ ns_status ns_muon_step(void* const* W, const void* const* G, float* const* M, vo
                        float lr, float beta, float weight_decay, int nesterov, int iters, const float* coeffs,
                        ns_precond precond, void* stream);
 
+/* The update half of a Muon step on its own (the distributed optimizer applies updates
+ * orthogonalised on other ranks; reading R13):  W <- W (1 - lr weight_decay) - lr *
+ * max(1, m/n)^(1/2) * U for `count` matrices, W[i] (w_dtype) and U[i] (bf16, e.g. an
+ * ns_orthogonalize result) m[i] x n[i] device matrices.  The same kernel ns_muon_step uses
+ * (bitwise the same W).  One launch, asynchronous on `stream`. */
+ns_status ns_muon_apply(void* const* W, const void* const* U, const int64_t* m, const int64_t* n,
+                        int64_t count, ns_dtype w_dtype, float lr, float weight_decay, void* stream);
+
 /* Bytes of device workspace the library will hold for this problem list (an upper bound:
  * matrices served by the cluster-resident small-matrix kernel need none). */
 ns_status ns_workspace_size(const int64_t* m, const int64_t* n, int64_t count,

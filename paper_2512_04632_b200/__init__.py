@@ -8,9 +8,11 @@ loudly if it is missing: there is no CPU fallback.
 """
 from ._lib import NSError, lib  # noqa: F401  (raises ImportError if libturbons.so is missing)
 from .api import (default_coeffs, gram, launch_count, orthogonalize, orthogonalize_list,  # noqa: F401
-                  poly, precondition, profile_enable, profile_read, read_flags, set_path, set_workspace, shutdown, update,
+                  muon_apply, poly, precondition, profile_enable, profile_read, read_flags, set_path, set_workspace,
+                  shutdown, update,
                   workspace_size)
-from .muon import TurboMuon  # noqa: F401
-from .parallel import lpt_owners, make_plan, ns_flops, orthogonalize_host, orthogonalize_sharded  # noqa: F401
+from .muon import DistributedTurboMuon, TurboMuon  # noqa: F401
+from .parallel import (lpt_owners, make_plan, ns_flops, orthogonalize_host, orthogonalize_sharded,  # noqa: F401
+                       reduce_scatter_owned)
 
 __version__ = "0.1.0"

@@ -17,7 +17,7 @@ DTYPE_BF16, DTYPE_FP32 = 0, 1
 FLAG_ZERO_SCALE, FLAG_NONFINITE = 1, 2
 
 EXPORTS = [
-    "ns_orthogonalize", "ns_orthogonalize_batched", "ns_orthogonalize_peers", "ns_muon_step", "ns_workspace_size", "ns_set_workspace", "ns_read_flags",
+    "ns_orthogonalize", "ns_orthogonalize_batched", "ns_orthogonalize_peers", "ns_muon_step", "ns_muon_apply", "ns_workspace_size", "ns_set_workspace", "ns_read_flags",
     "ns_launch_count", "ns_set_path", "ns_status_string", "ns_last_error", "ns_abi_version",
     "ns_shutdown", "ns_profile_enable", "ns_profile_read", "nsx_epilogue_counters", "nsx_gram", "nsx_precondition", "nsx_poly", "nsx_update",
 ]
@@ -46,6 +46,8 @@ def _load() -> ctypes.CDLL:
         ctypes.POINTER(c_vp), ctypes.POINTER(c_vp), ctypes.POINTER(c_vp), ctypes.POINTER(c_vp),
         ctypes.POINTER(c_i64), ctypes.POINTER(c_i64), c_i64, c_int, c_int, c_float, c_float, c_float, c_int,
         c_int, c_fp, c_int, c_vp]
+    lib.ns_muon_apply.argtypes = [ctypes.POINTER(c_vp), ctypes.POINTER(c_vp), ctypes.POINTER(c_i64),
+                                  ctypes.POINTER(c_i64), c_i64, c_int, c_float, c_float, c_vp]
     lib.ns_workspace_size.argtypes = [ctypes.POINTER(c_i64), ctypes.POINTER(c_i64), c_i64, c_int,
                                       ctypes.POINTER(ctypes.c_size_t)]
     lib.ns_set_workspace.argtypes = [c_vp, ctypes.c_size_t]

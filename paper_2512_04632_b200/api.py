@@ -16,7 +16,7 @@ from ._lib import DTYPE_BF16, DTYPE_FP32, PRECOND, check, lib
 
 __all__ = [
     "orthogonalize", "orthogonalize_list", "workspace_size", "read_flags", "launch_count",
-    "set_path", "set_workspace", "shutdown", "profile_enable", "profile_read", "gram", "precondition", "poly", "update", "default_coeffs",
+    "set_path", "set_workspace", "muon_apply", "shutdown", "profile_enable", "profile_read", "gram", "precondition", "poly", "update", "default_coeffs",
 ]
 
 
@@ -161,6 +161,27 @@ def workspace_size(shapes: Sequence[tuple[int, int]], dtype=torch.bfloat16) -> i
     check(lib.ns_workspace_size(M, N, cnt, DTYPE_BF16 if dtype == torch.bfloat16 else DTYPE_FP32,
                                 ctypes.byref(out)), "ns_workspace_size")
     return out.value
+
+
+def muon_apply(weights: Sequence[torch.Tensor], updates: Sequence[torch.Tensor], lr: float,
+               weight_decay: float = 0.0) -> None:
+    """ns_muon_apply: W <- W (1 - lr wd) - lr max(1, m/n)^(1/2) U for each pair (W fp32 or
+    bf16, U bf16 of the same shape); one launch on the current stream."""
+    ws, us = list(weights), list(updates)
+    if len(ws) != len(us) or not ws:
+        raise ValueError("weights and updates must be non-empty lists of equal length")
+    wdt = _dtype_code(ws[0])
+    for w, u in zip(ws, us):
+        _check_tensor(w, "weight")
+        _check_tensor(u, "update")
+        if w.dim() != 2 or w.shape != u.shape or u.dtype != torch.bfloat16 or _dtype_code(w) != wdt:
+            raise ValueError("weights: 2-D, one dtype; updates: bf16, same shapes")
+    cnt = len(ws)
+    arr = lambda xs: (ctypes.c_void_p * cnt)(*[t.data_ptr() for t in xs])  # noqa: E731
+    with torch.cuda.device(ws[0].device):
+        check(lib.ns_muon_apply(arr(ws), arr(us), (ctypes.c_int64 * cnt)(*[w.shape[0] for w in ws]),
+                                (ctypes.c_int64 * cnt)(*[w.shape[1] for w in ws]), cnt, wdt, float(lr),
+                                float(weight_decay), _stream()), "ns_muon_apply")
 
 
 def set_workspace(buf: torch.Tensor | None) -> None:

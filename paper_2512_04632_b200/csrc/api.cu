@@ -1071,6 +1071,48 @@ ns_status ns_muon_step(void* const* W, const void* const* G, float* const* M, vo
   return NS_OK;
 }
 
+ns_status ns_muon_apply(void* const* W, const void* const* U, const int64_t* m, const int64_t* n, int64_t count,
+                        ns_dtype w_dtype, float lr, float weight_decay, void* stream) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (count < 1) return fail(NS_ERR_INVALID_VALUE, "count must be >= 1");
+  if (count > 65535) return fail(NS_ERR_NOT_SUPPORTED, "more than 65535 matrices in one call");
+  if (!W || !U || !m || !n) return fail(NS_ERR_INVALID_VALUE, "NULL array argument");
+  if (w_dtype != NS_BF16 && w_dtype != NS_FP32) return fail(NS_ERR_INVALID_VALUE, "bad dtype");
+  if (!std::isfinite(lr) || !std::isfinite(weight_decay)) return fail(NS_ERR_INVALID_VALUE, "lr / weight_decay not finite");
+  ns_status st;
+  std::vector<MuonJob> jobs;
+  std::vector<uint64_t> key{0xA991ull};  // distinct from the ns_muon_step tables
+  int64_t max_numel = 0;
+  for (int64_t i = 0; i < count; ++i) {
+    if ((st = validate_mat(U[i], m[i], n[i], NS_BF16)) != NS_OK) return st;
+    if ((st = validate_mat(W[i], m[i], n[i], w_dtype)) != NS_OK) return st;
+    MuonJob J;
+    std::memset(&J, 0, sizeof(J));
+    J.U = const_cast<void*>(U[i]); J.W = W[i];
+    J.numel = m[i] * n[i];
+    J.scale = (float)std::sqrt(std::max(1.0, (double)m[i] / (double)n[i]));
+    jobs.push_back(J);
+    max_numel = std::max(max_numel, J.numel);
+    key.push_back(reinterpret_cast<uint64_t>(W[i])); key.push_back(reinterpret_cast<uint64_t>(U[i]));
+    key.push_back((uint64_t)m[i]); key.push_back((uint64_t)n[i]);
+  }
+  DevCtx* dc = nullptr;
+  if ((st = dev_ctx(&dc)) != NS_OK) return st;
+  auto it = g_muon_tabs.find(key);
+  void* dtab = nullptr;
+  if (it == g_muon_tabs.end()) {
+    CU_TRY(cudaMalloc(&dtab, jobs.size() * sizeof(MuonJob)));
+    CU_TRY(cudaMemcpy(dtab, jobs.data(), jobs.size() * sizeof(MuonJob), cudaMemcpyHostToDevice));
+    g_muon_tabs[key] = dtab;
+  } else {
+    dtab = it->second;
+  }
+  CU_TRY(launch_muon_apply(reinterpret_cast<const MuonJob*>(dtab), (int)count, max_numel, w_dtype == NS_BF16, lr,
+                           weight_decay, dc->sms, reinterpret_cast<cudaStream_t>(stream)));
+  ++g_launches;
+  return NS_OK;
+}
+
 ns_status ns_workspace_size(const int64_t* m, const int64_t* n, int64_t count, ns_dtype dtype, size_t* bytes) {
   if (!m || !n || !bytes || count < 1) return fail(NS_ERR_INVALID_VALUE, "bad arguments");
   if (dtype != NS_BF16 && dtype != NS_FP32) return fail(NS_ERR_INVALID_VALUE, "bad dtype");

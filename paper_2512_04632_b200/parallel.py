@@ -24,7 +24,7 @@ import torch
 import torch.distributed as dist
 
 __all__ = ["ns_flops", "lpt_owners", "ShardPlan", "make_plan", "orthogonalize_sharded",
-           "orthogonalize_host"]
+           "orthogonalize_host", "reduce_scatter_owned"]
 
 _ALIGN = 64  # elements; keeps every packed matrix 128-byte aligned in bf16
 
@@ -152,6 +152,45 @@ def _symm(key, plan, dtype, device, group):
         ent = (buf, hdl)
         _BUFFERS[key] = ent
     return ent
+
+
+def reduce_scatter_owned(tensors: Sequence[torch.Tensor], group=None, iters: int = 4,
+                         mean: bool = True) -> tuple[list[int], list[torch.Tensor]]:
+    """Reduce-scatter by ownership: every rank passes its local
+    gradients of the same matrix list; each rank gets back the cross-rank sum (or mean) of
+    only the matrices it OWNS (the same LPT ownership as orthogonalize_sharded), as views
+    into one packed buffer -- half the traffic of an all-reduce, since an owner is the only
+    rank that orthogonalises a matrix.  Returns (owned matrix indices, owned reduced views)."""
+    tensors = list(tensors)
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    shapes = [tuple(t.shape) for t in tensors]
+    plan = make_plan(shapes, world, iters, 1)
+    mine = plan.mine(rank)
+    dtype, device = tensors[0].dtype, tensors[0].device
+    key = ("rs", tuple(shapes), world, dtype, str(device), id(group))
+    packed = _cached(key + ("in",), lambda: torch.zeros(plan.total, dtype=dtype, device=device))
+    seg = plan.seg_elems
+    out = _cached(key + ("out",), lambda: torch.empty(seg, dtype=dtype, device=device))
+    for i, t in enumerate(tensors):
+        m, n = shapes[i]
+        packed[plan.offsets[i]:plan.offsets[i] + m * n].view(m, n).copy_(t)
+    if world == 1:
+        out.copy_(packed[:seg])
+    elif dist.get_backend(group) == "nccl":
+        dist.reduce_scatter_tensor(out, packed, op=dist.ReduceOp.SUM, group=group)
+    else:  # gloo has no reduce-scatter: all-reduce, keep this rank's segment (same result)
+        red = packed.clone()
+        dist.all_reduce(red, op=dist.ReduceOp.SUM, group=group)
+        out.copy_(red[rank * seg:(rank + 1) * seg])
+    if mean and world > 1:
+        out.div_(world)
+    views = []
+    for i in mine:
+        m, n = shapes[i]
+        o = plan.offsets[i] - rank * seg
+        views.append(out[o:o + m * n].view(m, n))
+    return mine, views
 
 
 def orthogonalize_sharded(xs: Sequence[torch.Tensor], group=None, iters: int = 4,

@@ -1,4 +1,6 @@
 """Muon optimizer step (ns_muon_step / TurboMuon) against the fp64 Muon-step oracle (GPU)."""
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -61,3 +63,45 @@ def test_muon_step_beta0_equals_plain_ns():
     exp = w - 0.1 * 2.0 * o.float()
     torch.cuda.synchronize()
     assert torch.allclose(p.detach(), exp, rtol=0, atol=1e-6)
+
+
+def test_muon_apply_matches_formula():
+    """ns_muon_apply: W <- W (1 - lr wd) - lr max(1, m/n)^(1/2) U (fp32 weights, bf16 U)."""
+    shapes = [(768, 256), (256, 768), (100, 37)]
+    ws = [torch.from_numpy(I.gaussian(m, n, seed=400 + i, bf16=False)).cuda() for i, (m, n) in enumerate(shapes)]
+    us = [torch.from_numpy(I.gaussian(m, n, seed=500 + i)).to(torch.bfloat16).cuda() for i, (m, n) in enumerate(shapes)]
+    ref = [w.clone() * (1 - 0.1 * 0.01) - 0.1 * MO.muon_scale(*w.shape) * u.float() for w, u in zip(ws, us)]
+    ns.muon_apply(ws, us, lr=0.1, weight_decay=0.01)
+    torch.cuda.synchronize()
+    for w, r in zip(ws, ref):
+        assert torch.allclose(w, r, rtol=1e-6, atol=1e-7)
+
+
+def test_distributed_turbo_muon_world1_equals_turbo_muon():
+    """DistributedTurboMuon (reduce-scatter by ownership -> owner's fused step -> all-gather
+    of U -> ns_muon_apply elsewhere) at NCCL world size 1 gives bitwise the TurboMuon result."""
+    import torch.distributed as dist
+    if dist.is_initialized():
+        pytest.skip("process group already initialised")
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ["MASTER_PORT"] = "29541"
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        shapes = [(768, 768), (3072, 768), (768, 3072), (64, 576)]
+        ws = [I.gaussian(m, n, seed=600 + i, bf16=False) for i, (m, n) in enumerate(shapes)]
+        pa = [torch.nn.Parameter(torch.from_numpy(w).cuda()) for w in ws]
+        pb = [torch.nn.Parameter(torch.from_numpy(w).cuda()) for w in ws]
+        oa = ns.TurboMuon(pa, lr=0.05, momentum=0.9, weight_decay=0.01)
+        ob = ns.DistributedTurboMuon(pb, lr=0.05, momentum=0.9, weight_decay=0.01)
+        for step in range(2):
+            for i, (m, n) in enumerate(shapes):
+                g = torch.from_numpy(I.gaussian(m, n, seed=700 + 10 * step + i)).cuda()
+                pa[i].grad = g.clone()
+                pb[i].grad = g.clone()
+            oa.step()
+            ob.step()
+            torch.cuda.synchronize()
+            for a, b in zip(pa, pb):
+                assert torch.equal(a, b)
+    finally:
+        dist.destroy_process_group()

@@ -110,3 +110,43 @@ def test_sharded_gloo_matches_single(world, buckets):
     for rank, outs in results:
         for a, b in zip(outs, single):
             assert np.array_equal(a, b.numpy())
+
+
+def _rs_worker(rank, world, port, shapes, q):
+    from paper_2512_04632_b200.parallel import reduce_scatter_owned
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    # rank-dependent local "gradients": g_r[i] = gaussian(i) * (r + 1)
+    gs = [torch.from_numpy(I.gaussian(m, n, seed=300 + i, bf16=False)) * (rank + 1) for i, (m, n) in enumerate(shapes)]
+    mine, views = reduce_scatter_owned(gs)
+    q.put((rank, mine, [v.clone().numpy() for v in views]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_reduce_scatter_owned_gloo(world):
+    """Each rank receives the cross-rank mean of exactly the matrices it owns (LPT
+    ownership identical to the sharded NS), and the owners partition the list."""
+    shapes = [(96, 64), (64, 160), (128, 128), (40, 24), (200, 56), (64, 64), (32, 96)]
+    ctx = mp.get_context("spawn")
+    q = ctx.SimpleQueue()
+    port = _free_port()
+    procs = [ctx.Process(target=_rs_worker, args=(r, world, port, shapes, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    results = [q.get() for _ in range(world)]
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    owners = lpt_owners(shapes, world)
+    seen = []
+    mean_factor = sum(r + 1 for r in range(world)) / world
+    for rank, mine, views in results:
+        assert mine == [i for i in range(len(shapes)) if owners[i] == rank]
+        seen += mine
+        for i, v in zip(mine, views):
+            ref = I.gaussian(*shapes[i], seed=300 + i, bf16=False) * mean_factor
+            np.testing.assert_allclose(v, ref, rtol=1e-6, atol=1e-6)
+    assert sorted(seen) == list(range(len(shapes)))
