@@ -127,6 +127,28 @@ def blas_threads() -> int:
         return len(os.sched_getaffinity(0))
 
 
+def oracle_single_thread() -> dict:
+    """the fp64 oracle with ONE BLAS thread on configs 1 (128^2 fp32) and 3
+    (the CIFAR conv set), whole problems, median of 3 (reported context, not a target)."""
+    import time
+    from threadpoolctl import threadpool_limits
+    from oracle import ns_oracle as O
+    out = {}
+    cases = {"fp32_128_ms": [I.gaussian(128, 128, seed=I.matrix_seed(1, 0), bf16=False)],
+             "cifar_ms": make_inputs(I.shape_set("cifar"), 3)}
+    with threadpool_limits(limits=1, user_api="blas"):
+        for name, xs in cases.items():
+            ts = []
+            for _ in range(3):
+                t0 = time.perf_counter()
+                for x in xs:
+                    O.newton_schulz(x.astype(np.float64), C.turbo(4), "aol")
+                ts.append((time.perf_counter() - t0) * 1e3)
+            out[name] = round(sorted(ts)[1], 2)
+    out["threads"] = 1
+    return out
+
+
 def make_inputs(shapes, config_id: int):
     return [I.gaussian(m, n, seed=I.matrix_seed(config_id, i)) for i, (m, n) in enumerate(shapes)]
 
@@ -375,6 +397,7 @@ def run_own(args):
         line["cpu_baseline"] = {"value": round(cpu_ms, 1), "unit": "ms", "cores": blas_threads(), "kind": "oracle",
                                 "sample": f"{len(done)} whole matrices ({summarize(done)}) in {secs:.1f} s, numpy fp64 "
                                           f"+ OpenBLAS; extrapolated to the {len(shapes)}-matrix set by algorithmic FLOPs"}
+        line["cpu_single_thread"] = oracle_single_thread()
     if rank == 0:
         print(json.dumps(line), flush=True)
     if distributed:
