@@ -409,3 +409,22 @@ def test_gpt2_large_set_full_size_sampled():
     for i, x in xs_np.items():
         out = ts[i].float().cpu().numpy().astype(np.float64)
         assert relF(out, oracle_run(x, C.turbo(4), "aol")) <= BF16_TOL, (i, shapes[i])
+
+
+@pytest.mark.parametrize("m,n", [(768, 256), (64, 216), (100, 37)])
+def test_nonfinite_input_raises_flag(m, n):
+    """A NaN / Inf in the input is not an error (reading R4: flags instead of a sync): the call
+    completes on every path (tcgen05 step engine, cluster kernel, SIMT) and raises flag bit 1
+    (NS_FLAG_NONFINITE)."""
+    for bad in (np.nan, np.inf):
+        x = I.gaussian(m, n, seed=77)
+        x[3, 2] = bad
+        ns.read_flags()
+        t = torch.from_numpy(x).to(torch.bfloat16).cuda()
+        ns.orthogonalize(t, iters=4)
+        torch.cuda.synchronize()
+        assert ns.read_flags() & 2
+    # and the flags clear: a clean call afterwards raises nothing
+    t = torch.from_numpy(I.gaussian(m, n, seed=78)).to(torch.bfloat16).cuda()
+    ns.orthogonalize(t, iters=4)
+    assert ns.read_flags() == 0
