@@ -146,7 +146,8 @@ uint64_t ns_launch_count(void);
 
 /* Execution-path override for testing: 0 = auto: matrices with short side N <= 128 whose
  * fp32 copy fits in shared memory (the "cluster-resident" small-matrix kernel: the whole
- * NS of one matrix in ONE launch of an 8-CTA thread-block cluster, X, A and B resident in
+ * NS of one matrix in ONE launch of a 16-CTA (when the matrix fits that layout) or 8-CTA
+ * thread-block cluster, X, A and B resident in
  * shared memory, rows exchanged over DSMEM), all
  * other matrices through the step engine (tcgen05, 256x256 tiles on CTA pairs, for aligned
  * bf16, else SIMT; one PDL-chained launch per step); when both kinds are present the

@@ -172,6 +172,7 @@ struct Phase {
   int64_t max_tiles = 0;  // largest GEMM step
   size_t coeff_off = 0;   // PH_CLUSTER: 3*iters floats
   size_t smem = 0;        // PH_CLUSTER: dynamic shared memory per CTA
+  int ctas = 8;           // PH_CLUSTER: CTAs per cluster
   // copies (PH_COPY)
   std::vector<std::pair<std::pair<void*, const void*>, size_t>> copies;
 };
@@ -398,22 +399,31 @@ static ns_status build_plan(Plan& P, HostTables& H, DevCtx* dc, const float* coe
   // -- small matrices: the whole NS in one cluster launch (enqueued first, on a side stream
   //    when the step engine has work too, so the two overlap)
   if (!P.tiny.empty()) {
-    std::vector<ClusterJob> cj;
-    size_t smem = 0;
-    for (const Mat& mt : P.tiny) {
-      ClusterJob J;
-      std::memset(&J, 0, sizeof(J));
-      J.x = mt.x; J.out = mt.out;
-      J.m = (int)mt.m; J.n = (int)mt.n; J.M = (int)mt.M; J.N = (int)mt.N; J.wide = mt.wide ? 1 : 0;
-      cj.push_back(J);
-      smem = std::max(smem, cl_layout(J.M, J.N).floats * 4 + kClHdr);
+    // 16-CTA clusters for the matrices that fit that layout, 8-CTA for the others: the
+    // choice depends on the matrix alone, so batched results stay bitwise equal to single
+    // calls (one cluster launch per group)
+    for (int ctas : {kClCtasMax, kClCtas}) {
+      std::vector<ClusterJob> cj;
+      size_t smem = 0;
+      for (const Mat& mt : P.tiny) {
+        const bool fits16 = cl_fits(mt.M, mt.N, kClCtasMax);
+        if (fits16 != (ctas == kClCtasMax)) continue;
+        ClusterJob J;
+        std::memset(&J, 0, sizeof(J));
+        J.x = mt.x; J.out = mt.out;
+        J.m = (int)mt.m; J.n = (int)mt.n; J.M = (int)mt.M; J.N = (int)mt.N; J.wide = mt.wide ? 1 : 0;
+        cj.push_back(J);
+        smem = std::max(smem, cl_layout(J.M, J.N, ctas).floats * 4 + kClHdr);
+      }
+      if (cj.empty()) continue;
+      Phase ph{PH_CLUSTER};
+      ph.dev_off = H.push(cj.data(), cj.size() * sizeof(ClusterJob), 64);
+      ph.coeff_off = H.push(coeffs, (size_t)3 * T * sizeof(float), 16);
+      ph.njobs = (int)cj.size();
+      ph.smem = smem;
+      ph.ctas = ctas;
+      P.phases.push_back(ph);
     }
-    Phase ph{PH_CLUSTER};
-    ph.dev_off = H.push(cj.data(), cj.size() * sizeof(ClusterJob), 64);
-    ph.coeff_off = H.push(coeffs, (size_t)3 * T * sizeof(float), 16);
-    ph.njobs = (int)cj.size();
-    ph.smem = smem;
-    P.phases.push_back(ph);
   }
   for (int k = 1; k <= T && !P.mats.empty(); ++k) {
     const float a = coeffs[3 * (k - 1)], b = coeffs[3 * (k - 1) + 1], c = coeffs[3 * (k - 1) + 2];
@@ -735,7 +745,7 @@ static ns_status enqueue_plan(Plan& P, DevCtx* dc, cudaStream_t stream) {
           ProfScope ps(7, s);
           CU_TRY(launch_cluster_ns(reinterpret_cast<const ClusterJob*>(dbase + ph.dev_off), ph.njobs,
                                    reinterpret_cast<const float*>(dbase + ph.coeff_off), P.iters, (int)P.precond,
-                                   P.dtype == NS_BF16, ph.smem, dc->flags, s));
+                                   P.dtype == NS_BF16, ph.smem, ph.ctas, dc->flags, s));
         }
         ++g_launches;
         if (fork) CU_TRY(cudaEventRecord(dc->ev_join, dc->side));

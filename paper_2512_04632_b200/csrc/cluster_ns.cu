@@ -1,7 +1,7 @@
 // Cluster-resident Newton-Schulz for small matrices (
 // small matrices are latency/communication-bound, not FLOP-bound).
 //
-// One thread-block cluster of kClCtas CTAs runs ALL steps of Alg. 2 for one
+// One thread-block cluster of C (8 or 16) CTAs runs ALL steps of Alg. 2 for one
 // matrix in ONE launch, with every operand resident in shared memory:
 //   load Xh (every CTA keeps a full fp32 copy, M x N, of the short-side orientation)
 //   for k = 1..T:
@@ -145,16 +145,16 @@ __device__ __forceinline__ void cl_gemm(const float* __restrict__ Lp, int ldl, c
   }
 }
 
-template <typename S>
+template <typename S, int C>
 __global__ void __launch_bounds__(kClThreads, 1)
     cluster_ns_kernel(const ClusterJob* __restrict__ jobs, const float* __restrict__ coeffs, int iters, int precond,
                       uint32_t* __restrict__ flags, int dbg) {
   extern __shared__ float4 cl_smem4[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(cl_smem4);  // data-arrival barriers: 0 A, 1 B, 2 X
   float* sm = reinterpret_cast<float*>(cl_smem4) + kClHdr / 4;
-  const ClusterJob J = jobs[blockIdx.x / kClCtas];
+  const ClusterJob J = jobs[blockIdx.x / C];
   const uint32_t rank = cluster_ctarank();
-  const ClLayout L = cl_layout(J.M, J.N);
+  const ClLayout L = cl_layout(J.M, J.N, C);
   const int M = J.M, N = J.N, lda = L.lda, ldx = L.ldx, C4 = L.N4 / 4;
   float* A = sm + L.offA;
   float* B = sm + L.offB;
@@ -168,10 +168,10 @@ __global__ void __launch_bounds__(kClThreads, 1)
 #define CL_TL(i) do { if (tl) atomicAdd(&g_cl_tl[i], (unsigned long long)(clock64() - T0)); } while (0)
   const int r0 = (int)rank * L.Nr, nr = max(0, min(L.Nr, N - r0));  // this CTA's rows of A, B
   const int o = (int)rank * L.Mr, mr = max(0, min(L.Mr, M - o));    // this CTA's rows of Xh
-  uint32_t peer[kClCtas], peer_bar[kClCtas];
+  uint32_t peer[C], peer_bar[C];
   const uint32_t sm_u32 = smem_u32(sm), bar_u32 = smem_u32(bars);
 #pragma unroll
-  for (int d = 0; d < kClCtas; ++d) {
+  for (int d = 0; d < C; ++d) {
     peer[d] = dsmem_addr(sm_u32, (uint32_t)d);
     peer_bar[d] = dsmem_addr(bar_u32, (uint32_t)d);
   }
@@ -181,7 +181,7 @@ __global__ void __launch_bounds__(kClThreads, 1)
     fence_proxy_async_smem();
     __syncthreads();
     if (tid == 0 && bytes > 0)
-      for (int d = 0; d < kClCtas; ++d)
+      for (int d = 0; d < C; ++d)
         if (d != (int)rank) dsmem_bulk(peer[d] + (uint32_t)(dst_off * 4), smem_u32(src), bytes, peer_bar[d] + 8u * b);
   };
   // bytes each CTA receives per phase: the other CTAs' rows
@@ -350,26 +350,30 @@ cudaError_t cluster_timeline(unsigned long long* out9, bool reset) {
   return e;
 }
 
-cudaError_t launch_cluster_ns(const ClusterJob* d_jobs, int njobs, const float* d_coeffs, int iters, int precond,
-                              bool is_bf16, size_t smem_bytes, uint32_t* d_flags, cudaStream_t stream) {
-  if (njobs <= 0) return cudaSuccess;
+template <int C>
+static cudaError_t launch_cl(const ClusterJob* d_jobs, int njobs, const float* d_coeffs, int iters, int precond,
+                             bool is_bf16, size_t smem_bytes, uint32_t* d_flags, cudaStream_t stream) {
   static bool attr_set[64][2] = {};
   int dev = 0;
   cudaGetDevice(&dev);
-  auto kern = is_bf16 ? cluster_ns_kernel<uint16_t> : cluster_ns_kernel<float>;
+  auto kern = is_bf16 ? cluster_ns_kernel<uint16_t, C> : cluster_ns_kernel<float, C>;
   if (!attr_set[dev & 63][is_bf16]) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kClMaxSmem);
     if (e != cudaSuccess) return e;
+    if (C > 8) {
+      e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      if (e != cudaSuccess) return e;
+    }
     attr_set[dev & 63][is_bf16] = true;
   }
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)(njobs * kClCtas));
+  cfg.gridDim = dim3((unsigned)(njobs * C));
   cfg.blockDim = dim3(kClThreads);
   cfg.dynamicSmemBytes = smem_bytes;
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = kClCtas;
+  attr[0].val.clusterDim.x = C;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
@@ -380,6 +384,13 @@ cudaError_t launch_cluster_ns(const ClusterJob* d_jobs, int njobs, const float* 
     dbg = e ? atoi(e) : 0;
   }
   return cudaLaunchKernelEx(&cfg, kern, d_jobs, d_coeffs, iters, precond, d_flags, dbg);
+}
+
+cudaError_t launch_cluster_ns(const ClusterJob* d_jobs, int njobs, const float* d_coeffs, int iters, int precond,
+                              bool is_bf16, size_t smem_bytes, int ctas, uint32_t* d_flags, cudaStream_t stream) {
+  if (njobs <= 0) return cudaSuccess;
+  return ctas == 16 ? launch_cl<16>(d_jobs, njobs, d_coeffs, iters, precond, is_bf16, smem_bytes, d_flags, stream)
+                    : launch_cl<8>(d_jobs, njobs, d_coeffs, iters, precond, is_bf16, smem_bytes, d_flags, stream);
 }
 
 }  // namespace tns

@@ -143,7 +143,10 @@ struct TaskDesc {
 // kClCtas CTAs (cluster_ns.cu).  Every CTA holds a full fp32 copy
 // of Xh (M x N), A and B in shared memory; CTA r computes rows [r*Nr, r*Nr+Nr) of A and B
 // and rows [r*Mr, r*Mr+Mr) of X_{k+1} and broadcasts them to its peers over DSMEM.
-constexpr int kClCtas = 8;
+// Cluster size: 16 CTAs (non-portable) when every matrix of the launch fits the 16-CTA
+// layout (half the rows per CTA: 128^2 fp32 82 -> 66 us), else the portable 8.
+constexpr int kClCtas = 8;       // eligibility is decided with the 8-CTA layout
+constexpr int kClCtasMax = 16;
 #ifndef TNS_CL_THREADS
 #define TNS_CL_THREADS 512
 #endif
@@ -160,24 +163,24 @@ struct ClLayout {
   int N4, Nr, Mr, ldx, lda;
   size_t offA, offB, offX, offXn, floats;  // in floats
 };
-__host__ __device__ inline ClLayout cl_layout(int M, int N) {
+__host__ __device__ inline ClLayout cl_layout(int M, int N, int C = kClCtas) {
   ClLayout L;
   L.N4 = (N + 3) & ~3;
-  L.Nr = ((N + kClCtas - 1) / kClCtas + 3) & ~3;
-  L.Mr = ((M + kClCtas - 1) / kClCtas + 3) & ~3;
+  L.Nr = ((N + C - 1) / C + 3) & ~3;
+  L.Mr = ((M + C - 1) / C + 3) & ~3;
   L.ldx = L.N4 + 4;  // X rows are also read with a row stride (XB): pad against bank conflicts
   L.lda = L.N4 + 4;  // A, B rows: padded too (the k-split lanes read 4 rows at once)
   size_t o = 0;
   L.offA = o; o += (size_t)L.N4 * L.lda;
   L.offB = o; o += (size_t)L.N4 * L.lda;
-  L.offX = o; o += (size_t)kClCtas * L.Mr * L.ldx;
+  L.offX = o; o += (size_t)C * L.Mr * L.ldx;
   L.offXn = o; o += (size_t)L.Mr * L.ldx;
   o += L.N4;  // s
   L.floats = o;
   return L;
 }
-__host__ __device__ inline bool cl_fits(int64_t M, int64_t N) {
-  return N >= 1 && N <= kClMaxN && M <= 4096 && cl_layout((int)M, (int)N).floats * 4 + kClHdr <= kClMaxSmem;
+__host__ __device__ inline bool cl_fits(int64_t M, int64_t N, int C = kClCtas) {
+  return N >= 1 && N <= kClMaxN && M <= 4096 && cl_layout((int)M, (int)N, C).floats * 4 + kClHdr <= kClMaxSmem;
 }
 
 }  // namespace tns

@@ -204,3 +204,23 @@ def test_cluster_repeated_calls_bitwise(precond, coeffs):
         else:
             assert torch.equal(o, ref)
     torch.cuda.synchronize()
+
+
+def test_cluster_size_groups_bitwise():
+    """Small matrices that fit the 16-CTA layout and ones that only fit the 8-CTA layout run
+    in separate cluster launches; every result is bitwise its single-call result."""
+    shapes = [(160, 128), (128, 128), (64, 576), (632, 64)]
+    xs = [torch.from_numpy(I.gaussian(m, n, seed=230 + i)).to(torch.bfloat16).cuda() for i, (m, n) in enumerate(shapes)]
+    singles = []
+    for x in xs:
+        t = x.clone()
+        ns.orthogonalize(t, iters=4)
+        singles.append(t)
+    outs = [torch.empty_like(x) for x in xs]
+    ns.orthogonalize_list(xs, out=outs, iters=4)
+    c0 = ns.launch_count()
+    ns.orthogonalize_list(xs, out=outs, iters=4)
+    torch.cuda.synchronize()
+    assert ns.launch_count() - c0 == 2
+    for o, s in zip(outs, singles):
+        assert torch.equal(o, s)
