@@ -862,11 +862,22 @@ static ns_status run(const std::vector<Mat>& mats_in, int iters, const float* co
   auto it = g_plans.find(key);
   Plan* P = nullptr;
   if (it == g_plans.end()) {
-    if (g_plans.size() >= kMaxPlans) {  // evict least recently used (synchronising)
+    // Evict least-recently-used plans (synchronising) while the cache is full by count or
+    // would hold more workspace than max(4 GiB, 2 x this list's): a caller that passes new
+    // buffers every step (fresh pointers, fresh plans) must not accumulate workspaces.
+    const size_t need = workspace_bytes_for(big, dtype);
+    const size_t budget = std::max<size_t>((size_t)4 << 30, 2 * need);
+    auto held = [&]() {
+      size_t b = 0;
+      for (auto& kv : g_plans) if (!kv.second->ws_borrowed) b += kv.second->ws_bytes;
+      return b;
+    };
+    bool synced = false;
+    while (!g_plans.empty() && (g_plans.size() >= kMaxPlans || held() + need > budget)) {
       auto victim = g_plans.begin();
       for (auto jt = g_plans.begin(); jt != g_plans.end(); ++jt)
         if (jt->second->last_use < victim->second->last_use) victim = jt;
-      cudaDeviceSynchronize();
+      if (!synced) { cudaDeviceSynchronize(); synced = true; }
       g_plans.erase(victim);
     }
     std::unique_ptr<Plan> np(new Plan());

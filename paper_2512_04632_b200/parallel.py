@@ -111,6 +111,31 @@ def _make_plan(shapes, world: int, iters: int, buckets: int) -> ShardPlan:
 
 
 _BUFFERS: dict = {}
+# Per-call caches (prepared argument arrays + views for one exact list of tensors) hold
+# strong references to the caller's tensors, so they are kept in a small LRU: a caller that
+# passes fresh tensors every step neither leaks them nor reuses a stale entry (an id()
+# cannot be recycled while its entry is alive).
+_CALLS: "collections.OrderedDict" = None
+_MAX_CALLS = 16
+
+
+def _call_get(key):
+    global _CALLS
+    if _CALLS is None:
+        import collections
+        _CALLS = collections.OrderedDict()
+    ent = _CALLS.get(key)
+    if ent is not None:
+        _CALLS.move_to_end(key)
+    return ent
+
+
+def _call_put(key, ent):
+    _call_get(key)
+    _CALLS[key] = ent
+    _CALLS.move_to_end(key)
+    while len(_CALLS) > _MAX_CALLS:
+        _CALLS.popitem(last=False)
 _STREAMS: dict = {}
 
 
@@ -220,7 +245,7 @@ def orthogonalize_sharded(xs: Sequence[torch.Tensor], group=None, iters: int = 4
     # argument arrays of every bucket are built once (host overhead ~tens of us per step)
     ckey = ("call", tuple(id(t) for t in xs), world, rank, buckets, iters, precond,
             None if coeffs is None else tuple(map(tuple, coeffs)), id(group), compute is None)
-    ent = _BUFFERS.get(ckey)
+    ent = _call_get(ckey)
     if ent is None or (ent["calls"] and not all(c.valid() for c in ent["calls"] if c is not None)):
         shapes = [tuple(t.shape) for t in xs]
         plan = make_plan(shapes, world, iters, buckets)
@@ -236,7 +261,7 @@ def orthogonalize_sharded(xs: Sequence[torch.Tensor], group=None, iters: int = 4
             else:
                 calls.append(None)
         ent = {"plan": plan, "buf": buf, "views": views, "calls": calls}
-        _BUFFERS[ckey] = ent
+        _call_put(ckey, ent)
     plan, buf, views = ent["plan"], ent["buf"], ent["views"]
     cuda = device.type == "cuda"
     overlap = on and cuda and len(plan.buckets) > 1
@@ -318,7 +343,7 @@ def orthogonalize_host(host_xs: Sequence[torch.Tensor], group=None, iters: int =
     # prepared NS calls are built once, so many small buckets stay cheap on the host
     ckey = ("hostcall", tuple(id(t) for t in host_xs), world, rank, buckets, iters, precond,
             None if coeffs is None else tuple(map(tuple, coeffs)), id(group), str(device))
-    ent = _BUFFERS.get(ckey)
+    ent = _call_get(ckey)
     if ent is None:
         shapes = [tuple(t.shape) for t in host_xs]
         plan = make_plan(shapes, world, iters, buckets)
@@ -332,7 +357,7 @@ def orthogonalize_host(host_xs: Sequence[torch.Tensor], group=None, iters: int =
                  if pr[rank] and device.type == "cuda" else None for pr in plan.buckets]
         ent = {"plan": plan, "dev_in": dev_in, "buf": buf, "hout": hout, "calls": calls,
                "outs": [hout[o:o + m * n].view(m, n) for o, (m, n) in zip(plan.offsets, shapes)]}
-        _BUFFERS[ckey] = ent
+        _call_put(ckey, ent)
     plan, dev_in, buf, hout = ent["plan"], ent["dev_in"], ent["buf"], ent["hout"]
     cur = torch.cuda.current_stream(device)
     h2d, d2h = _stream(device, "h2d"), _stream(device, "d2h")

@@ -428,3 +428,24 @@ def test_nonfinite_input_raises_flag(m, n):
     t = torch.from_numpy(I.gaussian(m, n, seed=78)).to(torch.bfloat16).cuda()
     ns.orthogonalize(t, iters=4)
     assert ns.read_flags() == 0
+
+
+def test_fresh_buffers_every_call_do_not_accumulate_workspace():
+    """A caller that passes new tensors every call gets a new plan each time; the plan cache
+    evicts by workspace bytes, so device memory stays bounded (no OOM, results correct)."""
+    shapes = [(4096, 1024)] * 8  # ~200 MB of workspace per plan
+    keep = []  # keep every step's inputs alive: each call sees new pointers -> a new plan
+    free0 = torch.cuda.mem_get_info()[0]
+    c0 = ns.launch_count()
+    for step in range(40):  # 40 plans x ~200 MB of workspace would be 8 GB without eviction
+        xs = [torch.randn(m, n, device="cuda").bfloat16() for m, n in shapes]
+        ns.orthogonalize_list(xs, iters=4)
+        keep.append(xs)
+    torch.cuda.synchronize()
+    assert ns.launch_count() - c0 == 40 * 13
+    inputs = 40 * sum(m * n * 2 for m, n in shapes)
+    used = free0 - torch.cuda.mem_get_info()[0] - inputs
+    assert used < 5 * 2 ** 30, used
+    t = keep[-1][0].clone()
+    ns.orthogonalize(t, iters=4)
+    assert torch.equal(t, keep[-1][0]) is False and torch.isfinite(t.float()).all()
