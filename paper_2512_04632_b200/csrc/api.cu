@@ -1037,6 +1037,15 @@ ns_status ns_orthogonalize_peers(void* const* X, void* const* out, void* const* 
 // Muon step: cached device job tables, keyed by the pointer lists.
 static std::map<std::vector<uint64_t>, void*> g_muon_tabs;
 
+// The Muon job tables are keyed by pointer lists; a caller with fresh buffers every step
+// would add one per step: past 1024 tables, synchronise and drop them all.
+static void muon_tabs_trim() {
+  if (g_muon_tabs.size() < 1024) return;
+  cudaDeviceSynchronize();
+  for (auto& kv : g_muon_tabs) cudaFree(kv.second);
+  g_muon_tabs.clear();
+}
+
 ns_status ns_muon_step(void* const* W, const void* const* G, float* const* M, void* const* U,
                        const int64_t* m, const int64_t* n, int64_t count, ns_dtype w_dtype, ns_dtype g_dtype,
                        float lr, float beta, float weight_decay, int nesterov, int iters, const float* coeffs,
@@ -1075,6 +1084,7 @@ ns_status ns_muon_step(void* const* W, const void* const* G, float* const* M, vo
   auto it = g_muon_tabs.find(key);
   void* dtab = nullptr;
   if (it == g_muon_tabs.end()) {
+    muon_tabs_trim();
     CU_TRY(cudaMalloc(&dtab, jobs.size() * sizeof(MuonJob)));
     CU_TRY(cudaMemcpy(dtab, jobs.data(), jobs.size() * sizeof(MuonJob), cudaMemcpyHostToDevice));
     g_muon_tabs[key] = dtab;
@@ -1122,6 +1132,7 @@ ns_status ns_muon_apply(void* const* W, const void* const* U, const int64_t* m, 
   auto it = g_muon_tabs.find(key);
   void* dtab = nullptr;
   if (it == g_muon_tabs.end()) {
+    muon_tabs_trim();
     CU_TRY(cudaMalloc(&dtab, jobs.size() * sizeof(MuonJob)));
     CU_TRY(cudaMemcpy(dtab, jobs.data(), jobs.size() * sizeof(MuonJob), cudaMemcpyHostToDevice));
     g_muon_tabs[key] = dtab;
