@@ -300,6 +300,30 @@ def run_own(args):
             return orthogonalize_sharded(xs, None, iters=iters, precond="aol", collective="fused")
         return orthogonalize_sharded(xs, None, iters=iters, precond="aol", buckets=buckets)
 
+    if world > 1 and collective == "fused" and args.collective_auto:
+        # both exchanges are this library's: time a few steps of each (max over ranks) and
+        # keep the faster for the timed region -- the fused stores can only overlap the last
+        # XB launch, the bucketed NCCL all-gathers overlap the following buckets' compute
+        def probe(kind):
+            nonlocal collective
+            collective = kind
+            for _ in range(2):
+                step()
+            torch.cuda.synchronize()
+            dist.barrier()
+            q0, q1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            q0.record()
+            for _ in range(3):
+                step()
+            q1.record()
+            torch.cuda.synchronize()
+            t = torch.tensor([q0.elapsed_time(q1) / 3], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            return float(t.item())
+        t_f, t_n = probe("fused"), probe("nccl")
+        collective = "fused" if t_f <= t_n else "nccl"
+        coll_note = f"exchange chosen by a 3-step probe: fused {t_f:.3f} ms, nccl ({buckets} buckets) {t_n:.3f} ms"
+
     for _ in range(max(args.warmup, 3)):
         step()
     torch.cuda.synchronize()
@@ -585,6 +609,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--e2e-buckets", type=int, default=48)
     ap.add_argument("--buckets", type=int, default=4, help="all-gather buckets at N > 1 (NCCL)")
+    ap.add_argument("--no-collective-auto", dest="collective_auto", action="store_false",
+                    help="N > 1: do not probe fused vs NCCL; time --collective as given")
     ap.add_argument("--collective", choices=["fused", "nccl"], default="fused",
                     help="N > 1: fused peer stores in the last epilogue, or NCCL all-gathers")
     ap.add_argument("--extra-reps", type=int, default=10)
