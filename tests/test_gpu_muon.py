@@ -105,3 +105,33 @@ def test_distributed_turbo_muon_world1_equals_turbo_muon():
                 assert torch.equal(a, b)
     finally:
         dist.destroy_process_group()
+
+
+def test_turbo_muon_step_cuda_graph():
+    """After the first (table-building) step, an optimizer step only enqueues launches: it
+    can be captured in a CUDA graph and replayed with results bitwise equal to eager steps."""
+    shapes = [(768, 768), (3072, 768), (64, 576)]
+    ws = [I.gaussian(m, n, seed=800 + i, bf16=False) for i, (m, n) in enumerate(shapes)]
+    gs = [torch.from_numpy(I.gaussian(m, n, seed=900 + i)).cuda() for i, (m, n) in enumerate(shapes)]
+    pa = [torch.nn.Parameter(torch.from_numpy(w).cuda()) for w in ws]
+    pb = [torch.nn.Parameter(torch.from_numpy(w).cuda()) for w in ws]
+    for p, g in zip(pa + pb, gs + gs):
+        p.grad = g.clone()
+    oa = ns.TurboMuon(pa, lr=0.02, momentum=0.9)
+    ob = ns.TurboMuon(pb, lr=0.02, momentum=0.9)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        oa.step()
+        ob.step()  # builds tables and plans
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        ob.step()
+    for _ in range(3):
+        oa.step()
+        g.replay()
+    torch.cuda.synchronize()
+    for a, b in zip(pa, pb):
+        assert torch.equal(a, b)
