@@ -17,7 +17,10 @@ constexpr int kBM = 128;  // UMMA M
 constexpr int kBN = 256;  // UMMA N
 constexpr int kBK = 64;   // K elements per pipeline stage = one 128-byte swizzle atom
 constexpr int kSymBlock = 256;  // symmetric phases tile the lower triangle in 256 x 256 blocks
-constexpr int kGroupP = 16;     // XB raster: tiles grouped 16 row-blocks deep for L2 reuse
+#ifndef TNS_GROUP_P
+#define TNS_GROUP_P 16
+#endif
+constexpr int kGroupP = TNS_GROUP_P;  // XB raster: tiles grouped 16 row-blocks deep for L2 reuse
 
 // One entry of a launch's tile list (built on the host in execution order):
 //   bits [0,20) job index | [20,40) p0 / 128 | [40,60) q0 / 256 | bit 63 mirrored store.
