@@ -449,3 +449,28 @@ def test_fresh_buffers_every_call_do_not_accumulate_workspace():
     t = keep[-1][0].clone()
     ns.orthogonalize(t, iters=4)
     assert torch.equal(t, keep[-1][0]) is False and torch.isfinite(t.float()).all()
+
+
+@pytest.mark.parametrize("m,n,dtype", [(300, 201, torch.bfloat16), (201, 300, torch.bfloat16),
+                                       (256, 200, torch.float32), (520, 136, torch.float32)])
+def test_simt_engine_paths(m, n, dtype):
+    """Shapes the TMA engine cannot address (m or n not a multiple of 8) and fp32 matrices
+    too big for the cluster kernel run on the CUDA-core step kernels: same gates."""
+    bf16 = dtype == torch.bfloat16
+    x = I.gaussian(m, n, seed=I.matrix_seed(11, m + n), bf16=bf16)
+    out = _run(x, C.turbo(4), "aol", dtype=dtype)
+    ref = oracle_run(x, C.turbo(4), "aol")
+    assert relF(out, ref) <= (BF16_TOL if bf16 else FP32_TOL)
+
+
+@pytest.mark.parametrize("path", [1, 2])
+def test_forced_paths_full_ns(path):
+    """ns_set_path(1) (SIMT kernels for everything) and (2) (single-CTA 128x256 tcgen05
+    tiles) run the whole iteration within the gates."""
+    old = ns.set_path(path)
+    try:
+        for (m, n) in [(768, 256), (256, 768), (520, 136)]:
+            x = I.gaussian(m, n, seed=I.matrix_seed(12, m + n))
+            assert relF(_run(x, C.turbo(4), "aol"), oracle_run(x, C.turbo(4), "aol")) <= BF16_TOL
+    finally:
+        ns.set_path(old)
