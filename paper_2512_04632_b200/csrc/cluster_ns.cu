@@ -233,21 +233,28 @@ __global__ void __launch_bounds__(kClThreads, 1)
     cl_wait(&bars[0], par);
     if (k == 0) CL_TL(1);
     if (k == 0 && precond != 0) {
+      // A0 is rescaled IN PLACE below, including this CTA's own rows, which the bulk copies
+      // of the G phase may still be reading.  Every CTA has received all of A0 once it gets
+      // here, so after a cluster barrier all those copies are complete: arrive now, rescale
+      // everything but the own rows, wait, then rescale the own rows (the data itself came
+      // with complete_tx, so the barrier needs no release fence).
+      cluster_arrive_relaxed();
       // every CTA derives the same s from its full copy of A0 (fixed order: identical)
-      // lanes over the <= 32 column groups of 4 (N <= 128), warps over rows: 16-byte accesses
       if (precond == 2) {  // AOL, Eq. 8: s_i = (sum_j |A0_ij|)^(-1/2), 0 for a zero row
-        for (int i = warp; i < N; i += kWarps) {
-          float acc = 0.f;
-          if (lane < C4) {
-            const float4 v = *reinterpret_cast<const float4*>(A + (size_t)i * lda + 4 * lane);
-            acc = (fabsf(v.x) + fabsf(v.y)) + (fabsf(v.z) + fabsf(v.w));
+        // one thread per row, columns in order (row stride lda: conflict-free 16-byte reads)
+        for (int i = tid; i < N; i += kClThreads) {
+          const float4* row = reinterpret_cast<const float4*>(A + (size_t)i * lda);
+          float s0 = 0.f, s1 = 0.f;
+#pragma unroll 4
+          for (int q = 0; q < C4; ++q) {
+            const float4 v = row[q];
+            s0 += fabsf(v.x) + fabsf(v.y);
+            s1 += fabsf(v.z) + fabsf(v.w);
           }
-          const float rs = cl_warp_sum(acc);
-          if (lane == 0) {
-            s[i] = rs > 0.f ? rsqrtf(rs) : 0.f;
-            if (!(rs > 0.f)) fl |= 1u;
-            if (!isfinite(rs)) fl |= 2u;
-          }
+          const float rs = s0 + s1;
+          s[i] = rs > 0.f ? rsqrtf(rs) : 0.f;
+          if (!(rs > 0.f)) fl |= 1u;
+          if (!isfinite(rs)) fl |= 2u;
         }
       } else if (warp == 0) {  // Frobenius, Eq. 10: s = 1/sqrt(trace A0) = 1/||X||_F
         float acc = 0.f;
@@ -258,23 +265,34 @@ __global__ void __launch_bounds__(kClThreads, 1)
         if (lane == 0 && !(tr > 0.f)) fl |= 1u;
         if (lane == 0 && !isfinite(tr)) fl |= 2u;
       }
-      // A0 is rescaled IN PLACE below, including this CTA's own rows, which the bulk copies
-      // of the G phase may still be reading: every CTA has received all of A0 once it
-      // reaches this barrier, so all those copies are complete after it
-      cluster_sync();
+      __syncthreads();
       // A1 = diag(s) A0 diag(s) (symmetric product: bitwise symmetric), X1 = X0 diag(s);
-      // s is zero beyond N, so the padding stays zero
-      if (lane < C4) {
-        const float4 sj = *reinterpret_cast<const float4*>(s + 4 * lane);
-        auto scale4 = [&](float* p, float f) {
-          float4 v = *reinterpret_cast<float4*>(p);
-          v.x = rnd<S>(v.x * (f * sj.x)); v.y = rnd<S>(v.y * (f * sj.y));
-          v.z = rnd<S>(v.z * (f * sj.z)); v.w = rnd<S>(v.w * (f * sj.w));
-          *reinterpret_cast<float4*>(p) = v;
-        };
-        for (int i = warp; i < N; i += kWarps) scale4(A + (size_t)i * lda + 4 * lane, s[i]);
-        // X: column scaling only (f = 1 keeps the products exact: v * (1 * s_j) = v * s_j)
-        for (int i = warp; i < M; i += kWarps) scale4(Xf + (size_t)i * ldx + 4 * lane, 1.f);
+      // s is zero beyond N, so the padding stays zero.  Flat over (row, 16-byte column group).
+      auto scale4 = [&](float* p, float f, float4 sj) {
+        float4 v = *reinterpret_cast<float4*>(p);
+        v.x = rnd<S>(v.x * (f * sj.x)); v.y = rnd<S>(v.y * (f * sj.y));
+        v.z = rnd<S>(v.z * (f * sj.z)); v.w = rnd<S>(v.w * (f * sj.w));
+        *reinterpret_cast<float4*>(p) = v;
+      };
+      // X: column scaling only (f = 1 keeps the products exact: v * (1 * s_j) = v * s_j)
+#pragma unroll 4
+      for (int e = tid; e < M * C4; e += kClThreads) {
+        const int i = e / C4, q = e - i * C4;
+        scale4(Xf + (size_t)i * ldx + 4 * q, 1.f, *reinterpret_cast<const float4*>(s + 4 * q));
+      }
+      // A: the peers' rows (rows [0, N) minus [r0, r0 + nr))
+      const int nother = N - nr;
+#pragma unroll 4
+      for (int e = tid; e < nother * C4; e += kClThreads) {
+        int i = e / C4;
+        const int q = e - i * C4;
+        i += i >= r0 ? nr : 0;
+        scale4(A + (size_t)i * lda + 4 * q, s[i], *reinterpret_cast<const float4*>(s + 4 * q));
+      }
+      cluster_wait();
+      for (int e = tid; e < nr * C4; e += kClThreads) {
+        const int i = r0 + e / C4, q = e % C4;
+        scale4(A + (size_t)i * lda + 4 * q, s[i], *reinterpret_cast<const float4*>(s + 4 * q));
       }
       __syncthreads();
     }
