@@ -144,8 +144,9 @@ struct Mat {
   bool wide;
   bool copy_in;
   // workspace byte offsets
-  size_t w_off, a_off, b_off, s_off, part_off;
+  size_t w_off, a_off, b_off, s_off, part_off, split_off;
   int part_ld;
+  int split;  // split-K factor of this matrix's Gram (0: none), see choose_splits
   // tensormap indices (tcgen05 path)
   int tm_x, tm_out, tm_w, tm_a, tm_b;
   // fused collective: extra destinations of the final result (peers' buffers)
@@ -153,7 +154,7 @@ struct Mat {
   int tm_peer;
 };
 
-enum PhaseKind { PH_GEMM = 0, PH_SIMT = 1, PH_PRECOND = 2, PH_COPY = 3, PH_FUSED = 4, PH_CLUSTER = 5 };
+enum PhaseKind { PH_GEMM = 0, PH_SIMT = 1, PH_PRECOND = 2, PH_COPY = 3, PH_FUSED = 4, PH_CLUSTER = 5, PH_SPLIT = 6 };
 struct Phase {
   PhaseKind kind;
   size_t dev_off;  // offset of the job array in the device table
@@ -225,6 +226,38 @@ static size_t s_floats(int64_t N) { return (size_t)((N + 255) / 256 * 256 + 32);
 // AOL row-sum partial slots per row (see GemmJob::part).
 static int part_ld_for(int64_t N) { return (int)((N + 127) / 128 + (N + 31) / 32); }
 
+// Split-K Gram.  For N <= 256 the Gram is one 256 x 256 block per matrix, walked over the
+// whole K = M by a single CTA pair: with a long K (tall matrices, e.g. 256 x 2304 conv
+// weights) and few matrices, a handful of pairs stream K at single-SM bandwidth while the
+// rest of the GPU idles.  When the call's Gram step is tile-starved (its tiles fill at most
+// half of the CTA-pair workers), such Grams are cut into S = ceil(nk / 8) k-ranges (nk =
+// k-blocks of 64, nk >= 16, S <= 16), computed as independent tiles whose fp32 partials a
+// reduction launch sums in a fixed order.  S depends on the matrix shape alone, so results
+// are bitwise the same in every tile-starved call (single matrices, small lists); a call
+// that fills the GPU does not split (the partials' traffic would cost more than the idle
+// SMs it recovers) and differs from a split call at rounding level.  Per-step launches only
+// (the opt-in fused and multicast paths do not split).
+static const int64_t kSplitLd = 256;  // floats per partial row; rows padded to 256 too
+static int split_factor(int64_t M, int64_t N) {
+  if (N > kSplitMaxN) return 0;
+  const int64_t nk = (M + kBK - 1) / kBK;
+  if (nk < 16) return 0;
+  return (int)std::min<int64_t>(16, (nk + 7) / 8);
+}
+static void choose_splits(std::vector<Mat>& mats, int cg, int workers) {
+  for (Mat& mt : mats) mt.split = 0;
+  if (const char* e = getenv("TNS_NOSPLIT"))  // measurement knob (A/B), read at plan build
+    if (atoi(e)) return;
+  int64_t tiles = 0;
+  for (const Mat& mt : mats) {
+    const int64_t nb = (mt.N + kSymBlock - 1) / kSymBlock;
+    tiles += nb * (nb + 1) / 2 * (2 / cg);
+  }
+  if (2 * tiles > workers) return;
+  for (Mat& mt : mats) mt.split = split_factor(mt.M, mt.N);
+}
+static size_t split_bytes(const Mat& mt) { return mt.split ? (size_t)mt.split * kSplitLd * kSplitLd * 4 : 0; }
+
 static size_t workspace_bytes_for(const std::vector<Mat>& mats, ns_dtype dt) {
   size_t off = 1024;  // [0,1024): grid-barrier words and fused-mode phase counters
   const size_t es = elem_size(dt);
@@ -234,6 +267,7 @@ static size_t workspace_bytes_for(const std::vector<Mat>& mats, ns_dtype dt) {
     off = align_up(off, 256) + (size_t)mt.N * mt.N * es;
     off = align_up(off, 256) + s_floats(mt.N) * 4;
     off = align_up(off, 256) + (size_t)mt.N * part_ld_for(mt.N) * 4;
+    if (dt == NS_BF16) off = align_up(off, 256) + (size_t)split_factor(mt.M, mt.N) * kSplitLd * kSplitLd * 4;
   }
   return align_up(off, 256);
 }
@@ -268,7 +302,9 @@ static bool half_storage_enabled() {
 static void balance_tasks(std::vector<TaskDesc>& tasks, const std::vector<GemmJob>& jobs, int workers) {
   const int64_t n = (int64_t)tasks.size();
   if (workers < 2 || n <= workers) return;
-  auto cost = [&](const TaskDesc& td) { return (int64_t)((jobs[td.tile & 0xFFFFFu].K + kBK - 1) / kBK) + 4; };
+  auto cost = [&](const TaskDesc& td) {
+    return (int64_t)(td.nkb ? td.nkb : (jobs[td.tile & 0xFFFFFu].K + kBK - 1) / kBK) + 4;
+  };
   int64_t cmin = INT64_MAX, cmax = 0;
   for (const TaskDesc& td : tasks) { cmin = std::min(cmin, cost(td)); cmax = std::max(cmax, cost(td)); }
   if (cmin == cmax) return;  // uniform tiles: round-robin is already balanced
@@ -299,6 +335,8 @@ static ns_status build_plan(Plan& P, HostTables& H, DevCtx* dc, const float* coe
   const int T = P.iters;
   const size_t es = elem_size(P.dtype);
   const bool bf16 = P.dtype == NS_BF16;
+  if (!P.simt && (P.cg == 1 || P.cg == 2) && g_path != 3) choose_splits(P.mats, P.cg, dc->sms / P.cg);
+  else for (Mat& mt : P.mats) mt.split = 0;
   // -- workspace layout
   size_t off = 1024;  // [0,16): preconditioner grid barrier; [64, 1024): phase counters
   for (Mat& mt : P.mats) {
@@ -309,6 +347,7 @@ static ns_status build_plan(Plan& P, HostTables& H, DevCtx* dc, const float* coe
     mt.part_ld = part_ld_for(mt.N);
     off = align_up(off, 256); mt.part_off = off;
     if (P.precond == NS_PRECOND_AOL && !P.simt) off += (size_t)mt.N * mt.part_ld * 4;
+    off = align_up(off, 256); mt.split_off = off; off += split_bytes(mt);
   }
   P.ws_bytes = align_up(off, 256);
   cudaError_t e = cudaSuccess;
@@ -377,6 +416,8 @@ static ns_status build_plan(Plan& P, HostTables& H, DevCtx* dc, const float* coe
     std::vector<PrecondJob> pj;
     int64_t rows = 0, items = 0;
     bool vec8 = false;
+    std::vector<int> jsplit;   // PHK_GEMM: split-K factor per job (0: none)
+    std::vector<SplitJob> sj;  // PHK_SPLIT
   };
   std::vector<Step> steps;
 
@@ -446,6 +487,12 @@ static ns_status build_plan(Plan& P, HostTables& H, DevCtx* dc, const float* coe
             J.out = Am(mt); J.aux = nullptr; J.ld = mt.N;
             J.half = hs;  // A: lower-triangle blocks only (readers take the upper transposed)
             if (k == 1 && use_part) { J.part = Part(mt); J.part_ld = mt.part_ld; }
+            if (mt.split) {  // partials only; the reduction launch writes A (and the AOL sums)
+              J.split_ws = reinterpret_cast<float*>(ws + mt.split_off);
+              J.split_stride = kSplitLd * kSplitLd;
+              J.split_ld = (int)kSplitLd;
+              J.part = nullptr; J.part_ld = 0;
+            }
           } else if (mode == MODE_POLY) {
             ta = tb = mt.tm_a;
             tout = mt.tm_b; taux = mt.tm_a;
@@ -484,7 +531,26 @@ static ns_status build_plan(Plan& P, HostTables& H, DevCtx* dc, const float* coe
         stp.gemm_kind = mode == MODE_GRAM ? 0 : (mode == MODE_POLY ? 2 : 3);
         stp.jobs = std::move(jobs);
         stp.tmi = std::move(tmi);
+        for (Mat& mt : P.mats) stp.jsplit.push_back(mode == MODE_GRAM ? mt.split : 0);
         steps.push_back(std::move(stp));
+        if (mode == MODE_GRAM) {
+          Step red;
+          red.kind = PHK_SPLIT;
+          for (Mat& mt : P.mats) {
+            if (!mt.split) continue;
+            SplitJob S;
+            std::memset(&S, 0, sizeof(S));
+            S.ws = reinterpret_cast<const float*>(ws + mt.split_off);
+            S.stride = kSplitLd * kSplitLd; S.ld = (int)kSplitLd;
+            S.S = mt.split; S.N = (int)mt.N;
+            S.A = Am(mt);
+            if (k == 1 && use_part) { S.part = Part(mt); S.part_ld = mt.part_ld; }
+            S.row_start = red.rows;
+            red.rows += mt.N;
+            red.sj.push_back(S);
+          }
+          if (!red.sj.empty()) steps.push_back(std::move(red));
+        }
       } else {
         std::vector<SimtJob> jobs;
         int64_t total = 0;
@@ -610,7 +676,19 @@ static ns_status build_plan(Plan& P, HostTables& H, DevCtx* dc, const float* coe
             }
           } else {
             std::vector<uint64_t> tl = tile_list(st, 0);
-            for (uint64_t w : tl) tasks.push_back(mk_task(w));
+            for (uint64_t w : tl) {
+              const size_t j = w & 0xFFFFFu;
+              const int S = j < st.jsplit.size() ? st.jsplit[j] : 0;
+              if (!S) { tasks.push_back(mk_task(w)); continue; }
+              const int nk = (st.jobs[j].K + kBK - 1) / kBK;
+              for (int sp = 0; sp < S; ++sp) {  // k-blocks [sp*nk/S, (sp+1)*nk/S)
+                TaskDesc td = mk_task(w);
+                td.kb0 = (uint32_t)(sp * nk / S);
+                td.nkb = (uint32_t)((sp + 1) * nk / S) - td.kb0;
+                td.split = (uint32_t)sp + 1;
+                tasks.push_back(td);
+              }
+            }
             balance_tasks(tasks, st.jobs, dc->sms / P.cg);
           }
           Phase ph{PH_GEMM};
@@ -623,6 +701,12 @@ static ns_status build_plan(Plan& P, HostTables& H, DevCtx* dc, const float* coe
           for (size_t j = 0; j < st.jobs.size(); ++j)
             fixes.push_back({ph.dev_off + j * sizeof(GemmJob), st.tmi[j][0], st.tmi[j][1], st.tmi[j][2], st.tmi[j][3],
                              st.tmi[j][4]});
+          P.phases.push_back(ph);
+        } else if (st.kind == PHK_SPLIT) {
+          Phase ph{PH_SPLIT};
+          ph.dev_off = H.push(st.sj.data(), st.sj.size() * sizeof(SplitJob), 64);
+          ph.njobs = (int)st.sj.size();
+          ph.total_rows = st.rows;
           P.phases.push_back(ph);
         } else {
           Phase ph{PH_PRECOND};
@@ -779,6 +863,13 @@ static ns_status enqueue_plan(Plan& P, DevCtx* dc, cudaStream_t stream) {
         ProfScope ps(4, stream);
         CU_TRY(launch_simt_gemm(reinterpret_cast<const SimtJob*>(dbase + ph.dev_off), ph.njobs, ph.total,
                                 dc->sms, P.dtype == NS_BF16, dc->flags, stream));
+        ++g_launches;
+        break;
+      }
+      case PH_SPLIT: {
+        ProfScope ps(0, stream);  // part of the Gram step
+        CU_TRY(launch_split_reduce(reinterpret_cast<const SplitJob*>(dbase + ph.dev_off), ph.njobs, ph.total_rows,
+                                   dc->flags, stream));
         ++g_launches;
         break;
       }

@@ -67,6 +67,11 @@ struct GemmJob {
   // POLY: added to diagonal elements before the column scaling, B' = bA + cA^2 + dI.  With
   // d = a_k the next XB needs no a*X term: X(aI + B) = aX + XB (Eq. 5 as one product).
   float diag_add;
+  // Split-K GRAM (tile-starved launches, see SplitJob): the tile's fp32 partial over its
+  // task's k-range goes to split_ws[(split - 1) * split_stride + p * split_ld + q], no epilogue.
+  float* split_ws;
+  int64_t split_stride;
+  int32_t split_ld;
 };
 
 // CUDA-core (SIMT) variant of a GemmJob: operands by pointer + strides (elements),
@@ -126,7 +131,7 @@ struct MuonJob {
 constexpr uint32_t kNoSlot = 0xFFFFFFFFu;
 enum TaskKind : uint32_t { TK_TILE = 0, TK_PRE_S = 1, TK_PRE_SCALE = 2, TK_NONE = 3 };  // NONE: schedule padding
 constexpr int kPreRows = 64;  // rows of one preconditioner task
-enum StepKind : int32_t { PHK_GEMM = 0, PHK_PRE_S = 1 };  // host-side step kinds (api.cu)
+enum StepKind : int32_t { PHK_GEMM = 0, PHK_PRE_S = 1, PHK_SPLIT = 2 };  // host-side step kinds (api.cu)
 // Bit 62 of a tile word: "shadow" tile -- computed (its operand loads feed the other pair of
 // a multicast cluster) but never stored.
 constexpr uint64_t kTileShadow = 1ull << 62;
@@ -139,7 +144,25 @@ struct TaskDesc {
   uint32_t my_slot;     // kNoSlot: no arrival
   uint32_t pjob;        // TK_PRE_*: matrix index into the launch's PrecondJob array
   uint32_t row0;        // TK_PRE_*: first row of the chunk
+  uint32_t kb0, nkb;    // TK_TILE: k-blocks [kb0, kb0 + nkb) of the contraction (nkb = 0: all)
+  uint32_t split;       // TK_TILE: 0, or 1 + index of this k-range's fp32 partial (split-K)
 };
+
+// Reduction of a split-K Gram (simt.cu): A = rnd(sum over s of ws[s]) in fixed order s = 0..S-1
+// (deterministic), plus the AOL row sums of |A0| when part != nullptr (written to slot 0 of
+// the row's part_ld slots; the others stay zero).  Only for N <= 256 (one symmetric block,
+// stored whole).
+struct SplitJob {
+  const float* ws;
+  int64_t stride;   // floats between consecutive partials
+  int32_t ld;       // floats per partial row
+  int32_t S, N;
+  void* A;          // N x N, ld N, storage type of the plan
+  float* part;
+  int32_t part_ld;
+  int64_t row_start;  // prefix over jobs of N (one warp per row)
+};
+constexpr int kSplitMaxN = 256;
 
 // ------------------------------------------------------------------ cluster-resident NS
 // Whole Newton-Schulz of one small matrix (short side N <= 128) inside one cluster of

@@ -39,6 +39,10 @@ cudaError_t launch_precondition(const PrecondJob* d_jobs, int njobs, int64_t tot
                                 int64_t total_elems_or_vecs, bool vec8, bool is_bf16,
                                 unsigned* d_barrier, uint32_t* d_flags, bool lane_rows, cudaStream_t stream);
 
+// Split-K Gram reduction (simt.cu): one warp per row of every job (bf16 storage).
+cudaError_t launch_split_reduce(const SplitJob* d_jobs, int njobs, int64_t total_rows, uint32_t* d_flags,
+                                cudaStream_t stream);
+
 // Whole NS of `njobs` small matrices, one cluster of `ctas` (8 or 16) CTAs each (cluster_ns.cu).
 // d_coeffs: 3*iters floats in device memory; smem_bytes: max cl_layout(..).floats * 4.
 cudaError_t launch_cluster_ns(const ClusterJob* d_jobs, int njobs, const float* d_coeffs, int iters, int precond,

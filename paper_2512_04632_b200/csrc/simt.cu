@@ -218,6 +218,71 @@ static cudaError_t launch_precond_t(const PrecondJob* d_jobs, int njobs, int64_t
   return cudaLaunchKernelEx(&cfg, kern, d_jobs, njobs, total_rows, total_items, d_barrier, d_flags, lane_rows);
 }
 
+// ------------------------------------------------------------------------------ split-K Gram
+// A = rnd(sum_s ws[s]) for the split-K Gram of tile-starved launches (SplitJob, jobs.h): one
+// warp per row, lanes over 8-column groups (N <= 256: one pass), partials summed in the
+// fixed order s = 0..S-1 (deterministic); AOL row sums of the rounded |A0| (Eq. 8) from the
+// same registers.  L2-resident: the partials were written by the immediately preceding Gram.
+__global__ void __launch_bounds__(256)
+    split_reduce_kernel(const SplitJob* __restrict__ jobs, int njobs, int64_t total_rows,
+                        uint32_t* __restrict__ flags) {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // the partials come from the Gram launch
+  const int lane = threadIdx.x & 31;
+  const int64_t row = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (row >= total_rows) return;
+  int lo = 0, hi = njobs - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (jobs[mid].row_start <= row) lo = mid; else hi = mid - 1;
+  }
+  const SplitJob& J = jobs[lo];
+  const int i = (int)(row - J.row_start);
+  float rs = 0.f;
+  bool bad = false;
+  for (int c0 = lane * 8; c0 < J.N; c0 += 256) {
+    float v[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    const float* src = J.ws + (int64_t)i * J.ld + c0;
+    for (int sp = 0; sp < J.S; ++sp) {
+      const float4 u0 = __ldcg(reinterpret_cast<const float4*>(src + sp * J.stride));
+      const float4 u1 = __ldcg(reinterpret_cast<const float4*>(src + sp * J.stride + 4));
+      v[0] += u0.x; v[1] += u0.y; v[2] += u0.z; v[3] += u0.w;
+      v[4] += u1.x; v[5] += u1.y; v[6] += u1.z; v[7] += u1.w;
+    }
+    uint16_t h[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      h[e] = __bfloat16_as_ushort(__float2bfloat16_rn(v[e]));
+      const float r = __uint_as_float((uint32_t)h[e] << 16);
+      rs += fabsf(r);
+      bad |= !isfinite(r);
+    }
+    uint4 w;
+    w.x = h[0] | ((uint32_t)h[1] << 16); w.y = h[2] | ((uint32_t)h[3] << 16);
+    w.z = h[4] | ((uint32_t)h[5] << 16); w.w = h[6] | ((uint32_t)h[7] << 16);
+    *reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(J.A) + (int64_t)i * J.N + c0) = w;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) rs += __shfl_xor_sync(0xffffffffu, rs, o);
+  if (J.part != nullptr && lane == 0) J.part[(int64_t)i * J.part_ld] = rs;
+  if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(flags, 2u);
+}
+
+cudaError_t launch_split_reduce(const SplitJob* d_jobs, int njobs, int64_t total_rows, uint32_t* d_flags,
+                                cudaStream_t stream) {
+  if (total_rows <= 0) return cudaSuccess;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)((total_rows + 7) / 8));
+  cfg.blockDim = dim3(256);
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // PDL
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, split_reduce_kernel, d_jobs, njobs, total_rows, d_flags);
+}
+
 cudaError_t launch_precondition(const PrecondJob* d_jobs, int njobs, int64_t total_rows,
                                 int64_t total_items, bool vec8, bool is_bf16, unsigned* d_barrier,
                                 uint32_t* d_flags, bool lane_rows, cudaStream_t stream) {

@@ -130,6 +130,9 @@ struct Epi {
   int npeer;
   float diag_add;
   int half;
+  float* split_ws;
+  int64_t split_stride;
+  int split_ld;
 };
 __device__ __forceinline__ Epi load_epi(const GemmJob* __restrict__ J) {
   Epi e;
@@ -144,6 +147,7 @@ __device__ __forceinline__ Epi load_epi(const GemmJob* __restrict__ J) {
   e.tmPeer = reinterpret_cast<const uint8_t*>(J->tmPeer); e.npeer = J->npeer;
   e.diag_add = J->diag_add;
   e.half = J->half;
+  e.split_ws = J->split_ws; e.split_stride = J->split_stride; e.split_ld = J->split_ld;
   return e;
 }
 
@@ -345,8 +349,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         const int pa = ti.p0 + (int)rank * G::kARows;  // this CTA's A rows
         const int qb = ti.q0 + (int)rank * G::kBRows;  // this CTA's B rows
-        const int nk = (K + kBK - 1) / kBK;
-        for (int kb = 0; kb < nk; ++kb) {
+        const int kbeg = (int)TD.kb0, kend = TD.nkb ? kbeg + (int)TD.nkb : (K + kBK - 1) / kBK;
+        for (int kb = kbeg; kb < kend; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
           uint8_t* sa = smem + (size_t)stage * G::kStageBytes;
           uint8_t* sb = sa + G::kABytes;
@@ -377,7 +381,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             else tma_load_2d(sb + i * kBoxBytes, tmB, &full_bar[stage], c0, c1);
           }
           if (++stage == G::kStages) { stage = 0; phase ^= 1; }
-          if (kb == 0 && t == cid) TL(2);  // first loads issued
+          if (kb == kbeg && t == cid) TL(2);  // first loads issued
         }
       }
       // tail: wait until the MMA released every stage, so no commit-arrive is still in
@@ -409,8 +413,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                      atomicAdd(&g_epi_prof[0], 1ull); }
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + as * kBN;
-        const int nk = (K + kBK - 1) / kBK;
-        for (int kb = 0; kb < nk; ++kb) {
+        const int kbeg = (int)TD.kb0, kend = TD.nkb ? kbeg + (int)TD.nkb : (K + kBK - 1) / kBK;
+        for (int kb = kbeg; kb < kend; ++kb) {
           if (mprof) {
             const long long m1 = clock64();
             atomicAdd(&g_epi_prof[3], (unsigned long long)(m1 - m0));
@@ -423,7 +427,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             m0 = m1;
           }
           tc_fence_after();
-          if (kb == 0 && t == cid) TL(3);  // first operands landed
+          if (kb == kbeg && t == cid) TL(3);  // first operands landed
           const uint32_t sa = smem_u32(smem + (size_t)stage * G::kStageBytes);
           const uint32_t sb = sa + G::kABytes;
           const int kblk = (kb * kBK) >> 8;
@@ -436,7 +440,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int kk = 0; kk < kBK / 16; ++kk) {
             const uint64_t adesc = make_sdesc(sa + kk * a_step, a_lbo, 1024u);
             const uint64_t bdesc = make_sdesc(sb + kk * b_step, b_lbo, 1024u);
-            umma_bf16<CG>(d_tmem, adesc, bdesc, idesc, (kb | kk) != 0 ? 1u : 0u);
+            umma_bf16<CG>(d_tmem, adesc, bdesc, idesc, (kb != kbeg || kk != 0) ? 1u : 0u);
           }
           if constexpr (MC == 2) umma_commit_mask(&empty_bar[stage], 0xF);  // both pairs' producers
           else umma_commit<CG>(&empty_bar[stage]);
@@ -547,6 +551,15 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_arrive_expect_tx(abar + xb, 2048);
             tma_load_2d(s_aux + 2048 * xb, E.tmAux, abar + xb, q + 64, prow);
           }
+        }
+        if (TD.split && !shadow) {  // split-K: this k-range's fp32 partial, no epilogue math
+          float4* dst = reinterpret_cast<float4*>(E.split_ws + (int64_t)(TD.split - 1) * E.split_stride +
+                                                  (int64_t)p * E.split_ld + q);
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            dst[j] = make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
+                                 __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3]));
+          continue;
         }
         if ((dbg & 1) || shadow) continue;
         // mirrored block: transposed box in smem for the mirrored store (full storage) and/or

@@ -158,7 +158,9 @@ def test_descent_alignment_and_determinism():
 
 def test_fused_equals_per_step_bitwise():
     """The fused single launch and the per-step launches run the same kernels on the same
-    tiles: outputs are bitwise equal."""
+    tiles: outputs are bitwise equal -- except where the per-step path splits the Gram's K
+    (N <= 256, M >= 1024: 256 x 2304 here; the fused and multicast paths do not split), which
+    moves the result at rounding level only."""
     shapes = [(256, 2304), (64, 216), (768, 768), (520, 136)]
     xs = [I.gaussian(m, n, seed=90 + i) for i, (m, n) in enumerate(shapes)]
     res = {}
@@ -171,9 +173,12 @@ def test_fused_equals_per_step_bitwise():
             res[path] = [t.float().cpu().numpy() for t in ts]
         finally:
             ns.set_path(old)
-    for a, b, c in zip(res[3], res[4], res[6]):
-        assert np.array_equal(a, b)
+    for (m, n), a, b, c in zip(shapes, res[3], res[4], res[6]):
         assert np.array_equal(a, c)
+        if min(m, n) <= 256 and max(m, n) >= 1024:  # split-K Gram on the per-step path
+            assert relF(a, b) <= 1e-2
+        else:
+            assert np.array_equal(a, b)
 
 
 def test_zero_column_flag():
