@@ -320,22 +320,23 @@ __global__ void __launch_bounds__(kThreads, 1)
   if constexpr (CG == 2) cluster_sync(); else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  // everything above overlaps the previous kernel's tail (PDL); data buffers are touched
-  // only after it has completed
+  // everything above overlaps the previous kernel's tail (PDL).  Each role waits for it
+  // (griddepcontrol.wait) right before its first access to data a previous launch writes or
+  // reads -- operands, aux, outputs, step counters -- so the static task / job / tensormap
+  // reads of its first tile overlap that tail too; the MMA issuer touches only smem and TMEM
+  // and never waits.
   if (warp == 0) TL(0);  // setup done
   pdl_trigger();
-  pdl_wait();
-  if (warp == 0) TL(1);  // dependency resolved
 
   if (warp == 0) {
     // ------------------------------------------------------------------ TMA producer
     if (lane == 0) {
       uint32_t stage = 0, phase = 0;
       int last_job = -1;
+      bool waited = false;
       for (int64_t t = cid; t < ntasks; t += ncl) {
         const TaskDesc TD = tasks[t];
         if (TD.kind != TK_TILE) continue;
-        if (TD.dep_slot != kNoSlot) wait_phase(done + TD.dep_slot, TD.dep_target);
         const TileInfo ti = decode_word(my_tile(TD));
         const GemmJob* J = jobs + ti.job;
         const void* tmA = J->tmA;
@@ -343,10 +344,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int a_mn = J->a_mn, b_mn = J->b_mn, K = J->K;
         const int a_sym = J->a_sym, b_sym = J->b_sym;
         if (ti.job != last_job) {
+          if (!waited) { tma_prefetch_desc(tmA); tma_prefetch_desc(tmB); }
           tma_desc_acquire(tmA);
           tma_desc_acquire(tmB);
           last_job = ti.job;
         }
+        if (!waited) {  // operands come from the previous launch
+          pdl_wait();
+          waited = true;
+          TL(1);  // dependency resolved
+        }
+        if (TD.dep_slot != kNoSlot) wait_phase(done + TD.dep_slot, TD.dep_target);
         const int pa = ti.p0 + (int)rank * G::kARows;  // this CTA's A rows
         const int qb = ti.q0 + (int)rank * G::kBRows;  // this CTA's B rows
         const int kbeg = (int)TD.kb0, kend = TD.nkb ? kbeg + (int)TD.nkb : (K + kBK - 1) / kBK;
@@ -468,8 +476,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     // register array stays live in production
 #define EPC(i, v) atomicAdd(&g_epi_prof[i], (unsigned long long)(v))
     uint32_t pfl = 0;
+    bool waited = false;
     for (int64_t t = cid; t < ntasks; t += ncl) {
       const TaskDesc TD = tasks[t];
+      if (!waited) {  // aux, outputs, counters and preconditioner rows: after the previous launch
+        pdl_wait();
+        waited = true;
+      }
       if (TD.dep_slot != kNoSlot) {  // the aux prefetch / preconditioner rows read that step
         if (lane == 0) wait_phase(done + TD.dep_slot, TD.dep_target);
         __syncwarp();
@@ -650,6 +663,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 #undef TL
   if (nslots > 0 && threadIdx.x == 0) {  // fused mode: the last CTA out resets the counters
+    pdl_wait();  // (a CTA without tile tasks has not waited yet)
     __threadfence();
     if (atomicAdd(done + nslots, 1u) == gridDim.x - 1) {
       for (int k = 0; k <= nslots; ++k) done[k] = 0;
