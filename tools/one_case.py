@@ -19,7 +19,7 @@ if not fp32:
     x = x.to(torch.bfloat16)
 o = torch.empty_like(x)
 dbg = int(os.environ.get("TNS_DBG", "0"))
-if dbg & (16 | 128):
+if dbg & (8 | 16 | 128):
     import ctypes
     from paper_2512_04632_b200._lib import lib
     ns.orthogonalize_list([x], out=[o], iters=4)
@@ -33,6 +33,11 @@ if dbg & 128:
     lib.nsx_epilogue_counters(c, 1)
     names = ["load", "G0", "precond", "P0", "Xcomp0", "Xbcast0", "loop_end", "end"]
     print({names[i]: int(c[i]) for i in range(7)}, "launches", c[7])
+elif dbg & 8:
+    lib.nsx_epilogue_counters(c, 1)
+    n = max(c[0], 1)
+    names = ["warp_tiles", "wait_acc", "tmem_ld", "aux_wait", "math", "bulk_read_wait", "store_issue"]
+    print({names[i]: (int(c[i]) if i == 0 else round(c[i] / n)) for i in range(7)})
 elif dbg & 16:
     lib.nsx_epilogue_counters(c, 1)
     n = max(c[7], 1)
