@@ -174,6 +174,7 @@ struct Phase {
   size_t coeff_off = 0;   // PH_CLUSTER: 3*iters floats
   size_t smem = 0;        // PH_CLUSTER: dynamic shared memory per CTA
   int ctas = 8;           // PH_CLUSTER: CTAs per cluster
+  bool has_split = false; // PH_GEMM: the task list holds split-K tasks
   // copies (PH_COPY)
   std::vector<std::pair<std::pair<void*, const void*>, size_t>> copies;
 };
@@ -693,6 +694,7 @@ static ns_status build_plan(Plan& P, HostTables& H, DevCtx* dc, const float* coe
           }
           Phase ph{PH_GEMM};
           ph.gemm_kind = st.gemm_kind;
+          for (const TaskDesc& td : tasks) ph.has_split = ph.has_split || td.split != 0;
           ph.dev_off = H.push(st.jobs.data(), st.jobs.size() * sizeof(GemmJob), 64);
           ph.njobs = (int)st.jobs.size();
           ph.tiles_off = H.push(tasks.data(), tasks.size() * sizeof(TaskDesc), 64);
@@ -845,7 +847,7 @@ static ns_status enqueue_plan(Plan& P, DevCtx* dc, cudaStream_t stream) {
         ProfScope ps(ph.gemm_kind, stream);
         CU_TRY(launch_umma_gemm(reinterpret_cast<const GemmJob*>(dbase + ph.dev_off),
                                 reinterpret_cast<const TaskDesc*>(dbase + ph.tiles_off), ph.total, nullptr, nullptr,
-                                0, ph.max_tiles, P.cg, dc->sms, dc->flags, stream));
+                                0, ph.max_tiles, P.cg, dc->sms, dc->flags, ph.has_split, stream));
         ++g_launches;
         break;
       }
@@ -855,7 +857,7 @@ static ns_status enqueue_plan(Plan& P, DevCtx* dc, cudaStream_t stream) {
                                 reinterpret_cast<const TaskDesc*>(dbase + ph.tiles_off), ph.total,
                                 ph.has_pjobs ? reinterpret_cast<const PrecondJob*>(dbase + ph.pjobs_off) : nullptr,
                                 reinterpret_cast<unsigned*>(dbase + ph.done_off), ph.nslots, ph.max_tiles, P.cg,
-                                dc->sms, dc->flags, stream));
+                                dc->sms, dc->flags, false, stream));
         ++g_launches;
         break;
       }
@@ -1342,7 +1344,7 @@ static ns_status one_gemm(GemmJob J, TDesc ta, TDesc tb, TDesc tout, TDesc taux,
     CU_TRY(cudaMemcpy(dmem, h.data(), bytes, cudaMemcpyHostToDevice));
     cudaError_t e = launch_umma_gemm(reinterpret_cast<const GemmJob*>(d + jo), reinterpret_cast<const TaskDesc*>(d + to),
                                      (int64_t)tasks.size(), nullptr, nullptr, 0, (int64_t)tasks.size(), cg, dc->sms,
-                                     dc->flags, stream);
+                                     dc->flags, false, stream);
     ++g_launches;
     cudaError_t e2 = cudaStreamSynchronize(stream);
     cudaFree(dmem);

@@ -15,10 +15,11 @@ namespace tns {
 // d_tasks: the launch's task list (TaskDesc) in execution order.  Per-step launches:
 // TK_TILE tasks without dependencies, d_pjobs = d_done = nullptr, nslots = 0.  Fused
 // launches: all steps, d_done = nslots + 1 zero-initialised counters (self-resetting).
-// max_tiles = largest GEMM step (grid sizing of per-step launches).
+// max_tiles = largest GEMM step (grid sizing of per-step launches).  split: the task list
+// holds split-K tasks (TaskDesc::split != 0; cg 1 or 2 only).
 cudaError_t launch_umma_gemm(const GemmJob* d_jobs, const TaskDesc* d_tasks, int64_t ntasks, const PrecondJob* d_pjobs,
                              unsigned* d_done, int nslots, int64_t max_tiles, int cg, int num_sms, uint32_t* d_flags,
-                             cudaStream_t stream);
+                             bool split, cudaStream_t stream);
 // Read (and optionally reset) the epilogue clock counters (TNS_DBG bit 8 measurement).
 cudaError_t umma_epi_prof(unsigned long long* out, bool reset);
 // Append the tiles of job `job` (host side).

@@ -269,7 +269,10 @@ __device__ __forceinline__ void epi_math(int var, const Epi& E, int p, int q, co
 // MC = CTA pairs per cluster (CG == 2 only): with MC == 2 the two pairs of a 4-CTA cluster
 // run tiles that share their A operand rows (same job, p0 and K) and each A box is loaded
 // once and multicast to both pairs: 25% fewer L2->SM bytes per MMA.
-template <int CG, int MC>
+// SPLIT: the launch carries split-K tasks (k-ranges with fp32 partial stores, TaskDesc
+// kb0/nkb/split); a separate instantiation so that the other launches keep the register
+// allocation of the plain kernel.
+template <int CG, int MC, bool SPLIT>
 __global__ void __launch_bounds__(kThreads, 1)
     umma_gemm_kernel(const GemmJob* __restrict__ jobs, const TaskDesc* __restrict__ tasks, int64_t ntasks,
                      const PrecondJob* __restrict__ pjobs, unsigned* done, int nslots,
@@ -357,7 +360,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (TD.dep_slot != kNoSlot) wait_phase(done + TD.dep_slot, TD.dep_target);
         const int pa = ti.p0 + (int)rank * G::kARows;  // this CTA's A rows
         const int qb = ti.q0 + (int)rank * G::kBRows;  // this CTA's B rows
-        const int kbeg = (int)TD.kb0, kend = TD.nkb ? kbeg + (int)TD.nkb : (K + kBK - 1) / kBK;
+        const int kbeg = SPLIT ? (int)TD.kb0 : 0;
+        const int kend = (SPLIT && TD.nkb) ? kbeg + (int)TD.nkb : (K + kBK - 1) / kBK;
         for (int kb = kbeg; kb < kend; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
           uint8_t* sa = smem + (size_t)stage * G::kStageBytes;
@@ -421,7 +425,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                      atomicAdd(&g_epi_prof[0], 1ull); }
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + as * kBN;
-        const int kbeg = (int)TD.kb0, kend = TD.nkb ? kbeg + (int)TD.nkb : (K + kBK - 1) / kBK;
+        const int kbeg = SPLIT ? (int)TD.kb0 : 0;
+        const int kend = (SPLIT && TD.nkb) ? kbeg + (int)TD.nkb : (K + kBK - 1) / kBK;
         for (int kb = kbeg; kb < kend; ++kb) {
           if (mprof) {
             const long long m1 = clock64();
@@ -565,7 +570,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             tma_load_2d(s_aux + 2048 * xb, E.tmAux, abar + xb, q + 64, prow);
           }
         }
-        if (TD.split && !shadow) {  // split-K: this k-range's fp32 partial, no epilogue math
+        if (SPLIT && TD.split && !shadow) {  // split-K: this k-range's fp32 partial, no epilogue math
           float4* dst = reinterpret_cast<float4*>(E.split_ws + (int64_t)(TD.split - 1) * E.split_stride +
                                                   (int64_t)p * E.split_ld + q);
 #pragma unroll
@@ -672,7 +677,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
-template <int CG, int MC>
+template <int CG, int MC, bool SPLIT>
 static cudaError_t launch_cg(const GemmJob* d_jobs, const TaskDesc* d_tasks, int64_t ntasks, const PrecondJob* d_pjobs,
                              unsigned* d_done, int nslots, int64_t max_tiles, int num_sms, uint32_t* d_flags,
                              cudaStream_t stream) {
@@ -680,7 +685,7 @@ static cudaError_t launch_cg(const GemmJob* d_jobs, const TaskDesc* d_tasks, int
   static int max_clusters[64] = {};
   int dev = 0;
   cudaGetDevice(&dev);
-  auto kern = umma_gemm_kernel<CG, MC>;
+  auto kern = umma_gemm_kernel<CG, MC, SPLIT>;
   constexpr int kCl = CG * MC;
   cudaLaunchConfig_t cfg = {};
   cfg.blockDim = dim3(kThreads);
@@ -730,12 +735,15 @@ static cudaError_t launch_cg(const GemmJob* d_jobs, const TaskDesc* d_tasks, int
 
 cudaError_t launch_umma_gemm(const GemmJob* d_jobs, const TaskDesc* d_tasks, int64_t ntasks, const PrecondJob* d_pjobs,
                              unsigned* d_done, int nslots, int64_t max_tiles, int cg, int num_sms, uint32_t* d_flags,
-                             cudaStream_t stream) {
+                             bool split, cudaStream_t stream) {
   if (ntasks <= 0) return cudaSuccess;
   if (cg == 4)  // two CTA pairs per cluster, A operand multicast (tasks carry tile pairs)
-    return launch_cg<2, 2>(d_jobs, d_tasks, ntasks, d_pjobs, d_done, nslots, max_tiles, num_sms, d_flags, stream);
-  return cg == 2 ? launch_cg<2, 1>(d_jobs, d_tasks, ntasks, d_pjobs, d_done, nslots, max_tiles, num_sms, d_flags, stream)
-                 : launch_cg<1, 1>(d_jobs, d_tasks, ntasks, d_pjobs, d_done, nslots, max_tiles, num_sms, d_flags, stream);
+    return launch_cg<2, 2, false>(d_jobs, d_tasks, ntasks, d_pjobs, d_done, nslots, max_tiles, num_sms, d_flags, stream);
+  if (cg == 2)
+    return split ? launch_cg<2, 1, true>(d_jobs, d_tasks, ntasks, d_pjobs, d_done, nslots, max_tiles, num_sms, d_flags, stream)
+                 : launch_cg<2, 1, false>(d_jobs, d_tasks, ntasks, d_pjobs, d_done, nslots, max_tiles, num_sms, d_flags, stream);
+  return split ? launch_cg<1, 1, true>(d_jobs, d_tasks, ntasks, d_pjobs, d_done, nslots, max_tiles, num_sms, d_flags, stream)
+               : launch_cg<1, 1, false>(d_jobs, d_tasks, ntasks, d_pjobs, d_done, nslots, max_tiles, num_sms, d_flags, stream);
 }
 
 cudaError_t umma_epi_prof(unsigned long long* out, bool reset) {
