@@ -418,7 +418,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int pblk = ti.p0 >> 8, qblk = ti.q0 >> 8;  // both CTAs' rows share the block
         // TNS_MEASURE builds, TNS_DBG bit 64: MMA-issuer stall cycles (slot 0 tiles, 1 waiting
         // for a free accumulator = epilogue-bound, 2 waiting for operands = feed-bound, 3 busy)
-        const bool mprof = kMeasure && (dbg & 64);
+        // (bits 256 / 512 / 1024 restrict the counting to GRAM / POLY / XB tiles)
+        const bool mprof = kMeasure && (dbg & 64) && (!(dbg & 1792) || (dbg & (256 << J->mode)));
         long long m0 = mprof ? clock64() : 0;
         mbar_wait(&tempty_bar[as], aphase ^ 1);
         if (mprof) { const long long m1 = clock64(); atomicAdd(&g_epi_prof[1], (unsigned long long)(m1 - m0)); m0 = m1;
