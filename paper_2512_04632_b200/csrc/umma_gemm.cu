@@ -524,7 +524,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           tma_load_2d(s_aux + b * 2048, E.tmAux, abar + b, qh + 32 * b, prow);
         }
       }
-      const bool prof = kMeasure && (dbg & 8) && lane == 0;
+      const bool prof = kMeasure && (dbg & 8) && lane == 0 && (!(dbg & 1792) || (dbg & (256 << E.mode)));
       long long t0 = prof ? clock64() : 0, t1;
       mbar_wait(&tfull_bar[as], aphase);
       tc_fence_after();
