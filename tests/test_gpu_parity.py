@@ -479,3 +479,39 @@ def test_forced_paths_full_ns(path):
             assert relF(_run(x, C.turbo(4), "aol"), oracle_run(x, C.turbo(4), "aol")) <= BF16_TOL
     finally:
         ns.set_path(old)
+
+
+def test_bench_workload_full_size_sampled():
+    """The bench workload itself: the GPT-2-medium set (144 matrices, 604 MB) with bench.py's
+    seeded inputs, run the way bench.py times it at N = 1 (orthogonalize_sharded, one bucket);
+    every output finite, a sample of matrices of each shape against the fp64 oracle, and the
+    sharded results bitwise equal to one grouped call."""
+    from paper_2512_04632_b200.parallel import orthogonalize_sharded
+
+    shapes = I.shape_set("gpt2-medium")
+    assert len(shapes) == 144
+    rng = np.random.default_rng(2025)
+    picks = set()
+    for s in sorted(set(shapes)):
+        idx = [i for i, t in enumerate(shapes) if t == s]
+        picks.update(int(i) for i in rng.choice(idx, size=2, replace=False))
+    xs_np = {}
+    ts = []
+    for i, (m, n) in enumerate(shapes):
+        x = I.gaussian(m, n, seed=I.matrix_seed(5, i))  # bench.py make_inputs(shapes, 5)
+        if i in picks:
+            xs_np[i] = x
+        ts.append(torch.from_numpy(x).to(torch.bfloat16).cuda())
+    outs = orthogonalize_sharded(ts, None, iters=4, precond="aol", buckets=1)
+    torch.cuda.synchronize()
+    assert all(bool(torch.isfinite(o.float()).all()) for o in outs)
+    grouped = [t.clone() for t in ts]
+    ns.orthogonalize_list(grouped, iters=4)
+    torch.cuda.synchronize()
+    for i in sorted(picks):
+        assert torch.equal(outs[i], grouped[i]), i
+        out = outs[i].float().cpu().numpy().astype(np.float64)
+        ref = oracle_run(xs_np[i], C.turbo(4), "aol")
+        assert relF(out, ref) <= BF16_TOL, (i, shapes[i])
+        eg, eo = polar_excess(out, ref, xs_np[i])
+        assert eg <= POLAR_SLACK * eo, (i, shapes[i], eg, eo)
