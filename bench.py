@@ -454,7 +454,8 @@ def run_e2e(args, xs, shapes, plan, mine, rank, world, dev, iters):
     from paper_2512_04632_b200.parallel import orthogonalize_host
     host_in = [x.cpu().pin_memory() for x in xs]
     nb = args.e2e_buckets
-    orthogonalize_host(host_in, iters=iters, buckets=nb)
+    for _ in range(2):  # warm-up: plans built on the first call, their CUDA graphs on the second
+        orthogonalize_host(host_in, iters=iters, buckets=nb)
     torch.cuda.synchronize()
     hp = _mk(shapes, world, iters, nb)
     h2d = sum(host_in[i].numel() * 2 for i in hp.mine(rank))

@@ -515,3 +515,32 @@ def test_bench_workload_full_size_sampled():
         assert relF(out, ref) <= BF16_TOL, (i, shapes[i])
         eg, eo = polar_excess(out, ref, xs_np[i])
         assert eg <= POLAR_SLACK * eo, (i, shapes[i], eg, eo)
+
+
+def test_internal_graph_replay_bitwise():
+    """From a plan's second use on, the library replays its launch sequence as one CUDA
+    graph: every replay equals the first (direct) call bitwise, the launch count per call is
+    unchanged, and with per-launch profiling on (direct launches again) the result is the same."""
+    shapes = [(256, 2304), (64, 216), (768, 768), (1024, 128)]
+    xs = [torch.from_numpy(I.gaussian(m, n, seed=700 + i)).to(torch.bfloat16).cuda() for i, (m, n) in enumerate(shapes)]
+    res, counts = [], []
+    for _ in range(4):
+        outs = [torch.full_like(x, float("nan")) for x in xs]
+        c0 = ns.launch_count()
+        ns.orthogonalize_list(xs, out=outs, iters=4)
+        torch.cuda.synchronize()
+        counts.append(ns.launch_count() - c0)
+        res.append(outs)
+    for r in res[1:]:
+        for a, b in zip(res[0], r):
+            assert torch.equal(a, b)
+    assert len(set(counts)) == 1
+    ns.profile_enable(True)
+    try:
+        outs = [torch.empty_like(x) for x in xs]
+        ns.orthogonalize_list(xs, out=outs, iters=4)
+        ns.profile_read()
+    finally:
+        ns.profile_enable(False)
+    for a, b in zip(res[0], outs):
+        assert torch.equal(a, b)
