@@ -32,9 +32,15 @@
  *     error nothing is enqueued and no memory is touched.  Numerical conditions
  *     (zero row-sum, zero matrix, non-finite values) do NOT fail a call: they set
  *     device flags readable with ns_read_flags (reading R4).
+ *   - From the second call with the same problem list on, the call's launches are
+ *     replayed as one CUDA graph captured by the library (same kernels, same results;
+ *     not while `stream` is itself being captured; TNS_NOGRAPH=1 disables it).
  *   - Thread-safety: calls are serialised by an internal mutex; distinct streams are
- *     fine.  Determinism: results are bitwise reproducible for identical inputs,
- *     independent of how matrices are grouped into calls.
+ *     fine.  Determinism: results are bitwise reproducible for identical inputs, and
+ *     independent of how matrices are grouped into calls -- except that a matrix with
+ *     N <= 256 and M >= 1024 takes the split-K Gram only in calls whose Gram step
+ *     leaves at least half of the GPU idle (its result then differs from an unsplit
+ *     call at rounding level).
  */
 #ifndef TURBO_NS_H_
 #define TURBO_NS_H_
