@@ -608,7 +608,7 @@ def main():
     ap.add_argument("--workload", default="gpt2-medium")
     ap.add_argument("--iters", type=int, default=4)
     ap.add_argument("--e2e-steps", type=int, default=5)
-    ap.add_argument("--e2e-buckets", type=int, default=48)
+    ap.add_argument("--e2e-buckets", type=int, default=72)
     ap.add_argument("--buckets", type=int, default=4, help="all-gather buckets at N > 1 (NCCL)")
     ap.add_argument("--no-collective-auto", dest="collective_auto", action="store_false",
                     help="N > 1: do not probe fused vs NCCL; time --collective as given")
