@@ -187,6 +187,14 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
+    if int(os.environ.get("WORLD_SIZE", "1")) > 1:
+        # under torchrun (OMP_NUM_THREADS=1 per rank) rank 0 runs alone: give the oracle the
+        # host's cores, as at N = 1
+        try:
+            from threadpoolctl import threadpool_limits
+            threadpool_limits(limits=len(os.sched_getaffinity(0)), user_api="blas")
+        except Exception:
+            pass
     shapes = I.shape_set(args.workload)
     vals = []
     for w in range(args.warmup):
