@@ -232,7 +232,7 @@ static bool tma_ok(const Mat& mt, ns_dtype dt) {
 // s[q .. q+32) and s[p] for whole tiles without bounds checks.
 static size_t s_floats(int64_t N) { return (size_t)((N + 255) / 256 * 256 + 32); }
 // AOL row-sum partial slots per row (see GemmJob::part).
-static int part_ld_for(int64_t N) { return (int)((N + 127) / 128 + (N + 31) / 32); }
+static int part_ld_for(int64_t N) { return (int)((N + 63) / 64 + (N + 31) / 32); }
 
 // Split-K Gram.  For N <= 256 the Gram is one 256 x 256 block per matrix, walked over the
 // whole K = M by a single CTA pair: with a long K (tall matrices, e.g. 256 x 2304 conv

@@ -50,8 +50,8 @@ struct GemmJob {
   int32_t s_by_row;    // XB: scale a*aux by s[p] (1) or s[q] (0)
   float a, b, c;
   // GRAM with AOL (iteration 1): per-tile |A0| row-sum partials, written once each (no
-  // atomics): part[i * part_ld + slot]; slots [0, ceil(N/128)) = direct 128-column blocks,
-  // [ceil(N/128), + ceil(N/32)) = mirrored 32-row blocks.  nullptr = not collected.
+  // atomics): part[i * part_ld + slot]; slots [0, ceil(N/64)) = direct 64-column blocks,
+  // [ceil(N/64), + ceil(N/32)) = mirrored 32-row blocks.  nullptr = not collected.
   float* part;
   int32_t part_ld;
   // XB of the last iteration, fused collective: also store every output tile into `npeer`
@@ -96,7 +96,7 @@ struct SimtJob {
 constexpr int kSimtTile = 64;
 
 // Per-matrix descriptor for the preconditioning kernel (AOL / Frobenius).
-// AOL rows with at most this many Gram-epilogue partial slots (N <= 1536) are summed by
+// AOL rows with at most this many Gram-epilogue partial slots (N <= 1344) are summed by
 // one lane in slot order; larger ones by a warp tree (precond_rows.cuh).
 constexpr int kSeqPartials = 64;
 struct PrecondJob {

@@ -34,14 +34,14 @@ __device__ __forceinline__ float warp_sum(float v) {
   return v;
 }
 
-// AOL row sum of |A0| for row i from the Gram epilogue's partials: direct 128-column slots
+// AOL row sum of |A0| for row i from the Gram epilogue's partials: direct 64-column slots
 // of the blocks <= bi, mirrored 32-row slots of the blocks > bi (each |A0_ij| counted once),
 // summed sequentially in slot order (independent loads, fixed order: deterministic).
 __device__ __forceinline__ float aol_rowsum_partials(const PrecondJob& J, int i) {
   const int N = J.N, bi = i / 256;
-  const int n1 = (N + 127) / 128, n2 = (N + 31) / 32;
+  const int n1 = (N + 63) / 64, n2 = (N + 31) / 32;
   const float* pr = J.part + (int64_t)i * J.part_ld;
-  const int d_end = min(2 * (bi + 1), n1), m_beg = min(8 * (bi + 1), n2);
+  const int d_end = min(4 * (bi + 1), n1), m_beg = min(8 * (bi + 1), n2);
   float acc = 0.f;
   for (int k = 0; k < d_end; ++k) acc += pr[k];
   for (int k = m_beg; k < n2; ++k) acc += pr[n1 + k];
@@ -66,9 +66,9 @@ __device__ __forceinline__ void precond_row_s(const PrecondJob& J, int i, int la
   } else if (J.precond == 2 && J.part != nullptr) {
     // many partials per row (large N): warp-parallel, fixed-order tree
     const int bi = i / 256;
-    const int n1 = (J.N + 127) / 128, n2 = (J.N + 31) / 32;
+    const int n1 = (J.N + 63) / 64, n2 = (J.N + 31) / 32;
     const float* pr = J.part + (int64_t)i * J.part_ld;
-    const int d_end = min(2 * (bi + 1), n1), m_beg = min(8 * (bi + 1), n2);
+    const int d_end = min(4 * (bi + 1), n1), m_beg = min(8 * (bi + 1), n2);
     float acc = 0.f;
     for (int k = lane; k < d_end; k += 32) acc += pr[k];
     for (int k = m_beg + lane; k < n2; k += 32) acc += pr[n1 + k];

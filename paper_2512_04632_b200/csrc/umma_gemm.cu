@@ -516,7 +516,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int prow = ti.p0 + (int)rank * kBM + quad * 32;  // first of this warp's 32 rows
       const int p = prow + lane;
       const int qh = ti.q0 + half * 128;
-      float rsum = 0.f;
+      float rsum = 0.f, rsum1 = 0.f;  // |A0| row sums of columns [qh, qh+64) and [qh+64, qh+128)
       if (has_aux && lane == 0) {  // prefetch aux chunks 0 and 1 before the accumulator is ready
 #pragma unroll
         for (int b = 0; b < 2; ++b) {
@@ -589,9 +589,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         // chunk rows [prow, prow+32) x cols [q, q+32) contain diagonal elements iff they overlap
         const bool dg = (E.diag_add != 0.f) && !ti.mirror && (q < prow + 32) && (prow < q + 32);
         epi_math(var, E, p, q, r, x, o, m, dg, bad);
-        if (E.part != nullptr) {  // AOL row sums of |A0| over this warp's 128 columns (Eq. 8)
+        if (E.part != nullptr) {  // AOL row sums of |A0| per 64-column slot (Eq. 8)
+          float cs = 0.f;
 #pragma unroll
-          for (int i = 0; i < 16; ++i) rsum += fabsf(lo_bf(o[i])) + fabsf(hi_bf(o[i]));
+          for (int i = 0; i < 16; ++i) cs += fabsf(lo_bf(o[i])) + fabsf(hi_bf(o[i]));
+          if (c < 2) rsum += cs; else rsum1 += cs;
         }
         if (prof) { t1 = clock64(); EPC(4, t1 - t0); t0 = t1; }
         // the bulk stores that last read these staging boxes (chunk c - 2's group) must be
@@ -638,11 +640,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                   fabsf(lo_bf(u.z)) + fabsf(hi_bf(u.z)) + fabsf(lo_bf(u.w)) + fabsf(hi_bf(u.w));
           }
           if (q + lane < E.Q && prow < E.P)
-            E.part[(int64_t)(q + lane) * E.part_ld + (E.Q + 127) / 128 + prow / 32] = cs;
+            E.part[(int64_t)(q + lane) * E.part_ld + (E.Q + 63) / 64 + prow / 32] = cs;
         }
         if (prof) { t1 = clock64(); EPC(6, t1 - t0); t0 = t1; }
       }
-      if (E.part != nullptr && p < E.P && qh < E.Q && !shadow) E.part[(int64_t)p * E.part_ld + qh / 128] = rsum;
+      if (E.part != nullptr && p < E.P && !shadow) {
+        if (qh < E.Q) E.part[(int64_t)p * E.part_ld + qh / 64] = rsum;
+        if (qh + 64 < E.Q) E.part[(int64_t)p * E.part_ld + qh / 64 + 1] = rsum1;
+      }
       if (++as == 2) { as = 0; aphase ^= 1; }
       if (TD.my_slot != kNoSlot) {  // fused mode: this warp's part of the tile is visible
         __syncwarp();
