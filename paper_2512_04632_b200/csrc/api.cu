@@ -186,6 +186,7 @@ struct Plan {
   bool simt = false;
   bool fused = false;  // all 3T+1 steps in one launch (small problems)
   int cg = 2;  // tcgen05 CTA group (2: 256x256 tiles on CTA pairs)
+  int bn = 256;  // tile width: 128 for tile-starved plans (see choose_bn)
   int iters = 0;
   ns_precond precond = NS_PRECOND_AOL;
   std::vector<Mat> mats;   // tcgen05 / SIMT step engine
@@ -264,6 +265,26 @@ static void choose_splits(std::vector<Mat>& mats, int cg, int workers) {
   if (2 * tiles > workers) return;
   for (Mat& mt : mats) mt.split = split_factor(mt.M, mt.N);
 }
+// Tile width.  A plan whose every GEMM step has at most half as many 256-wide tiles as there
+// are CTA-pair workers (small problems: one tile per pair, latency-bound) uses 128-wide
+// tiles: twice the tiles, and each epilogue warp drains 2 chunks instead of 4 -- the
+// epilogue is the longest stretch of such a launch.  Results are bitwise the same as with
+// 256-wide tiles (every output element is the same sequence of K = 16 UMMA steps; the AOL
+// partials are per 64 columns either way), so the choice never breaks batch invariance.
+// Per-step launches on CTA pairs only; TNS_BN=256 forces the wide tiles (A/B knob).
+static int choose_bn(const std::vector<Mat>& mats, int cg, int workers) {
+  if (cg != 2 || g_path == 3) return 256;
+  if (const char* e = getenv("TNS_BN")) if (atoi(e) == 256) return 256;
+  int64_t sym = 0, xb = 0;
+  for (const Mat& mt : mats) {
+    const int64_t nb = (mt.N + kSymBlock - 1) / kSymBlock;
+    sym += nb * (nb + 1) / 2;
+    const int64_t P = mt.wide ? mt.N : mt.M, Q = mt.wide ? mt.M : mt.N;
+    xb += ((P + 255) / 256) * ((Q + 255) / 256);
+  }
+  return 2 * std::max(sym, xb) <= workers ? 128 : 256;
+}
+
 static size_t split_bytes(const Mat& mt) { return mt.split ? (size_t)mt.split * kSplitLd * kSplitLd * 4 : 0; }
 
 static size_t workspace_bytes_for(const std::vector<Mat>& mats, ns_dtype dt) {
@@ -345,6 +366,7 @@ static ns_status build_plan(Plan& P, HostTables& H, DevCtx* dc, const float* coe
   const bool bf16 = P.dtype == NS_BF16;
   if (!P.simt && (P.cg == 1 || P.cg == 2) && g_path != 3) choose_splits(P.mats, P.cg, dc->sms / P.cg);
   else for (Mat& mt : P.mats) mt.split = 0;
+  P.bn = P.simt ? 256 : choose_bn(P.mats, P.cg, dc->sms / 2);
   // -- workspace layout
   size_t off = 1024;  // [0,16): preconditioner grid barrier; [64, 1024): phase counters
   for (Mat& mt : P.mats) {
@@ -655,7 +677,7 @@ static ns_status build_plan(Plan& P, HostTables& H, DevCtx* dc, const float* coe
       for (size_t j = 0; j < st.jobs.size(); ++j) order[j] = j;
       std::stable_sort(order.begin(), order.end(), [&](size_t x, size_t y) { return st.jobs[x].K > st.jobs[y].K; });
       std::vector<uint64_t> tl;
-      for (size_t j : order) umma_tile_list(st.jobs[j], (uint32_t)(job_base + j), P.cg, tl);
+      for (size_t j : order) umma_tile_list(st.jobs[j], (uint32_t)(job_base + j), P.cg, P.bn, tl);
       return tl;
     };
     auto mk_task = [](uint64_t w) {
@@ -854,7 +876,7 @@ static ns_status enqueue_plan(Plan& P, DevCtx* dc, cudaStream_t stream) {
         ProfScope ps(ph.gemm_kind, stream);
         CU_TRY(launch_umma_gemm(reinterpret_cast<const GemmJob*>(dbase + ph.dev_off),
                                 reinterpret_cast<const TaskDesc*>(dbase + ph.tiles_off), ph.total, nullptr, nullptr,
-                                0, ph.max_tiles, P.cg, dc->sms, dc->flags, ph.has_split, stream));
+                                0, ph.max_tiles, P.cg, dc->sms, dc->flags, ph.has_split, P.bn, stream));
         ++g_launches;
         break;
       }
@@ -864,7 +886,7 @@ static ns_status enqueue_plan(Plan& P, DevCtx* dc, cudaStream_t stream) {
                                 reinterpret_cast<const TaskDesc*>(dbase + ph.tiles_off), ph.total,
                                 ph.has_pjobs ? reinterpret_cast<const PrecondJob*>(dbase + ph.pjobs_off) : nullptr,
                                 reinterpret_cast<unsigned*>(dbase + ph.done_off), ph.nslots, ph.max_tiles, P.cg,
-                                dc->sms, dc->flags, false, stream));
+                                dc->sms, dc->flags, false, P.bn, stream));
         ++g_launches;
         break;
       }
@@ -1396,7 +1418,7 @@ static ns_status one_gemm(GemmJob J, TDesc ta, TDesc tb, TDesc tout, TDesc taux,
     if (taux.ptr && (st = encode_pair(tm, taux.ptr, taux.rows, taux.cols, &ix)) != NS_OK) return st;
     const int cg = g_path == 2 ? 1 : 2;
     std::vector<uint64_t> tl;
-    umma_tile_list(J, 0, cg, tl);
+    umma_tile_list(J, 0, cg, 256, tl);
     std::vector<TaskDesc> tasks(tl.size());
     for (size_t i = 0; i < tl.size(); ++i) {
       std::memset(&tasks[i], 0, sizeof(TaskDesc));
@@ -1417,7 +1439,7 @@ static ns_status one_gemm(GemmJob J, TDesc ta, TDesc tb, TDesc tout, TDesc taux,
     CU_TRY(cudaMemcpy(dmem, h.data(), bytes, cudaMemcpyHostToDevice));
     cudaError_t e = launch_umma_gemm(reinterpret_cast<const GemmJob*>(d + jo), reinterpret_cast<const TaskDesc*>(d + to),
                                      (int64_t)tasks.size(), nullptr, nullptr, 0, (int64_t)tasks.size(), cg, dc->sms,
-                                     dc->flags, false, stream);
+                                     dc->flags, false, 256, stream);
     ++g_launches;
     cudaError_t e2 = cudaStreamSynchronize(stream);
     cudaFree(dmem);

@@ -14,7 +14,7 @@ enum GemmMode : int32_t {
 
 // Tile geometry of the tcgen05 kernel (one CTA = one 128 x 256 output tile at a time).
 constexpr int kBM = 128;  // UMMA M
-constexpr int kBN = 256;  // UMMA N
+constexpr int kBN = 256;  // UMMA N (default tile width; 128 for tile-starved plans)
 constexpr int kBK = 64;   // K elements per pipeline stage = one 128-byte swizzle atom
 constexpr int kSymBlock = 256;  // symmetric phases tile the lower triangle in 256 x 256 blocks
 #ifndef TNS_GROUP_P
@@ -23,9 +23,10 @@ constexpr int kSymBlock = 256;  // symmetric phases tile the lower triangle in 2
 constexpr int kGroupP = TNS_GROUP_P;  // XB raster: tiles grouped 16 row-blocks deep for L2 reuse
 
 // One entry of a launch's tile list (built on the host in execution order):
-//   bits [0,20) job index | [20,40) p0 / 128 | [40,60) q0 / 256 | bit 63 mirrored store.
-__host__ __device__ inline uint64_t pack_tile(uint32_t job, uint32_t p0, uint32_t q0, bool mirror) {
-  return (uint64_t)job | ((uint64_t)(p0 / 128) << 20) | ((uint64_t)(q0 / 256) << 40) |
+//   bits [0,20) job index | [20,40) p0 / 128 | [40,60) q0 / bn | bit 63 mirrored store
+// (bn = the launch's tile width, 256 or 128).
+__host__ __device__ inline uint64_t pack_tile(uint32_t job, uint32_t p0, uint32_t q0, bool mirror, uint32_t bn = 256) {
+  return (uint64_t)job | ((uint64_t)(p0 / 128) << 20) | ((uint64_t)(q0 / bn) << 40) |
          ((uint64_t)(mirror ? 1 : 0) << 63);
 }
 

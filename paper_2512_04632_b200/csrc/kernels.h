@@ -16,14 +16,15 @@ namespace tns {
 // TK_TILE tasks without dependencies, d_pjobs = d_done = nullptr, nslots = 0.  Fused
 // launches: all steps, d_done = nslots + 1 zero-initialised counters (self-resetting).
 // max_tiles = largest GEMM step (grid sizing of per-step launches).  split: the task list
-// holds split-K tasks (TaskDesc::split != 0; cg 1 or 2 only).
+// holds split-K tasks (TaskDesc::split != 0; cg 1 or 2 only).  bn: tile width 256, or 128
+// (cg = 2 only) -- the tile list must have been built with the same bn.
 cudaError_t launch_umma_gemm(const GemmJob* d_jobs, const TaskDesc* d_tasks, int64_t ntasks, const PrecondJob* d_pjobs,
                              unsigned* d_done, int nslots, int64_t max_tiles, int cg, int num_sms, uint32_t* d_flags,
-                             bool split, cudaStream_t stream);
+                             bool split, int bn, cudaStream_t stream);
 // Read (and optionally reset) the epilogue clock counters (TNS_DBG bit 8 measurement).
 cudaError_t umma_epi_prof(unsigned long long* out, bool reset);
-// Append the tiles of job `job` (host side).
-void umma_tile_list(const GemmJob& J, uint32_t job, int cg, std::vector<uint64_t>& out);
+// Append the tiles of job `job` (host side), bn = tile width (256 or 128).
+void umma_tile_list(const GemmJob& J, uint32_t job, int cg, int bn, std::vector<uint64_t>& out);
 // cg = 4 (two CTA pairs per cluster, A multicast): the job's tiles as pairs sharing p0.
 void umma_pair_list(const GemmJob& J, uint32_t job, std::vector<std::pair<uint64_t, uint64_t>>& out);
 

@@ -59,12 +59,16 @@ constexpr int kNumEpiWarps = 8;
 constexpr bool kMeasure = TNS_MEASURE != 0;
 constexpr int kEpiWarp0 = 2;                        // epilogue = warps 2..9 (TMEM lane quarter = warp % 4)
 constexpr int kThreads = (kEpiWarp0 + kNumEpiWarps) * 32;  // 320: up to 204 registers per thread
-constexpr uint32_t kTmemCols = 2 * kBN;            // double-buffered accumulator
 
-template <int CG>
+// BN = tile width (UMMA N): 256, or 128 for tile-starved plans (small problems), where
+// halving the tile halves each warp's epilogue chunks -- the epilogue is the longest part
+// of a launch that has one tile per CTA pair.
+template <int CG, int BN>
 struct Geo {
+  static constexpr uint32_t kTmemCols = 2 * BN;  // double-buffered accumulator
+  static constexpr int kChunks = BN / 64;        // 32-column epilogue chunks per warp
   static constexpr int kARows = kBM;               // A rows staged per CTA
-  static constexpr int kBRows = kBN / CG;          // B rows staged per CTA
+  static constexpr int kBRows = BN / CG;           // B rows staged per CTA
   static constexpr int kTileM = kBM * CG;          // output rows per tile
   static constexpr int kABytes = kARows * kBK * 2;
   static constexpr int kBBytes = kBRows * kBK * 2;
@@ -105,11 +109,12 @@ struct TileInfo {
   bool mirror;
 };
 
+template <int BN>
 __device__ __forceinline__ TileInfo decode_word(uint64_t w) {
   TileInfo ti;
   ti.job = (int)(w & 0xFFFFFu);
   ti.p0 = (int)((w >> 20) & 0xFFFFFu) * 128;
-  ti.q0 = (int)((w >> 40) & 0xFFFFFu) * 256;
+  ti.q0 = (int)((w >> 40) & 0xFFFFFu) * BN;
   ti.mirror = (w >> 63) != 0;
   return ti;
 }
@@ -272,12 +277,12 @@ __device__ __forceinline__ void epi_math(int var, const Epi& E, int p, int q, co
 // SPLIT: the launch carries split-K tasks (k-ranges with fp32 partial stores, TaskDesc
 // kb0/nkb/split); a separate instantiation so that the other launches keep the register
 // allocation of the plain kernel.
-template <int CG, int MC, bool SPLIT>
+template <int CG, int MC, bool SPLIT, int BN>
 __global__ void __launch_bounds__(kThreads, 1)
     umma_gemm_kernel(const GemmJob* __restrict__ jobs, const TaskDesc* __restrict__ tasks, int64_t ntasks,
                      const PrecondJob* __restrict__ pjobs, unsigned* done, int nslots,
                      uint32_t* __restrict__ flags, int dbg) {
-  using G = Geo<CG>;
+  using G = Geo<CG, BN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
@@ -316,7 +321,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     fence_mbar_init();
   }
   if (warp == 1) {
-    tmem_alloc<CG>(tmem_slot, kTmemCols);
+    tmem_alloc<CG>(tmem_slot, G::kTmemCols);
     tmem_relinquish<CG>();
   }
   tc_fence_before();
@@ -340,7 +345,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int64_t t = cid; t < ntasks; t += ncl) {
         const TaskDesc TD = tasks[t];
         if (TD.kind != TK_TILE) continue;
-        const TileInfo ti = decode_word(my_tile(TD));
+        const TileInfo ti = decode_word<BN>(my_tile(TD));
         const GemmJob* J = jobs + ti.job;
         const void* tmA = J->tmA;
         const void* tmB = J->tmB;
@@ -410,7 +415,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int64_t t = cid; t < ntasks; t += ncl) {
         const TaskDesc TD = tasks[t];
         if (TD.kind != TK_TILE) continue;
-        const TileInfo ti = decode_word(my_tile(TD));
+        const TileInfo ti = decode_word<BN>(my_tile(TD));
         const GemmJob* J = jobs + ti.job;
         const uint32_t a_mn = (uint32_t)J->a_mn, b_mn = (uint32_t)J->b_mn;
         const int K = J->K;
@@ -425,7 +430,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (mprof) { const long long m1 = clock64(); atomicAdd(&g_epi_prof[1], (unsigned long long)(m1 - m0)); m0 = m1;
                      atomicAdd(&g_epi_prof[0], 1ull); }
         tc_fence_after();
-        const uint32_t d_tmem = tmem_base + as * kBN;
+        const uint32_t d_tmem = tmem_base + as * BN;
         const int kbeg = SPLIT ? (int)TD.kb0 : 0;
         const int kend = (SPLIT && TD.nkb) ? kbeg + (int)TD.nkb : (K + kBK - 1) / kBK;
         for (int kb = kbeg; kb < kend; ++kb) {
@@ -447,7 +452,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int kblk = (kb * kBK) >> 8;
           const uint32_t a_e = a_mn ^ (uint32_t)(a_sym && kblk > pblk);
           const uint32_t b_e = b_mn ^ (uint32_t)(b_sym && kblk > qblk);
-          const uint32_t idesc = make_idesc_bf16(kBM * CG, kBN, a_e, b_e);
+          const uint32_t idesc = make_idesc_bf16(kBM * CG, BN, a_e, b_e);
           const uint32_t a_lbo = a_e ? 8192u : 16u, a_step = a_e ? 2048u : 32u;
           const uint32_t b_lbo = b_e ? 8192u : 16u, b_step = b_e ? 2048u : 32u;
 #pragma unroll
@@ -509,13 +514,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       const uint64_t tw = my_tile(TD);
       const bool shadow = (tw & kTileShadow) != 0;  // computed for the multicast, never stored
-      const TileInfo ti = decode_word(tw);
+      const TileInfo ti = decode_word<BN>(tw);
       const Epi E = load_epi(jobs + ti.job);
       const int var = epi_variant(E);
       const bool has_aux = epi_needs_aux(E) && !(dbg & 4) && !shadow;
       const int prow = ti.p0 + (int)rank * kBM + quad * 32;  // first of this warp's 32 rows
       const int p = prow + lane;
-      const int qh = ti.q0 + half * 128;
+      const int qh = ti.q0 + half * (BN / 2);
       float rsum = 0.f, rsum1 = 0.f;  // |A0| row sums of columns [qh, qh+64) and [qh+64, qh+128)
       if (has_aux && lane == 0) {  // prefetch aux chunks 0 and 1 before the accumulator is ready
 #pragma unroll
@@ -531,10 +536,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (ew == 0 && t == cid) TL(4);  // first accumulator ready
       if (prof) { t1 = clock64(); EPC(1, t1 - t0); t0 = t1; EPC(0, 1); }
 #pragma unroll 1
-      for (int c = 0; c < 4; ++c) {
+      for (int c = 0; c < G::kChunks; ++c) {
         const int q = qh + c * 32;
         uint32_t r[32];
-        tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(quad * 32) << 16) + as * kBN + (uint32_t)(q - ti.q0), r);
+        tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(quad * 32) << 16) + as * BN + (uint32_t)(q - ti.q0), r);
         uint32_t x[16];
         const int xb = c & 1;  // aux / output buffer of this chunk
         if (has_aux) {
@@ -555,7 +560,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         tmem_ld_wait();
         if (prof) { t1 = clock64(); EPC(2, t1 - t0); t0 = t1; }
-        if (c == 3) {
+        if (c == G::kChunks - 1) {
           tc_fence_before();
           __syncwarp();
           if (lane == 0) {
@@ -563,7 +568,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             else mbar_arrive_relaxed(&tempty_bar[as]);
           }
         }
-        if (has_aux && c < 2) {  // refill this aux buffer with chunk c + 2
+        if (has_aux && c + 2 < G::kChunks) {  // refill this aux buffer with chunk c + 2
           fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) {
@@ -646,7 +651,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       if (E.part != nullptr && p < E.P && !shadow) {
         if (qh < E.Q) E.part[(int64_t)p * E.part_ld + qh / 64] = rsum;
-        if (qh + 64 < E.Q) E.part[(int64_t)p * E.part_ld + qh / 64 + 1] = rsum1;
+        if (G::kChunks > 2 && qh + 64 < E.Q) E.part[(int64_t)p * E.part_ld + qh / 64 + 1] = rsum1;
       }
       if (++as == 2) { as = 0; aphase ^= 1; }
       if (TD.my_slot != kNoSlot) {  // fused mode: this warp's part of the tile is visible
@@ -668,7 +673,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if constexpr (CG == 2) cluster_sync(); else __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc<CG>(tmem_base, kTmemCols);
+    tmem_dealloc<CG>(tmem_base, G::kTmemCols);
     TL(6);
     if (tl) atomicAdd(&g_epi_prof[7], 1ull);
   }
@@ -683,7 +688,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
-template <int CG, int MC, bool SPLIT>
+template <int CG, int MC, bool SPLIT, int BN>
 static cudaError_t launch_cg(const GemmJob* d_jobs, const TaskDesc* d_tasks, int64_t ntasks, const PrecondJob* d_pjobs,
                              unsigned* d_done, int nslots, int64_t max_tiles, int num_sms, uint32_t* d_flags,
                              cudaStream_t stream) {
@@ -691,11 +696,11 @@ static cudaError_t launch_cg(const GemmJob* d_jobs, const TaskDesc* d_tasks, int
   static int max_clusters[64] = {};
   int dev = 0;
   cudaGetDevice(&dev);
-  auto kern = umma_gemm_kernel<CG, MC, SPLIT>;
+  auto kern = umma_gemm_kernel<CG, MC, SPLIT, BN>;
   constexpr int kCl = CG * MC;
   cudaLaunchConfig_t cfg = {};
   cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = Geo<CG>::kSmemBytes;
+  cfg.dynamicSmemBytes = Geo<CG, BN>::kSmemBytes;
   cfg.stream = stream;
   cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -708,7 +713,7 @@ static cudaError_t launch_cg(const GemmJob* d_jobs, const TaskDesc* d_tasks, int
   cfg.numAttrs = 2;
   if (!attr_set[dev & 63]) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)Geo<CG>::kSmemBytes);
+                                         (int)Geo<CG, BN>::kSmemBytes);
     if (e != cudaSuccess) return e;
     if (CG == 2) {
       e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
@@ -741,15 +746,18 @@ static cudaError_t launch_cg(const GemmJob* d_jobs, const TaskDesc* d_tasks, int
 
 cudaError_t launch_umma_gemm(const GemmJob* d_jobs, const TaskDesc* d_tasks, int64_t ntasks, const PrecondJob* d_pjobs,
                              unsigned* d_done, int nslots, int64_t max_tiles, int cg, int num_sms, uint32_t* d_flags,
-                             bool split, cudaStream_t stream) {
+                             bool split, int bn, cudaStream_t stream) {
   if (ntasks <= 0) return cudaSuccess;
+#define TNS_LAUNCH(CG_, MC_, SP_, BN_) \
+  launch_cg<CG_, MC_, SP_, BN_>(d_jobs, d_tasks, ntasks, d_pjobs, d_done, nslots, max_tiles, num_sms, d_flags, stream)
   if (cg == 4)  // two CTA pairs per cluster, A operand multicast (tasks carry tile pairs)
-    return launch_cg<2, 2, false>(d_jobs, d_tasks, ntasks, d_pjobs, d_done, nslots, max_tiles, num_sms, d_flags, stream);
-  if (cg == 2)
-    return split ? launch_cg<2, 1, true>(d_jobs, d_tasks, ntasks, d_pjobs, d_done, nslots, max_tiles, num_sms, d_flags, stream)
-                 : launch_cg<2, 1, false>(d_jobs, d_tasks, ntasks, d_pjobs, d_done, nslots, max_tiles, num_sms, d_flags, stream);
-  return split ? launch_cg<1, 1, true>(d_jobs, d_tasks, ntasks, d_pjobs, d_done, nslots, max_tiles, num_sms, d_flags, stream)
-               : launch_cg<1, 1, false>(d_jobs, d_tasks, ntasks, d_pjobs, d_done, nslots, max_tiles, num_sms, d_flags, stream);
+    return TNS_LAUNCH(2, 2, false, 256);
+  if (cg == 2) {
+    if (bn == 128) return split ? TNS_LAUNCH(2, 1, true, 128) : TNS_LAUNCH(2, 1, false, 128);
+    return split ? TNS_LAUNCH(2, 1, true, 256) : TNS_LAUNCH(2, 1, false, 256);
+  }
+  return split ? TNS_LAUNCH(1, 1, true, 256) : TNS_LAUNCH(1, 1, false, 256);
+#undef TNS_LAUNCH
 }
 
 cudaError_t umma_epi_prof(unsigned long long* out, bool reset) {
@@ -764,23 +772,24 @@ cudaError_t umma_epi_prof(unsigned long long* out, bool reset) {
 // Tiles of one job in execution order (host).  Symmetric jobs: lower-triangle 256 x 256
 // blocks row by row, (2 / cg) row parts each.  Rectangular jobs: grouped raster, kGroupP
 // tile-rows deep, so concurrently running tiles share operand rows/columns in L2.
-void umma_tile_list(const GemmJob& J, uint32_t job, int cg, std::vector<uint64_t>& out) {
+void umma_tile_list(const GemmJob& J, uint32_t job, int cg, int bn, std::vector<uint64_t>& out) {
   if (J.sym) {
     const int nb = (J.P + kSymBlock - 1) / kSymBlock;
     for (int bi = 0; bi < nb; ++bi)
       for (int bj = 0; bj <= bi; ++bj)
-        for (int h = 0; h < 2 / cg; ++h) {
-          const int p0 = bi * kSymBlock + h * kBM;
-          if (p0 < J.P) out.push_back(pack_tile(job, p0, bj * kSymBlock, bi != bj));
-        }
+        for (int h = 0; h < 2 / cg; ++h)
+          for (int qq = 0; qq < kSymBlock / bn; ++qq) {
+            const int p0 = bi * kSymBlock + h * kBM, q0 = bj * kSymBlock + qq * bn;
+            if (p0 < J.P && q0 < J.Q) out.push_back(pack_tile(job, p0, q0, bi != bj, bn));
+          }
     return;
   }
   const int tm = kBM * cg;
-  const int tp = (J.P + tm - 1) / tm, tq = (J.Q + kBN - 1) / kBN;
+  const int tp = (J.P + tm - 1) / tm, tq = (J.Q + bn - 1) / bn;
   for (int g0 = 0; g0 < tp; g0 += kGroupP) {
     const int gsz = tp - g0 < kGroupP ? tp - g0 : kGroupP;
     for (int qb = 0; qb < tq; ++qb)
-      for (int i = 0; i < gsz; ++i) out.push_back(pack_tile(job, (g0 + i) * tm, qb * kBN, false));
+      for (int i = 0; i < gsz; ++i) out.push_back(pack_tile(job, (g0 + i) * tm, qb * bn, false, bn));
   }
 }
 

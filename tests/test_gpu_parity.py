@@ -544,3 +544,28 @@ def test_internal_graph_replay_bitwise():
         ns.profile_enable(False)
     for a, b in zip(res[0], outs):
         assert torch.equal(a, b)
+
+
+def test_narrow_tiles_bitwise_equal_wide_tiles():
+    """Tile-starved plans use 128-wide tiles (api.cu choose_bn); TNS_BN=256 forces the
+    256-wide ones.  Every output element is the same UMMA K-sequence and the AOL partials
+    are per 64 columns either way: bitwise equal results, for AOL, Frobenius and split-K."""
+    import os
+    shapes = [(256, 2304), (768, 256), (520, 136), (2304, 256)]
+    xs = [torch.from_numpy(I.gaussian(m, n, seed=800 + i)).to(torch.bfloat16).cuda() for i, (m, n) in enumerate(shapes)]
+    res = {}
+    for bn in ("128", "256"):
+        os.environ["TNS_BN"] = bn
+        try:
+            ns.shutdown()
+            for precond in ("aol", "frobenius"):
+                outs = [torch.empty_like(x) for x in xs]
+                ns.orthogonalize_list(xs, out=outs, iters=4, precond=precond)
+                torch.cuda.synchronize()
+                res[(bn, precond)] = outs
+        finally:
+            del os.environ["TNS_BN"]
+            ns.shutdown()
+    for precond in ("aol", "frobenius"):
+        for a, b in zip(res[("128", precond)], res[("256", precond)]):
+            assert torch.equal(a, b)
