@@ -14,8 +14,9 @@ import paper_2512_04632_b200 as ns  # noqa: E402
 from synth import coeffs as C  # noqa: E402
 from synth import inputs as I  # noqa: E402
 
-for name, reps in (("gpt2-small", 30), ("cifar", 50), ("square2048", 30)):
-    shapes = I.shape_set(name)
+TALL = [(256, 8192), (2304, 256), (128, 8192)]  # split-K Gram + 128-wide tiles
+for name, reps in (("gpt2-small", 30), ("cifar", 50), ("square2048", 30), ("tall", 40)):
+    shapes = TALL if name == "tall" else I.shape_set(name)
     xs = [torch.from_numpy(I.gaussian(m, n, seed=i)).to(torch.bfloat16).cuda() for i, (m, n) in enumerate(shapes)]
     for path in (0, 3, 4, 6):
         for pc, cf in (("aol", C.turbo(4)), ("frobenius", C.muon_plus(5))):
