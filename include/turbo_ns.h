@@ -36,7 +36,8 @@
  *     replayed as one CUDA graph captured by the library (same kernels, same results;
  *     not while `stream` is itself being captured; TNS_NOGRAPH=1 disables it).
  *   - Thread-safety: calls are serialised by an internal mutex; distinct streams are
- *     fine.  Determinism: results are bitwise reproducible for identical inputs, and
+ *     fine for distinct problem lists.  Calls with the SAME problem list share its cached
+ *     workspace: on different streams the caller must order them (events).  Determinism: results are bitwise reproducible for identical inputs, and
  *     independent of how matrices are grouped into calls -- except that a matrix with
  *     N <= 256 and M >= 1024 takes the split-K Gram only in calls whose Gram step
  *     leaves at least half of the GPU idle (its result then differs from an unsplit
