@@ -152,7 +152,8 @@ ns_status ns_read_flags(void* stream, uint32_t* flags);
 uint64_t ns_launch_count(void);
 
 /* Execution-path override for testing: 0 = auto: matrices with short side N <= 128 whose
- * fp32 copy fits in shared memory (the "cluster-resident" small-matrix kernel: the whole
+ * fp32 copy fits in shared memory -- bf16 ones only while M*N^2 <= 2.2e6, where this is
+ * measured faster than the step engine -- (the "cluster-resident" small-matrix kernel: the whole
  * NS of one matrix in ONE launch of a 16-CTA (when the matrix fits that layout) or 8-CTA
  * thread-block cluster, X, A and B resident in
  * shared memory, rows exchanged over DSMEM), all
@@ -161,7 +162,7 @@ uint64_t ns_launch_count(void);
  * cluster launch runs on an internal side stream joined back by events; 1 = force the SIMT
  * (CUDA-core) step kernels, 2 = tcgen05 with single-CTA 128x256 tiles, 3 = all 3T+1 steps
  * in ONE fused dataflow launch, 4 = per-step launches for every matrix (no cluster kernel),
- * 5 = same as 0, 6 = per-step launches on 4-CTA clusters: two CTA pairs run tiles sharing
+ * 5 = as 0 but every matrix that fits takes the cluster kernel, 6 = per-step launches on 4-CTA clusters: two CTA pairs run tiles sharing
  * their A operand, loaded once by TMA multicast (bitwise equal to 4; measured slower on
  * B200 because only 33 4-CTA clusters fit on the 148 SMs).  Returns the previous value. */
 int ns_set_path(int path);

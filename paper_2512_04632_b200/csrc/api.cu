@@ -477,7 +477,8 @@ static ns_status build_plan(Plan& P, HostTables& H, DevCtx* dc, const float* coe
       std::vector<ClusterJob> cj;
       size_t smem = 0;
       for (const Mat& mt : P.tiny) {
-        const bool fits16 = cl_fits(mt.M, mt.N, kClCtasMax);
+        static const bool only8 = [] { const char* e = getenv("TNS_CL_CTAS"); return e && atoi(e) == 8; }();
+        const bool fits16 = !only8 && cl_fits(mt.M, mt.N, kClCtasMax);  // TNS_CL_CTAS=8: A/B knob
         if (fits16 != (ctas == kClCtasMax)) continue;
         ClusterJob J;
         std::memset(&J, 0, sizeof(J));
@@ -1018,7 +1019,17 @@ static ns_status run(const std::vector<Mat>& mats_in, int iters, const float* co
   bool any_peer = false;
   for (const Mat& mt : mats_in) any_peer = any_peer || !mt.peer.empty();
   const bool use_cluster = (g_path == 0 || g_path == 5) && !any_peer && dc->cc_major == 10;
-  for (const Mat& mt : mats_in) (use_cluster && cl_fits(mt.M, mt.N) ? tiny : big).push_back(mt);
+  // Path 0 routes by measured cost (tools/cl_sizes.py, profiles/r01_v12_cluster_routing.log):
+  // the bf16 step engine of a lone small matrix costs ~63 us (13 launches, graph replay),
+  // the cluster kernel grows with its FMA work M*N^2 (64x216: 43 us, 128^2: 64 us, 64x576:
+  // 79 us) -- so bf16 matrices take it up to M*N^2 = 2.2e6; fp32 always (the SIMT step
+  // kernels are slower).  Path 5 takes it whenever the matrix fits.  Shape-only: batching
+  // never changes a result.
+  auto to_cluster = [&](const Mat& mt) {
+    if (!use_cluster || !cl_fits(mt.M, mt.N)) return false;
+    return g_path == 5 || dtype != NS_BF16 || (double)mt.M * (double)mt.N * (double)mt.N <= 2.2e6;
+  };
+  for (const Mat& mt : mats_in) (to_cluster(mt) ? tiny : big).push_back(mt);
   bool simt = (g_path == 1) || dtype != NS_BF16 || dc->cc_major != 10;
   bool peers = false;
   for (const Mat& mt : big) {

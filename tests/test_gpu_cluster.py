@@ -26,7 +26,16 @@ BF16_TOL = 2e-2
 FP32_TOL = 1e-4
 
 
-def _run(x32, coeffs, precond, dtype=torch.bfloat16, path=0):
+@pytest.fixture(autouse=True)
+def _cluster_whenever_it_fits():
+    """Path 5: every matrix that fits takes the cluster kernel (path 0 routes bf16 matrices
+    with M*N^2 > 2.2e6 to the step engine, measured faster there; see test_auto_routing)."""
+    old = ns.set_path(5)
+    yield
+    ns.set_path(old)
+
+
+def _run(x32, coeffs, precond, dtype=torch.bfloat16, path=5):
     t = torch.from_numpy(np.ascontiguousarray(x32, dtype=np.float32)).to(dtype).cuda()
     old = ns.set_path(path)
     try:
@@ -82,7 +91,7 @@ def test_cluster_matches_step_engine():
     """Cluster kernel (path 0) and the per-step tcgen05 engine (path 4) both meet the gate
     and agree with each other to bf16 rounding."""
     x = I.gaussian(128, 160, seed=12)
-    a, la = _run(x, C.turbo(4), "aol", path=0)
+    a, la = _run(x, C.turbo(4), "aol", path=5)
     b, lb = _run(x, C.turbo(4), "aol", path=4)
     assert la == 1 and lb == 13
     ref = oracle_run(x, C.turbo(4), "aol")
@@ -224,3 +233,19 @@ def test_cluster_size_groups_bitwise():
     assert ns.launch_count() - c0 == 2
     for o, s in zip(outs, singles):
         assert torch.equal(o, s)
+
+
+def test_auto_routing_by_cost():
+    """Path 0: bf16 matrices that fit take the cluster kernel only while M*N^2 <= 2.2e6
+    (64 x 216: yes; 64 x 576, 160 x 128: step engine); fp32 ones always.  Both routes meet
+    the gate and agree to bf16 rounding."""
+    cases = [(64, 216, torch.bfloat16, 1), (64, 576, torch.bfloat16, 13), (160, 128, torch.bfloat16, 13),
+             (64, 576, torch.float32, 1), (128, 128, torch.bfloat16, 1)]
+    for m, n, dt, want in cases:
+        x = I.gaussian(m, n, seed=240, bf16=(dt == torch.bfloat16))
+        a, la = _run(x, C.turbo(4), "aol", dt, path=0)
+        b, lb = _run(x, C.turbo(4), "aol", dt, path=5)
+        assert la == want and lb == 1, (m, n, dt, la, lb)
+        tol = BF16_TOL if dt == torch.bfloat16 else FP32_TOL
+        ref = oracle_run(x, C.turbo(4), "aol")
+        assert relF(a, ref) <= tol and relF(b, ref) <= tol
