@@ -189,10 +189,6 @@ __device__ __forceinline__ uint32_t pack_bf2(float a, float b) {
   asm("cvt.rn.bf16x2.f32 %0, %2, %1;" : "=r"(r) : "f"(a), "f"(b));
   return r;
 }
-// any bf16 of the pair is Inf/NaN (exponent all ones)
-__device__ __forceinline__ bool nonfinite2(uint32_t w) {
-  return ((w & 0x7F800000u) == 0x7F800000u) | ((w & 0x7F80u) == 0x7F80u);
-}
 // s[q .. q+32) as fp32 (the same for all lanes: broadcast loads; s is padded with zeros).
 __device__ __forceinline__ void load_s32(const float* s, int q, float (&sv)[32]) {
   const float4* src = reinterpret_cast<const float4*>(s + q);
@@ -265,10 +261,12 @@ __device__ __forceinline__ void epi_math(int var, const Epi& E, int p, int q, co
       break;
     }
   }
-  bool nf = false;
+  // non-finite check of the 32 stored bf16 values: per half, (h & 0x7F80) + 0x80 reaches
+  // bit 15 iff the exponent is all ones (Inf/NaN); OR over the words, one test at the end
+  uint32_t nf = 0;
 #pragma unroll
-  for (int i = 0; i < 16; ++i) nf |= nonfinite2(o[i]);
-  bad |= nf;
+  for (int i = 0; i < 16; ++i) nf |= (o[i] & 0x7F807F80u) + 0x00800080u;
+  bad |= (nf & 0x80008000u) != 0;
 }
 
 // MC = CTA pairs per cluster (CG == 2 only): with MC == 2 the two pairs of a 4-CTA cluster
