@@ -84,6 +84,18 @@ ns_status ns_orthogonalize(void* X, int64_t m, int64_t n, int64_t batch, int ite
                            const float* coeffs, ns_precond precond, ns_dtype dtype,
                            void* stream);
 
+/* Mixed precision: as ns_orthogonalize_batched with dtype NS_BF16,
+ * but X[i] / out[i] are fp32 device matrices (4-byte aligned; out = NULL or out[i] == X[i]
+ * for in place).  Each X[i] is cast to bf16 (round to nearest even) into a workspace
+ * staging copy in one grouped launch, the NS runs in bf16 on the copies exactly as for a
+ * bf16 caller, and the bf16 results are widened into out[i] in one more launch -- so the
+ * result is bitwise float(NS_bf16(bf16(X[i]))).  X[i] is read once and not modified unless
+ * it is also the output.  The workspace holds 2*m*n bytes per matrix more than
+ * ns_workspace_size(..., NS_BF16) reports. */
+ns_status ns_orthogonalize_cast(const void* const* X, void* const* out, const int64_t* m,
+                                const int64_t* n, int64_t count, int iters, const float* coeffs,
+                                ns_precond precond, void* stream);
+
 /* Grouped: `count` matrices of arbitrary shapes m[i] x n[i].  X is a HOST array of
  * device pointers (inputs); out is a HOST array of device pointers receiving the
  * results (out may be NULL, or out[i] == X[i], for in place; out[i] must not

@@ -17,7 +17,7 @@ DTYPE_BF16, DTYPE_FP32 = 0, 1
 FLAG_ZERO_SCALE, FLAG_NONFINITE = 1, 2
 
 EXPORTS = [
-    "ns_orthogonalize", "ns_orthogonalize_batched", "ns_orthogonalize_peers", "ns_muon_step", "ns_muon_apply", "ns_workspace_size", "ns_set_workspace", "ns_read_flags",
+    "ns_orthogonalize", "ns_orthogonalize_batched", "ns_orthogonalize_cast", "ns_orthogonalize_peers", "ns_muon_step", "ns_muon_apply", "ns_workspace_size", "ns_set_workspace", "ns_read_flags",
     "ns_launch_count", "ns_set_path", "ns_status_string", "ns_last_error", "ns_abi_version",
     "ns_shutdown", "ns_profile_enable", "ns_profile_read", "nsx_epilogue_counters", "nsx_gram", "nsx_precondition", "nsx_poly", "nsx_update",
 ]
@@ -39,6 +39,9 @@ def _load() -> ctypes.CDLL:
     lib.ns_orthogonalize_batched.argtypes = [
         ctypes.POINTER(c_vp), ctypes.POINTER(c_vp), ctypes.POINTER(c_i64), ctypes.POINTER(c_i64),
         c_i64, c_int, c_fp, c_int, c_int, c_vp]
+    lib.ns_orthogonalize_cast.argtypes = [
+        ctypes.POINTER(c_vp), ctypes.POINTER(c_vp), ctypes.POINTER(c_i64), ctypes.POINTER(c_i64),
+        c_i64, c_int, c_fp, c_int, c_vp]
     lib.ns_orthogonalize_peers.argtypes = [
         ctypes.POINTER(c_vp), ctypes.POINTER(c_vp), ctypes.POINTER(c_vp), c_int, ctypes.POINTER(c_i64),
         ctypes.POINTER(c_i64), c_i64, c_int, c_fp, c_int, c_int, c_vp]

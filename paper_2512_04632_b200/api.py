@@ -93,11 +93,14 @@ def _check_list(xs, out):
 
 def orthogonalize_list(xs: Sequence[torch.Tensor], out: Sequence[torch.Tensor] | None = None,
                        iters: int = 4, precond: str = "aol", coeffs=None,
-                       peer_ptrs: Sequence[Sequence[int]] | None = None) -> list[torch.Tensor]:
+                       peer_ptrs: Sequence[Sequence[int]] | None = None,
+                       compute: torch.dtype | None = None) -> list[torch.Tensor]:
     """Grouped call: one launch per NS step over all matrices.  In place unless `out`.
 
     peer_ptrs[i] = device addresses (ints) where matrix i's result is ALSO stored by the
-    last iteration's epilogue (fused collective, ns_orthogonalize_peers)."""
+    last iteration's epilogue (fused collective, ns_orthogonalize_peers).
+    compute=torch.bfloat16 with fp32 matrices: mixed precision (ns_orthogonalize_cast) --
+    cast to bf16 on the GPU, bf16 NS, results widened back to fp32."""
     xs = list(xs)
     if not xs:
         return []
@@ -109,8 +112,14 @@ def orthogonalize_list(xs: Sequence[torch.Tensor], out: Sequence[torch.Tensor] |
     M = (ctypes.c_int64 * cnt)(*[t.shape[0] for t in xs])
     N = (ctypes.c_int64 * cnt)(*[t.shape[1] for t in xs])
     c = _coeff_array(iters, coeffs, precond)
+    mixed = compute is not None and compute != xs[0].dtype
+    if mixed and (xs[0].dtype != torch.float32 or compute != torch.bfloat16 or peer_ptrs is not None):
+        raise ValueError("mixed precision: fp32 matrices with compute=torch.bfloat16 (no peer stores)")
     with torch.cuda.device(xs[0].device):
-        if peer_ptrs is None:
+        if mixed:
+            st = lib.ns_orthogonalize_cast(X, O, M, N, cnt, iters, c, PRECOND[precond], _stream(xs[0]))
+            check(st, "ns_orthogonalize_cast")
+        elif peer_ptrs is None:
             st = lib.ns_orthogonalize_batched(X, O, M, N, cnt, iters, c, PRECOND[precond], dt,
                                               _stream(xs[0]))
             check(st, "ns_orthogonalize_batched")

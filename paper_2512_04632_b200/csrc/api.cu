@@ -148,6 +148,11 @@ struct Mat {
   size_t w_off, a_off, b_off, s_off, part_off, split_off;
   int part_ld;
   int split;  // split-K factor of this matrix's Gram (0: none), see choose_splits
+  // mixed-precision call (ns_orthogonalize_cast): the caller's fp32 buffers; x / out then
+  // point at a bf16 staging copy in the workspace (stage_off)
+  const void* user_x = nullptr;
+  void* user_out = nullptr;
+  size_t stage_off = 0;
   // tensormap indices (tcgen05 path)
   int tm_x, tm_out, tm_w, tm_a, tm_b;
   // fused collective: extra destinations of the final result (peers' buffers)
@@ -155,7 +160,8 @@ struct Mat {
   int tm_peer;
 };
 
-enum PhaseKind { PH_GEMM = 0, PH_SIMT = 1, PH_PRECOND = 2, PH_COPY = 3, PH_FUSED = 4, PH_CLUSTER = 5, PH_SPLIT = 6 };
+enum PhaseKind { PH_GEMM = 0, PH_SIMT = 1, PH_PRECOND = 2, PH_COPY = 3, PH_FUSED = 4, PH_CLUSTER = 5, PH_SPLIT = 6,
+                 PH_CAST_IN = 7, PH_CAST_OUT = 8 };
 struct Phase {
   PhaseKind kind;
   size_t dev_off;  // offset of the job array in the device table
@@ -176,6 +182,7 @@ struct Phase {
   size_t smem = 0;        // PH_CLUSTER: dynamic shared memory per CTA
   int ctas = 8;           // PH_CLUSTER: CTAs per cluster
   bool has_split = false; // PH_GEMM: the task list holds split-K tasks
+  int64_t max_numel = 0;  // PH_CAST_*: largest matrix
   // copies (PH_COPY)
   std::vector<std::pair<std::pair<void*, const void*>, size_t>> copies;
 };
@@ -187,6 +194,7 @@ struct Plan {
   bool fused = false;  // all 3T+1 steps in one launch (small problems)
   int cg = 2;  // tcgen05 CTA group (2: 256x256 tiles on CTA pairs)
   int bn = 256;  // tile width: 128 for tile-starved plans (see choose_bn)
+  bool cast = false;  // fp32 caller buffers, bf16 compute (ns_orthogonalize_cast)
   int iters = 0;
   ns_precond precond = NS_PRECOND_AOL;
   std::vector<Mat> mats;   // tcgen05 / SIMT step engine
@@ -379,6 +387,10 @@ static ns_status build_plan(Plan& P, HostTables& H, DevCtx* dc, const float* coe
     if (P.precond == NS_PRECOND_AOL && !P.simt) off += (size_t)mt.N * mt.part_ld * 4;
     off = align_up(off, 256); mt.split_off = off; off += split_bytes(mt);
   }
+  if (P.cast) {  // bf16 staging copies of the caller's fp32 matrices
+    for (Mat& mt : P.mats) { off = align_up(off, 256); mt.stage_off = off; off += (size_t)mt.m * mt.n * 2; }
+    for (Mat& mt : P.tiny) { off = align_up(off, 256); mt.stage_off = off; off += (size_t)mt.m * mt.n * 2; }
+  }
   P.ws_bytes = align_up(off, 256);
   cudaError_t e = cudaSuccess;
   UserWs& uw = g_uws[P.device & 63];
@@ -407,6 +419,29 @@ static ns_status build_plan(Plan& P, HostTables& H, DevCtx* dc, const float* coe
   auto Sv = [&](const Mat& mt) { return (float*)(ws + mt.s_off); };
   auto Part = [&](const Mat& mt) { return (float*)(ws + mt.part_off); };
   const bool use_part = (P.precond == NS_PRECOND_AOL) && !P.simt;
+
+  // -- mixed precision: cast the caller's fp32 matrices into bf16 staging (in place from
+  //    then on), cast the results back at the end
+  std::vector<CastJob> cast_out;
+  if (P.cast) {
+    std::vector<CastJob> cin;
+    int64_t mx = 0;
+    for (std::vector<Mat>* v : {&P.mats, &P.tiny})
+      for (Mat& mt : *v) {
+        mt.user_x = mt.x; mt.user_out = mt.out;
+        void* st = ws + mt.stage_off;
+        cin.push_back({mt.user_x, st, mt.m * mt.n});
+        cast_out.push_back({st, mt.user_out, mt.m * mt.n});
+        mt.x = mt.out = st;
+        mt.copy_in = (T % 2 == 1);
+        mx = std::max<int64_t>(mx, mt.m * mt.n);
+      }
+    Phase ph{PH_CAST_IN};
+    ph.dev_off = H.push(cin.data(), cin.size() * sizeof(CastJob), 64);
+    ph.njobs = (int)cin.size();
+    ph.max_numel = mx;
+    P.phases.push_back(ph);
+  }
 
   // -- tensormaps (tcgen05 path)
   std::vector<CUtensorMap> tmaps;
@@ -819,6 +854,14 @@ static ns_status build_plan(Plan& P, HostTables& H, DevCtx* dc, const float* coe
     }
   }
 
+  if (P.cast) {
+    Phase ph{PH_CAST_OUT};
+    ph.dev_off = H.push(cast_out.data(), cast_out.size() * sizeof(CastJob), 64);
+    ph.njobs = (int)cast_out.size();
+    for (const CastJob& c : cast_out) ph.max_numel = std::max<int64_t>(ph.max_numel, c.numel);
+    P.phases.push_back(ph);
+  }
+
   // -- upload
   if (!H.bytes.empty()) {
     P.dtab_bytes = align_up(H.bytes.size(), 256);
@@ -895,6 +938,18 @@ static ns_status enqueue_plan(Plan& P, DevCtx* dc, cudaStream_t stream) {
         ProfScope ps(4, stream);
         CU_TRY(launch_simt_gemm(reinterpret_cast<const SimtJob*>(dbase + ph.dev_off), ph.njobs, ph.total,
                                 dc->sms, P.dtype == NS_BF16, dc->flags, stream));
+        ++g_launches;
+        break;
+      }
+      case PH_CAST_IN:
+      case PH_CAST_OUT: {
+        if (ph.kind == PH_CAST_OUT && !joined) {  // after the side-stream cluster launch too
+          CU_TRY(cudaStreamWaitEvent(stream, dc->ev_join, 0));
+          joined = true;
+        }
+        ProfScope ps(5, stream);
+        CU_TRY(launch_cast(reinterpret_cast<const CastJob*>(dbase + ph.dev_off), ph.njobs, ph.max_numel,
+                           ph.kind == PH_CAST_IN, dc->sms, stream));
         ++g_launches;
         break;
       }
@@ -1009,7 +1064,7 @@ static ns_status validate_mat(const void* x, int64_t m, int64_t n, ns_dtype dtyp
 }
 
 static ns_status run(const std::vector<Mat>& mats_in, int iters, const float* coeffs, ns_precond precond,
-                     ns_dtype dtype, cudaStream_t stream) {
+                     ns_dtype dtype, cudaStream_t stream, bool cast = false) {
   DevCtx* dc = nullptr;
   ns_status st = dev_ctx(&dc);
   if (st != NS_OK) return st;
@@ -1033,7 +1088,9 @@ static ns_status run(const std::vector<Mat>& mats_in, int iters, const float* co
   bool simt = (g_path == 1) || dtype != NS_BF16 || dc->cc_major != 10;
   bool peers = false;
   for (const Mat& mt : big) {
-    simt = simt || !tma_ok(mt, dtype);
+    Mat chk = mt;  // mixed precision: the step engine reads the 256-byte aligned staging copy
+    if (cast) chk.x = chk.out = reinterpret_cast<void*>(256);
+    simt = simt || !tma_ok(chk, dtype);
     peers = peers || !mt.peer.empty();
     for (void* pp : mt.peer) simt = simt || (reinterpret_cast<uintptr_t>(pp) & 15);
   }
@@ -1046,6 +1103,7 @@ static ns_status run(const std::vector<Mat>& mats_in, int iters, const float* co
   key.reserve(mats_in.size() * 4 + 8 + 3 * iters);
   const int cg = (g_path == 2) ? 1 : (g_path == 6 ? 4 : 2);
   key.push_back((uint64_t)dev); key.push_back((uint64_t)dtype); key.push_back(simt ? 1 : 0);
+  key.push_back(cast ? 1 : 0);
   key.push_back((uint64_t)cg);
   key.push_back((uint64_t)g_path);
   key.push_back((uint64_t)iters); key.push_back((uint64_t)precond);
@@ -1080,6 +1138,7 @@ static ns_status run(const std::vector<Mat>& mats_in, int iters, const float* co
     }
     std::unique_ptr<Plan> np(new Plan());
     np->device = dev; np->dtype = dtype; np->simt = simt; np->cg = cg; np->iters = iters; np->precond = precond;
+    np->cast = cast;
     np->mats = big;
     np->tiny = tiny;
     HostTables H;
@@ -1188,6 +1247,25 @@ ns_status ns_orthogonalize(void* X, int64_t m, int64_t n, int64_t batch, int ite
     mats.push_back(make_mat(xi, xi, m, n, iters));
   }
   return run(mats, iters, coeffs, precond, dtype, reinterpret_cast<cudaStream_t>(stream));
+}
+
+ns_status ns_orthogonalize_cast(const void* const* X, void* const* out, const int64_t* m, const int64_t* n,
+                                int64_t count, int iters, const float* coeffs, ns_precond precond, void* stream) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  ns_status st = validate_common(count, iters, coeffs, precond, NS_BF16);
+  if (st != NS_OK) return st;
+  if (!X || !m || !n) return fail(NS_ERR_INVALID_VALUE, "NULL array argument");
+  std::vector<Mat> mats;
+  for (int64_t i = 0; i < count; ++i) {
+    void* x = const_cast<void*>(X[i]);
+    if ((st = validate_mat(x, m[i], n[i], NS_FP32)) != NS_OK) return st;
+    void* o = out ? out[i] : nullptr;
+    if (o && (st = validate_mat(o, m[i], n[i], NS_FP32)) != NS_OK) return st;
+    Mat mt = make_mat(x, o, m[i], n[i], iters);
+    mt.copy_in = false;  // decided on the staging copy (build_plan)
+    mats.push_back(mt);
+  }
+  return run(mats, iters, coeffs, precond, NS_BF16, reinterpret_cast<cudaStream_t>(stream), true);
 }
 
 ns_status ns_orthogonalize_batched(void* const* X, void* const* out, const int64_t* m, const int64_t* n,

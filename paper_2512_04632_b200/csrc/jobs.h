@@ -96,6 +96,14 @@ struct SimtJob {
 };
 constexpr int kSimtTile = 64;
 
+// One matrix of a storage cast (muon.cu cast_kernel): fp32 -> bf16 (round to nearest even)
+// before a mixed-precision call, bf16 -> fp32 after it.
+struct CastJob {
+  const void* src;
+  void* dst;
+  int64_t numel;
+};
+
 // Per-matrix descriptor for the preconditioning kernel (AOL / Frobenius).
 // AOL rows with at most this many Gram-epilogue partial slots (N <= 1344) are summed by
 // one lane in slot order; larger ones by a warp tree (precond_rows.cuh).

@@ -53,6 +53,10 @@ cudaError_t launch_cluster_ns(const ClusterJob* d_jobs, int njobs, const float* 
 // (8 phase marks + launch count).
 cudaError_t cluster_timeline(unsigned long long* out9, bool reset);
 
+// fp32 <-> bf16 storage casts of a mixed-precision call (muon.cu), one launch for all jobs.
+cudaError_t launch_cast(const CastJob* d_jobs, int count, int64_t max_numel, bool to_bf16, int sms,
+                        cudaStream_t stream);
+
 // Muon step around the path (muon.cu): momentum + nesterov -> bf16 U; W update from U.
 cudaError_t launch_muon_momentum(const MuonJob* d_jobs, int count, int64_t max_numel, bool g_bf16, float beta,
                                  int nesterov, int sms, cudaStream_t stream);

@@ -104,6 +104,67 @@ __global__ void __launch_bounds__(256) muon_apply_kernel(const MuonJob* __restri
   for (int64_t i = t0; i < J.numel; i += nt) stf<TW>(W, i, fmaf(-step, bfv(O[i]), ldf<TW>(W, i) * keep));
 }
 
+__device__ __forceinline__ uint32_t pack_rn(float lo, float hi) {
+  return (uint32_t)tobf(lo) | ((uint32_t)tobf(hi) << 16);
+}
+
+// fp32 <-> bf16 storage casts of a mixed-precision call, all matrices in one launch
+// (blockIdx.y strides over matrices, 8 elements per thread; 16-byte aligned buffers).
+template <bool TO_BF16>
+__global__ void __launch_bounds__(256) cast_kernel(const CastJob* __restrict__ jobs, int count) {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // the previous launch's results
+  for (int jb = blockIdx.y; jb < count; jb += gridDim.y) {
+    const CastJob J = jobs[jb];
+    const int64_t nt = (int64_t)gridDim.x * blockDim.x, t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const bool vec = ((reinterpret_cast<uintptr_t>(J.src) | reinterpret_cast<uintptr_t>(J.dst)) & 15) == 0;
+    const int64_t nv = vec ? J.numel / 8 : 0;
+    for (int64_t v = t0; v < nv; v += nt) {
+      if constexpr (TO_BF16) {
+        const float4 a = reinterpret_cast<const float4*>(J.src)[2 * v];
+        const float4 b = reinterpret_cast<const float4*>(J.src)[2 * v + 1];
+        uint4 w;
+        w.x = pack_rn(a.x, a.y); w.y = pack_rn(a.z, a.w); w.z = pack_rn(b.x, b.y); w.w = pack_rn(b.z, b.w);
+        reinterpret_cast<uint4*>(J.dst)[v] = w;
+      } else {
+        const uint4 w = reinterpret_cast<const uint4*>(J.src)[v];
+        float4* d = reinterpret_cast<float4*>(J.dst) + 2 * v;
+        d[0] = make_float4(__uint_as_float(w.x << 16), __uint_as_float(w.x & 0xFFFF0000u),
+                           __uint_as_float(w.y << 16), __uint_as_float(w.y & 0xFFFF0000u));
+        d[1] = make_float4(__uint_as_float(w.z << 16), __uint_as_float(w.z & 0xFFFF0000u),
+                           __uint_as_float(w.w << 16), __uint_as_float(w.w & 0xFFFF0000u));
+      }
+    }
+    for (int64_t e = nv * 8 + t0; e < J.numel; e += nt) {
+      if constexpr (TO_BF16)
+        reinterpret_cast<uint16_t*>(J.dst)[e] =
+            __bfloat16_as_ushort(__float2bfloat16_rn(reinterpret_cast<const float*>(J.src)[e]));
+      else
+        reinterpret_cast<float*>(J.dst)[e] = __uint_as_float((uint32_t)reinterpret_cast<const uint16_t*>(J.src)[e] << 16);
+    }
+  }
+}
+
+cudaError_t launch_cast(const CastJob* d_jobs, int count, int64_t max_numel, bool to_bf16, int sms,
+                        cudaStream_t stream) {
+  if (count <= 0) return cudaSuccess;
+  int64_t want = (max_numel + 2047) / 2048;
+  const int64_t cap = (int64_t)sms * 8 / count + 1;
+  if (want > cap) want = cap;
+  if (want < 1) want = 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)want, (unsigned)(count < 65535 ? count : 65535));
+  cfg.blockDim = dim3(256);
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // PDL
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (to_bf16) return cudaLaunchKernelEx(&cfg, cast_kernel<true>, d_jobs, count);
+  return cudaLaunchKernelEx(&cfg, cast_kernel<false>, d_jobs, count);
+}
+
 static dim3 muon_grid(int64_t max_numel, int count, int sms) {
   int64_t want = (max_numel + 2047) / 2048;  // 8 elements per thread
   const int64_t cap = (int64_t)sms * 8 / (count > 0 ? count : 1) + 1;
