@@ -282,7 +282,10 @@ static void choose_splits(std::vector<Mat>& mats, int cg, int workers) {
 // Per-step launches on CTA pairs only; TNS_BN=256 forces the wide tiles (A/B knob).
 static int choose_bn(const std::vector<Mat>& mats, int cg, int workers) {
   if (cg != 2 || g_path == 3) return 256;
-  if (const char* e = getenv("TNS_BN")) if (atoi(e) == 256) return 256;
+  if (const char* e = getenv("TNS_BN")) {  // A/B knob: force either width
+    if (atoi(e) == 256) return 256;
+    if (atoi(e) == 128) return 128;
+  }
   int64_t sym = 0, xb = 0;
   for (const Mat& mt : mats) {
     const int64_t nb = (mt.N + kSymBlock - 1) / kSymBlock;
