@@ -25,6 +25,8 @@ FLAGS = [
 # counters / timeline read through nsx_epilogue_counters under TNS_DBG bits 8 and 16.
 if os.environ.get("TNS_MEASURE"):
     FLAGS += ["-DTNS_MEASURE=1"]
+# A/B builds: extra -D flags (e.g. TNS_EXTRA_FLAGS=-DTNS_NO_DIAG); never set in production
+FLAGS += os.environ.get("TNS_EXTRA_FLAGS", "").split()
 
 
 def _stale() -> bool:
