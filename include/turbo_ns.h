@@ -101,8 +101,9 @@ ns_status ns_orthogonalize_cast(const void* const* X, void* const* out, const in
  * results (out may be NULL, or out[i] == X[i], for in place; out[i] must not
  * otherwise overlap any X[j]).  Every NS step runs as ONE launch over all matrices
  * (3*iters + 1 launches in total), plus ONE cluster launch for all small matrices
- * (see ns_set_path).  Results are bitwise identical to calling
- * ns_orthogonalize on each matrix alone. */
+ * (see ns_set_path); bf16 matrices whose row pitch TMA cannot address (not a multiple of
+ * 16 bytes) run as a second group on the CUDA-core kernels.  Results are bitwise identical
+ * to calling ns_orthogonalize on each matrix alone (split-K exception: see above). */
 ns_status ns_orthogonalize_batched(void* const* X, void* const* out, const int64_t* m,
                                    const int64_t* n, int64_t count, int iters,
                                    const float* coeffs, ns_precond precond, ns_dtype dtype,

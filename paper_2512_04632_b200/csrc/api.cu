@@ -1066,8 +1066,33 @@ static ns_status validate_mat(const void* x, int64_t m, int64_t n, ns_dtype dtyp
   return NS_OK;
 }
 
+static ns_status run_plan(const std::vector<Mat>& mats_in, int iters, const float* coeffs, ns_precond precond,
+                          ns_dtype dtype, cudaStream_t stream, bool cast);
+
+// A bf16 list that mixes TMA-addressable matrices with ones TMA cannot address (a row pitch
+// that is not a multiple of 16 bytes) runs as two plans on the stream: the unaligned ones on
+// the CUDA-core step kernels, the rest on the tcgen05 engine -- so one unaligned matrix
+// neither slows the others down nor changes their results (batching stays invisible).
 static ns_status run(const std::vector<Mat>& mats_in, int iters, const float* coeffs, ns_precond precond,
                      ns_dtype dtype, cudaStream_t stream, bool cast = false) {
+  if (dtype == NS_BF16 && g_path != 1 && mats_in.size() > 1) {
+    std::vector<Mat> aligned, unaligned;
+    for (const Mat& mt : mats_in) {
+      Mat chk = mt;
+      if (cast) chk.x = chk.out = reinterpret_cast<void*>(256);
+      (tma_ok(chk, dtype) ? aligned : unaligned).push_back(mt);
+    }
+    if (!aligned.empty() && !unaligned.empty()) {
+      ns_status st = run_plan(unaligned, iters, coeffs, precond, dtype, stream, cast);
+      if (st != NS_OK) return st;
+      return run_plan(aligned, iters, coeffs, precond, dtype, stream, cast);
+    }
+  }
+  return run_plan(mats_in, iters, coeffs, precond, dtype, stream, cast);
+}
+
+static ns_status run_plan(const std::vector<Mat>& mats_in, int iters, const float* coeffs, ns_precond precond,
+                          ns_dtype dtype, cudaStream_t stream, bool cast) {
   DevCtx* dc = nullptr;
   ns_status st = dev_ctx(&dc);
   if (st != NS_OK) return st;

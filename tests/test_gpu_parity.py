@@ -569,3 +569,27 @@ def test_narrow_tiles_bitwise_equal_wide_tiles():
     for precond in ("aol", "frobenius"):
         for a, b in zip(res[("128", precond)], res[("256", precond)]):
             assert torch.equal(a, b)
+
+
+def test_unaligned_matrix_does_not_change_the_others():
+    """A bf16 list with a matrix TMA cannot address (row pitch not a multiple of 16 bytes,
+    short side > 128) runs that one on the CUDA-core kernels and the rest on tcgen05: every
+    result bitwise equals its single call, and the aligned ones keep the tensor-core path."""
+    shapes = [(768, 768), (300, 201), (1024, 256), (64, 216)]
+    xs = [torch.from_numpy(I.gaussian(m, n, seed=900 + i)).to(torch.bfloat16).cuda() for i, (m, n) in enumerate(shapes)]
+    singles = []
+    for x in xs:
+        t = x.clone()
+        ns.orthogonalize(t, iters=4)
+        singles.append(t)
+    outs = [torch.empty_like(x) for x in xs]
+    ns.orthogonalize_list(xs, out=outs, iters=4)
+    ns.profile_enable(True)
+    try:
+        ns.orthogonalize_list(xs, out=outs, iters=4)
+        prof = ns.profile_read()
+    finally:
+        ns.profile_enable(False)
+    assert prof["simt"][1] == 12 and prof["update"][1] == 4  # both engines ran (3T SIMT GEMMs)
+    for o, s in zip(outs, singles):
+        assert torch.equal(o, s)
