@@ -64,20 +64,22 @@ def test_fuzz_against_oracle(k, m, n, mode, precond, iters, path):
         assert relF(got, ref) <= tol, (relF(got, ref), tol)
 
 
-def test_fuzz_grouped_equals_single_bitwise():
-    bf = [(k, m, n) for (k, m, n, mode, precond, iters, path) in CASES if mode == "bf16"]
-    xs = [torch.from_numpy(I.gaussian(m, n, seed=6000 + k)).to(torch.bfloat16).cuda() for k, m, n in bf]
+@pytest.mark.parametrize("mode", ["bf16", "fp32", "cast"])
+def test_fuzz_grouped_equals_single_bitwise(mode):
+    bf = [(k, m, n) for (k, m, n, _, precond, iters, path) in CASES]
+    xs = [torch.from_numpy(I.gaussian(m, n, seed=6000 + k, bf16=(mode == "bf16"))).cuda() for k, m, n in bf]
+    if mode == "bf16":
+        xs = [x.to(torch.bfloat16) for x in xs]
+    compute = torch.bfloat16 if mode == "cast" else None
     singles = []
     for x in xs:
-        t = x.clone()
-        ns.orthogonalize(t, iters=4)
-        singles.append(t)
+        singles.append(ns.orthogonalize_list([x], out=[torch.empty_like(x)], iters=4, compute=compute)[0])
     outs = [torch.empty_like(x) for x in xs]
-    ns.orthogonalize_list(xs, out=outs, iters=4)
+    ns.orthogonalize_list(xs, out=outs, iters=4, compute=compute)
     torch.cuda.synchronize()
     for (k, m, n), o, s in zip(bf, outs, singles):
         # the split-K Gram is the one batch-dependent choice (tile-starved calls only)
-        if min(m, n) <= 256 and max(m, n) >= 1024:
+        if mode != "fp32" and min(m, n) <= 256 and max(m, n) >= 1024:
             assert relF(o.float().cpu().numpy(), s.float().cpu().numpy()) <= 1e-2
         else:
             assert torch.equal(o, s), (m, n)
