@@ -173,17 +173,15 @@ uint64_t ns_launch_count(void);
  * other matrices through the step engine (tcgen05, 256x256 tiles on CTA pairs, for aligned
  * bf16, else SIMT; one PDL-chained launch per step); when both kinds are present the
  * cluster launch runs on an internal side stream joined back by events; 1 = force the SIMT
- * (CUDA-core) step kernels, 2 = tcgen05 with single-CTA 128x256 tiles, 3 = all 3T+1 steps
- * in ONE fused dataflow launch, 4 = per-step launches for every matrix (no cluster kernel),
- * 5 = as 0 but every matrix that fits takes the cluster kernel, 6 = per-step launches on 4-CTA clusters: two CTA pairs run tiles sharing
- * their A operand, loaded once by TMA multicast (bitwise equal to 4; measured slower on
- * B200 because only 33 4-CTA clusters fit on the 148 SMs).  Returns the previous value. */
+ * (CUDA-core) step kernels, 2 = tcgen05 with single-CTA 128x256 tiles, 4 = per-step launches
+ * for every matrix (no cluster kernel), 5 = as 0 but every matrix that fits takes the cluster
+ * kernel.  Returns the previous value; any other `path` returns -1 and changes nothing. */
 int ns_set_path(int path);
 
 /* Per-kernel event timing (measurement support for bench.py; off by default).
  * When enabled, every launch the library enqueues is bracketed by CUDA events recorded
  * on the SAME stream.  ns_profile_read SYNCHRONISES on the last event, writes for each
- * kind k (0 GRAM, 1 PRECOND, 2 POLY, 3 XB, 4 SIMT, 5 COPY, 6 FUSED, 7 CLUSTER; nkinds <= 8) the summed
+ * kind k (0 GRAM, 1 PRECOND, 2 POLY, 3 XB, 4 SIMT, 5 COPY, 6 unused, 7 CLUSTER; nkinds <= 8) the summed
  * device milliseconds ms[k] and the launch count counts[k], then clears the records. */
 void ns_profile_enable(int on);
 ns_status ns_profile_read(double* ms, uint64_t* counts, int nkinds);

@@ -219,12 +219,13 @@ def launch_count() -> int:
 
 
 def set_path(path: int) -> int:
-    """0 auto, 1 CUDA-core kernels, 2 tcgen05 1-CTA tiles, 3 force fused single launch,
-    4 never fuse (one launch per step)."""
+    """0 auto, 1 CUDA-core kernels, 2 tcgen05 1-CTA tiles, 4 per-step launches for every
+    matrix (no cluster kernel), 5 every matrix that fits takes the cluster kernel.  Returns
+    the previous path, or -1 (and changes nothing) for any other value."""
     return int(lib.ns_set_path(int(path)))
 
 
-KERNEL_KINDS = ("gram", "precondition", "poly", "update", "simt", "copy", "fused", "cluster")
+KERNEL_KINDS = ("gram", "precondition", "poly", "update", "simt", "copy", "unused", "cluster")
 
 
 def profile_enable(on: bool = True) -> None:

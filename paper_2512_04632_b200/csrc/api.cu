@@ -160,7 +160,7 @@ struct Mat {
   int tm_peer;
 };
 
-enum PhaseKind { PH_GEMM = 0, PH_SIMT = 1, PH_PRECOND = 2, PH_COPY = 3, PH_FUSED = 4, PH_CLUSTER = 5, PH_SPLIT = 6,
+enum PhaseKind { PH_GEMM = 0, PH_SIMT = 1, PH_PRECOND = 2, PH_COPY = 3, PH_CLUSTER = 5, PH_SPLIT = 6,
                  PH_CAST_IN = 7, PH_CAST_OUT = 8 };
 struct Phase {
   PhaseKind kind;
@@ -171,13 +171,8 @@ struct Phase {
   bool vec8;
   bool lane_rows = false;  // PH_PRECOND: AOL partials, every part_ld <= kSeqPartials
   int gemm_kind;  // profiling kind: 0 GRAM, 2 POLY, 3 XB
-  size_t tiles_off = 0;   // offset of the TaskDesc list (PH_GEMM / PH_FUSED)
-  size_t jobs_off = 0;    // offset of the GemmJob array (PH_FUSED)
-  size_t pjobs_off = 0;   // offset of the PrecondJob array (PH_FUSED)
-  bool has_pjobs = false;
-  size_t done_off = 0;    // offset of the dependency counters (PH_FUSED)
-  int nslots = 0;         // PH_FUSED: dependency counters
-  int64_t max_tiles = 0;  // largest GEMM step
+  size_t tiles_off = 0;   // offset of the TaskDesc list (PH_GEMM)
+  int64_t max_tiles = 0;  // tiles of the GEMM step
   size_t coeff_off = 0;   // PH_CLUSTER: 3*iters floats
   size_t smem = 0;        // PH_CLUSTER: dynamic shared memory per CTA
   int ctas = 8;           // PH_CLUSTER: CTAs per cluster
@@ -191,7 +186,6 @@ struct Plan {
   int device = 0;
   ns_dtype dtype = NS_BF16;
   bool simt = false;
-  bool fused = false;  // all 3T+1 steps in one launch (small problems)
   int cg = 2;  // tcgen05 CTA group (2: 256x256 tiles on CTA pairs)
   int bn = 256;  // tile width: 128 for tile-starved plans (see choose_bn)
   bool cast = false;  // fp32 caller buffers, bf16 compute (ns_orthogonalize_cast)
@@ -281,7 +275,7 @@ static void choose_splits(std::vector<Mat>& mats, int cg, int workers) {
 // partials are per 64 columns either way), so the choice never breaks batch invariance.
 // Per-step launches on CTA pairs only; TNS_BN=256 forces the wide tiles (A/B knob).
 static int choose_bn(const std::vector<Mat>& mats, int cg, int workers) {
-  if (cg != 2 || g_path == 3) return 256;
+  if (cg != 2) return 256;
   if (const char* e = getenv("TNS_BN")) {  // A/B knob: force either width
     if (atoi(e) == 256) return 256;
     if (atoi(e) == 128) return 128;
@@ -363,7 +357,7 @@ static void balance_tasks(std::vector<TaskDesc>& tasks, const std::vector<GemmJo
   for (auto& l : lists) { std::sort(l.begin(), l.end()); rounds = std::max(rounds, l.size()); }
   TaskDesc pad;
   std::memset(&pad, 0, sizeof(pad));
-  pad.kind = TK_NONE; pad.dep_slot = kNoSlot; pad.my_slot = kNoSlot;
+  pad.kind = TK_NONE;
   std::vector<TaskDesc> out(rounds * workers, pad);
   for (int w = 0; w < workers; ++w)
     for (size_t r = 0; r < lists[w].size(); ++r) out[r * workers + w] = tasks[lists[w][r]];
@@ -375,7 +369,7 @@ static ns_status build_plan(Plan& P, HostTables& H, DevCtx* dc, const float* coe
   const int T = P.iters;
   const size_t es = elem_size(P.dtype);
   const bool bf16 = P.dtype == NS_BF16;
-  if (!P.simt && (P.cg == 1 || P.cg == 2) && g_path != 3) choose_splits(P.mats, P.cg, dc->sms / P.cg);
+  if (!P.simt) choose_splits(P.mats, P.cg, dc->sms / P.cg);
   else for (Mat& mt : P.mats) mt.split = 0;
   P.bn = P.simt ? 256 : choose_bn(P.mats, P.cg, dc->sms / 2);
   // -- workspace layout
@@ -706,154 +700,71 @@ static ns_status build_plan(Plan& P, HostTables& H, DevCtx* dc, const float* coe
     }
   }
 
-  // -- tcgen05 steps: one launch each (PDL-chained), or all in one fused launch
+  // -- tcgen05 steps: one launch each (PDL-chained)
   if (!P.simt && !steps.empty()) {
-    const int nm = (int)P.mats.size();
-    int64_t max_tiles = 0;
-    auto tile_list = [&](const Step& st, size_t job_base) {
+    auto tile_list = [&](const Step& st) {
       // longest-K jobs first (LPT-like): long tiles do not end up in the last wave
       std::vector<size_t> order(st.jobs.size());
       for (size_t j = 0; j < st.jobs.size(); ++j) order[j] = j;
       std::stable_sort(order.begin(), order.end(), [&](size_t x, size_t y) { return st.jobs[x].K > st.jobs[y].K; });
       std::vector<uint64_t> tl;
-      for (size_t j : order) umma_tile_list(st.jobs[j], (uint32_t)(job_base + j), P.cg, P.bn, tl);
+      for (size_t j : order) umma_tile_list(st.jobs[j], (uint32_t)j, P.cg, P.bn, tl);
       return tl;
     };
     auto mk_task = [](uint64_t w) {
       TaskDesc td;
       std::memset(&td, 0, sizeof(td));
-      td.tile = w; td.kind = TK_TILE; td.dep_slot = kNoSlot; td.my_slot = kNoSlot;
+      td.tile = w; td.kind = TK_TILE;
       return td;
     };
-    // The fused single launch is opt-in (path 3): measured against PDL-chained per-step
-    // launches in profiles/README.md.
-    P.fused = (g_path == 3);
-    if (!P.fused) {
-      for (Step& st : steps) {
-        if (st.kind == PHK_GEMM) {
-          std::vector<TaskDesc> tasks;
-          if (P.cg == 4) {  // multicast clusters: tile pairs sharing the A operand
-            std::vector<size_t> order(st.jobs.size());
-            for (size_t j = 0; j < st.jobs.size(); ++j) order[j] = j;
-            std::stable_sort(order.begin(), order.end(), [&](size_t x, size_t y) { return st.jobs[x].K > st.jobs[y].K; });
-            std::vector<std::pair<uint64_t, uint64_t>> pl;
-            for (size_t j : order) umma_pair_list(st.jobs[j], (uint32_t)j, pl);
-            for (auto& pr : pl) {
-              TaskDesc td = mk_task(pr.first);
-              td.tile2 = pr.second;
-              tasks.push_back(td);
-            }
-          } else {
-            std::vector<uint64_t> tl = tile_list(st, 0);
-            for (uint64_t w : tl) {
-              const size_t j = w & 0xFFFFFu;
-              const int S = j < st.jsplit.size() ? st.jsplit[j] : 0;
-              if (!S) { tasks.push_back(mk_task(w)); continue; }
-              const int nk = (st.jobs[j].K + kBK - 1) / kBK;
-              for (int sp = 0; sp < S; ++sp) {  // k-blocks [sp*nk/S, (sp+1)*nk/S)
-                TaskDesc td = mk_task(w);
-                td.kb0 = (uint32_t)(sp * nk / S);
-                td.nkb = (uint32_t)((sp + 1) * nk / S) - td.kb0;
-                td.split = (uint32_t)sp + 1;
-                tasks.push_back(td);
-              }
-            }
-            balance_tasks(tasks, st.jobs, dc->sms / P.cg);
-          }
-          Phase ph{PH_GEMM};
-          ph.gemm_kind = st.gemm_kind;
-          for (const TaskDesc& td : tasks) ph.has_split = ph.has_split || td.split != 0;
-          ph.dev_off = H.push(st.jobs.data(), st.jobs.size() * sizeof(GemmJob), 64);
-          ph.njobs = (int)st.jobs.size();
-          ph.tiles_off = H.push(tasks.data(), tasks.size() * sizeof(TaskDesc), 64);
-          ph.total = (int64_t)tasks.size();
-          ph.max_tiles = ph.total;
-          for (size_t j = 0; j < st.jobs.size(); ++j)
-            fixes.push_back({ph.dev_off + j * sizeof(GemmJob), st.tmi[j][0], st.tmi[j][1], st.tmi[j][2], st.tmi[j][3],
-                             st.tmi[j][4]});
-          P.phases.push_back(ph);
-        } else if (st.kind == PHK_SPLIT) {
-          Phase ph{PH_SPLIT};
-          ph.dev_off = H.push(st.sj.data(), st.sj.size() * sizeof(SplitJob), 64);
-          ph.njobs = (int)st.sj.size();
-          ph.total_rows = st.rows;
-          P.phases.push_back(ph);
-        } else {
-          Phase ph{PH_PRECOND};
-          ph.dev_off = H.push(st.pj.data(), st.pj.size() * sizeof(PrecondJob), 64);
-          ph.njobs = (int)st.pj.size();
-          ph.total = st.items;
-          ph.total_rows = st.rows;
-          ph.vec8 = st.vec8;
-          ph.lane_rows = true;
-          for (const PrecondJob& pj : st.pj)
-            ph.lane_rows = ph.lane_rows && pj.precond == 2 && pj.part != nullptr && pj.part_ld <= kSeqPartials;
-          P.phases.push_back(ph);
-        }
-      }
-    } else {
-      // fused: expand the preconditioner into its two row steps; slot (step, matrix)
-      // counts the epilogue-warp arrivals of that step's tasks for that matrix
-      const uint32_t per_task = (uint32_t)(8 * P.cg);  // kNumEpiWarps * CTAs per task
-      std::vector<GemmJob> alljobs;
-      std::vector<std::array<int, 5>> alltmi;
-      std::vector<TaskDesc> tasks;
-      std::vector<uint32_t> count;  // arrivals per slot
-      std::vector<PrecondJob> pjs;
-      int si = 0;  // expanded step index
-      for (Step& st : steps) {
-        const int nsub = (st.kind == PHK_GEMM) ? 1 : 2;
-        for (int sub = 0; sub < nsub; ++sub, ++si) {
-          count.resize((size_t)(si + 1) * nm, 0);
-          auto dep_of = [&](int j, TaskDesc& td) {
-            if (si == 0) return;
-            td.dep_slot = (uint32_t)((si - 1) * nm + j);
-            td.dep_target = count[(size_t)(si - 1) * nm + j];
-          };
-          if (st.kind == PHK_GEMM) {
-            const size_t base = alljobs.size();
-            alljobs.insert(alljobs.end(), st.jobs.begin(), st.jobs.end());
-            alltmi.insert(alltmi.end(), st.tmi.begin(), st.tmi.end());
-            std::vector<uint64_t> tl = tile_list(st, base);
-            for (uint64_t w : tl) {
-              TaskDesc td = mk_task(w);
-              const int j = (int)((w & 0xFFFFFu) - base);  // job index within the step = matrix
-              dep_of(j, td);
-              td.my_slot = (uint32_t)(si * nm + j);
-              count[(size_t)si * nm + j] += per_task;
-              tasks.push_back(td);
-            }
-            max_tiles = std::max(max_tiles, (int64_t)tl.size());
-          } else {
-            if (pjs.empty()) pjs = st.pj;
-            for (int j = 0; j < nm; ++j)
-              for (int r0 = 0; r0 < pjs[j].N; r0 += kPreRows) {
-                TaskDesc td = mk_task(0);
-                td.kind = sub == 0 ? TK_PRE_S : TK_PRE_SCALE;
-                td.pjob = (uint32_t)j;
-                td.row0 = (uint32_t)r0;
-                dep_of(j, td);
-                td.my_slot = (uint32_t)(si * nm + j);
-                count[(size_t)si * nm + j] += per_task;
-                tasks.push_back(td);
-              }
+    for (Step& st : steps) {
+      if (st.kind == PHK_GEMM) {
+        std::vector<TaskDesc> tasks;
+        std::vector<uint64_t> tl = tile_list(st);
+        for (uint64_t w : tl) {
+          const size_t j = w & 0xFFFFFu;
+          const int S = j < st.jsplit.size() ? st.jsplit[j] : 0;
+          if (!S) { tasks.push_back(mk_task(w)); continue; }
+          const int nk = (st.jobs[j].K + kBK - 1) / kBK;
+          for (int sp = 0; sp < S; ++sp) {  // k-blocks [sp*nk/S, (sp+1)*nk/S)
+            TaskDesc td = mk_task(w);
+            td.kb0 = (uint32_t)(sp * nk / S);
+            td.nkb = (uint32_t)((sp + 1) * nk / S) - td.kb0;
+            td.split = (uint32_t)sp + 1;
+            tasks.push_back(td);
           }
         }
+        balance_tasks(tasks, st.jobs, dc->sms / P.cg);
+        Phase ph{PH_GEMM};
+        ph.gemm_kind = st.gemm_kind;
+        for (const TaskDesc& td : tasks) ph.has_split = ph.has_split || td.split != 0;
+        ph.dev_off = H.push(st.jobs.data(), st.jobs.size() * sizeof(GemmJob), 64);
+        ph.njobs = (int)st.jobs.size();
+        ph.tiles_off = H.push(tasks.data(), tasks.size() * sizeof(TaskDesc), 64);
+        ph.total = (int64_t)tasks.size();
+        ph.max_tiles = ph.total;
+        for (size_t j = 0; j < st.jobs.size(); ++j)
+          fixes.push_back({ph.dev_off + j * sizeof(GemmJob), st.tmi[j][0], st.tmi[j][1], st.tmi[j][2], st.tmi[j][3],
+                           st.tmi[j][4]});
+        P.phases.push_back(ph);
+      } else if (st.kind == PHK_SPLIT) {
+        Phase ph{PH_SPLIT};
+        ph.dev_off = H.push(st.sj.data(), st.sj.size() * sizeof(SplitJob), 64);
+        ph.njobs = (int)st.sj.size();
+        ph.total_rows = st.rows;
+        P.phases.push_back(ph);
+      } else {
+        Phase ph{PH_PRECOND};
+        ph.dev_off = H.push(st.pj.data(), st.pj.size() * sizeof(PrecondJob), 64);
+        ph.njobs = (int)st.pj.size();
+        ph.total = st.items;
+        ph.total_rows = st.rows;
+        ph.vec8 = st.vec8;
+        ph.lane_rows = true;
+        for (const PrecondJob& pj : st.pj)
+          ph.lane_rows = ph.lane_rows && pj.precond == 2 && pj.part != nullptr && pj.part_ld <= kSeqPartials;
+        P.phases.push_back(ph);
       }
-      Phase ph{PH_FUSED};
-      ph.jobs_off = H.push(alljobs.data(), alljobs.size() * sizeof(GemmJob), 64);
-      for (size_t j = 0; j < alljobs.size(); ++j)
-        fixes.push_back({ph.jobs_off + j * sizeof(GemmJob), alltmi[j][0], alltmi[j][1], alltmi[j][2], alltmi[j][3],
-                         alltmi[j][4]});
-      ph.tiles_off = H.push(tasks.data(), tasks.size() * sizeof(TaskDesc), 64);
-      ph.total = (int64_t)tasks.size();
-      ph.pjobs_off = pjs.empty() ? 0 : H.push(pjs.data(), pjs.size() * sizeof(PrecondJob), 64);
-      ph.has_pjobs = !pjs.empty();
-      ph.nslots = (int)count.size();
-      std::vector<unsigned> zeros(count.size() + 1, 0u);  // done counters (+1 exit counter)
-      ph.done_off = H.push(zeros.data(), zeros.size() * sizeof(unsigned), 64);
-      ph.max_tiles = max_tiles;
-      P.phases.push_back(ph);
     }
   }
 
@@ -922,18 +833,8 @@ static ns_status enqueue_plan(Plan& P, DevCtx* dc, cudaStream_t stream) {
       case PH_GEMM: {
         ProfScope ps(ph.gemm_kind, stream);
         CU_TRY(launch_umma_gemm(reinterpret_cast<const GemmJob*>(dbase + ph.dev_off),
-                                reinterpret_cast<const TaskDesc*>(dbase + ph.tiles_off), ph.total, nullptr, nullptr,
-                                0, ph.max_tiles, P.cg, dc->sms, dc->flags, ph.has_split, P.bn, stream));
-        ++g_launches;
-        break;
-      }
-      case PH_FUSED: {
-        ProfScope ps(6, stream);
-        CU_TRY(launch_umma_gemm(reinterpret_cast<const GemmJob*>(dbase + ph.jobs_off),
-                                reinterpret_cast<const TaskDesc*>(dbase + ph.tiles_off), ph.total,
-                                ph.has_pjobs ? reinterpret_cast<const PrecondJob*>(dbase + ph.pjobs_off) : nullptr,
-                                reinterpret_cast<unsigned*>(dbase + ph.done_off), ph.nslots, ph.max_tiles, P.cg,
-                                dc->sms, dc->flags, false, P.bn, stream));
+                                reinterpret_cast<const TaskDesc*>(dbase + ph.tiles_off), ph.total, ph.max_tiles, P.cg,
+                                dc->sms, dc->flags, ph.has_split, P.bn, stream));
         ++g_launches;
         break;
       }
@@ -1129,7 +1030,7 @@ static ns_status run_plan(const std::vector<Mat>& mats_in, int iters, const floa
   // plan key
   std::vector<uint64_t> key;
   key.reserve(mats_in.size() * 4 + 8 + 3 * iters);
-  const int cg = (g_path == 2) ? 1 : (g_path == 6 ? 4 : 2);
+  const int cg = (g_path == 2) ? 1 : 2;
   key.push_back((uint64_t)dev); key.push_back((uint64_t)dtype); key.push_back(simt ? 1 : 0);
   key.push_back(cast ? 1 : 0);
   key.push_back((uint64_t)cg);
@@ -1257,6 +1158,7 @@ ns_status nsx_epilogue_counters(uint64_t* out8, int reset) {
 
 int ns_set_path(int path) {
   std::lock_guard<std::mutex> lk(g_mu);
+  if (path != 0 && path != 1 && path != 2 && path != 4 && path != 5) return -1;
   int old = g_path;
   g_path = path;
   return old;
@@ -1539,7 +1441,7 @@ static ns_status one_gemm(GemmJob J, TDesc ta, TDesc tb, TDesc tout, TDesc taux,
     std::vector<TaskDesc> tasks(tl.size());
     for (size_t i = 0; i < tl.size(); ++i) {
       std::memset(&tasks[i], 0, sizeof(TaskDesc));
-      tasks[i].tile = tl[i]; tasks[i].kind = TK_TILE; tasks[i].dep_slot = kNoSlot; tasks[i].my_slot = kNoSlot;
+      tasks[i].tile = tl[i]; tasks[i].kind = TK_TILE;
     }
     const size_t jo = tm.size() * sizeof(CUtensorMap), to = jo + align_up(sizeof(GemmJob), 64);
     const size_t bytes = to + tasks.size() * sizeof(TaskDesc);
@@ -1555,8 +1457,8 @@ static ns_status one_gemm(GemmJob J, TDesc ta, TDesc tb, TDesc tout, TDesc taux,
     std::memcpy(h.data() + to, tasks.data(), tasks.size() * sizeof(TaskDesc));
     CU_TRY(cudaMemcpy(dmem, h.data(), bytes, cudaMemcpyHostToDevice));
     cudaError_t e = launch_umma_gemm(reinterpret_cast<const GemmJob*>(d + jo), reinterpret_cast<const TaskDesc*>(d + to),
-                                     (int64_t)tasks.size(), nullptr, nullptr, 0, (int64_t)tasks.size(), cg, dc->sms,
-                                     dc->flags, false, 256, stream);
+                                     (int64_t)tasks.size(), (int64_t)tasks.size(), cg, dc->sms, dc->flags, false, 256,
+                                     stream);
     ++g_launches;
     cudaError_t e2 = cudaStreamSynchronize(stream);
     cudaFree(dmem);

@@ -130,29 +130,13 @@ struct MuonJob {
   float scale;     // max(1, m/n)^(1/2)
 };
 
-// One unit of work of a launch (umma_gemm_kernel).  A per-step launch is a list of
-// TK_TILE tasks without dependencies.  The fused single launch (ns_set_path(3)) carries all
-// 3T+1 steps of every matrix as one list in topological order: each task waits until its
-// matrix's previous step is complete (device counter `done[dep_slot] >= dep_target`) and,
-// once its outputs are visible, arrives on `done[my_slot]` (one arrival per epilogue warp
-// of the CTA pair).  Matrices therefore pipeline through the steps independently, with no
-// grid-wide barrier.
-constexpr uint32_t kNoSlot = 0xFFFFFFFFu;
-enum TaskKind : uint32_t { TK_TILE = 0, TK_PRE_S = 1, TK_PRE_SCALE = 2, TK_NONE = 3 };  // NONE: schedule padding
-constexpr int kPreRows = 64;  // rows of one preconditioner task
+// One unit of work of a per-step launch (umma_gemm_kernel): a tile, or padding of the
+// balanced per-worker task lists (api.cu balance_tasks).
+enum TaskKind : uint32_t { TK_TILE = 0, TK_NONE = 3 };
 enum StepKind : int32_t { PHK_GEMM = 0, PHK_PRE_S = 1, PHK_SPLIT = 2 };  // host-side step kinds (api.cu)
-// Bit 62 of a tile word: "shadow" tile -- computed (its operand loads feed the other pair of
-// a multicast cluster) but never stored.
-constexpr uint64_t kTileShadow = 1ull << 62;
 struct TaskDesc {
   uint64_t tile;        // TK_TILE: pack_tile(job, p0, q0, mirror)
-  uint64_t tile2;       // multicast clusters (2 CTA pairs): the second pair's tile, same job/p0/K
   uint32_t kind;        // TaskKind
-  uint32_t dep_slot;    // kNoSlot: no dependency
-  uint32_t dep_target;  // arrivals that complete the dependency
-  uint32_t my_slot;     // kNoSlot: no arrival
-  uint32_t pjob;        // TK_PRE_*: matrix index into the launch's PrecondJob array
-  uint32_t row0;        // TK_PRE_*: first row of the chunk
   uint32_t kb0, nkb;    // TK_TILE: k-blocks [kb0, kb0 + nkb) of the contraction (nkb = 0: all)
   uint32_t split;       // TK_TILE: 0, or 1 + index of this k-range's fp32 partial (split-K)
 };

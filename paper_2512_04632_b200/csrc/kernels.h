@@ -10,23 +10,17 @@
 namespace tns {
 
 // tcgen05 bf16 engine (umma_gemm.cu).  One persistent launch over all jobs' tiles.
-// cg = 1: 128 x 256 tiles per CTA; cg = 2: 256 x 256 tiles per CTA pair (cta_group::2);
-// cg = 4: two such pairs per 4-CTA cluster sharing the A operand by TMA multicast.
-// d_tasks: the launch's task list (TaskDesc) in execution order.  Per-step launches:
-// TK_TILE tasks without dependencies, d_pjobs = d_done = nullptr, nslots = 0.  Fused
-// launches: all steps, d_done = nslots + 1 zero-initialised counters (self-resetting).
-// max_tiles = largest GEMM step (grid sizing of per-step launches).  split: the task list
-// holds split-K tasks (TaskDesc::split != 0; cg 1 or 2 only).  bn: tile width 256, or 128
-// (cg = 2 only) -- the tile list must have been built with the same bn.
-cudaError_t launch_umma_gemm(const GemmJob* d_jobs, const TaskDesc* d_tasks, int64_t ntasks, const PrecondJob* d_pjobs,
-                             unsigned* d_done, int nslots, int64_t max_tiles, int cg, int num_sms, uint32_t* d_flags,
-                             bool split, int bn, cudaStream_t stream);
+// cg = 1: 128 x 256 tiles per CTA; cg = 2: 256 x 256 tiles per CTA pair (cta_group::2).
+// d_tasks: the launch's task list (TaskDesc, TK_TILE or TK_NONE padding) in execution
+// order; max_tiles = tiles of the step (grid sizing).  split: the task list holds split-K
+// tasks (TaskDesc::split != 0).  bn: tile width 256, or 128 (cg = 2 only) -- the tile list
+// must have been built with the same bn.
+cudaError_t launch_umma_gemm(const GemmJob* d_jobs, const TaskDesc* d_tasks, int64_t ntasks, int64_t max_tiles,
+                             int cg, int num_sms, uint32_t* d_flags, bool split, int bn, cudaStream_t stream);
 // Read (and optionally reset) the epilogue clock counters (TNS_DBG bit 8 measurement).
 cudaError_t umma_epi_prof(unsigned long long* out, bool reset);
 // Append the tiles of job `job` (host side), bn = tile width (256 or 128).
 void umma_tile_list(const GemmJob& J, uint32_t job, int cg, int bn, std::vector<uint64_t>& out);
-// cg = 4 (two CTA pairs per cluster, A multicast): the job's tiles as pairs sharing p0.
-void umma_pair_list(const GemmJob& J, uint32_t job, std::vector<std::pair<uint64_t, uint64_t>>& out);
 
 // CUDA-core engine (simt.cu); is_bf16 selects the storage type.
 cudaError_t launch_simt_gemm(const SimtJob* d_jobs, int njobs, int64_t total_tiles, int num_sms,
@@ -36,7 +30,7 @@ cudaError_t launch_simt_gemm(const SimtJob* d_jobs, int njobs, int64_t total_til
 // barrier, then A <- diag(s) A diag(s).  `barrier` points at two zero-initialised uint32
 // words (arrival count, generation) owned by the caller; the barrier resets itself.  vec8 = all N are multiples of 8 (16-byte vectors).
 // lane_rows: AOL from Gram partials with part_ld <= kSeqPartials for every job -> phase 1
-// runs one lane per row (precond_rows.cuh, same summation order as the fused mode).
+// runs one lane per row (precond_rows.cuh).
 cudaError_t launch_precondition(const PrecondJob* d_jobs, int njobs, int64_t total_rows,
                                 int64_t total_elems_or_vecs, bool vec8, bool is_bf16,
                                 unsigned* d_barrier, uint32_t* d_flags, bool lane_rows, cudaStream_t stream);

@@ -113,18 +113,6 @@ __device__ __forceinline__ void tma_load_2d_cg2(void* smem_dst, const void* tmap
       : "memory");
 }
 
-// As above, multicast to the CTAs in `mask` (same smem offset in each); every destination
-// CTA's bytes are counted on the leader mbarrier of that CTA's own pair.
-__device__ __forceinline__ void tma_load_2d_cg2_mc(void* smem_dst, const void* tmap, uint64_t* bar,
-                                                   int32_t c0, int32_t c1, uint16_t mask) {
-  const uint32_t bar_leader = smem_u32(bar) & 0xFEFFFFFFu;
-  asm volatile(
-      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
-      ".multicast::cluster [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(smem_dst)),
-      "l"(tmap), "r"(c0), "r"(c1), "r"(bar_leader), "h"(mask)
-      : "memory");
-}
-
 // ----------------------------------------------------------------------------- PDL
 // Programmatic dependent launch: wait until the preceding grid in the stream has completed
 // (and its writes are visible); allow the next grid to be scheduled early.
@@ -223,13 +211,6 @@ __device__ __forceinline__ void umma_commit(uint64_t* bar) {
         "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
         " [%0], %1;" ::"r"(smem_u32(bar)), "h"((uint16_t)0x3)
         : "memory");
-}
-// cta_group::2 commit arriving on the barrier at the same offset in every CTA of `mask`.
-__device__ __forceinline__ void umma_commit_mask(uint64_t* bar, uint16_t mask) {
-  asm volatile(
-      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
-      " [%0], %1;" ::"r"(smem_u32(bar)), "h"(mask)
-      : "memory");
 }
 // 32 lanes x 32 bit, 32 repetitions along columns: thread i gets columns [c, c+32) of
 // TMEM lane (lane_base + i).

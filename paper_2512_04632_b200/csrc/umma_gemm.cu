@@ -38,7 +38,6 @@
 
 #include "jobs.h"
 #include "kernels.h"
-#include "precond_rows.cuh"
 #include "ptx.cuh"
 
 namespace tns {
@@ -82,23 +81,6 @@ struct Geo {
   static constexpr int kEpiBytes = kNumEpiWarps * 6 * 2048;
   static constexpr size_t kSmemBytes = (size_t)kEpiOff + kEpiBytes + 1024 + 512;
 };
-
-// Fused mode: spin until `target` arrivals were counted on a dependency slot, then order
-// later async-proxy (TMA) reads after it.
-__device__ __forceinline__ void wait_phase(const unsigned* cnt, unsigned target) {
-  while (true) {
-    unsigned v;
-    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(cnt) : "memory");
-    if (v >= target) break;
-    __nanosleep(64);
-  }
-  asm volatile("fence.proxy.async.global;" ::: "memory");
-}
-__device__ __forceinline__ void arrive_phase(unsigned* cnt) {
-  asm volatile("fence.proxy.async.global;" ::: "memory");
-  __threadfence();
-  atomicAdd(cnt, 1u);
-}
 
 // Measurement counters (TNS_DBG bit 8): per-epilogue-warp clock64 deltas summed over tiles.
 __device__ unsigned long long g_epi_prof[8];
@@ -269,16 +251,12 @@ __device__ __forceinline__ void epi_math(int var, const Epi& E, int p, int q, co
   bad |= (nf & 0x80008000u) != 0;
 }
 
-// MC = CTA pairs per cluster (CG == 2 only): with MC == 2 the two pairs of a 4-CTA cluster
-// run tiles that share their A operand rows (same job, p0 and K) and each A box is loaded
-// once and multicast to both pairs: 25% fewer L2->SM bytes per MMA.
 // SPLIT: the launch carries split-K tasks (k-ranges with fp32 partial stores, TaskDesc
 // kb0/nkb/split); a separate instantiation so that the other launches keep the register
 // allocation of the plain kernel.
-template <int CG, int MC, bool SPLIT, int BN>
+template <int CG, bool SPLIT, int BN>
 __global__ void __launch_bounds__(kThreads, 1)
     umma_gemm_kernel(const GemmJob* __restrict__ jobs, const TaskDesc* __restrict__ tasks, int64_t ntasks,
-                     const PrecondJob* __restrict__ pjobs, unsigned* done, int nslots,
                      uint32_t* __restrict__ flags, int dbg) {
   using G = Geo<CG, BN>;
   extern __shared__ uint8_t smem_raw[];
@@ -297,19 +275,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   const bool tl = kMeasure && (dbg & 16) && blockIdx.x == 0 && lane == 0;
   const long long T0 = tl ? clock64() : 0;
 #define TL(slot) do { if (tl) atomicAdd(&g_epi_prof[slot], (unsigned long long)(clock64() - T0)); } while (0)
-  const uint32_t crank = (CG == 2) ? cluster_ctarank() : 0u;  // CTA rank within the cluster
-  const uint32_t rank = crank & 1u;                            // CTA rank within the pair
-  const uint32_t pair_id = crank >> 1;                         // pair within the cluster (MC == 2)
-  const uint32_t lead = crank & ~1u;                           // cluster rank of this pair's leader
-  const int64_t cid = blockIdx.x / (CG * MC);                  // cluster (tile worker) index
-  const int64_t ncl = gridDim.x / (CG * MC);
-  // MC == 2: this pair's tile of a task
-  auto my_tile = [&](const TaskDesc& TD) -> uint64_t { return (MC == 2 && pair_id) ? TD.tile2 : TD.tile; };
+  const uint32_t rank = (CG == 2) ? cluster_ctarank() : 0u;  // CTA rank within the pair
+  const int64_t cid = blockIdx.x / CG;                         // CTA pair (tile worker) index
+  const int64_t ncl = gridDim.x / CG;
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < G::kStages; ++i) {
       mbar_init(&full_bar[i], 1);
-      mbar_init(&empty_bar[i], MC);  // one commit per pair that reads the stage
+      mbar_init(&empty_bar[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull_bar[i], 1);
@@ -343,7 +316,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int64_t t = cid; t < ntasks; t += ncl) {
         const TaskDesc TD = tasks[t];
         if (TD.kind != TK_TILE) continue;
-        const TileInfo ti = decode_word<BN>(my_tile(TD));
+        const TileInfo ti = decode_word<BN>(TD.tile);
         const GemmJob* J = jobs + ti.job;
         const void* tmA = J->tmA;
         const void* tmB = J->tmB;
@@ -360,7 +333,6 @@ __global__ void __launch_bounds__(kThreads, 1)
           waited = true;
           TL(1);  // dependency resolved
         }
-        if (TD.dep_slot != kNoSlot) wait_phase(done + TD.dep_slot, TD.dep_target);
         const int pa = ti.p0 + (int)rank * G::kARows;  // this CTA's A rows
         const int qb = ti.q0 + (int)rank * G::kBRows;  // this CTA's B rows
         const int kbeg = SPLIT ? (int)TD.kb0 : 0;
@@ -374,20 +346,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           // half-storage symmetric operand: an upper-triangle block is read transposed
           const int a_e = a_mn ^ (a_sym && (k0 >> 8) > (pa >> 8));
           const int b_e = b_mn ^ (b_sym && (k0 >> 8) > (qb >> 8));
-          if constexpr (MC == 2) {
-            // A rows are the same in both pairs: this CTA loads box `pair_id` of its 128 rows
-            // for itself and its counterpart in the other pair
-            const int i = (int)pair_id;
-            const int c0 = a_e ? pa + 64 * i : k0, c1 = a_e ? k0 : pa + 64 * i;
-            tma_load_2d_cg2_mc(sa + i * kBoxBytes, tmA, &full_bar[stage], c0, c1,
-                               (uint16_t)((1u << crank) | (1u << (crank ^ 2u))));
-          } else {
 #pragma unroll
-            for (int i = 0; i < G::kARows / 64; ++i) {
-              const int c0 = a_e ? pa + 64 * i : k0, c1 = a_e ? k0 : pa + 64 * i;
-              if constexpr (CG == 2) tma_load_2d_cg2(sa + i * kBoxBytes, tmA, &full_bar[stage], c0, c1);
-              else tma_load_2d(sa + i * kBoxBytes, tmA, &full_bar[stage], c0, c1);
-            }
+          for (int i = 0; i < G::kARows / 64; ++i) {
+            const int c0 = a_e ? pa + 64 * i : k0, c1 = a_e ? k0 : pa + 64 * i;
+            if constexpr (CG == 2) tma_load_2d_cg2(sa + i * kBoxBytes, tmA, &full_bar[stage], c0, c1);
+            else tma_load_2d(sa + i * kBoxBytes, tmA, &full_bar[stage], c0, c1);
           }
 #pragma unroll
           for (int i = 0; i < G::kBRows / 64; ++i) {
@@ -413,7 +376,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int64_t t = cid; t < ntasks; t += ncl) {
         const TaskDesc TD = tasks[t];
         if (TD.kind != TK_TILE) continue;
-        const TileInfo ti = decode_word<BN>(my_tile(TD));
+        const TileInfo ti = decode_word<BN>(TD.tile);
         const GemmJob* J = jobs + ti.job;
         const uint32_t a_mn = (uint32_t)J->a_mn, b_mn = (uint32_t)J->b_mn;
         const int K = J->K;
@@ -459,12 +422,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint64_t bdesc = make_sdesc(sb + kk * b_step, b_lbo, 1024u);
             umma_bf16<CG>(d_tmem, adesc, bdesc, idesc, (kb != kbeg || kk != 0) ? 1u : 0u);
           }
-          if constexpr (MC == 2) umma_commit_mask(&empty_bar[stage], 0xF);  // both pairs' producers
-          else umma_commit<CG>(&empty_bar[stage]);
+          umma_commit<CG>(&empty_bar[stage]);
           if (++stage == G::kStages) { stage = 0; phase ^= 1; }
         }
-        if constexpr (MC == 2) umma_commit_mask(&tfull_bar[as], (uint16_t)(0x3u << lead));
-        else umma_commit<CG>(&tfull_bar[as]);
+        umma_commit<CG>(&tfull_bar[as]);
         if (++as == 2) { as = 0; aphase ^= 1; }
       }
     }
@@ -484,38 +445,18 @@ __global__ void __launch_bounds__(kThreads, 1)
     // measurement counters (TNS_DBG bit 8): accumulated straight into g_epi_prof so that no
     // register array stays live in production
 #define EPC(i, v) atomicAdd(&g_epi_prof[i], (unsigned long long)(v))
-    uint32_t pfl = 0;
     bool waited = false;
     for (int64_t t = cid; t < ntasks; t += ncl) {
       const TaskDesc TD = tasks[t];
-      if (!waited) {  // aux, outputs, counters and preconditioner rows: after the previous launch
+      if (!waited) {  // aux and outputs: after the previous launch
         pdl_wait();
         waited = true;
       }
-      if (TD.dep_slot != kNoSlot) {  // the aux prefetch / preconditioner rows read that step
-        if (lane == 0) wait_phase(done + TD.dep_slot, TD.dep_target);
-        __syncwarp();
-      }
       if (TD.kind == TK_NONE) continue;  // schedule padding (balanced per-step task lists)
-      if (TD.kind != TK_TILE) {
-        // preconditioner rows (fused mode): the pair's 8*CG epilogue warps share the chunk
-        const PrecondJob& PJ = pjobs[TD.pjob];
-        const int w = (int)rank * kNumEpiWarps + ew;
-        const int end = min((int)TD.row0 + kPreRows, PJ.N);
-        for (int i = (int)TD.row0 + w; i < end; i += kNumEpiWarps * CG) {
-          if (TD.kind == TK_PRE_S) precond_row_s<uint16_t, true>(PJ, i, lane, pfl);
-          else precond_row_scale<uint16_t, true>(PJ, i, lane);
-        }
-        __syncwarp();
-        if (lane == 0 && TD.my_slot != kNoSlot) arrive_phase(done + TD.my_slot);
-        continue;
-      }
-      const uint64_t tw = my_tile(TD);
-      const bool shadow = (tw & kTileShadow) != 0;  // computed for the multicast, never stored
-      const TileInfo ti = decode_word<BN>(tw);
+      const TileInfo ti = decode_word<BN>(TD.tile);
       const Epi E = load_epi(jobs + ti.job);
       const int var = epi_variant(E);
-      const bool has_aux = epi_needs_aux(E) && !(dbg & 4) && !shadow;
+      const bool has_aux = epi_needs_aux(E) && !(dbg & 4);
       const int prow = ti.p0 + (int)rank * kBM + quad * 32;  // first of this warp's 32 rows
       const int p = prow + lane;
       const int qh = ti.q0 + half * (BN / 2);
@@ -562,7 +503,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           tc_fence_before();
           __syncwarp();
           if (lane == 0) {
-            if constexpr (CG == 2) mbar_arrive_cluster(&tempty_bar[as], lead);
+            if constexpr (CG == 2) mbar_arrive_cluster(&tempty_bar[as], 0);
             else mbar_arrive_relaxed(&tempty_bar[as]);
           }
         }
@@ -574,7 +515,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             tma_load_2d(s_aux + 2048 * xb, E.tmAux, abar + xb, q + 64, prow);
           }
         }
-        if (SPLIT && TD.split && !shadow) {  // split-K: this k-range's fp32 partial, no epilogue math
+        if (SPLIT && TD.split) {  // split-K: this k-range's fp32 partial, no epilogue math
           float4* dst = reinterpret_cast<float4*>(E.split_ws + (int64_t)(TD.split - 1) * E.split_stride +
                                                   (int64_t)p * E.split_ld + q);
 #pragma unroll
@@ -583,7 +524,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                                  __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3]));
           continue;
         }
-        if ((dbg & 1) || shadow) continue;
+        if (dbg & 1) continue;
         // mirrored block: transposed box in smem for the mirrored store (full storage) and/or
         // the AOL column sums (iteration-1 Gram); half storage skips the store
         const bool mir_store = ti.mirror && !E.half && !(dbg & 2);
@@ -647,20 +588,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         if (prof) { t1 = clock64(); EPC(6, t1 - t0); t0 = t1; }
       }
-      if (E.part != nullptr && p < E.P && !shadow) {
+      if (E.part != nullptr && p < E.P) {
         if (qh < E.Q) E.part[(int64_t)p * E.part_ld + qh / 64] = rsum;
         if (G::kChunks > 2 && qh + 64 < E.Q) E.part[(int64_t)p * E.part_ld + qh / 64 + 1] = rsum1;
       }
       if (++as == 2) { as = 0; aphase ^= 1; }
-      if (TD.my_slot != kNoSlot) {  // fused mode: this warp's part of the tile is visible
-        __syncwarp();
-        if (lane == 0) {
-          bulk_wait<0>();
-          arrive_phase(done + TD.my_slot);
-        }
-      }
     }
-    if (pfl && lane == 0) atomicOr(flags, pfl);
     if (lane == 0) bulk_wait<0>();
     if (ew == 0) TL(5);  // epilogue stores complete
 #undef EPC
@@ -676,33 +609,22 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (tl) atomicAdd(&g_epi_prof[7], 1ull);
   }
 #undef TL
-  if (nslots > 0 && threadIdx.x == 0) {  // fused mode: the last CTA out resets the counters
-    pdl_wait();  // (a CTA without tile tasks has not waited yet)
-    __threadfence();
-    if (atomicAdd(done + nslots, 1u) == gridDim.x - 1) {
-      for (int k = 0; k <= nslots; ++k) done[k] = 0;
-      __threadfence();
-    }
-  }
 }
 
-template <int CG, int MC, bool SPLIT, int BN>
-static cudaError_t launch_cg(const GemmJob* d_jobs, const TaskDesc* d_tasks, int64_t ntasks, const PrecondJob* d_pjobs,
-                             unsigned* d_done, int nslots, int64_t max_tiles, int num_sms, uint32_t* d_flags,
-                             cudaStream_t stream) {
+template <int CG, bool SPLIT, int BN>
+static cudaError_t launch_cg(const GemmJob* d_jobs, const TaskDesc* d_tasks, int64_t ntasks, int64_t max_tiles,
+                             int num_sms, uint32_t* d_flags, cudaStream_t stream) {
   static bool attr_set[64] = {};
-  static int max_clusters[64] = {};
   int dev = 0;
   cudaGetDevice(&dev);
-  auto kern = umma_gemm_kernel<CG, MC, SPLIT, BN>;
-  constexpr int kCl = CG * MC;
+  auto kern = umma_gemm_kernel<CG, SPLIT, BN>;
   cudaLaunchConfig_t cfg = {};
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = Geo<CG, BN>::kSmemBytes;
   cfg.stream = stream;
   cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = kCl;
+  attr[0].val.clusterDim.x = CG;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -713,48 +635,30 @@ static cudaError_t launch_cg(const GemmJob* d_jobs, const TaskDesc* d_tasks, int
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)Geo<CG, BN>::kSmemBytes);
     if (e != cudaSuccess) return e;
-    if (CG == 2) {
-      e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-      if (e != cudaSuccess) return e;
-    }
-    // persistent grid: as many clusters as can be co-resident (4-CTA clusters cannot use
-    // every SM of a GPC whose SM count is not a multiple of 4)
-    int nc = 0;
-    cfg.gridDim = dim3((unsigned)(num_sms / kCl * kCl));
-    if (cudaOccupancyMaxActiveClusters(&nc, kern, &cfg) != cudaSuccess || nc <= 0) {
-      cudaGetLastError();
-      nc = num_sms / kCl;
-    }
-    max_clusters[dev & 63] = nc < num_sms / kCl ? nc : num_sms / kCl;
-    if (getenv("TNS_VERBOSE")) fprintf(stderr, "umma_gemm<%d,%d>: %d co-resident clusters of %d CTAs\n", CG, MC, nc, kCl);
     attr_set[dev & 63] = true;
   }
-  // persistent: one CTA (pair) per SM (pair); the fused mode uses every SM (its dependency
-  // waits need all CTAs co-resident, which one CTA per SM guarantees)
-  const int64_t workers = MC == 1 ? num_sms / CG : max_clusters[dev & 63];
-  const int64_t nclusters = (nslots > 0 || max_tiles > workers) ? workers : max_tiles;
-  cfg.gridDim = dim3((unsigned)(nclusters * kCl));
+  // persistent: one CTA (pair) per SM (pair), or one per tile when there are fewer tiles
+  const int64_t workers = num_sms / CG;
+  const int64_t nclusters = max_tiles > workers ? workers : max_tiles;
+  cfg.gridDim = dim3((unsigned)(nclusters * CG));
   static int dbg = -1;
   if (dbg < 0) {  // measurement knob (never set in production): TNS_DBG bits 1 skip epilogue,
     const char* e = getenv("TNS_DBG");  // 2 skip mirrored stores, 4 skip aux prefetch, 8 counters, 16 timeline
     dbg = e ? atoi(e) : 0;
   }
-  return cudaLaunchKernelEx(&cfg, kern, d_jobs, d_tasks, ntasks, d_pjobs, d_done, nslots, d_flags, dbg);
+  return cudaLaunchKernelEx(&cfg, kern, d_jobs, d_tasks, ntasks, d_flags, dbg);
 }
 
-cudaError_t launch_umma_gemm(const GemmJob* d_jobs, const TaskDesc* d_tasks, int64_t ntasks, const PrecondJob* d_pjobs,
-                             unsigned* d_done, int nslots, int64_t max_tiles, int cg, int num_sms, uint32_t* d_flags,
-                             bool split, int bn, cudaStream_t stream) {
+cudaError_t launch_umma_gemm(const GemmJob* d_jobs, const TaskDesc* d_tasks, int64_t ntasks, int64_t max_tiles,
+                             int cg, int num_sms, uint32_t* d_flags, bool split, int bn, cudaStream_t stream) {
   if (ntasks <= 0) return cudaSuccess;
-#define TNS_LAUNCH(CG_, MC_, SP_, BN_) \
-  launch_cg<CG_, MC_, SP_, BN_>(d_jobs, d_tasks, ntasks, d_pjobs, d_done, nslots, max_tiles, num_sms, d_flags, stream)
-  if (cg == 4)  // two CTA pairs per cluster, A operand multicast (tasks carry tile pairs)
-    return TNS_LAUNCH(2, 2, false, 256);
+#define TNS_LAUNCH(CG_, SP_, BN_) \
+  launch_cg<CG_, SP_, BN_>(d_jobs, d_tasks, ntasks, max_tiles, num_sms, d_flags, stream)
   if (cg == 2) {
-    if (bn == 128) return split ? TNS_LAUNCH(2, 1, true, 128) : TNS_LAUNCH(2, 1, false, 128);
-    return split ? TNS_LAUNCH(2, 1, true, 256) : TNS_LAUNCH(2, 1, false, 256);
+    if (bn == 128) return split ? TNS_LAUNCH(2, true, 128) : TNS_LAUNCH(2, false, 128);
+    return split ? TNS_LAUNCH(2, true, 256) : TNS_LAUNCH(2, false, 256);
   }
-  return split ? TNS_LAUNCH(1, 1, true, 256) : TNS_LAUNCH(1, 1, false, 256);
+  return split ? TNS_LAUNCH(1, true, 256) : TNS_LAUNCH(1, false, 256);
 #undef TNS_LAUNCH
 }
 
@@ -788,33 +692,6 @@ void umma_tile_list(const GemmJob& J, uint32_t job, int cg, int bn, std::vector<
     const int gsz = tp - g0 < kGroupP ? tp - g0 : kGroupP;
     for (int qb = 0; qb < tq; ++qb)
       for (int i = 0; i < gsz; ++i) out.push_back(pack_tile(job, (g0 + i) * tm, qb * bn, false, bn));
-  }
-}
-
-// Tiles of job `job` as multicast pairs sharing p0 (A operand rows): (p, q) with the next
-// q of the same p in the same order as umma_tile_list; an odd one out gets a shadow partner.
-void umma_pair_list(const GemmJob& J, uint32_t job, std::vector<std::pair<uint64_t, uint64_t>>& out) {
-  auto emit = [&](uint64_t a, bool has_b, uint64_t b) { out.push_back({a, has_b ? b : (a | kTileShadow)}); };
-  if (J.sym) {
-    const int nb = (J.P + kSymBlock - 1) / kSymBlock;
-    for (int bi = 0; bi < nb; ++bi)
-      for (int bj = 0; bj <= bi; bj += 2) {
-        const bool two = bj + 1 <= bi;
-        emit(pack_tile(job, bi * kSymBlock, bj * kSymBlock, bi != bj), two,
-             two ? pack_tile(job, bi * kSymBlock, (bj + 1) * kSymBlock, bi != bj + 1) : 0);
-      }
-    return;
-  }
-  const int tm = kBM * 2;
-  const int tp = (J.P + tm - 1) / tm, tq = (J.Q + kBN - 1) / kBN;
-  for (int g0 = 0; g0 < tp; g0 += kGroupP) {
-    const int gsz = tp - g0 < kGroupP ? tp - g0 : kGroupP;
-    for (int qb = 0; qb < tq; qb += 2)
-      for (int i = 0; i < gsz; ++i) {
-        const bool two = qb + 1 < tq;
-        emit(pack_tile(job, (g0 + i) * tm, qb * kBN, false), two,
-             two ? pack_tile(job, (g0 + i) * tm, (qb + 1) * kBN, false) : 0);
-      }
   }
 }
 
