@@ -264,3 +264,55 @@ def test_app_b_levy_turbo4_vs_muonplus5():
     q = O.polar_exact(x)
     assert (O.polar_error(O.turbo_muon(x, C.turbo(4)), q)
             < O.polar_error(O.muon_plus(x, C.muon_plus(5)), q))
+
+
+# ----------------------------------------------------------------- polar factor via the Gram
+@pytest.mark.parametrize("shape", [(5, 5), (9, 4), (4, 9), (300, 300), (700, 200)])
+def test_polar_exact_gram_equals_svd_route(shape):
+    """X (X^T X)^(-1/2) from LAPACK syevd == U V^T from LAPACK gesdd (two different library
+    routines for the same definition)."""
+    x = I.gaussian(*shape, seed=11, bf16=False).astype(np.float64)
+    np.testing.assert_allclose(O.polar_exact_gram(x), O.polar_exact(x), atol=1e-9)
+
+
+def test_polar_exact_gram_2x2_rotation():
+    """Closed form: the polar factor of a 2 x 2 matrix with positive determinant is the
+    rotation [[a+d, b-c], [c-b, a+d]] / sqrt((a+d)^2 + (c-b)^2)."""
+    a, b, c, d = 1.0, 1.0, 0.0, 1.0
+    r = np.hypot(a + d, c - b)
+    q = np.array([[a + d, b - c], [c - b, a + d]]) / r
+    np.testing.assert_allclose(O.polar_exact_gram(np.array([[a, b], [c, d]])), q, atol=1e-15)
+    with pytest.raises(ValueError):
+        O.polar_exact_gram(np.array([[1.0, 2.0], [2.0, 4.0]]))
+
+
+# ----------------------------------------------------------------- eps_bias (§6, P:L367-370)
+def test_bias_error_hand_computed_2x2():
+    """X = [[1, 1], [0, 1]]: A0 = X^T X = [[1, 1], [1, 2]], row sums of |A0| (2, 3), so
+    s = (2^-1/2, 3^-1/2) (Eq. 8) and X1 = X diag(s).  Both polar factors are rotations
+    (closed form above): Q = R(theta), theta = -atan(1/2); Q_aol = R(phi),
+    phi = -atan(3^-1/2 / (2^-1/2 + 3^-1/2)).  ||R(t) - R(p)||_F = 2 sqrt(2) |sin((t - p)/2)|,
+    so eps_bias = ||Q - Q_aol||_F / sqrt(2) = 2 |sin((theta - phi) / 2)| = 0.04122...
+    A wrong scaling (1/r instead of 1/sqrt(r), rows instead of columns, no |.|) or a wrong
+    normalisation (sqrt(n)) changes the value."""
+    x = np.array([[1.0, 1.0], [0.0, 1.0]])
+    theta = -np.arctan(0.5)
+    phi = -np.arctan((1 / np.sqrt(3)) / (1 / np.sqrt(2) + 1 / np.sqrt(3)))
+    want = 2 * abs(np.sin((theta - phi) / 2))
+    assert want == pytest.approx(0.0412152, abs=1e-6)
+    assert O.bias_error(x) == pytest.approx(want, rel=1e-12)
+
+
+def test_bias_error_exact_zero_cases():
+    """AOL changes nothing when s is constant: orthonormal columns (A0 = I, s = 1) and a
+    Gram with constant absolute row sums (s = c 1; a scalar does not move the polar
+    factor) -- eps_bias = 0 up to rounding; a generic matrix has eps_bias > 0."""
+    q = I.orthonormal(40, 12, seed=3)
+    assert O.bias_error(q) == pytest.approx(0.0, abs=1e-12)
+    # X = Q diag(d) with the columns of Q orthonormal: A0 = diag(d^2); constant row sums iff
+    # |d| constant -> take d = 3 (a multiple of an orthonormal frame)
+    assert O.bias_error(3.0 * q) == pytest.approx(0.0, abs=1e-12)
+    # circulant-like Gram with constant |row| sums: X^T X = [[2, 1], [1, 2]] (row sums 3, 3)
+    l = np.linalg.cholesky(np.array([[2.0, 1.0], [1.0, 2.0]]))
+    assert O.bias_error(l.T) == pytest.approx(0.0, abs=1e-12)
+    assert O.bias_error(I.gaussian(30, 10, seed=4, bf16=False).astype(np.float64)) > 1e-3
