@@ -47,6 +47,21 @@ def ns_flops(m: int, n: int, iters: int) -> int:
     return iters * (M * N * (N + 1) + N * N * (N + 1) + 2 * M * N * N)
 
 
+def precond_bytes(N: int) -> int:
+    """Bytes the AOL preconditioner launch moves for one N x N Gram: A0 is stored
+    as its lower-triangle 256-blocks (half storage), row i holding min(N, 256 (i // 256 + 1))
+    columns; the launch reads and rewrites exactly those (bf16), reads the Gram epilogue's
+    row-sum partials (fp32, the slots row i sums: its direct 64-column slots of blocks <= i's
+    and mirrored 32-row slots of blocks > i's) and writes s (fp32)."""
+    stored = sum(min(N, 256 * (i // 256 + 1)) for i in range(0, N, 256) for _ in range(min(256, N - i)))
+    n1, n2 = -(-N // 64), -(-N // 32)
+    parts = 0
+    for i in range(N):
+        bi = i // 256
+        parts += min(4 * (bi + 1), n1) + max(0, n2 - min(8 * (bi + 1), n2))
+    return 2 * 2 * stored + 4 * parts + 4 * N
+
+
 def kernel_units(shapes, iters):
     """Per-launch algorithmic work of each kernel kind over the given matrices (one launch
     covers all of them): FLOPs for the GEMMs, bytes for the preconditioner."""
@@ -56,7 +71,7 @@ def kernel_units(shapes, iters):
         g += M * N * (N + 1)
         p += N * N * (N + 1)
         u += 2 * M * N * N
-        pre += 4 * N * N + 4 * N  # read A0 + write A1 (bf16) + write s (fp32)
+        pre += precond_bytes(N)
     return {"gram": g, "poly": p, "update": u, "precondition": pre}
 
 
@@ -153,33 +168,52 @@ def make_inputs(shapes, config_id: int):
     return [I.gaussian(m, n, seed=I.matrix_seed(config_id, i)) for i, (m, n) in enumerate(shapes)]
 
 
-def oracle_sample_ms(shapes, iters, budget_s: float, precond="aol", start: int = 0):
-    """Time the fp64 oracle on whole matrices of the workload (one per distinct shape,
-    cycling) until `budget_s` is spent; extrapolate to the full set by FLOPs."""
+def workload_config(workload: str, shapes, iters: int) -> dict:
+    """The `config` object of both arms (identical, so the driver can pair them)."""
+    return {"workload": WORKLOAD if workload == "gpt2-medium" else workload, "matrices": len(shapes),
+            "iters": iters, "precond": "aol", "coeffs": f"Muon+ last {iters} (App. D)"}
+
+
+def oracle_sample(xs_np, shapes, iters, budget_s: float, picks):
+    """cpu_baseline leg: time the fp64 oracle on whole matrices of the workload -- the bench's
+    own seeded inputs, indices `picks` in order -- until `budget_s` is spent; extrapolate to
+    the full set by algorithmic FLOPs.  Returns (ms, done shapes, seconds, {index: output})."""
     from oracle import ns_oracle as O
-    coeffs = C.turbo(iters) if precond == "aol" else C.muon_plus(iters)
-    distinct = []
-    for s in shapes:
-        if s not in distinct:
-            distinct.append(s)
-    t_tot = 0.0
-    f_tot = 0
-    done = []
-    k = start
-    while True:
-        m, n = distinct[k % len(distinct)]
-        x = I.gaussian(m, n, seed=I.matrix_seed(99, k)).astype(np.float64)
+    coeffs = C.turbo(iters)
+    t_tot, f_tot, done, outs = 0.0, 0, [], {}
+    for i in picks:
+        m, n = shapes[i]
+        x = xs_np[i].astype(np.float64)
         t0 = time.perf_counter()
-        O.newton_schulz(x, coeffs, precond)
+        outs[i] = O.newton_schulz(x, coeffs, "aol")
         t_tot += time.perf_counter() - t0
         f_tot += ns_flops(m, n, iters)
         done.append(f"{m}x{n}")
-        k += 1
-        if t_tot >= budget_s or len(done) >= 64:
+        if t_tot >= budget_s:
             break
     total = sum(ns_flops(m, n, iters) for m, n in shapes)
-    ms = t_tot * 1e3 * total / f_tot
-    return ms, done, t_tot
+    return t_tot * 1e3 * total / f_tot, done, t_tot, outs
+
+
+def accuracy_rows(xs_np, gpu_out, oracle_out, with_polar: bool = True):
+    """SURVEY §5 metrics rows: per checked matrix relF(GPU, oracle) and the polar errors of
+    both against the exact polar factor U V^T, from the cpu_baseline leg's oracle
+    outputs; the worst of each over the sample."""
+    from oracle import ns_oracle as O
+    rel, ratio, eg_max = [], [], 0.0
+    for i, ref in oracle_out.items():
+        out = gpu_out[i]
+        rel.append(float(np.linalg.norm(out - ref) / np.linalg.norm(ref)))
+        if with_polar:
+            q = O.polar_exact(xs_np[i].astype(np.float64))
+            eg, eo = O.polar_error(out, q), O.polar_error(ref, q)
+            ratio.append(eg / eo)
+            eg_max = max(eg_max, eg)
+    row = {"checked": len(rel), "relF_max": round(max(rel), 6) if rel else None, "relF_gate": 2e-2}
+    if with_polar and ratio:
+        row.update({"polar_err_max": round(eg_max, 5), "polar_ratio_gpu_over_oracle_max": round(max(ratio), 4),
+                    "polar_ratio_gate": 1.05})
+    return row
 
 
 # ------------------------------------------------------------------------------ reference arm
@@ -195,25 +229,29 @@ def run_reference(args):
             threadpool_limits(limits=len(os.sched_getaffinity(0)), user_api="blas")
         except Exception:
             pass
+    from oracle import ns_oracle as O
     shapes = I.shape_set(args.workload)
+    xs = [x.astype(np.float64) for x in make_inputs(shapes, 5)]  # the own arm's inputs
+    coeffs = C.turbo(args.iters)
+    for w in range(args.warmup):  # warm-up: BLAS thread pool and allocator, one matrix each
+        O.newton_schulz(xs[w % len(xs)], coeffs, "aol")
     vals = []
-    for w in range(args.warmup):
-        oracle_sample_ms(shapes, args.iters, 0.0, start=w)
-    samples = []
-    for k in range(args.steps):
-        ms, done, secs = oracle_sample_ms(shapes, args.iters, 0.0, start=k)
-        vals.append(ms)
-        samples += done
+    for k in range(args.steps):  # every timed step: the WHOLE workload, all matrices
+        t0 = time.perf_counter()
+        for x in xs:
+            O.newton_schulz(x, coeffs, "aol")
+        vals.append((time.perf_counter() - t0) * 1e3)
     v = float(np.mean(vals))
     cores = blas_threads()
     line = {
         "impl": "reference", "metric": METRIC, "value": round(v, 3), "unit": "ms", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(v, 3), "higher_is_better": False,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": args.workload, "matrices": len(shapes), "iters": args.iters, "precond": "aol"},
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (the own arm's seeded inputs)",
+        "config": workload_config(args.workload, shapes, args.iters),
         "cpu_baseline": {"value": round(v, 3), "unit": "ms", "cores": cores, "kind": "oracle",
-                         "sample": f"one whole matrix per step ({', '.join(sorted(set(samples)))}), "
-                                   f"numpy fp64 + OpenBLAS, extrapolated to the {len(shapes)}-matrix set by algorithmic FLOPs"},
+                         "sample": f"every timed step is the whole {len(shapes)}-matrix workload (no extrapolation), "
+                                   f"numpy fp64 + OpenBLAS; warm-up steps one matrix each"},
         "e2e": {"value": round(v, 3), "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -272,9 +310,8 @@ def run_own(args):
 
     shapes = I.shape_set(args.workload)
     iters = args.iters
-    xs_np = make_inputs(shapes, 5)
+    xs_np = make_inputs(shapes, 5)  # kept on the host for the cpu_baseline leg's accuracy check
     xs = [torch.from_numpy(x).to(torch.bfloat16).to(dev) for x in xs_np]
-    del xs_np
     plan = make_plan(shapes, world, iters)
     mine = plan.mine(rank)
 
@@ -345,7 +382,7 @@ def run_own(args):
     torch.cuda.synchronize()
     e0.record()
     for _ in range(args.steps):
-        step()
+        res = step()
     e1.record()
     torch.cuda.synchronize()
     clocks = sampler.stop()
@@ -399,6 +436,10 @@ def run_own(args):
         roof["measured_in"] = (f"second pass of the same {args.steps} steps with CUDA events around every "
                                f"launch ({ms_prof:.3f} ms/step there vs {ms:.3f} ms/step in the headline region)")
 
+    # ---- the timed outputs (last step; the profiling pass rewrote the same values): all
+    #      finite, and a sample of them checked against the oracle in the cpu_baseline leg
+    finite = bool(all(bool(torch.isfinite(v).all()) for v in res))
+    flags = ns.read_flags()
     # ---- e2e through the public API with host buffers (pinned), copies inside the region
     e2e = run_e2e(args, xs, shapes, plan, mine, rank, world, dev, iters)
 
@@ -407,16 +448,16 @@ def run_own(args):
         "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": False,
         "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic (seeded Gaussian N(0,1) matrices, bf16-rounded, GPT-2-medium hidden-matrix shapes)",
-        "config": {"workload": WORKLOAD if args.workload == "gpt2-medium" else args.workload,
-                   "matrices": len(shapes), "iters": iters, "precond": "aol", "coeffs": "Muon+ last 4 (App. D)",
-                   "sharding": (f"LPT whole-matrix ownership over {world} ranks; " + (
-                       "all-gather fused into the last XB epilogue (TMA stores to every peer's "
-                       "symmetric-memory buffer over NVLink)" if collective == "fused" else
-                       f"{buckets} bucketed NCCL all-gathers overlapped with the NS launches")
-                       + (f" [{coll_note}]" if coll_note else "")) if world > 1
-                   else "1 rank, grouped launch (13 launches / step)",
-                   "l2": f"inputs {sum(m * n for m, n in shapes) * 2 / 1e6:.0f} MB > 126 MB L2, no flush",
-                   "parallelism": f"dp{world} (matrix ownership)"},
+        "config": workload_config(args.workload, shapes, iters),
+        "run": {"sharding": (f"LPT whole-matrix ownership over {world} ranks; " + (
+                    "all-gather fused into the last XB epilogue (TMA stores to every peer's "
+                    "symmetric-memory buffer over NVLink)" if collective == "fused" else
+                    f"{buckets} bucketed NCCL all-gathers overlapped with the NS launches")
+                    + (f" [{coll_note}]" if coll_note else "")) if world > 1
+                else "1 rank, grouped launch (13 launches / step)",
+                "l2": f"inputs {sum(m * n for m, n in shapes) * 2 / 1e6:.0f} MB > 126 MB L2, no flush",
+                "parallelism": f"dp{world} (matrix ownership)"},
+        "outputs": {"all_finite": finite, "flags": flags},
         "tflops_alg": round(total_flops / (ms * 1e-3) / 1e12, 1),
         "e2e": e2e,
         "gpu_launches": int(launches),
@@ -424,11 +465,21 @@ def run_own(args):
         "clocks": clocks,
     }
     if world == 1 and rank == 0 and not args.quick:
-        line["extras"] = run_extras(args, peaks)
-        cpu_ms, done, secs = oracle_sample_ms(shapes, iters, args.cpu_budget)
+        extra_outs = {}
+        line["extras"] = run_extras(args, peaks, extra_outs)
+        # cpu_baseline leg: the oracle timed on the bench's own inputs (one matrix of each
+        # shape first, then round robin), and its outputs compared with the timed GPU outputs
+        order = sorted(range(len(shapes)), key=lambda i: (shapes[:i + 1].count(shapes[i]), i))
+        cpu_ms, done, secs, oouts = oracle_sample(xs_np, shapes, iters, args.cpu_budget, order)
+        gpu = {i: res[i].float().cpu().numpy().astype(np.float64) for i in oouts}
+        acc = accuracy_rows(xs_np, gpu, {i: oouts[i] for i in list(oouts)[:3]})
+        acc["relF_max_all_sampled"] = accuracy_rows(xs_np, gpu, oouts, with_polar=False)["relF_max"]
+        acc["checked_relF"] = len(oouts)
         line["cpu_baseline"] = {"value": round(cpu_ms, 1), "unit": "ms", "cores": blas_threads(), "kind": "oracle",
-                                "sample": f"{len(done)} whole matrices ({summarize(done)}) in {secs:.1f} s, numpy fp64 "
-                                          f"+ OpenBLAS; extrapolated to the {len(shapes)}-matrix set by algorithmic FLOPs"}
+                                "sample": f"{len(done)} whole matrices of the bench's inputs ({summarize(done)}) in "
+                                          f"{secs:.1f} s, numpy fp64 + OpenBLAS; extrapolated to the {len(shapes)}-matrix "
+                                          f"set by algorithmic FLOPs"}
+        line["accuracy"] = {"gpt2-medium (timed outputs)": acc, **extras_accuracy(extra_outs)}
         line["cpu_single_thread"] = oracle_single_thread()
     if rank == 0:
         print(json.dumps(line), flush=True)
@@ -488,8 +539,28 @@ def run_e2e(args, xs, shapes, plan, mine, rank, world, dev, iters):
                     f"{nb}-bucket pipeline on separate copy/compute/comm streams (orthogonalize_host)"}
 
 
-def run_extras(args, peaks):
-    """The other workloads the metric names (N = 1 only)."""
+def extras_accuracy(extra_outs):
+    """cpu_baseline leg, continued: the oracle on the extras' sampled inputs, compared with
+    their GPU outputs (relF and polar-error ratio; the fp32 case against its 1e-4 gate)."""
+    from oracle import ns_oracle as O
+    rows = {}
+    for name, (xs_np, gpu, coeffs, gate) in extra_outs.items():
+        oo = {i: O.newton_schulz(x.astype(np.float64), coeffs, "aol") for i, x in xs_np.items()}
+        row = accuracy_rows(xs_np, gpu, oo)
+        row["relF_gate"] = gate
+        rows[name] = row
+    return rows
+
+
+def run_extras(args, peaks, extra_outs=None):
+    """The other workloads the metric names (N = 1 only).  extra_outs receives, per config,
+    (sampled inputs, their GPU outputs, coeffs, relF gate) for the accuracy check."""
+    extra_outs = {} if extra_outs is None else extra_outs
+
+    def keep(name, xs_np, outs, picks, coeffs, gate):
+        extra_outs[name] = ({i: xs_np[i] for i in picks},
+                            {i: outs[i].float().cpu().numpy().astype(np.float64) for i in picks}, coeffs, gate)
+
     import torch
 
     import paper_2512_04632_b200 as ns
@@ -514,6 +585,8 @@ def run_extras(args, peaks):
     ns.profile_read()
     ns.profile_enable(False)
     ms_dense = time_calls(lambda: torch_dense_ns(x0, C.turbo(4)), max(3, reps // 2), flush)
+    ns.orthogonalize_list([x0], out=[out_t], iters=4, precond="aol")
+    finite_8192 = bool(torch.isfinite(out_t.float()).all())
     f4 = ns_flops(n, n, 4)
     units = kernel_units([(n, n)], 4)
     kern = {}
@@ -540,14 +613,18 @@ def run_extras(args, peaks):
         "speedup_vs_cublas_dense": round(ms_dense / ms_turbo, 3),
         "kernels": kern,
         "timing": f"median of {reps} calls, L2 flushed (256 MB write) before each",
+        "output_all_finite": finite_8192,
+        "oracle_check": "not in the bench (fp64 oracle ~1 min at 8192^2): tests/test_gpu_fullsize.py",
     }
     del x0, out_t
     # --- GPT-2 small set (config 2)
     shapes = I.shape_set("gpt2-small")
-    xs = [torch.from_numpy(x).to(torch.bfloat16).cuda() for x in make_inputs(shapes, 2)]
+    xs_np = make_inputs(shapes, 2)
+    xs = [torch.from_numpy(x).to(torch.bfloat16).cuda() for x in xs_np]
     outs = [torch.empty_like(t) for t in xs]
     ns.orthogonalize_list(xs, out=outs, iters=4)
     ms_s = time_calls(lambda: ns.orthogonalize_list(xs, out=outs, iters=4), reps, flush)
+    keep("gpt2-small", xs_np, outs, [shapes.index(sh) for sh in sorted(set(shapes))], C.turbo(4), 2e-2)
     fs = sum(ns_flops(m, n, 4) for m, n in shapes)
     out["gpt2_small"] = {"ms": round(ms_s, 4), "tflops_alg": round(fs / (ms_s * 1e-3) / 1e12, 1),
                          "matrices": len(shapes)}
@@ -594,17 +671,80 @@ def run_extras(args, peaks):
     # --- CIFAR conv set (config 3), latency-bound: the two N = 64 matrices run in the
     #     cluster-resident kernel on a side stream, the four N = 256 ones in the step engine
     shapes = I.shape_set("cifar")
-    xs = [torch.from_numpy(x).to(torch.bfloat16).cuda() for x in make_inputs(shapes, 3)]
+    xs_np = make_inputs(shapes, 3)
+    xs = [torch.from_numpy(x).to(torch.bfloat16).cuda() for x in xs_np]
     outs = [torch.empty_like(t) for t in xs]
     us, gus, nl = small(lambda: ns.orthogonalize_list(xs, out=outs, iters=4))
+    keep("cifar", xs_np, outs, list(range(len(shapes))), C.turbo(4), 2e-2)
     out["cifar"] = {"us": round(us, 1), "us_graph_replay": round(gus, 1), "launches": nl, "matrices": len(shapes)}
     # --- config 1: one 128 x 128 fp32 matrix, fp32 "exact" mode (cluster-resident kernel)
-    x1 = torch.from_numpy(I.gaussian(128, 128, seed=I.matrix_seed(1, 0), bf16=False)).cuda()
+    x1_np = I.gaussian(128, 128, seed=I.matrix_seed(1, 0), bf16=False)
+    x1 = torch.from_numpy(x1_np).cuda()
     o1 = torch.empty_like(x1)
     us, gus, nl = small(lambda: ns.orthogonalize_list([x1], out=[o1], iters=4))
+    keep("fp32_128", [x1_np], [o1], [0], C.turbo(4), 1e-4)
     out["fp32_128"] = {"us": round(us, 1), "us_graph_replay": round(gus, 1), "launches": nl,
                        "tflops_alg": round(ns_flops(128, 128, 4) / (us * 1e-6) / 1e12, 3)}
     return out
+
+
+def spawn_ranks(args) -> int:
+    """`python bench.py --gpus N` without a launcher: start N ranks of this script with
+    torch.distributed.run on 127.0.0.1 (one process per GPU) and return its exit code.  NCCL
+    logs its communicator set-up (INIT, and NVLS when the switch reduces) on stderr."""
+    import socket
+    import subprocess
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    env = dict(os.environ)
+    if not args.cpu_launch_check:
+        env.setdefault("NCCL_DEBUG", "INFO")
+        env.setdefault("NCCL_DEBUG_SUBSYS", "INIT,NVLS")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd, env=env)
+
+
+def run_cpu_launch_check(args):
+    """Launcher / multi-rank plumbing check on CPU (gloo): the rank environment, process
+    group, sharded call with an injected copy compute, barrier + max-over-ranks timing and
+    the rank-0 JSON line -- the code path of an N-GPU run without GPUs.  Not a measurement."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2512_04632_b200.parallel import orthogonalize_sharded
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world > 1:
+        dist.init_process_group("gloo")
+    shapes = I.shape_set("cifar")
+    xs = [torch.from_numpy(x) for x in make_inputs(shapes, 3)]
+
+    def copy(ins, outs):
+        for i, o in zip(ins, outs):
+            o.copy_(i)
+
+    for _ in range(max(args.warmup, 3)):
+        orthogonalize_sharded(xs, None, iters=args.iters, compute=copy)
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        outs = orthogonalize_sharded(xs, None, iters=args.iters, compute=copy)
+    ms = (time.perf_counter() - t0) * 1e3 / args.steps
+    t = torch.tensor([ms])
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ok = all(torch.equal(o, x) for o, x in zip(outs, xs))
+    if rank == 0:
+        print(json.dumps({"metric": "launcher check (copy compute, gloo)", "value": round(float(t.item()), 4),
+                          "unit": "ms", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+                          "gathered_equal_inputs": ok, "data": "not a measurement"}), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0 if ok else 1
 
 
 def main():
@@ -622,10 +762,22 @@ def main():
                     help="N > 1: do not probe fused vs NCCL; time --collective as given")
     ap.add_argument("--collective", choices=["fused", "nccl"], default="fused",
                     help="N > 1: fused peer stores in the last epilogue, or NCCL all-gathers")
-    ap.add_argument("--extra-reps", type=int, default=10)
+    ap.add_argument("--extra-reps", type=int, default=20)
     ap.add_argument("--cpu-budget", type=float, default=12.0, help="seconds of oracle CPU work")
     ap.add_argument("--quick", action="store_true", help="skip extras and cpu_baseline (profiling runs)")
+    ap.add_argument("--cpu-launch-check", action="store_true",
+                    help="test only: run the multi-rank plumbing on CPU (gloo) with a copy compute")
     args = ap.parse_args()
+    if "WORLD_SIZE" in os.environ:
+        ws = int(os.environ["WORLD_SIZE"])
+        if ws != args.gpus:
+            print(f"bench.py: WORLD_SIZE={ws} but --gpus {args.gpus}; launch one rank per GPU "
+                  f"(torchrun --nproc-per-node {args.gpus}) or drop the launcher", file=sys.stderr)
+            return 2
+    elif args.gpus > 1 and args.impl == "own":
+        return spawn_ranks(args)
+    if args.cpu_launch_check:
+        return run_cpu_launch_check(args)
     if args.impl == "reference":
         return run_reference(args)
     return run_own(args)

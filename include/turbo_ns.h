@@ -23,11 +23,19 @@
  *   - `coeffs` is a HOST array of 3*iters floats (a_1,b_1,c_1,a_2,...); it is read
  *     before the call returns (the caller may free it afterwards).
  *   - Calls are asynchronous on `stream` (a cudaStream_t; NULL = legacy default
- *     stream) and never synchronise, except ns_read_flags and the first call for a
- *     given problem list (plan build: workspace allocation + descriptor upload).
+ *     stream) and never block the host on the device -- including the first call for
+ *     a problem list, whose plan build allocates (cudaMallocAsync), zeroes
+ *     (cudaMemsetAsync) and uploads its tables (cudaMemcpyAsync) stream-ordered on
+ *     `stream`.  Exceptions, each documented at its entry point: ns_read_flags,
+ *     ns_profile_read, nsx_epilogue_counters, ns_shutdown, the nsx_* single-step test
+ *     entry points, and the first call of the process on a device (context set-up).
+ *     The plan-building call cannot itself be stream-captured (NS_ERR_NOT_SUPPORTED);
+ *     later calls can.
  *   - Caller-owned memory is never freed by the library.  Workspace (a ping-pong
  *     buffer of the matrix size plus two N x N buffers and small tables per matrix)
- *     is owned by the library, cached per problem list, and released by ns_shutdown.
+ *     is owned by the library, cached per problem list (keyed by device pointers and
+ *     shapes), and released stream-ordered (cudaFreeAsync after an event recorded at
+ *     the plan's last launch) when the cache evicts it, or by ns_shutdown.
  *   - All argument checks happen on the host before anything is enqueued; on any
  *     error nothing is enqueued and no memory is touched.  Numerical conditions
  *     (zero row-sum, zero matrix, non-finite values) do NOT fail a call: they set
@@ -37,11 +45,11 @@
  *     not while `stream` is itself being captured; TNS_NOGRAPH=1 disables it).
  *   - Thread-safety: calls are serialised by an internal mutex; distinct streams are
  *     fine for distinct problem lists.  Calls with the SAME problem list share its cached
- *     workspace: on different streams the caller must order them (events).  Determinism: results are bitwise reproducible for identical inputs, and
- *     independent of how matrices are grouped into calls -- except that a matrix with
- *     N <= 256 and M >= 1024 takes the split-K Gram only in calls whose Gram step
- *     leaves at least half of the GPU idle (its result then differs from an unsplit
- *     call at rounding level).
+ *     workspace: on different streams the caller must order them (events).
+ *   - Determinism: results are bitwise reproducible for identical inputs, and
+ *     independent of how matrices are grouped into calls: every routing and tiling
+ *     decision that changes the arithmetic (cluster kernel vs step engine, split-K Gram
+ *     of N <= 256 matrices) depends on the matrix shape alone.
  */
 #ifndef TURBO_NS_H_
 #define TURBO_NS_H_
@@ -53,7 +61,7 @@
 extern "C" {
 #endif
 
-#define NS_ABI_VERSION 1
+#define NS_ABI_VERSION 2
 
 typedef enum {
   NS_OK = 0,
@@ -78,8 +86,13 @@ typedef enum {
 #define NS_FLAG_ZERO_SCALE 0x1u /* a zero AOL row-sum (zero column) or zero matrix (Frobenius) */
 #define NS_FLAG_NONFINITE 0x2u  /* a non-finite value was produced                        */
 
-/* In place: `batch` matrices of m x n at X, X + m*n, ... (contiguous) are each
- * overwritten with NS_T(precond(X_i)), T = iters (1..64). */
+/* The north-star call (Alg. 2 P:L163-176 for AOL, Alg. 1
+ * for FROBENIUS / NONE, Eqs. 3-5 P:L116-118 per iteration).  In place: `batch` matrices of
+ * m x n at X, X + m*n, ... (contiguous, device) are each overwritten with
+ * NS_T(precond(X_i)), T = iters (1..64), coeffs = T triples (host).  Errors:
+ * NS_ERR_INVALID_VALUE (m, n, batch < 1; iters outside 1..64; NULL or non-finite coeffs;
+ * bad enum), NS_ERR_NOT_SUPPORTED (X not aligned to its element size; stream-captured
+ * plan build), NS_ERR_WORKSPACE (allocation), NS_ERR_CUDA; nothing enqueued on error. */
 ns_status ns_orthogonalize(void* X, int64_t m, int64_t n, int64_t batch, int iters,
                            const float* coeffs, ns_precond precond, ns_dtype dtype,
                            void* stream);
@@ -96,7 +109,9 @@ ns_status ns_orthogonalize_cast(const void* const* X, void* const* out, const in
                                 const int64_t* n, int64_t count, int iters, const float* coeffs,
                                 ns_precond precond, void* stream);
 
-/* Grouped: `count` matrices of arbitrary shapes m[i] x n[i].  X is a HOST array of
+/* Grouped (the paper batches layer matrices, "batches of 32"):
+ * the same computation as ns_orthogonalize for `count` matrices of arbitrary shapes
+ * m[i] x n[i] (count < 2^20).  X is a HOST array of
  * device pointers (inputs); out is a HOST array of device pointers receiving the
  * results (out may be NULL, or out[i] == X[i], for in place; out[i] must not
  * otherwise overlap any X[j]).  Every NS step runs as ONE launch over all matrices
@@ -143,22 +158,33 @@ ns_status ns_muon_step(void* const* W, const void* const* G, float* const* M, vo
 ns_status ns_muon_apply(void* const* W, const void* const* U, const int64_t* m, const int64_t* n,
                         int64_t count, ns_dtype w_dtype, float lr, float weight_decay, void* stream);
 
-/* Bytes of device workspace the library will hold for this problem list (an upper bound:
- * matrices served by the cluster-resident small-matrix kernel need none). */
-ns_status ns_workspace_size(const int64_t* m, const int64_t* n, int64_t count,
+/* Workspace of the north-star signature: bytes of device workspace the
+ * library holds for the problem list of `count` shapes m[i] x n[i], each repeated `batch`
+ * times (ns_orthogonalize with `batch`, or a grouped list) -- per matrix W (m x n), A and B
+ * (N x N), s and the AOL partials (Eq. 8 row sums), plus a 1 KiB header per plan
+ * (a list mixing TMA-unaligned bf16 shapes runs as two plans).  An upper bound for any
+ * device and path: matrices served by the cluster-resident kernel need none.  Host only
+ * (no device call).  NS_ERR_INVALID_VALUE for NULL pointers, count/batch/m/n < 1, bad
+ * dtype. */
+ns_status ns_workspace_size(const int64_t* m, const int64_t* n, int64_t count, int64_t batch,
                             ns_dtype dtype, size_t* bytes);
 
 /* Optional caller-owned workspace: `ptr` (device memory of the current
  * device, 256-byte aligned, `bytes` >= 256) from which every plan built afterwards carves
  * its workspace (bump allocation; a problem list needs at most ns_workspace_size bytes)
  * instead of allocating its own.  A call whose new plan does not fit fails with
- * NS_ERR_WORKSPACE and enqueues nothing.  Synchronises the device and drops the cached
- * plans that used the previous caller buffer; the caller keeps `ptr` alive until the next
+ * NS_ERR_WORKSPACE and enqueues nothing.  Drops the cached plans that used the previous
+ * caller buffer without synchronising: `stream` is made to wait (events) for their last
+ * launches, so work enqueued on `stream` afterwards is ordered after them; the caller keeps
+ * the previous buffer alive until that work has run, and `ptr` alive until the next
  * ns_set_workspace or ns_shutdown.  ptr = NULL returns to library-owned workspace. */
-ns_status ns_set_workspace(void* ptr, size_t bytes);
+ns_status ns_set_workspace(void* ptr, size_t bytes, void* stream);
 
-/* SYNCHRONISES `stream`, returns the OR of NS_FLAG_* raised since the last read on
- * the current device, and clears them. */
+/* Numerical conditions of the path (reading R4: the paper's Eq. 8 has no epsilon, P:L206;
+ * SPEC's zero-column / non-finite errors, become flags so that no call has
+ * to synchronise).  SYNCHRONISES `stream`, returns the OR of NS_FLAG_* raised since the
+ * last read on the current device, and clears them.  NS_ERR_INVALID_VALUE if flags is
+ * NULL. */
 ns_status ns_read_flags(void* stream, uint32_t* flags);
 
 /* Number of kernels the library launched on this process since load (host counter). */
@@ -200,13 +226,21 @@ void ns_shutdown(void); /* synchronises the device, frees workspace and plan cac
  * parity tests).  X is m x n row-major; N = min(m,n); all outputs are dtype.
  * --------------------------------------------------------------------------------- */
 
-/* A = Xh^T Xh (N x N, both triangles written)        -- Eq. 3 / Eq. 7. */
-ns_status nsx_gram(const void* X, int64_t m, int64_t n, void* A, ns_dtype dtype,
+/* A = Xh^T Xh (N x N, both triangles written)        -- Eq. 3 / Eq. 7.  part != NULL
+ * (aligned bf16 only, else NS_ERR_NOT_SUPPORTED): also the AOL row-sum partials of |A|
+ * that the iteration-1 Gram epilogue emits (Eq. 8), fp32[N * L] with
+ * L = ceil(N/64) + ceil(N/32): part[i*L + c] = sum of |A_ij| over the 64 columns of
+ * direct slot c, part[i*L + ceil(N/64) + r] = the same over the 32 rows of mirrored slot r
+ * (only slots the lower-triangle tiling writes; zero the buffer first). */
+ns_status nsx_gram(const void* X, int64_t m, int64_t n, void* A, float* part, ns_dtype dtype,
                    void* stream);
 
 /* In place on A (N x N symmetric): s from A (AOL: Eq. 8; FROBENIUS: 1/sqrt(trace A) =
- * 1/||X||_F, Eq. 10), then A <- diag(s) A diag(s) (Alg. 2 l.4).  s: device fp32[N]. */
-ns_status nsx_precondition(void* A, int64_t N, ns_precond precond, float* s,
+ * 1/||X||_F, Eq. 10), then A <- diag(s) A diag(s) (Alg. 2 l.4).  s: device fp32[N].
+ * part != NULL (AOL, bf16): the row sums come from nsx_gram's partials instead of A --
+ * the production branches (one lane per row while L <= 64, i.e. N <= 1344, else a warp
+ * tree). */
+ns_status nsx_precondition(void* A, int64_t N, ns_precond precond, const float* part, float* s,
                            ns_dtype dtype, void* stream);
 
 /* B = (b A + c A A) diag(s)  (Eq. 4; s == NULL means s = 1). */

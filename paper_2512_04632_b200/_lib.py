@@ -51,9 +51,9 @@ def _load() -> ctypes.CDLL:
         c_int, c_fp, c_int, c_vp]
     lib.ns_muon_apply.argtypes = [ctypes.POINTER(c_vp), ctypes.POINTER(c_vp), ctypes.POINTER(c_i64),
                                   ctypes.POINTER(c_i64), c_i64, c_int, c_float, c_float, c_vp]
-    lib.ns_workspace_size.argtypes = [ctypes.POINTER(c_i64), ctypes.POINTER(c_i64), c_i64, c_int,
+    lib.ns_workspace_size.argtypes = [ctypes.POINTER(c_i64), ctypes.POINTER(c_i64), c_i64, c_i64, c_int,
                                       ctypes.POINTER(ctypes.c_size_t)]
-    lib.ns_set_workspace.argtypes = [c_vp, ctypes.c_size_t]
+    lib.ns_set_workspace.argtypes = [c_vp, ctypes.c_size_t, c_vp]
     lib.ns_read_flags.argtypes = [c_vp, ctypes.POINTER(ctypes.c_uint32)]
     lib.ns_launch_count.restype = ctypes.c_uint64
     lib.ns_launch_count.argtypes = []
@@ -70,8 +70,8 @@ def _load() -> ctypes.CDLL:
     lib.ns_profile_enable.restype = None
     lib.ns_profile_read.argtypes = [ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_uint64), c_int]
     lib.nsx_epilogue_counters.argtypes = [ctypes.POINTER(ctypes.c_uint64), c_int]
-    lib.nsx_gram.argtypes = [c_vp, c_i64, c_i64, c_vp, c_int, c_vp]
-    lib.nsx_precondition.argtypes = [c_vp, c_i64, c_int, c_vp, c_int, c_vp]
+    lib.nsx_gram.argtypes = [c_vp, c_i64, c_i64, c_vp, c_vp, c_int, c_vp]
+    lib.nsx_precondition.argtypes = [c_vp, c_i64, c_int, c_vp, c_vp, c_int, c_vp]
     lib.nsx_poly.argtypes = [c_vp, c_i64, c_float, c_float, c_vp, c_vp, c_int, c_vp]
     lib.nsx_update.argtypes = [c_vp, c_i64, c_i64, c_vp, c_float, c_vp, c_vp, c_int, c_vp]
     for name in EXPORTS:

@@ -162,12 +162,13 @@ class PreparedCall:
         check(st, "ns_orthogonalize_batched")
 
 
-def workspace_size(shapes: Sequence[tuple[int, int]], dtype=torch.bfloat16) -> int:
+def workspace_size(shapes: Sequence[tuple[int, int]], dtype=torch.bfloat16, batch: int = 1) -> int:
+    """ns_workspace_size: bytes of workspace for `shapes`, each repeated `batch` times."""
     cnt = len(shapes)
     M = (ctypes.c_int64 * cnt)(*[s[0] for s in shapes])
     N = (ctypes.c_int64 * cnt)(*[s[1] for s in shapes])
     out = ctypes.c_size_t(0)
-    check(lib.ns_workspace_size(M, N, cnt, DTYPE_BF16 if dtype == torch.bfloat16 else DTYPE_FP32,
+    check(lib.ns_workspace_size(M, N, cnt, int(batch), DTYPE_BF16 if dtype == torch.bfloat16 else DTYPE_FP32,
                                 ctypes.byref(out)), "ns_workspace_size")
     return out.value
 
@@ -198,11 +199,11 @@ def set_workspace(buf: torch.Tensor | None) -> None:
     workspace from `buf` (a contiguous CUDA tensor, 256-byte aligned); None returns to
     library-owned workspace.  Keep `buf` alive while it is set."""
     if buf is None:
-        check(lib.ns_set_workspace(None, 0), "ns_set_workspace")
+        check(lib.ns_set_workspace(None, 0, _stream()), "ns_set_workspace")
         return
     _check_tensor(buf, "workspace")
     with torch.cuda.device(buf.device):
-        check(lib.ns_set_workspace(ctypes.c_void_p(buf.data_ptr()), buf.numel() * buf.element_size()),
+        check(lib.ns_set_workspace(ctypes.c_void_p(buf.data_ptr()), buf.numel() * buf.element_size(), _stream(buf)),
               "ns_set_workspace")
 
 
@@ -250,25 +251,35 @@ def _short(m: int, n: int) -> int:
     return min(m, n)
 
 
-def gram(x: torch.Tensor) -> torch.Tensor:
-    """A = Xh^T Xh (N x N), Eq. 3 / Eq. 7."""
+def partials_ld(N: int) -> int:
+    """Slots per row of the AOL row-sum partials (nsx_gram): ceil(N/64) + ceil(N/32)."""
+    return (N + 63) // 64 + (N + 31) // 32
+
+
+def gram(x: torch.Tensor, partials: bool = False):
+    """A = Xh^T Xh (N x N), Eq. 3 / Eq. 7.  partials=True: returns (A, part) with the AOL
+    row-sum partials of the Gram epilogue (Eq. 8), fp32 [N, partials_ld(N)]."""
     _check_tensor(x, "x")
     m, n = x.shape
     N = _short(m, n)
     a = torch.empty((N, N), dtype=x.dtype, device=x.device)
+    part = torch.zeros((N, partials_ld(N)), dtype=torch.float32, device=x.device) if partials else None
     with torch.cuda.device(x.device):
         check(lib.nsx_gram(ctypes.c_void_p(x.data_ptr()), m, n, ctypes.c_void_p(a.data_ptr()),
-                           _dtype_code(x), _stream(x)), "nsx_gram")
-    return a
+                           ctypes.c_void_p(part.data_ptr()) if partials else None, _dtype_code(x), _stream(x)),
+              "nsx_gram")
+    return (a, part) if partials else a
 
 
-def precondition(a: torch.Tensor, precond: str = "aol") -> torch.Tensor:
-    """In place a <- diag(s) a diag(s); returns s (fp32).  Eqs. 8-10, Alg. 2 l.4."""
+def precondition(a: torch.Tensor, precond: str = "aol", part: torch.Tensor | None = None) -> torch.Tensor:
+    """In place a <- diag(s) a diag(s); returns s (fp32).  Eqs. 8-10, Alg. 2 l.4.  part: the
+    Gram's AOL partials (gram(x, partials=True)) -- the production row-sum branches."""
     _check_tensor(a, "a")
     N = a.shape[0]
     s = torch.empty((N,), dtype=torch.float32, device=a.device)
     with torch.cuda.device(a.device):
         check(lib.nsx_precondition(ctypes.c_void_p(a.data_ptr()), N, PRECOND[precond],
+                                   ctypes.c_void_p(part.data_ptr()) if part is not None else None,
                                    ctypes.c_void_p(s.data_ptr()), _dtype_code(a), _stream(a)),
               "nsx_precondition")
     return s

@@ -76,6 +76,9 @@ struct DevCtx {
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   cudaStream_t cap = nullptr;  // private stream on which plans are captured into CUDA graphs
+  // private stream on which evicted plans' device memory is released (cudaFreeAsync), ordered
+  // after the plan's last use by an event -- eviction never synchronises the host
+  cudaStream_t freer = nullptr;
 };
 static DevCtx g_dev[64];
 static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
@@ -94,6 +97,7 @@ static ns_status dev_ctx(DevCtx** out) {
     CU_TRY(cudaStreamCreateWithFlags(&d.side, cudaStreamNonBlocking));
     CU_TRY(cudaEventCreateWithFlags(&d.ev_fork, cudaEventDisableTiming));
     CU_TRY(cudaEventCreateWithFlags(&d.ev_join, cudaEventDisableTiming));
+    CU_TRY(cudaStreamCreateWithFlags(&d.freer, cudaStreamNonBlocking));
     if (!g_encode) {
       cudaDriverEntryPointQueryResult q;
       void* fn = nullptr;
@@ -109,6 +113,21 @@ static ns_status dev_ctx(DevCtx** out) {
 }
 
 static inline size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+// Stream-ordered release of library-owned device memory (allocated with cudaMallocAsync):
+// the private `freer` stream waits for `last` (an event recorded after the memory's last
+// use) and frees there -- no host synchronisation.
+static void release_async(int dev, void* p, cudaEvent_t last) {
+  if (!p) return;
+  int cur = 0;
+  cudaGetDevice(&cur);
+  if (cur != dev) cudaSetDevice(dev);
+  DevCtx& d = g_dev[dev & 63];
+  cudaStream_t s = d.init ? d.freer : nullptr;
+  if (last && s) cudaStreamWaitEvent(s, last, 0);
+  if (cudaFreeAsync(p, s) != cudaSuccess) cudaGetLastError();
+  if (cur != dev) cudaSetDevice(cur);
+}
 
 // Row-major R x C bf16 matrix, zero OOB fill.  box = 64: 64 x 64 boxes with 128-byte
 // swizzle (GEMM operands); box = 32: 32 x 32 boxes with 64-byte swizzle (epilogue).
@@ -206,10 +225,15 @@ struct Plan {
   uint64_t glaunches = 0;
   uint64_t uses = 0;
   bool graph_failed = false;
+  bool pinned = false;             // resolved for a call in progress: never evicted
+  cudaEvent_t last = nullptr;      // recorded on the caller's stream after every launch
   ~Plan() {
+    // an executable graph still in flight is released on completion (cudaGraphExecDestroy);
+    // device memory is freed stream-ordered after the last launch (release_async)
     if (gexec) cudaGraphExecDestroy(gexec);
-    if (ws && !ws_borrowed) cudaFree(ws);
-    if (dtab) cudaFree(dtab);
+    if (ws && !ws_borrowed) release_async(device, ws, last);
+    if (dtab) release_async(device, dtab, last);
+    if (last) cudaEventDestroy(last);
   }
 };
 
@@ -239,15 +263,12 @@ static int part_ld_for(int64_t N) { return (int)((N + 63) / 64 + (N + 31) / 32);
 
 // Split-K Gram.  For N <= 256 the Gram is one 256 x 256 block per matrix, walked over the
 // whole K = M by a single CTA pair: with a long K (tall matrices, e.g. 256 x 2304 conv
-// weights) and few matrices, a handful of pairs stream K at single-SM bandwidth while the
-// rest of the GPU idles.  When the call's Gram step is tile-starved (its tiles fill at most
-// half of the CTA-pair workers), such Grams are cut into S = ceil(nk / 8) k-ranges (nk =
-// k-blocks of 64, nk >= 16, S <= 16), computed as independent tiles whose fp32 partials a
-// reduction launch sums in a fixed order.  S depends on the matrix shape alone, so results
-// are bitwise the same in every tile-starved call (single matrices, small lists); a call
-// that fills the GPU does not split (the partials' traffic would cost more than the idle
-// SMs it recovers) and differs from a split call at rounding level.  Per-step launches only
-// (the opt-in fused and multicast paths do not split).
+// weights) a handful of pairs would stream K at single-SM bandwidth while the rest of the GPU
+// idles.  Such Grams (N <= 256, nk = ceil(M / 64) >= 16 k-blocks) are cut into
+// S = min(16, ceil(nk / 8)) k-ranges, computed as independent tiles whose fp32 partials a
+// reduction launch sums in a fixed order.  S depends on the matrix shape ALONE -- never on
+// the rest of the call -- so a matrix's result is bitwise the same in every call (single,
+// batched, or on any rank of the sharded path, §8(e)).  Per-step launches only.
 static const int64_t kSplitLd = 256;  // floats per partial row; rows padded to 256 too
 static int split_factor(int64_t M, int64_t N) {
   if (N > kSplitMaxN) return 0;
@@ -255,17 +276,9 @@ static int split_factor(int64_t M, int64_t N) {
   if (nk < 16) return 0;
   return (int)std::min<int64_t>(16, (nk + 7) / 8);
 }
-static void choose_splits(std::vector<Mat>& mats, int cg, int workers) {
-  for (Mat& mt : mats) mt.split = 0;
-  if (const char* e = getenv("TNS_NOSPLIT"))  // measurement knob (A/B), read at plan build
-    if (atoi(e)) return;
-  int64_t tiles = 0;
-  for (const Mat& mt : mats) {
-    const int64_t nb = (mt.N + kSymBlock - 1) / kSymBlock;
-    tiles += nb * (nb + 1) / 2 * (2 / cg);
-  }
-  if (2 * tiles > workers) return;
-  for (Mat& mt : mats) mt.split = split_factor(mt.M, mt.N);
+static void choose_splits(std::vector<Mat>& mats) {
+  static const bool off = [] { const char* e = getenv("TNS_NOSPLIT"); return e && atoi(e); }();  // A/B knob
+  for (Mat& mt : mats) mt.split = off ? 0 : split_factor(mt.M, mt.N);
 }
 // Tile width.  A plan whose every GEMM step has at most half as many 256-wide tiles as there
 // are CTA-pair workers (small problems: one tile per pair, latency-bound) uses 128-wide
@@ -364,12 +377,12 @@ static void balance_tasks(std::vector<TaskDesc>& tasks, const std::vector<GemmJo
   tasks.swap(out);
 }
 
-static ns_status build_plan(Plan& P, HostTables& H, DevCtx* dc, const float* coeffs) {
+static ns_status build_plan(Plan& P, HostTables& H, DevCtx* dc, const float* coeffs, cudaStream_t stream) {
   const int hs = half_storage_enabled() ? 1 : 0;
   const int T = P.iters;
   const size_t es = elem_size(P.dtype);
   const bool bf16 = P.dtype == NS_BF16;
-  if (!P.simt) choose_splits(P.mats, P.cg, dc->sms / P.cg);
+  if (!P.simt) choose_splits(P.mats);
   else for (Mat& mt : P.mats) mt.split = 0;
   P.bn = P.simt ? 256 : choose_bn(P.mats, P.cg, dc->sms / 2);
   // -- workspace layout
@@ -401,15 +414,16 @@ static ns_status build_plan(Plan& P, HostTables& H, DevCtx* dc, const float* coe
     P.ws_borrowed = true;
     uw.used = at + P.ws_bytes;
   } else {
-    e = cudaMalloc(&P.ws, P.ws_bytes);
+    e = cudaMallocAsync(&P.ws, P.ws_bytes, stream);  // stream-ordered: no host synchronisation
     if (e != cudaSuccess) {
       cudaGetLastError();
-      return fail(NS_ERR_WORKSPACE, "workspace cudaMalloc(" + std::to_string(P.ws_bytes) + ") failed");
+      P.ws = nullptr;
+      return fail(NS_ERR_WORKSPACE, "workspace cudaMallocAsync(" + std::to_string(P.ws_bytes) + ") failed");
     }
   }
   uint8_t* ws = reinterpret_cast<uint8_t*>(P.ws);
   P.barrier = reinterpret_cast<unsigned*>(ws);
-  CU_TRY(cudaMemset(P.ws, 0, P.ws_bytes));  // zero padding of s (and everything else) once
+  CU_TRY(cudaMemsetAsync(P.ws, 0, P.ws_bytes, stream));  // zero padding of s (and everything else) once
   auto W = [&](const Mat& mt) { return (void*)(ws + mt.w_off); };
   auto Am = [&](const Mat& mt) { return (void*)(ws + mt.a_off); };
   auto Bm = [&](const Mat& mt) { return (void*)(ws + mt.b_off); };
@@ -674,9 +688,9 @@ static ns_status build_plan(Plan& P, HostTables& H, DevCtx* dc, const float* coe
           J.A = Am(mt); J.s = Sv(mt); J.N = (int)mt.N; J.precond = (int)P.precond;
           if (use_part) { J.part = Part(mt); J.part_ld = mt.part_ld; }
           J.half = P.simt ? 0 : hs;
-          J.row_start = rows; J.vec_start = items;
+          J.row_start = rows; J.seg_start = items;
           rows += mt.N;
-          items += vec8 ? (mt.N * mt.N) / 8 : mt.N * mt.N;
+          items += precond_segments(J.N, J.half);  // phase-2 work units (256-column row segments)
           pj.push_back(J);
         }
         if (P.simt) {
@@ -779,10 +793,11 @@ static ns_status build_plan(Plan& P, HostTables& H, DevCtx* dc, const float* coe
   // -- upload
   if (!H.bytes.empty()) {
     P.dtab_bytes = align_up(H.bytes.size(), 256);
-    e = cudaMalloc(&P.dtab, P.dtab_bytes);
+    e = cudaMallocAsync(&P.dtab, P.dtab_bytes, stream);
     if (e != cudaSuccess) {
       cudaGetLastError();
-      return fail(NS_ERR_WORKSPACE, "job-table cudaMalloc failed");
+      P.dtab = nullptr;
+      return fail(NS_ERR_WORKSPACE, "job-table cudaMallocAsync failed");
     }
     uint8_t* dbase = reinterpret_cast<uint8_t*>(P.dtab);
     for (const Fix& f : fixes) {
@@ -793,7 +808,9 @@ static ns_status build_plan(Plan& P, HostTables& H, DevCtx* dc, const float* coe
       J->tmAux = f.taux >= 0 ? dbase + tm_off + (size_t)(f.taux + 1) * sizeof(CUtensorMap) : nullptr;
       J->tmPeer = f.tpeer >= 0 ? dbase + tm_off + (size_t)f.tpeer * sizeof(CUtensorMap) : nullptr;
     }
-    CU_TRY(cudaMemcpy(P.dtab, H.bytes.data(), H.bytes.size(), cudaMemcpyHostToDevice));
+    // pageable host -> device, stream-ordered: the runtime stages the bytes before returning
+    // and does not wait for the stream's earlier work
+    CU_TRY(cudaMemcpyAsync(P.dtab, H.bytes.data(), H.bytes.size(), cudaMemcpyHostToDevice, stream));
   }
   (void)dc;
   return NS_OK;
@@ -935,12 +952,22 @@ static ns_status launch_plan(Plan& P, DevCtx* dc, cudaStream_t stream) {
   }
   if (graph && !P.gexec && P.uses >= 1) capture_plan(P, dc);
   ++P.uses;
+  ns_status st = NS_OK;
   if (graph && P.gexec) {
     CU_TRY(cudaGraphLaunch(P.gexec, stream));
     g_launches += P.glaunches;
-    return NS_OK;
+  } else {
+    st = enqueue_plan(P, dc, stream);
   }
-  return enqueue_plan(P, dc, stream);
+  // last use, for the stream-ordered release of the plan's memory on eviction (not while
+  // the caller captures `stream`: its graph then owns the ordering)
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (st == NS_OK && cudaStreamIsCapturing(stream, &cs) == cudaSuccess && cs == cudaStreamCaptureStatusNone) {
+    if (!P.last && cudaEventCreateWithFlags(&P.last, cudaEventDisableTiming) != cudaSuccess) P.last = nullptr;
+    if (P.last) CU_TRY(cudaEventRecord(P.last, stream));
+  }
+  cudaGetLastError();
+  return st;
 }
 
 // ---------------------------------------------------------------------------- validation
@@ -967,69 +994,81 @@ static ns_status validate_mat(const void* x, int64_t m, int64_t n, ns_dtype dtyp
   return NS_OK;
 }
 
-static ns_status run_plan(const std::vector<Mat>& mats_in, int iters, const float* coeffs, ns_precond precond,
-                          ns_dtype dtype, cudaStream_t stream, bool cast);
+// Tile words pack the job index and p0/128, q0/bn in 20 bits each (jobs.h pack_tile): a
+// tcgen05 matrix needs M < 2^27 rows and a call fewer than 2^20 matrices.
+static const int64_t kMaxTmaRows = (int64_t)1 << 27;
+static const int64_t kMaxJobs = (int64_t)1 << 20;
 
-// A bf16 list that mixes TMA-addressable matrices with ones TMA cannot address (a row pitch
-// that is not a multiple of 16 bytes) runs as two plans on the stream: the unaligned ones on
-// the CUDA-core step kernels, the rest on the tcgen05 engine -- so one unaligned matrix
-// neither slows the others down nor changes their results (batching stays invisible).
-static ns_status run(const std::vector<Mat>& mats_in, int iters, const float* coeffs, ns_precond precond,
-                     ns_dtype dtype, cudaStream_t stream, bool cast = false) {
-  if (dtype == NS_BF16 && g_path != 1 && mats_in.size() > 1) {
-    std::vector<Mat> aligned, unaligned;
-    for (const Mat& mt : mats_in) {
-      Mat chk = mt;
-      if (cast) chk.x = chk.out = reinterpret_cast<void*>(256);
-      (tma_ok(chk, dtype) ? aligned : unaligned).push_back(mt);
-    }
-    if (!aligned.empty() && !unaligned.empty()) {
-      ns_status st = run_plan(unaligned, iters, coeffs, precond, dtype, stream, cast);
-      if (st != NS_OK) return st;
-      return run_plan(aligned, iters, coeffs, precond, dtype, stream, cast);
-    }
-  }
-  return run_plan(mats_in, iters, coeffs, precond, dtype, stream, cast);
+// Does matrix `mt` take the cluster-resident whole-NS kernel?  Path 0 routes by measured
+// cost (tools/cl_sizes.py, profiles/r01_v12_cluster_routing.log): the bf16 step engine of a
+// lone small matrix costs ~63 us (13 launches, graph replay), the cluster kernel grows with
+// its FMA work M*N^2 (64x216: 43 us, 128^2: 64 us, 64x576: 79 us) -- so bf16 matrices take
+// it up to M*N^2 = 2.2e6; fp32 always (the SIMT step kernels are slower).  Path 5 takes it
+// whenever the matrix fits.  Shape-only: batching never changes a result.
+static bool to_cluster(const Mat& mt, ns_dtype dtype, bool any_peer, int cc_major) {
+  const bool use_cluster = (g_path == 0 || g_path == 5) && !any_peer && cc_major == 10;
+  if (!use_cluster || !cl_fits(mt.M, mt.N)) return false;
+  return g_path == 5 || dtype != NS_BF16 || (double)mt.M * (double)mt.N * (double)mt.N <= 2.2e6;
 }
 
-static ns_status run_plan(const std::vector<Mat>& mats_in, int iters, const float* coeffs, ns_precond precond,
-                          ns_dtype dtype, cudaStream_t stream, bool cast) {
-  DevCtx* dc = nullptr;
-  ns_status st = dev_ctx(&dc);
-  if (st != NS_OK) return st;
-  // small matrices (short side <= 128, full copy fits in shared memory) run the whole NS
-  // in one cluster launch (paths 0 and 5); the others go through the step engine
+static bool tma_ok_call(const Mat& mt, ns_dtype dtype, bool cast) {
+  Mat chk = mt;  // mixed precision: the step engine reads the 256-byte aligned staging copy
+  if (cast) chk.x = chk.out = reinterpret_cast<void*>(256);
+  if (!tma_ok(chk, dtype) || chk.M >= kMaxTmaRows) return false;
+  for (void* pp : mt.peer)
+    if (reinterpret_cast<uintptr_t>(pp) & 15) return false;
+  return true;
+}
+
+// A call's matrices as plans.  A bf16 list that mixes TMA-addressable matrices with step-
+// engine matrices TMA cannot address (a row pitch that is not a multiple of 16 bytes) runs as
+// two plans on the stream: the unaligned ones on the CUDA-core step kernels, the rest on the
+// tcgen05 engine (and the cluster kernel) -- so one unaligned matrix neither slows the others
+// down nor changes their results (batching stays invisible).  Matrices that take the cluster
+// kernel stay with the aligned group, whatever their pitch (the cluster kernel reads any
+// layout), so they keep running beside the tcgen05 launches.
+static void group_mats(const std::vector<Mat>& mats, ns_dtype dtype, bool cast, int cc_major,
+                       std::vector<std::vector<Mat>>& groups) {
+  groups.clear();
+  if (dtype == NS_BF16 && g_path != 1 && mats.size() > 1) {
+    bool any_peer = false;
+    for (const Mat& mt : mats) any_peer = any_peer || !mt.peer.empty();
+    std::vector<Mat> aligned, unaligned;
+    for (const Mat& mt : mats) {
+      const bool un = !to_cluster(mt, dtype, any_peer, cc_major) && !tma_ok_call(mt, dtype, cast);
+      (un ? unaligned : aligned).push_back(mt);
+    }
+    if (!aligned.empty() && !unaligned.empty()) {
+      groups.push_back(std::move(unaligned));
+      groups.push_back(std::move(aligned));
+      return;
+    }
+  }
+  groups.push_back(mats);
+}
+
+// Find the cached plan of this problem list, or build it (workspace and tables allocated and
+// uploaded stream-ordered on `stream`).  The plan comes back pinned: it cannot be evicted
+// until unpinned, so a call can resolve all its plans before launching any.
+static ns_status resolve_plan(const std::vector<Mat>& mats_in, int iters, const float* coeffs, ns_precond precond,
+                              ns_dtype dtype, cudaStream_t stream, bool cast, DevCtx* dc, Plan** out) {
   std::vector<Mat> tiny, big;
   bool any_peer = false;
   for (const Mat& mt : mats_in) any_peer = any_peer || !mt.peer.empty();
-  const bool use_cluster = (g_path == 0 || g_path == 5) && !any_peer && dc->cc_major == 10;
-  // Path 0 routes by measured cost (tools/cl_sizes.py, profiles/r01_v12_cluster_routing.log):
-  // the bf16 step engine of a lone small matrix costs ~63 us (13 launches, graph replay),
-  // the cluster kernel grows with its FMA work M*N^2 (64x216: 43 us, 128^2: 64 us, 64x576:
-  // 79 us) -- so bf16 matrices take it up to M*N^2 = 2.2e6; fp32 always (the SIMT step
-  // kernels are slower).  Path 5 takes it whenever the matrix fits.  Shape-only: batching
-  // never changes a result.
-  auto to_cluster = [&](const Mat& mt) {
-    if (!use_cluster || !cl_fits(mt.M, mt.N)) return false;
-    return g_path == 5 || dtype != NS_BF16 || (double)mt.M * (double)mt.N * (double)mt.N <= 2.2e6;
-  };
-  for (const Mat& mt : mats_in) (to_cluster(mt) ? tiny : big).push_back(mt);
+  for (const Mat& mt : mats_in) (to_cluster(mt, dtype, any_peer, dc->cc_major) ? tiny : big).push_back(mt);
   bool simt = (g_path == 1) || dtype != NS_BF16 || dc->cc_major != 10;
   bool peers = false;
   for (const Mat& mt : big) {
-    Mat chk = mt;  // mixed precision: the step engine reads the 256-byte aligned staging copy
-    if (cast) chk.x = chk.out = reinterpret_cast<void*>(256);
-    simt = simt || !tma_ok(chk, dtype);
+    simt = simt || !tma_ok_call(mt, dtype, cast);
     peers = peers || !mt.peer.empty();
-    for (void* pp : mt.peer) simt = simt || (reinterpret_cast<uintptr_t>(pp) & 15);
   }
   if (peers && simt)
     return fail(NS_ERR_NOT_SUPPORTED, "fused peer stores need the bf16 tcgen05 path (aligned shapes/pointers)");
   int dev = 0;
   CU_TRY(cudaGetDevice(&dev));
-  // plan key
+  // plan key: device, routing, coefficients, and per matrix the buffers and shape
   std::vector<uint64_t> key;
-  key.reserve(mats_in.size() * 4 + 8 + 3 * iters);
+  key.reserve(mats_in.size() * 5 + 8 + 3 * iters);
   const int cg = (g_path == 2) ? 1 : 2;
   key.push_back((uint64_t)dev); key.push_back((uint64_t)dtype); key.push_back(simt ? 1 : 0);
   key.push_back(cast ? 1 : 0);
@@ -1047,9 +1086,10 @@ static ns_status run_plan(const std::vector<Mat>& mats_in, int iters, const floa
   auto it = g_plans.find(key);
   Plan* P = nullptr;
   if (it == g_plans.end()) {
-    // Evict least-recently-used plans (synchronising) while the cache is full by count or
-    // would hold more workspace than max(4 GiB, 2 x this list's): a caller that passes new
-    // buffers every step (fresh pointers, fresh plans) must not accumulate workspaces.
+    // Evict least-recently-used plans while the cache is full by count or would hold more
+    // workspace than max(4 GiB, 2 x this list's): a caller that passes new buffers every step
+    // (fresh pointers, fresh plans) must not accumulate workspaces.  Eviction releases the
+    // victim's memory stream-ordered after its last launch (Plan::~Plan): no host sync.
     const size_t need = workspace_bytes_for(big, dtype);
     const size_t budget = std::max<size_t>((size_t)4 << 30, 2 * need);
     auto held = [&]() {
@@ -1057,29 +1097,70 @@ static ns_status run_plan(const std::vector<Mat>& mats_in, int iters, const floa
       for (auto& kv : g_plans) if (!kv.second->ws_borrowed) b += kv.second->ws_bytes;
       return b;
     };
-    bool synced = false;
-    while (!g_plans.empty() && (g_plans.size() >= kMaxPlans || held() + need > budget)) {
-      auto victim = g_plans.begin();
+    while (g_plans.size() >= kMaxPlans || held() + need > budget) {
+      auto victim = g_plans.end();
       for (auto jt = g_plans.begin(); jt != g_plans.end(); ++jt)
-        if (jt->second->last_use < victim->second->last_use) victim = jt;
-      if (!synced) { cudaDeviceSynchronize(); synced = true; }
+        if (!jt->second->pinned && (victim == g_plans.end() || jt->second->last_use < victim->second->last_use))
+          victim = jt;
+      if (victim == g_plans.end()) break;
       g_plans.erase(victim);
     }
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    CU_TRY(cudaStreamIsCapturing(stream, &cs));
+    if (cs != cudaStreamCaptureStatusNone)
+      return fail(NS_ERR_NOT_SUPPORTED, "the first call of a problem list builds its plan (device allocations, "
+                                        "table upload) and cannot be stream-captured: call it once uncaptured");
     std::unique_ptr<Plan> np(new Plan());
     np->device = dev; np->dtype = dtype; np->simt = simt; np->cg = cg; np->iters = iters; np->precond = precond;
     np->cast = cast;
     np->mats = big;
     np->tiny = tiny;
     HostTables H;
-    st = build_plan(*np, H, dc, coeffs);
-    if (st != NS_OK) return st;
+    ns_status st = build_plan(*np, H, dc, coeffs, stream);
+    if (st != NS_OK) {
+      // nothing was launched; the partly built plan's memory goes back stream-ordered, after
+      // the memset / upload already enqueued on `stream`
+      if (np->ws_borrowed && np->ws)
+        g_uws[dev & 63].used = (size_t)(reinterpret_cast<uint8_t*>(np->ws) - g_uws[dev & 63].base);
+      if (cudaEventCreateWithFlags(&np->last, cudaEventDisableTiming) == cudaSuccess) cudaEventRecord(np->last, stream);
+      cudaGetLastError();
+      return st;
+    }
     P = np.get();
     g_plans[key] = std::move(np);
   } else {
     P = it->second.get();
   }
+  P->pinned = true;
   P->last_use = ++g_tick;
-  return launch_plan(*P, dc, stream);
+  *out = P;
+  return NS_OK;
+}
+
+// One call: resolve (find or build) every plan of the call first, then launch them in order,
+// so a failure while building the second plan leaves nothing enqueued and no caller memory
+// touched (the header's error contract).
+static ns_status run(const std::vector<Mat>& mats_in, int iters, const float* coeffs, ns_precond precond,
+                     ns_dtype dtype, cudaStream_t stream, bool cast = false) {
+  if ((int64_t)mats_in.size() >= kMaxJobs)
+    return fail(NS_ERR_NOT_SUPPORTED, "more than 2^20 - 1 matrices in one call");
+  DevCtx* dc = nullptr;
+  ns_status st = dev_ctx(&dc);
+  if (st != NS_OK) return st;
+  std::vector<std::vector<Mat>> groups;
+  group_mats(mats_in, dtype, cast, dc->cc_major, groups);
+  std::vector<Plan*> plans;
+  for (const auto& g : groups) {
+    Plan* P = nullptr;
+    st = resolve_plan(g, iters, coeffs, precond, dtype, stream, cast, dc, &P);
+    if (st != NS_OK) break;
+    plans.push_back(P);
+  }
+  if (st == NS_OK)
+    for (Plan* P : plans)
+      if ((st = launch_plan(*P, dc, stream)) != NS_OK) break;
+  for (Plan* P : plans) P->pinned = false;
+  return st;
 }
 
 static Mat make_mat(void* x, void* out, int64_t m, int64_t n, int iters) {
@@ -1240,16 +1321,49 @@ ns_status ns_orthogonalize_peers(void* const* X, void* const* out, void* const* 
   return run(mats, iters, coeffs, precond, dtype, reinterpret_cast<cudaStream_t>(stream));
 }
 
-// Muon step: cached device job tables, keyed by the pointer lists.
-static std::map<std::vector<uint64_t>, void*> g_muon_tabs;
+// Muon step: cached device job tables, keyed by the pointer lists (allocated and uploaded
+// stream-ordered; `last` = event after the table's last use).
+struct MuonTab {
+  int device = 0;
+  void* d = nullptr;
+  cudaEvent_t last = nullptr;
+  ~MuonTab() {
+    release_async(device, d, last);
+    if (last) cudaEventDestroy(last);
+  }
+};
+static std::map<std::vector<uint64_t>, std::unique_ptr<MuonTab>> g_muon_tabs;
 
 // The Muon job tables are keyed by pointer lists; a caller with fresh buffers every step
-// would add one per step: past 1024 tables, synchronise and drop them all.
+// would add one per step: past 1024 tables, drop them all (stream-ordered release).
 static void muon_tabs_trim() {
   if (g_muon_tabs.size() < 1024) return;
-  cudaDeviceSynchronize();
-  for (auto& kv : g_muon_tabs) cudaFree(kv.second);
   g_muon_tabs.clear();
+}
+
+static ns_status muon_table(const std::vector<uint64_t>& key, const std::vector<MuonJob>& jobs, cudaStream_t s,
+                            MuonTab** out) {
+  auto it = g_muon_tabs.find(key);
+  if (it != g_muon_tabs.end()) { *out = it->second.get(); return NS_OK; }
+  muon_tabs_trim();
+  std::unique_ptr<MuonTab> t(new MuonTab());
+  CU_TRY(cudaGetDevice(&t->device));
+  const size_t bytes = jobs.size() * sizeof(MuonJob);
+  if (cudaMallocAsync(&t->d, bytes, s) != cudaSuccess) {
+    cudaGetLastError();
+    t->d = nullptr;
+    return fail(NS_ERR_WORKSPACE, "Muon job-table cudaMallocAsync failed");
+  }
+  CU_TRY(cudaMemcpyAsync(t->d, jobs.data(), bytes, cudaMemcpyHostToDevice, s));
+  CU_TRY(cudaEventCreateWithFlags(&t->last, cudaEventDisableTiming));
+  *out = t.get();
+  g_muon_tabs[key] = std::move(t);
+  return NS_OK;
+}
+static void muon_table_used(MuonTab* t, cudaStream_t s) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(s, &cs) == cudaSuccess && cs == cudaStreamCaptureStatusNone) cudaEventRecord(t->last, s);
+  cudaGetLastError();
 }
 
 ns_status ns_muon_step(void* const* W, const void* const* G, float* const* M, void* const* U,
@@ -1287,25 +1401,19 @@ ns_status ns_muon_step(void* const* W, const void* const* G, float* const* M, vo
   if (count > 65535) return fail(NS_ERR_NOT_SUPPORTED, "more than 65535 matrices in one Muon step");
   DevCtx* dc = nullptr;
   if ((st = dev_ctx(&dc)) != NS_OK) return st;
-  auto it = g_muon_tabs.find(key);
-  void* dtab = nullptr;
-  if (it == g_muon_tabs.end()) {
-    muon_tabs_trim();
-    CU_TRY(cudaMalloc(&dtab, jobs.size() * sizeof(MuonJob)));
-    CU_TRY(cudaMemcpy(dtab, jobs.data(), jobs.size() * sizeof(MuonJob), cudaMemcpyHostToDevice));
-    g_muon_tabs[key] = dtab;
-  } else {
-    dtab = it->second;
-  }
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  CU_TRY(launch_muon_momentum(reinterpret_cast<const MuonJob*>(dtab), (int)count, max_numel, g_dtype == NS_BF16,
-                              beta, nesterov, dc->sms, s));
+  MuonTab* tab = nullptr;
+  if ((st = muon_table(key, jobs, s, &tab)) != NS_OK) return st;
+  const MuonJob* dtab = reinterpret_cast<const MuonJob*>(tab->d);
+  CU_TRY(launch_muon_momentum(dtab, (int)count, max_numel, g_dtype == NS_BF16, beta, nesterov, dc->sms, s));
   ++g_launches;
-  if ((st = run(mats, iters, coeffs, precond, NS_BF16, s)) != NS_OK) return st;
-  CU_TRY(launch_muon_apply(reinterpret_cast<const MuonJob*>(dtab), (int)count, max_numel, w_dtype == NS_BF16, lr,
-                           weight_decay, dc->sms, s));
-  ++g_launches;
-  return NS_OK;
+  st = run(mats, iters, coeffs, precond, NS_BF16, s);
+  if (st == NS_OK) {
+    CU_TRY(launch_muon_apply(dtab, (int)count, max_numel, w_dtype == NS_BF16, lr, weight_decay, dc->sms, s));
+    ++g_launches;
+  }
+  muon_table_used(tab, s);
+  return st;
 }
 
 ns_status ns_muon_apply(void* const* W, const void* const* U, const int64_t* m, const int64_t* n, int64_t count,
@@ -1335,47 +1443,62 @@ ns_status ns_muon_apply(void* const* W, const void* const* U, const int64_t* m, 
   }
   DevCtx* dc = nullptr;
   if ((st = dev_ctx(&dc)) != NS_OK) return st;
-  auto it = g_muon_tabs.find(key);
-  void* dtab = nullptr;
-  if (it == g_muon_tabs.end()) {
-    muon_tabs_trim();
-    CU_TRY(cudaMalloc(&dtab, jobs.size() * sizeof(MuonJob)));
-    CU_TRY(cudaMemcpy(dtab, jobs.data(), jobs.size() * sizeof(MuonJob), cudaMemcpyHostToDevice));
-    g_muon_tabs[key] = dtab;
-  } else {
-    dtab = it->second;
-  }
-  CU_TRY(launch_muon_apply(reinterpret_cast<const MuonJob*>(dtab), (int)count, max_numel, w_dtype == NS_BF16, lr,
-                           weight_decay, dc->sms, reinterpret_cast<cudaStream_t>(stream)));
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  MuonTab* tab = nullptr;
+  if ((st = muon_table(key, jobs, s, &tab)) != NS_OK) return st;
+  CU_TRY(launch_muon_apply(reinterpret_cast<const MuonJob*>(tab->d), (int)count, max_numel, w_dtype == NS_BF16, lr,
+                           weight_decay, dc->sms, s));
   ++g_launches;
+  muon_table_used(tab, s);
   return NS_OK;
 }
 
-ns_status ns_workspace_size(const int64_t* m, const int64_t* n, int64_t count, ns_dtype dtype, size_t* bytes) {
-  if (!m || !n || !bytes || count < 1) return fail(NS_ERR_INVALID_VALUE, "bad arguments");
+ns_status ns_workspace_size(const int64_t* m, const int64_t* n, int64_t count, int64_t batch, ns_dtype dtype,
+                            size_t* bytes) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (!m || !n || !bytes || count < 1 || batch < 1) return fail(NS_ERR_INVALID_VALUE, "bad arguments");
   if (dtype != NS_BF16 && dtype != NS_FP32) return fail(NS_ERR_INVALID_VALUE, "bad dtype");
   std::vector<Mat> mats;
   for (int64_t i = 0; i < count; ++i) {
     if (m[i] < 1 || n[i] < 1) return fail(NS_ERR_INVALID_VALUE, "m and n must be >= 1");
-    mats.push_back(make_mat((void*)16, nullptr, m[i], n[i], 2));
+    for (int64_t b = 0; b < batch; ++b) mats.push_back(make_mat((void*)256, nullptr, m[i], n[i], 2));
   }
-  *bytes = workspace_bytes_for(mats, dtype);
+  // the same plan grouping as a call (group_mats), with every matrix counted as needing
+  // workspace (cluster routing depends on the device): an upper bound for any device/path
+  std::vector<std::vector<Mat>> groups;
+  const int old = g_path;
+  g_path = 4;  // no cluster routing: every matrix is counted in its step-engine group
+  group_mats(mats, dtype, false, 10, groups);
+  g_path = old;
+  size_t total = 0;
+  for (const auto& g : groups) total += workspace_bytes_for(g, dtype);
+  *bytes = total;
   return NS_OK;
 }
 
-ns_status ns_set_workspace(void* ptr, size_t bytes) {
+ns_status ns_set_workspace(void* ptr, size_t bytes, void* stream) {
   std::lock_guard<std::mutex> lk(g_mu);
   if (ptr && (bytes < 256 || (reinterpret_cast<uintptr_t>(ptr) & 255)))
     return fail(NS_ERR_INVALID_VALUE, "workspace must be >= 256 bytes and 256-byte aligned");
   int dev = 0;
   CU_TRY(cudaGetDevice(&dev));
   if (dev < 0 || dev >= 64) return fail(NS_ERR_NOT_SUPPORTED, "device index >= 64");
-  CU_TRY(cudaDeviceSynchronize());
-  // drop the cached plans that live in the previous caller buffer
+  DevCtx* dc = nullptr;
+  ns_status st = dev_ctx(&dc);
+  if (st != NS_OK) return st;
+  // drop the cached plans that live in the previous caller buffer; their job tables are
+  // released stream-ordered after their last launch, and work already enqueued keeps its
+  // buffers (the caller keeps the old buffer alive until that work is done, or orders the
+  // new buffer's first use after it on `stream`)
   for (auto it = g_plans.begin(); it != g_plans.end();) {
-    if (it->second->ws_borrowed && it->second->device == dev) it = g_plans.erase(it);
-    else ++it;
+    if (it->second->ws_borrowed && it->second->device == dev) {
+      if (it->second->last && stream) cudaStreamWaitEvent(reinterpret_cast<cudaStream_t>(stream), it->second->last, 0);
+      it = g_plans.erase(it);
+    } else {
+      ++it;
+    }
   }
+  cudaGetLastError();
   g_uws[dev] = UserWs{reinterpret_cast<uint8_t*>(ptr), ptr ? bytes : 0, 0};
   return NS_OK;
 }
@@ -1399,14 +1522,15 @@ void ns_shutdown(void) {
   std::lock_guard<std::mutex> lk(g_mu);
   cudaDeviceSynchronize();
   g_plans.clear();
-  for (auto& kv : g_muon_tabs) cudaFree(kv.second);
   g_muon_tabs.clear();
+  cudaDeviceSynchronize();
   for (auto& d : g_dev) {
     if (d.init && d.flags) cudaFree(d.flags);
     if (d.init && d.side) cudaStreamDestroy(d.side);
     if (d.init && d.ev_fork) cudaEventDestroy(d.ev_fork);
     if (d.init && d.ev_join) cudaEventDestroy(d.ev_join);
     if (d.init && d.cap) cudaStreamDestroy(d.cap);
+    if (d.init && d.freer) cudaStreamDestroy(d.freer);
     d = DevCtx();
   }
 }
@@ -1494,7 +1618,7 @@ static void finish_tiles(GemmJob& J, SimtJob& S) {
   S.tiles = ((S.P + kSimtTile - 1) / kSimtTile) * S.tiles_q;
 }
 
-ns_status nsx_gram(const void* X, int64_t m, int64_t n, void* A, ns_dtype dtype, void* stream) {
+ns_status nsx_gram(const void* X, int64_t m, int64_t n, void* A, float* part, ns_dtype dtype, void* stream) {
   std::lock_guard<std::mutex> lk(g_mu);
   ns_status st;
   if ((st = validate_mat(X, m, n, dtype)) != NS_OK) return st;
@@ -1511,6 +1635,10 @@ ns_status nsx_gram(const void* X, int64_t m, int64_t n, void* A, ns_dtype dtype,
   if (!wide) { S.sa_p = S.sb_q = 1; S.sa_k = S.sb_k = n; } else { S.sa_p = S.sb_q = n; S.sa_k = S.sb_k = 1; }
   finish_tiles(J, S);
   const bool simt = step_simt(dtype, m, n, {X, A});
+  if (part) {  // AOL row-sum partials of the Gram epilogue (production layout, GemmJob::part)
+    if (simt) return fail(NS_ERR_NOT_SUPPORTED, "Gram partials come from the tcgen05 epilogue (aligned bf16 only)");
+    J.part = part; J.part_ld = part_ld_for(N);
+  }
   return one_gemm(J, {X, (int)m, (int)n}, {X, (int)m, (int)n}, {A, (int)N, (int)N}, {nullptr, 0, 0}, S, simt, dtype,
                   reinterpret_cast<cudaStream_t>(stream));
 }
@@ -1564,7 +1692,8 @@ ns_status nsx_update(const void* X, int64_t m, int64_t n, const void* B, float a
                   reinterpret_cast<cudaStream_t>(stream), N);
 }
 
-ns_status nsx_precondition(void* A, int64_t N, ns_precond precond, float* s, ns_dtype dtype, void* stream) {
+ns_status nsx_precondition(void* A, int64_t N, ns_precond precond, const float* part, float* s, ns_dtype dtype,
+                           void* stream) {
   std::lock_guard<std::mutex> lk(g_mu);
   ns_status st;
   if ((st = validate_mat(A, N, N, dtype)) != NS_OK) return st;
@@ -1578,13 +1707,19 @@ ns_status nsx_precondition(void* A, int64_t N, ns_precond precond, float* s, ns_
   PrecondJob J;
   std::memset(&J, 0, sizeof(J));
   J.A = A; J.s = s; J.N = (int)N; J.precond = (int)precond;
+  if (part) {
+    if (precond != NS_PRECOND_AOL || dtype != NS_BF16)
+      return fail(NS_ERR_INVALID_VALUE, "partials are AOL row sums of a bf16 Gram");
+    J.part = part; J.part_ld = part_ld_for(N);
+  }
+  const bool lane_rows = part && J.part_ld <= kSeqPartials;
   void* dmem = nullptr;
   CU_TRY(cudaMalloc(&dmem, 256 + sizeof(J)));
   CU_TRY(cudaMemset(dmem, 0, 256));  // grid-barrier words
   CU_TRY(cudaMemcpy(reinterpret_cast<uint8_t*>(dmem) + 256, &J, sizeof(J), cudaMemcpyHostToDevice));
   cudaError_t e = launch_precondition(reinterpret_cast<const PrecondJob*>(reinterpret_cast<uint8_t*>(dmem) + 256), 1,
-                                      N, vec8 ? N * N / 8 : N * N, vec8, dtype == NS_BF16,
-                                      reinterpret_cast<unsigned*>(dmem), dc->flags, false, strm);
+                                      N, precond_segments((int)N, 0), vec8, dtype == NS_BF16,
+                                      reinterpret_cast<unsigned*>(dmem), dc->flags, lane_rows, strm);
   ++g_launches;
   cudaError_t e2 = cudaStreamSynchronize(strm);
   cudaFree(dmem);

@@ -116,9 +116,18 @@ struct PrecondJob {
   int32_t half;       // A stored as lower-triangle 256-blocks: rescale only those
   int32_t N;
   int32_t precond;  // 1 Frobenius, 2 AOL
-  int64_t row_start;  // prefix over jobs of N (AOL: one warp per row)
-  int64_t vec_start;  // prefix over jobs of ceil(N*N / 8) (rescale: 16-byte vectors)
+  int64_t row_start;  // prefix over jobs of N (phase 1: one warp per row)
+  int64_t seg_start;  // prefix over jobs of precond_segments(N, half) (phase 2: one warp per segment)
 };
+// Phase-2 work units of one matrix (precond_rows.cuh): stored rows cut into 256-column
+// segments; with half storage row i (in 256-block bi) holds columns [0, min(N, 256 (bi + 1))).
+__host__ __device__ inline int64_t precond_segments(int N, int half) {
+  const int64_t nb = (N + 255) / 256;
+  if (!half) return (int64_t)N * nb;
+  // full blocks 0..nb-2 have 256 rows of bi + 1 segments; the last block N - 256 (nb - 1) rows
+  return 256 * (nb - 1) * nb / 2 + (int64_t)(N - 256 * (nb - 1)) * nb;
+}
+
 
 // One matrix of a Muon optimizer step (muon.cu).
 struct MuonJob {

@@ -28,11 +28,13 @@ cudaError_t launch_simt_gemm(const SimtJob* d_jobs, int njobs, int64_t total_til
 
 // Fused AOL / Frobenius preconditioner (simt.cu): row-abs-sum (or trace) + rsqrt, grid
 // barrier, then A <- diag(s) A diag(s).  `barrier` points at two zero-initialised uint32
-// words (arrival count, generation) owned by the caller; the barrier resets itself.  vec8 = all N are multiples of 8 (16-byte vectors).
+// words (arrival count, generation) owned by the caller; the barrier resets itself.
+// total_segs = sum of precond_segments(N, half) over jobs (PrecondJob::seg_start prefix);
+// vec8 = all N are multiples of 8 and A 16-byte aligned (16-byte vectors).
 // lane_rows: AOL from Gram partials with part_ld <= kSeqPartials for every job -> phase 1
 // runs one lane per row (precond_rows.cuh).
 cudaError_t launch_precondition(const PrecondJob* d_jobs, int njobs, int64_t total_rows,
-                                int64_t total_elems_or_vecs, bool vec8, bool is_bf16,
+                                int64_t total_segs, bool vec8, bool is_bf16,
                                 unsigned* d_barrier, uint32_t* d_flags, bool lane_rows, cudaStream_t stream);
 
 // Split-K Gram reduction (simt.cu): one warp per row of every job (bf16 storage).

@@ -1,6 +1,7 @@
-// Row-level work of the AOL / Frobenius preconditioner (Eqs. 7-11, Alg. 2 l.2-4),
-// shared by the standalone cooperative kernel (simt.cu) and the fused single-launch mode of
-// the tcgen05 engine (umma_gemm.cu).  One warp handles one row of one matrix.
+// Work units of the AOL / Frobenius preconditioner kernel (simt.cu; Eqs. 7-11,
+// Alg. 2 l.2-4).  Phase 1 (scaling vector s): one warp per row of one matrix.  Phase 2
+// (A1 = diag(s) A0 diag(s)): one warp per 256-column segment of a stored row, so every warp
+// moves the same bytes whatever the matrix sizes and the half storage.
 #pragma once
 #include <cuda_bf16.h>
 
@@ -111,45 +112,56 @@ __device__ __forceinline__ void precond_row_s(const PrecondJob& J, int i, int la
   }
 }
 
-// Phase 2 for row i: A1[i][:] = s_i A0[i][:] s_:  (Alg. 2 l.4), 16-byte vectors along the row.
+// Phase 2 segments of one matrix.  A stored row is cut into 256-column segments; with half
+// storage row i (in 256-block bi) holds columns [0, min(N, 256 (bi + 1))), i.e. bi + 1
+// segments, else ceil(N / 256).  Segments are numbered row by row (columns fastest), so
+// consecutive segment indices are consecutive bytes of A.
+// Segment g of a matrix -> (row, first column).
+__device__ __forceinline__ void precond_seg_pos(int N, int half, int64_t g, int& row, int& col) {
+  if (!half) {
+    const int nb = (N + 255) / 256;
+    row = (int)(g / nb);
+    col = (int)(g % nb) * 256;
+    return;
+  }
+  // block bi starts at segment 128 bi (bi + 1): solve, then correct the float estimate
+  int bi = (int)((sqrtf(1.f + (float)g / 32.f) - 1.f) * 0.5f);
+  while (bi > 0 && 128 * (int64_t)bi * (bi + 1) > g) --bi;
+  while (128 * (int64_t)(bi + 1) * (bi + 2) <= g) ++bi;
+  const int64_t r = g - 128 * (int64_t)bi * (bi + 1);
+  row = 256 * bi + (int)(r / (bi + 1));
+  col = (int)(r % (bi + 1)) * 256;
+}
+
+// Phase 2 for one segment: A1[i][c..c+256) = s_i A0[i][c..c+256) s_c..  (Alg. 2 l.4); each
+// lane owns 8 consecutive elements (one 16-byte vector in bf16).
 template <typename T, bool VEC8>
-__device__ __forceinline__ void precond_row_scale(const PrecondJob& J, int i, int lane) {
-  // half storage: row i holds blocks 0..bi only (the rest is never read)
+__device__ __forceinline__ void precond_seg_scale(const PrecondJob& J, int i, int c0, int lane) {
   const int N = J.half ? min(J.N, (i / 256 + 1) * 256) : J.N;
   const float si = J.s[i];
   T* Ai = reinterpret_cast<T*>(J.A) + (int64_t)i * J.N;
+  const int j = c0 + lane * 8;
   if (VEC8 && sizeof(T) == 2) {
-    // up to 4 vectors per lane in flight: all loads of a batch before any store
-    for (int j0 = lane * 8; j0 < N; j0 += 4 * 256) {
-      uint4 u[4];
-      float4 s0[4], s1[4];
+    if (j < N) {
+      const uint4 u = *reinterpret_cast<const uint4*>(Ai + j);
+      const float4 s0 = *reinterpret_cast<const float4*>(J.s + j);
+      const float4 s1 = *reinterpret_cast<const float4*>(J.s + j + 4);
+      const float sj[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
+      uint32_t w[4] = {u.x, u.y, u.z, u.w};
 #pragma unroll
-      for (int v = 0; v < 4; ++v) {
-        const int j = j0 + v * 256;
-        if (j < N) {
-          u[v] = *reinterpret_cast<const uint4*>(Ai + j);
-          s0[v] = *reinterpret_cast<const float4*>(J.s + j);
-          s1[v] = *reinterpret_cast<const float4*>(J.s + j + 4);
-        }
+      for (int e = 0; e < 4; ++e) {
+        const float lo = (si * __uint_as_float(w[e] << 16)) * sj[2 * e];
+        const float hi = (si * __uint_as_float(w[e] & 0xFFFF0000u)) * sj[2 * e + 1];
+        w[e] = (uint32_t)st_conv<uint16_t>(lo) | ((uint32_t)st_conv<uint16_t>(hi) << 16);
       }
-#pragma unroll
-      for (int v = 0; v < 4; ++v) {
-        const int j = j0 + v * 256;
-        if (j < N) {
-          const float sj[8] = {s0[v].x, s0[v].y, s0[v].z, s0[v].w, s1[v].x, s1[v].y, s1[v].z, s1[v].w};
-          uint32_t w[4] = {u[v].x, u[v].y, u[v].z, u[v].w};
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const float lo = (si * __uint_as_float(w[e] << 16)) * sj[2 * e];
-            const float hi = (si * __uint_as_float(w[e] & 0xFFFF0000u)) * sj[2 * e + 1];
-            w[e] = (uint32_t)st_conv<uint16_t>(lo) | ((uint32_t)st_conv<uint16_t>(hi) << 16);
-          }
-          *reinterpret_cast<uint4*>(Ai + j) = make_uint4(w[0], w[1], w[2], w[3]);
-        }
-      }
+      *reinterpret_cast<uint4*>(Ai + j) = make_uint4(w[0], w[1], w[2], w[3]);
     }
   } else {
-    for (int j = lane; j < N; j += 32) Ai[j] = st_conv<T>((si * ld_val<T>(Ai + j)) * J.s[j]);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const int jj = c0 + e * 32 + lane;  // lanes side by side: coalesced scalar accesses
+      if (jj < N) Ai[jj] = st_conv<T>((si * ld_val<T>(Ai + jj)) * J.s[jj]);
+    }
   }
 }
 

@@ -6,8 +6,11 @@
 //     phase 1: one warp per row of A0, s_i = rsqrt(sum_j |A0_ij|) (Eq. 8) with vectorised
 //     16-byte loads and a fixed-order warp-shuffle reduction (deterministic); Frobenius:
 //     s = rsqrt(trace A0) = 1/||X||_F (Eq. 10);  grid barrier;  phase 2: A1 = s_i A0_ij s_j
-//     in place (Alg. 2 l.4, "Update A to avoid recomputation").  HBM-bound.
+//     in place (Alg. 2 l.4, "Update A to avoid recomputation"), one warp per 256-column
+//     segment of a stored row (equal bytes per warp under half storage).  HBM-bound.
 #include <cuda_bf16.h>
+
+#include <algorithm>
 #include <cuda_runtime.h>
 
 #include "jobs.h"
@@ -145,20 +148,18 @@ __device__ __forceinline__ void grid_barrier(unsigned* bar) {
 template <typename T, bool VEC8>
 __global__ void __launch_bounds__(256)
     precondition_kernel(const PrecondJob* __restrict__ jobs, int njobs, int64_t total_rows,
-                        int64_t total_items, unsigned* barrier, uint32_t* __restrict__ flags, int lane_rows) {
+                        int64_t total_segs, unsigned* barrier, uint32_t* __restrict__ flags, int lane_rows) {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   asm volatile("griddepcontrol.wait;" ::: "memory");  // A0 comes from the preceding Gram launch
-  (void)total_items;
   const int lane = threadIdx.x & 31;
   const int64_t gwarp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   uint32_t fl = 0;
-  // each warp owns a contiguous run of rows: one job lookup per run, not per row
+  // ---- phase 1: scaling vector s (Eq. 8 / Eq. 10); each warp owns a contiguous run of rows
   const int64_t per = (total_rows + nwarps - 1) / nwarps;
   const int64_t r_beg = gwarp * per, r_end = min(total_rows, r_beg + per);
-  // ---- phase 1: scaling vector s (Eq. 8 / Eq. 10)
   if (lane_rows) {  // AOL from partials, every job with part_ld <= kSeqPartials
-    // AOL from partials: one LANE per row (<= 40 independent loads each), 32 rows per warp
+    // AOL from partials: one LANE per row (<= 64 independent loads each), 32 rows per warp
     // at a time -- the row sums are short, so rows, not columns, carry the parallelism
     for (int64_t row0 = r_beg; row0 < r_end; row0 += 32) {
       const int64_t row = row0 + lane;
@@ -180,12 +181,61 @@ __global__ void __launch_bounds__(256)
     }
   }
   grid_barrier(barrier);
-  // ---- phase 2: A1 = diag(s) A0 diag(s)  (Alg. 2 l.4)
-  if (r_beg < r_end) {
-    int jb = find_pjob(jobs, njobs, r_beg);
-    for (int64_t row = r_beg; row < r_end; ++row) {
-      while (jb + 1 < njobs && jobs[jb + 1].row_start <= row) ++jb;
-      precond_row_scale<T, VEC8>(jobs[jb], (int)(row - jobs[jb].row_start), lane);
+  // ---- phase 2: A1 = diag(s) A0 diag(s)  (Alg. 2 l.4), one warp per 256-column segment of a
+  // stored row (equal bytes per warp under half storage), 4 consecutive segments per warp
+  // per round with all loads issued before any store
+  constexpr int kU = 4;
+  for (int64_t g0 = gwarp * kU; g0 < total_segs; g0 += nwarps * kU) {
+    int jb[kU], row[kU], col[kU];
+#pragma unroll
+    for (int v = 0; v < kU; ++v) {
+      const int64_t g = g0 + v;
+      jb[v] = -1;
+      if (g < total_segs) {
+        int lo = 0, hi = njobs - 1;
+        while (lo < hi) {
+          const int mid = (lo + hi + 1) >> 1;
+          if (jobs[mid].seg_start <= g) lo = mid; else hi = mid - 1;
+        }
+        jb[v] = lo;
+        precond_seg_pos(jobs[lo].N, jobs[lo].half, g - jobs[lo].seg_start, row[v], col[v]);
+      }
+    }
+    if constexpr (VEC8 && sizeof(T) == 2) {
+      uint4 u[kU];
+      float4 s0[kU], s1[kU];
+      float si[kU];
+#pragma unroll
+      for (int v = 0; v < kU; ++v) {
+        if (jb[v] < 0) continue;
+        const PrecondJob& J = jobs[jb[v]];
+        const int lim = J.half ? min(J.N, (row[v] / 256 + 1) * 256) : J.N;
+        const int j = col[v] + lane * 8;
+        if (j >= lim) { jb[v] = -1; continue; }
+        u[v] = *reinterpret_cast<const uint4*>(reinterpret_cast<const uint16_t*>(J.A) + (int64_t)row[v] * J.N + j);
+        s0[v] = *reinterpret_cast<const float4*>(J.s + j);
+        s1[v] = *reinterpret_cast<const float4*>(J.s + j + 4);
+        si[v] = J.s[row[v]];
+      }
+#pragma unroll
+      for (int v = 0; v < kU; ++v) {
+        if (jb[v] < 0) continue;
+        const PrecondJob& J = jobs[jb[v]];
+        const float sj[8] = {s0[v].x, s0[v].y, s0[v].z, s0[v].w, s1[v].x, s1[v].y, s1[v].z, s1[v].w};
+        uint32_t w[4] = {u[v].x, u[v].y, u[v].z, u[v].w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float lo = (si[v] * __uint_as_float(w[e] << 16)) * sj[2 * e];
+          const float hi = (si[v] * __uint_as_float(w[e] & 0xFFFF0000u)) * sj[2 * e + 1];
+          w[e] = (uint32_t)st_conv<uint16_t>(lo) | ((uint32_t)st_conv<uint16_t>(hi) << 16);
+        }
+        *reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(J.A) + (int64_t)row[v] * J.N + col[v] + lane * 8) =
+            make_uint4(w[0], w[1], w[2], w[3]);
+      }
+    } else {
+#pragma unroll
+      for (int v = 0; v < kU; ++v)
+        if (jb[v] >= 0) precond_seg_scale<T, false>(jobs[jb[v]], row[v], col[v], lane);
     }
   }
   if (fl) atomicOr(flags, fl);
@@ -193,7 +243,7 @@ __global__ void __launch_bounds__(256)
 
 template <typename T, bool V>
 static cudaError_t launch_precond_t(const PrecondJob* d_jobs, int njobs, int64_t total_rows,
-                                    int64_t total_items, unsigned* d_barrier, uint32_t* d_flags,
+                                    int64_t total_segs, unsigned* d_barrier, uint32_t* d_flags,
                                     int lane_rows, cudaStream_t stream) {
   auto kern = precondition_kernel<T, V>;
   int dev = 0, sms = 0, occ = 0;
@@ -201,7 +251,10 @@ static cudaError_t launch_precond_t(const PrecondJob* d_jobs, int njobs, int64_t
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, 0);
   if (occ < 1) occ = 1;
-  const int64_t want = (total_rows * 32 + 255) / 256;  // one warp per row
+  // one warp per row (phase 1) and per 4 segments (phase 2), at most the co-resident grid
+  // (cooperative launch: the grid barrier needs every CTA resident)
+  const int64_t warps = std::max<int64_t>(total_rows, (total_segs + 3) / 4);
+  const int64_t want = (warps * 32 + 255) / 256;
   int64_t cap = (int64_t)sms * occ;
   int grid = (int)(want < cap ? (want < 1 ? 1 : want) : cap);
   cudaLaunchConfig_t cfg = {};
@@ -215,7 +268,7 @@ static cudaError_t launch_precond_t(const PrecondJob* d_jobs, int njobs, int64_t
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 2;
-  return cudaLaunchKernelEx(&cfg, kern, d_jobs, njobs, total_rows, total_items, d_barrier, d_flags, lane_rows);
+  return cudaLaunchKernelEx(&cfg, kern, d_jobs, njobs, total_rows, total_segs, d_barrier, d_flags, lane_rows);
 }
 
 // ------------------------------------------------------------------------------ split-K Gram
@@ -284,14 +337,14 @@ cudaError_t launch_split_reduce(const SplitJob* d_jobs, int njobs, int64_t total
 }
 
 cudaError_t launch_precondition(const PrecondJob* d_jobs, int njobs, int64_t total_rows,
-                                int64_t total_items, bool vec8, bool is_bf16, unsigned* d_barrier,
+                                int64_t total_segs, bool vec8, bool is_bf16, unsigned* d_barrier,
                                 uint32_t* d_flags, bool lane_rows, cudaStream_t stream) {
   const int lr = lane_rows ? 1 : 0;
   if (is_bf16) {
-    return vec8 ? launch_precond_t<uint16_t, true>(d_jobs, njobs, total_rows, total_items, d_barrier, d_flags, lr, stream)
-                : launch_precond_t<uint16_t, false>(d_jobs, njobs, total_rows, total_items, d_barrier, d_flags, lr, stream);
+    return vec8 ? launch_precond_t<uint16_t, true>(d_jobs, njobs, total_rows, total_segs, d_barrier, d_flags, lr, stream)
+                : launch_precond_t<uint16_t, false>(d_jobs, njobs, total_rows, total_segs, d_barrier, d_flags, lr, stream);
   }
-  return launch_precond_t<float, false>(d_jobs, njobs, total_rows, total_items, d_barrier, d_flags, lr, stream);
+  return launch_precond_t<float, false>(d_jobs, njobs, total_rows, total_segs, d_barrier, d_flags, lr, stream);
 }
 
 }  // namespace tns

@@ -111,10 +111,11 @@ def _make_plan(shapes, world: int, iters: int, buckets: int) -> ShardPlan:
 
 
 _BUFFERS: dict = {}
-# Per-call caches (prepared argument arrays + views for one exact list of tensors) hold
-# strong references to the caller's tensors, so they are kept in a small LRU: a caller that
-# passes fresh tensors every step neither leaks them nor reuses a stale entry (an id()
-# cannot be recycled while its entry is alive).
+# Per-call caches (prepared argument arrays + views for one exact list of tensors) are keyed
+# by the tensors' ids, shapes and dtype and hold strong references to the tensors themselves
+# (ent["xs"]), so an id cannot be recycled while its entry is alive; they are kept in a small
+# LRU, so a caller that passes fresh tensors every step neither leaks them nor reuses a stale
+# entry.
 _CALLS: "collections.OrderedDict" = None
 _MAX_CALLS = 16
 
@@ -243,8 +244,8 @@ def orthogonalize_sharded(xs: Sequence[torch.Tensor], group=None, iters: int = 4
     dtype, device = xs[0].dtype, xs[0].device
     # steady state: same tensors every step -> packed buffer, views and the prepared
     # argument arrays of every bucket are built once (host overhead ~tens of us per step)
-    ckey = ("call", tuple(id(t) for t in xs), world, rank, buckets, iters, precond,
-            None if coeffs is None else tuple(map(tuple, coeffs)), id(group), compute is None)
+    ckey = ("call", tuple(id(t) for t in xs), tuple(tuple(t.shape) for t in xs), dtype, world, rank, buckets,
+            iters, precond, None if coeffs is None else tuple(map(tuple, coeffs)), id(group), compute is None)
     ent = _call_get(ckey)
     if ent is None or (ent["calls"] and not all(c.valid() for c in ent["calls"] if c is not None)):
         shapes = [tuple(t.shape) for t in xs]
@@ -260,7 +261,7 @@ def orthogonalize_sharded(xs: Sequence[torch.Tensor], group=None, iters: int = 4
                 calls.append(PreparedCall([xs[i] for i in mine], [views[i] for i in mine], iters, precond, coeffs))
             else:
                 calls.append(None)
-        ent = {"plan": plan, "buf": buf, "views": views, "calls": calls}
+        ent = {"plan": plan, "buf": buf, "views": views, "calls": calls, "xs": xs}
         _call_put(ckey, ent)
     plan, buf, views = ent["plan"], ent["buf"], ent["views"]
     cuda = device.type == "cuda"
@@ -341,8 +342,8 @@ def orthogonalize_host(host_xs: Sequence[torch.Tensor], group=None, iters: int =
     dtype = host_xs[0].dtype
     # steady state (same host tensors every step): buffers, views, per-bucket copy lists and
     # prepared NS calls are built once, so many small buckets stay cheap on the host
-    ckey = ("hostcall", tuple(id(t) for t in host_xs), world, rank, buckets, iters, precond,
-            None if coeffs is None else tuple(map(tuple, coeffs)), id(group), str(device))
+    ckey = ("hostcall", tuple(id(t) for t in host_xs), tuple(tuple(t.shape) for t in host_xs), dtype, world, rank,
+            buckets, iters, precond, None if coeffs is None else tuple(map(tuple, coeffs)), id(group), str(device))
     ent = _call_get(ckey)
     if ent is None:
         shapes = [tuple(t.shape) for t in host_xs]
@@ -355,7 +356,7 @@ def orthogonalize_host(host_xs: Sequence[torch.Tensor], group=None, iters: int =
         from .api import PreparedCall
         calls = [PreparedCall([dev_in[i] for i in pr[rank]], [views[i] for i in pr[rank]], iters, precond, coeffs)
                  if pr[rank] and device.type == "cuda" else None for pr in plan.buckets]
-        ent = {"plan": plan, "dev_in": dev_in, "buf": buf, "hout": hout, "calls": calls,
+        ent = {"plan": plan, "dev_in": dev_in, "buf": buf, "hout": hout, "calls": calls, "xs": host_xs,
                "outs": [hout[o:o + m * n].view(m, n) for o, (m, n) in zip(plan.offsets, shapes)]}
         _call_put(ckey, ent)
     plan, dev_in, buf, hout = ent["plan"], ent["dev_in"], ent["buf"], ent["hout"]

@@ -30,7 +30,7 @@ def test_library_exports_every_declared_symbol():
     for s in declared_symbols():
         assert hasattr(_lib.lib, s), s
     assert set(_lib.EXPORTS) == set(declared_symbols())
-    assert _lib.lib.ns_abi_version() == 1
+    assert _lib.lib.ns_abi_version() == 2
 
 
 def test_invalid_arguments_rejected_on_host():
@@ -72,10 +72,12 @@ def test_product_does_not_import_oracle():
                 assert not re.search(r"^\s*(import|from)\s+oracle\b|ns_oracle|#include.*oracle", src, re.M), f
 
 
-def test_product_polar_express_matches_test_generator():
-    from paper_2512_04632_b200 import coeffs as P
-    from synth import polar_express as PE
-    for t in (1, 3, 5, 9):
-        for saf in (0.0, 2e-2):
-            a, b = P.polar_express(t, safety=saf), PE.polar_express(t, safety=saf)
-            np.testing.assert_allclose(np.array(a), np.array(b), rtol=1e-12, atol=1e-12)
+def test_workspace_size_groups_and_batch():
+    """ns_workspace_size sizes a call as the planner runs it: a bf16 list mixing a TMA-
+    unaligned shape (n = 49) with aligned ones is two plans, each with its own 1 KiB header;
+    `batch` repeats every shape (the two-plan split was under-counted)."""
+    import paper_2512_04632_b200 as ns
+    a, u = (1024, 1024), (960, 49)
+    assert ns.workspace_size([a, u]) == ns.workspace_size([a]) + ns.workspace_size([u])
+    assert ns.workspace_size([a, a, a]) == ns.workspace_size([a], batch=3)
+    assert ns.workspace_size([a, u], batch=2) == ns.workspace_size([a, a]) + ns.workspace_size([u, u])

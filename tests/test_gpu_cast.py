@@ -9,7 +9,7 @@ import torch
 
 from synth import coeffs as C
 from synth import inputs as I
-from tests.helpers import oracle_run, relF
+from tests.helpers import oracle_run, relF, assert_parity
 
 pytestmark = pytest.mark.gpu
 
@@ -52,7 +52,7 @@ def test_cast_parity_with_oracle_and_repeat():
     torch.cuda.synchronize()
     for o, x in zip(outs, xs):
         ref = oracle_run(I.round_bf16(x), C.turbo(4), "aol")
-        assert relF(o.cpu().numpy().astype(np.float64), ref) <= 2e-2
+        assert_parity(o.cpu().numpy().astype(np.float64), ref, 2e-2)
 
 
 def test_cast_rejects_bad_combinations():

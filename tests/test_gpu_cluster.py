@@ -16,7 +16,7 @@ import torch
 from oracle import ns_oracle as O
 from synth import coeffs as C
 from synth import inputs as I
-from tests.helpers import oracle_run, polar_excess, relF
+from tests.helpers import oracle_run, polar_excess, relF, assert_parity
 
 pytestmark = pytest.mark.gpu
 
@@ -59,9 +59,7 @@ def test_cluster_aol4(m, n, dtype):
     out, launches = _run(x, C.turbo(4), "aol", dtype)
     assert launches == 1  # the whole NS in one cluster launch
     ref = oracle_run(x, C.turbo(4), "aol")
-    assert np.all(np.isfinite(out))
-    r = relF(out, ref)
-    assert r <= (BF16_TOL if dtype == torch.bfloat16 else FP32_TOL), r
+    assert_parity(out, ref, BF16_TOL if dtype == torch.bfloat16 else FP32_TOL, f"{m}x{n}")
     if min(m, n) > 1:
         eg, eo = polar_excess(out, ref, x)
         assert eg <= 1.05 * eo + (1e-6 if dtype == torch.float32 else 0.0), (eg, eo)
@@ -76,7 +74,7 @@ def test_cluster_preconds_and_odd_iters(m, n, precond, coeffs):
         x = I.round_bf16(x / np.float32(4 * np.sqrt(max(m, n))))
     out, launches = _run(x, coeffs, precond)
     assert launches == 1
-    assert relF(out, oracle_run(x, coeffs, precond)) <= BF16_TOL
+    assert_parity(out, oracle_run(x, coeffs, precond), BF16_TOL)
 
 
 @pytest.mark.parametrize("dist", ["lowrank", "levy1.0", "levy1.5"])
@@ -84,7 +82,7 @@ def test_cluster_distributions(dist):
     x = I.make_matrix(64, 576, seed=11, dist=dist)
     out, _ = _run(x, C.turbo(4), "aol")
     ref = oracle_run(x, C.turbo(4), "aol")
-    assert relF(out, ref) <= BF16_TOL
+    assert_parity(out, ref, BF16_TOL)
 
 
 def test_cluster_matches_step_engine():
@@ -106,7 +104,7 @@ def test_cluster_eligibility_boundary():
         x = I.gaussian(m, 128, seed=13)
         out, launches = _run(x, C.turbo(4), "aol")
         assert launches == want, (m, launches)
-        assert relF(out, oracle_run(x, C.turbo(4), "aol")) <= BF16_TOL
+        assert_parity(out, oracle_run(x, C.turbo(4), "aol"), BF16_TOL)
 
 
 def test_cluster_determinism_and_scale_invariance_bitwise():
@@ -133,7 +131,7 @@ def test_cluster_zero_column_and_zero_matrix_flags():
     out, _ = _run(x, C.turbo(4), "aol")
     assert ns.read_flags() & 1
     assert np.all(np.isfinite(out)) and np.all(out[:, 9] == 0)
-    assert relF(out, oracle_run(x, C.turbo(4), "aol")) <= BF16_TOL
+    assert_parity(out, oracle_run(x, C.turbo(4), "aol"), BF16_TOL)
     z = np.zeros((32, 48), dtype=np.float32)
     out, _ = _run(z, C.muon_plus(5), "frobenius")
     assert ns.read_flags() & 1

@@ -1,0 +1,123 @@
+"""Oracle parity at the metric's own configurations and the paper's stress cases (GPU).
+
+* Square sweep (BASELINE configs[3]; the headline 8192^2 of Fig. 1, and
+  the App. C sizes, L704-707): 2048^2, 4096^2, 8192^2, Turbo-Muon (AOL, T = 4) and the
+  Muon+ comparator (Frobenius, T = 5), element by element against the fp64 oracle (global,
+  per-row, per-column and max-abs gates, tests/helpers.assert_parity) and the polar error
+  of both against the exact polar factor (X (X^T X)^(-1/2) via syevd at these
+  sizes, oracle.polar_exact_gram).  N >= 1376 runs the warp-tree branch of the AOL row-sum
+  reduction over the Gram epilogue's partials (precond_rows.cuh) and, at 8192^2, the
+  32-block partial layout.
+* Polar-Express schedules t = 1..9 (Fig. 4, App. D; reading R14):
+  first-step coefficients up to a = 8.29, c = 17.3 through the CUDA path.
+* Levy alpha = 1 at 4096 x 1024 (App. B): the heavy-tailed stress family at a
+  GPT-2-medium shape.
+* The AOL row sums from the Gram epilogue's partials (the production branches) in the
+  single-step entry points nsx_gram / nsx_precondition.
+
+The fp64 oracle at 8192^2 takes ~30-60 s on the box's host cores; each size runs once.
+"""
+import numpy as np
+import pytest
+import torch
+
+from oracle import ns_oracle as O
+from synth import coeffs as C
+from synth import inputs as I
+from synth import polar_express as PE
+from tests.helpers import assert_parity, oracle_run
+
+pytestmark = pytest.mark.gpu
+
+ns = pytest.importorskip("paper_2512_04632_b200")
+
+BF16_TOL = 2e-2
+POLAR_SLACK = 1.05
+
+
+def _gpu(x32: np.ndarray, coeffs, precond: str) -> np.ndarray:
+    t = torch.from_numpy(np.ascontiguousarray(x32, dtype=np.float32)).to(torch.bfloat16).cuda()
+    ns.orthogonalize(t, iters=len(coeffs), precond=precond, coeffs=coeffs)
+    torch.cuda.synchronize()
+    out = t.float().cpu().numpy().astype(np.float64)
+    del t
+    return out
+
+
+@pytest.mark.parametrize("n", [2048, 4096, 8192])
+def test_square_sweep_full_size(n):
+    """Config 4 at full size: AOL T=4 and Frobenius T=5 on the same Gaussian matrix."""
+    x = I.gaussian(n, n, seed=I.matrix_seed(4, n))
+    q = O.polar_exact_gram(x.astype(np.float64))
+    for precond, coeffs in (("aol", C.turbo(4)), ("frobenius", C.muon_plus(5))):
+        out = _gpu(x, coeffs, precond)
+        ref = oracle_run(x, coeffs, precond)
+        res = assert_parity(out, ref, BF16_TOL, f"{n}^2 {precond}")
+        eg, eo = O.polar_error(out, q), O.polar_error(ref, q)
+        print(f"{n}^2 {precond}: {res}, polar gpu {eg:.5f} oracle {eo:.5f}")
+        assert eg <= POLAR_SLACK * eo, (precond, eg, eo)
+        del out, ref
+    assert ns.read_flags() == 0
+
+
+@pytest.mark.parametrize("m,n", [(1536, 1536), (1400, 3000)])
+def test_aol_large_n_partials_tree(m, n):
+    """N >= 1376 (part_ld > 64): the AOL row sums run the warp-tree branch; a wide shape
+    (m < n, orientation by descriptors) with a ragged last 256-block (1400 = 5 * 256 + 120)."""
+    x = I.gaussian(m, n, seed=I.matrix_seed(13, m + n))
+    out = _gpu(x, C.turbo(4), "aol")
+    ref = oracle_run(x, C.turbo(4), "aol")
+    assert_parity(out, ref, BF16_TOL, f"{m}x{n}")
+    q = O.polar_exact_gram(x.astype(np.float64))
+    assert O.polar_error(out, q) <= POLAR_SLACK * O.polar_error(ref, q)
+
+
+@pytest.mark.parametrize("t", list(range(1, 10)))
+def test_polar_express_schedules(t):
+    """Fig. 4's recomputed Polar-Express schedules (t = 1..9, default l, cushion and safety of
+    App. D) through the CUDA path, AOL and Frobenius, against the oracle with the same
+    coefficient array.  t = 1 is a single large-coefficient step (a = 8.29, c = 17.3)."""
+    cf = [tuple(map(float, c)) for c in PE.polar_express(t)]
+    x = I.gaussian(1024, 768, seed=I.matrix_seed(14, t))
+    for precond in ("aol", "frobenius"):
+        out = _gpu(x, cf, precond)
+        ref = oracle_run(x, cf, precond)
+        assert_parity(out, ref, BF16_TOL, f"PE t={t} {precond}")
+        if t >= 4:  # the polar-error comparison is meaningful once the iteration has converged
+            q = O.polar_exact(x.astype(np.float64))
+            assert O.polar_error(out, q) <= POLAR_SLACK * O.polar_error(ref, q)
+
+
+def test_levy_alpha1_gpt2_medium_shape():
+    """App. B's heaviest tail (alpha = 1, Cauchy-like entries) at 4096 x 1024."""
+    x = I.levy(4096, 1024, seed=I.matrix_seed(15, 1), alpha=1.0)
+    for precond, coeffs in (("aol", C.turbo(4)), ("frobenius", C.muon_plus(5))):
+        out = _gpu(x, coeffs, precond)
+        ref = oracle_run(x, coeffs, precond)
+        assert_parity(out, ref, BF16_TOL, f"levy1 {precond}")
+        q = O.polar_exact_gram(x.astype(np.float64))
+        assert O.polar_error(out, q) <= POLAR_SLACK * O.polar_error(ref, q)
+
+
+@pytest.mark.parametrize("m,n", [(768, 512), (2048, 1536), (1000, 2048)])
+def test_precondition_from_gram_partials(m, n):
+    """nsx_gram emits the iteration-1 Gram epilogue's AOL partials; nsx_precondition sums
+    them (one lane per row while N <= 1344, a warp tree above) exactly as the production
+    launch does.  s must equal the oracle's Eq. 8 on the GPU's stored bf16 A0 (fp32 sums of
+    the same bf16 values: relative 1e-5), and A1 = diag(s) A0 diag(s) rounded once."""
+    x = I.gaussian(m, n, seed=I.matrix_seed(16, m + n))
+    t = torch.from_numpy(x).to(torch.bfloat16).cuda()
+    a0, part = ns.gram(t, partials=True)
+    a0_np = a0.float().cpu().numpy().astype(np.float64)
+    a1 = a0.clone()
+    s = ns.precondition(a1, "aol", part=part)
+    torch.cuda.synchronize()
+    s_ref = O.aol_scaling(a0_np)
+    np.testing.assert_allclose(s.cpu().numpy(), s_ref, rtol=1e-5, atol=0)
+    # the same s as the row sums taken from A0 itself (the non-partials branch)
+    a1b = a0.clone()
+    s2 = ns.precondition(a1b, "aol")
+    np.testing.assert_allclose(s.cpu().numpy(), s2.cpu().numpy(), rtol=1e-5, atol=0)
+    want = O.rescale_gram(a0_np, s.cpu().numpy().astype(np.float64))
+    got = a1.float().cpu().numpy().astype(np.float64)
+    np.testing.assert_allclose(got, want, rtol=2 ** -8, atol=1e-30)

@@ -8,7 +8,7 @@ import torch
 
 from synth import coeffs as C
 from synth import inputs as I
-from tests.helpers import oracle_run, relF
+from tests.helpers import oracle_run, relF, assert_parity
 
 pytestmark = pytest.mark.gpu
 
@@ -61,7 +61,7 @@ def test_fuzz_against_oracle(k, m, n, mode, precond, iters, path):
     assert np.all(np.isfinite(got))
     tol = 1e-4 if mode == "fp32" else 2e-2
     if np.linalg.norm(ref) > 0:
-        assert relF(got, ref) <= tol, (relF(got, ref), tol)
+        assert_parity(got, ref, tol)
 
 
 @pytest.mark.parametrize("mode", ["bf16", "fp32", "cast"])
