@@ -70,9 +70,16 @@ __device__ __forceinline__ void precond_row_s(const PrecondJob& J, int i, int la
     const int n1 = (J.N + 63) / 64, n2 = (J.N + 31) / 32;
     const float* pr = J.part + (int64_t)i * J.part_ld;
     const int d_end = min(4 * (bi + 1), n1), m_beg = min(8 * (bi + 1), n2);
-    float acc = 0.f;
-    for (int k = lane; k < d_end; k += 32) acc += pr[k];
-    for (int k = m_beg + lane; k < n2; k += 32) acc += pr[n1 + k];
+    // two independent chains (lanes' even / odd passes), combined in a fixed order:
+    // deterministic, and twice the loads in flight of one chain
+    float acc = 0.f, acc2 = 0.f;
+    int k = lane;
+    for (; k + 32 < d_end; k += 64) { acc += pr[k]; acc2 += pr[k + 32]; }
+    if (k < d_end) acc += pr[k];
+    k = m_beg + lane;
+    for (; k + 32 < n2; k += 64) { acc += pr[n1 + k]; acc2 += pr[n1 + k + 32]; }
+    if (k < n2) acc += pr[n1 + k];
+    acc += acc2;
     const float r = warp_sum(acc);
     if (lane == 0) {
       J.s[i] = r > 0.f ? rsqrtf(r) : 0.f;
@@ -112,55 +119,78 @@ __device__ __forceinline__ void precond_row_s(const PrecondJob& J, int i, int la
   }
 }
 
-// Phase 2 segments of one matrix.  A stored row is cut into 256-column segments; with half
-// storage row i (in 256-block bi) holds columns [0, min(N, 256 (bi + 1))), i.e. bi + 1
-// segments, else ceil(N / 256).  Segments are numbered row by row (columns fastest), so
-// consecutive segment indices are consecutive bytes of A.
-// Segment g of a matrix -> (row, first column).
-__device__ __forceinline__ void precond_seg_pos(int N, int half, int64_t g, int& row, int& col) {
+// Phase 2 work order.  A stored row is cut into 256-column segments; with half storage
+// row i (in 256-block bi) holds columns [0, min(N, 256 (bi + 1))), i.e. bi + 1 segments, else
+// ceil(N / 256) (precond_segments, jobs.h).  Segments are numbered strip by strip: block row
+// bi (half storage; the whole matrix otherwise), then column segment cb, then the row -- so a
+// warp's run of consecutive segments walks DOWN a 256-column strip: s_j of its columns is
+// loaded once per strip and each row of the strip is one coalesced 512-byte access.
+struct SegPos { int row0, rows, cb; };  // strip = rows [row0, row0 + rows) x segment cb
+__device__ __forceinline__ void precond_seg_pos(int N, int half, int64_t g, SegPos& sp, int& r) {
   if (!half) {
-    const int nb = (N + 255) / 256;
-    row = (int)(g / nb);
-    col = (int)(g % nb) * 256;
+    sp.row0 = 0; sp.rows = N;
+    sp.cb = (int)(g / N);
+    r = (int)(g % N);
     return;
   }
-  // block bi starts at segment 128 bi (bi + 1): solve, then correct the float estimate
+  // block row bi starts at segment 128 bi (bi + 1) (all earlier block rows are full)
   int bi = (int)((sqrtf(1.f + (float)g / 32.f) - 1.f) * 0.5f);
   while (bi > 0 && 128 * (int64_t)bi * (bi + 1) > g) --bi;
   while (128 * (int64_t)(bi + 1) * (bi + 2) <= g) ++bi;
-  const int64_t r = g - 128 * (int64_t)bi * (bi + 1);
-  row = 256 * bi + (int)(r / (bi + 1));
-  col = (int)(r % (bi + 1)) * 256;
+  const int64_t q = g - 128 * (int64_t)bi * (bi + 1);
+  sp.row0 = 256 * bi;
+  sp.rows = min(256, N - 256 * bi);
+  sp.cb = (int)(q / sp.rows);
+  r = (int)(q % sp.rows);
 }
 
-// Phase 2 for one segment: A1[i][c..c+256) = s_i A0[i][c..c+256) s_c..  (Alg. 2 l.4); each
-// lane owns 8 consecutive elements (one 16-byte vector in bf16).
+// Phase 2 for rows [r, r + cnt) of a strip: A1[i][c..c+256) = s_i A0[i][c..c+256) s_c..
+// (Alg. 2 l.4).  Lane owns columns c + 8 lane .. + 8 (one 16-byte vector in bf16) with their
+// s_j in registers; 8 rows in flight (all loads of a batch before any store).
 template <typename T, bool VEC8>
-__device__ __forceinline__ void precond_seg_scale(const PrecondJob& J, int i, int c0, int lane) {
-  const int N = J.half ? min(J.N, (i / 256 + 1) * 256) : J.N;
-  const float si = J.s[i];
-  T* Ai = reinterpret_cast<T*>(J.A) + (int64_t)i * J.N;
-  const int j = c0 + lane * 8;
+__device__ __forceinline__ void precond_strip(const PrecondJob& J, const SegPos& sp, int r, int cnt, int lane) {
+  const int c0 = sp.cb * 256;
+  const int lim = J.half ? min(J.N, sp.row0 + 256) : J.N;  // stored columns of these rows
   if (VEC8 && sizeof(T) == 2) {
-    if (j < N) {
-      const uint4 u = *reinterpret_cast<const uint4*>(Ai + j);
-      const float4 s0 = *reinterpret_cast<const float4*>(J.s + j);
-      const float4 s1 = *reinterpret_cast<const float4*>(J.s + j + 4);
-      const float sj[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
-      uint32_t w[4] = {u.x, u.y, u.z, u.w};
+    const int j = c0 + lane * 8;
+    if (j >= lim) return;
+    const float4 s0 = *reinterpret_cast<const float4*>(J.s + j);
+    const float4 s1 = *reinterpret_cast<const float4*>(J.s + j + 4);
+    const float sj[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
+    uint16_t* base = reinterpret_cast<uint16_t*>(J.A) + j;
+#ifndef TNS_PRE_ROWS
+#define TNS_PRE_ROWS 6
+#endif
+    constexpr int kR = TNS_PRE_ROWS;
+    for (int i0 = sp.row0 + r; i0 < sp.row0 + r + cnt; i0 += kR) {
+      const int n = min(kR, sp.row0 + r + cnt - i0);
+      uint4 u[kR];
+      float si[kR];
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const float lo = (si * __uint_as_float(w[e] << 16)) * sj[2 * e];
-        const float hi = (si * __uint_as_float(w[e] & 0xFFFF0000u)) * sj[2 * e + 1];
-        w[e] = (uint32_t)st_conv<uint16_t>(lo) | ((uint32_t)st_conv<uint16_t>(hi) << 16);
-      }
-      *reinterpret_cast<uint4*>(Ai + j) = make_uint4(w[0], w[1], w[2], w[3]);
+      for (int v = 0; v < kR; ++v)
+        if (v < n) {
+          u[v] = *reinterpret_cast<const uint4*>(base + (int64_t)(i0 + v) * J.N);
+          si[v] = J.s[i0 + v];
+        }
+#pragma unroll
+      for (int v = 0; v < kR; ++v)
+        if (v < n) {
+          uint32_t w[4] = {u[v].x, u[v].y, u[v].z, u[v].w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float lo = (si[v] * __uint_as_float(w[e] << 16)) * sj[2 * e];
+            const float hi = (si[v] * __uint_as_float(w[e] & 0xFFFF0000u)) * sj[2 * e + 1];
+            w[e] = (uint32_t)st_conv<uint16_t>(lo) | ((uint32_t)st_conv<uint16_t>(hi) << 16);
+          }
+          *reinterpret_cast<uint4*>(base + (int64_t)(i0 + v) * J.N) = make_uint4(w[0], w[1], w[2], w[3]);
+        }
     }
   } else {
-#pragma unroll
-    for (int e = 0; e < 8; ++e) {
-      const int jj = c0 + e * 32 + lane;  // lanes side by side: coalesced scalar accesses
-      if (jj < N) Ai[jj] = st_conv<T>((si * ld_val<T>(Ai + jj)) * J.s[jj]);
+    T* A = reinterpret_cast<T*>(J.A);
+    for (int i = sp.row0 + r; i < sp.row0 + r + cnt; ++i) {
+      const float si = J.s[i];
+      for (int jj = c0 + lane; jj < min(c0 + 256, lim); jj += 32)
+        A[(int64_t)i * J.N + jj] = st_conv<T>((si * ld_val<T>(A + (int64_t)i * J.N + jj)) * J.s[jj]);
     }
   }
 }

@@ -126,6 +126,15 @@ cudaError_t launch_simt_gemm(const SimtJob* d_jobs, int njobs, int64_t total_til
 // Self-resetting grid barrier (all CTAs co-resident: cooperative launch).  bar[0] counts
 // arrivals, bar[1] is a generation number; the last arriver resets the count and bumps the
 // generation, so no host-side reset (memset) is needed between launches.
+__device__ __forceinline__ int find_seg_job(const PrecondJob* __restrict__ jobs, int njobs, int64_t g) {
+  int lo = 0, hi = njobs - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (jobs[mid].seg_start <= g) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
 __device__ __forceinline__ void grid_barrier(unsigned* bar) {
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -146,7 +155,7 @@ __device__ __forceinline__ void grid_barrier(unsigned* bar) {
 }
 
 template <typename T, bool VEC8>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 3)
     precondition_kernel(const PrecondJob* __restrict__ jobs, int njobs, int64_t total_rows,
                         int64_t total_segs, unsigned* barrier, uint32_t* __restrict__ flags, int lane_rows) {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
@@ -181,61 +190,28 @@ __global__ void __launch_bounds__(256)
     }
   }
   grid_barrier(barrier);
-  // ---- phase 2: A1 = diag(s) A0 diag(s)  (Alg. 2 l.4), one warp per 256-column segment of a
-  // stored row (equal bytes per warp under half storage), 4 consecutive segments per warp
-  // per round with all loads issued before any store
-  constexpr int kU = 4;
-  for (int64_t g0 = gwarp * kU; g0 < total_segs; g0 += nwarps * kU) {
-    int jb[kU], row[kU], col[kU];
-#pragma unroll
-    for (int v = 0; v < kU; ++v) {
-      const int64_t g = g0 + v;
-      jb[v] = -1;
-      if (g < total_segs) {
-        int lo = 0, hi = njobs - 1;
-        while (lo < hi) {
-          const int mid = (lo + hi + 1) >> 1;
-          if (jobs[mid].seg_start <= g) lo = mid; else hi = mid - 1;
-        }
-        jb[v] = lo;
-        precond_seg_pos(jobs[lo].N, jobs[lo].half, g - jobs[lo].seg_start, row[v], col[v]);
+  // ---- phase 2: A1 = diag(s) A0 diag(s)  (Alg. 2 l.4).  Work is counted in 256-column
+  // segments of stored rows (precond_segments): each warp takes an equal contiguous run of
+  // segments -- equal bytes per warp under half storage, whatever the mix of matrix sizes --
+  // ordered down 256-column strips (precond_seg_pos), 8 rows per lane in flight.
+  const int64_t sper = (total_segs + nwarps - 1) / nwarps;
+  int64_t g = gwarp * sper;
+  const int64_t g_end = min(total_segs, g + sper);
+  if (g < g_end) {
+    int jb = find_seg_job(jobs, njobs, g);
+    SegPos sp;
+    int r;
+    precond_seg_pos(jobs[jb].N, jobs[jb].half, g - jobs[jb].seg_start, sp, r);
+    while (g < g_end) {
+      const PrecondJob& J = jobs[jb];
+      const int cnt = (int)min((int64_t)(sp.rows - r), g_end - g);
+      precond_strip<T, VEC8>(J, sp, r, cnt, lane);
+      g += cnt;
+      r += cnt;
+      if (g < g_end && r >= sp.rows) {  // next strip (or the next matrix)
+        if (g >= jobs[jb].seg_start + precond_segments(J.N, J.half)) ++jb;
+        precond_seg_pos(jobs[jb].N, jobs[jb].half, g - jobs[jb].seg_start, sp, r);
       }
-    }
-    if constexpr (VEC8 && sizeof(T) == 2) {
-      uint4 u[kU];
-      float4 s0[kU], s1[kU];
-      float si[kU];
-#pragma unroll
-      for (int v = 0; v < kU; ++v) {
-        if (jb[v] < 0) continue;
-        const PrecondJob& J = jobs[jb[v]];
-        const int lim = J.half ? min(J.N, (row[v] / 256 + 1) * 256) : J.N;
-        const int j = col[v] + lane * 8;
-        if (j >= lim) { jb[v] = -1; continue; }
-        u[v] = *reinterpret_cast<const uint4*>(reinterpret_cast<const uint16_t*>(J.A) + (int64_t)row[v] * J.N + j);
-        s0[v] = *reinterpret_cast<const float4*>(J.s + j);
-        s1[v] = *reinterpret_cast<const float4*>(J.s + j + 4);
-        si[v] = J.s[row[v]];
-      }
-#pragma unroll
-      for (int v = 0; v < kU; ++v) {
-        if (jb[v] < 0) continue;
-        const PrecondJob& J = jobs[jb[v]];
-        const float sj[8] = {s0[v].x, s0[v].y, s0[v].z, s0[v].w, s1[v].x, s1[v].y, s1[v].z, s1[v].w};
-        uint32_t w[4] = {u[v].x, u[v].y, u[v].z, u[v].w};
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const float lo = (si[v] * __uint_as_float(w[e] << 16)) * sj[2 * e];
-          const float hi = (si[v] * __uint_as_float(w[e] & 0xFFFF0000u)) * sj[2 * e + 1];
-          w[e] = (uint32_t)st_conv<uint16_t>(lo) | ((uint32_t)st_conv<uint16_t>(hi) << 16);
-        }
-        *reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(J.A) + (int64_t)row[v] * J.N + col[v] + lane * 8) =
-            make_uint4(w[0], w[1], w[2], w[3]);
-      }
-    } else {
-#pragma unroll
-      for (int v = 0; v < kU; ++v)
-        if (jb[v] >= 0) precond_seg_scale<T, false>(jobs[jb[v]], row[v], col[v], lane);
     }
   }
   if (fl) atomicOr(flags, fl);

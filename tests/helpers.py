@@ -32,11 +32,13 @@ def assert_parity(out, ref, tol: float, what: str = "") -> dict:
     * the same gate per row and per column (lines of >= 64 elements; shorter lines 2 tol), so
       a corrupted strip -- a ragged edge tile, one wrong row block -- cannot hide in the
       global norm;
-    * every element: |out - ref| <= tol * rms(ref) * sqrt(2 ln(numel) + 8).  Error model: each
-      output element carries the sum of many independent bf16 roundings (stored X, A, B,
-      fp32 accumulation), i.e. an approximately Gaussian error of standard deviation
-      relF * rms(ref); the gate's relF bound `tol` as that deviation and the Gaussian maximum
-      over numel samples (sqrt(2 ln numel), plus margin) bound the worst element.
+    * every element: |out - ref|_ij <= tol * max(rms(ref row i), rms(ref column j))
+      * sqrt(2 ln(numel) + 8).  Error model: each output element carries the sum of many
+      independent bf16 roundings (stored X, A, B, fp32 accumulation), i.e. an approximately
+      Gaussian error whose deviation scales with the local magnitude of the result (rows and
+      columns of a heavy-tailed input's result differ by orders of magnitude, App. B) --
+      relF * (local rms); the gate's relF bound `tol` as that deviation and the Gaussian
+      maximum over numel samples (sqrt(2 ln numel), plus margin) bound the worst element.
     Returns the measured values."""
     out = np.asarray(out, dtype=np.float64)
     ref = np.asarray(ref, dtype=np.float64)
@@ -56,9 +58,53 @@ def assert_parity(out, ref, tol: float, what: str = "") -> dict:
         assert worst <= lim, f"{what}: worst {name} relF {worst:.3e} > {lim}"
         assert np.all(dn[~ok] == 0), f"{what}: {name} with zero reference is not zero"
         res[name] = worst
-    rms = float(np.sqrt(np.mean(ref * ref)))
-    bound = tol * rms * np.sqrt(2 * np.log(max(ref.size, 2)) + 8)
-    mx = float(np.abs(d).max())
-    assert mx <= bound, f"{what}: max |diff| {mx:.3e} > {bound:.3e}"
-    res["max_abs"], res["max_abs_bound"] = mx, float(bound)
+    rr = np.sqrt(np.mean(ref * ref, axis=1))
+    rc = np.sqrt(np.mean(ref * ref, axis=0))
+    scale = np.maximum(rr[:, None], rc[None, :]) * (tol * np.sqrt(2 * np.log(max(ref.size, 2)) + 8))
+    ratio = np.abs(d) / np.maximum(scale, 1e-300)
+    worst = float(ratio.max())
+    k = np.unravel_index(int(ratio.argmax()), ratio.shape)
+    assert worst <= 1.0, f"{what}: |diff| {abs(d[k]):.3e} at {k} > local bound {scale[k]:.3e}"
+    res["max_abs_over_bound"] = worst
     return res
+
+
+def _bf16(a: np.ndarray) -> np.ndarray:
+    from synth.inputs import round_bf16
+    return round_bf16(np.asarray(a, dtype=np.float32)).astype(np.float64)
+
+
+def bf16_model_relF(x, coeffs, precond: str) -> float:
+    """relF of bf16_model_out against the fp64 oracle (see there)."""
+    ref = oracle_run(np.asarray(x, dtype=np.float32), coeffs, precond)
+    return relF(bf16_model_out(x, coeffs, precond), ref)
+
+
+def bf16_model_out(x, coeffs, precond: str) -> np.ndarray:
+    """Tolerance model for schedules whose bf16 error the north-star gate was not set for
+    (reading R6): the paper's iteration (Alg. 1/2, Eqs. 3-5, AXPY form) with
+    every stored operand -- X_k, A_k, B_k -- rounded once to bf16 and exact products (fp64
+    standing in for fp32 accumulation), compared with the fp64 oracle.  An unconverged
+    large-coefficient schedule (Polar-Express t <= 4: a_1 ~ 8) amplifies the storage
+    rounding by prod_k |p_k'| in its small-singular-value directions, so even ideal bf16
+    arithmetic exceeds 2e-2 there; the CUDA path is then held to 1.5 x this model."""
+    y = np.asarray(x, dtype=np.float64)
+    tr = y.shape[0] < y.shape[1]
+    if tr:
+        y = y.T
+    y = _bf16(y)
+    a_cached = None
+    if precond == "aol":
+        a0 = _bf16(y.T @ y)
+        r = np.abs(a0).sum(axis=1)
+        s = np.where(r > 0, 1.0 / np.sqrt(np.where(r > 0, r, 1.0)), 0.0)
+        y = _bf16(y * s[None, :])
+        a_cached = _bf16(s[:, None] * a0 * s[None, :])
+    elif precond == "frobenius":
+        f = np.sqrt(np.sum(y * y))
+        y = _bf16(y / f) if f > 0 else y
+    for k, (a, b, c) in enumerate(coeffs):
+        A = a_cached if (k == 0 and a_cached is not None) else _bf16(y.T @ y)
+        B = _bf16(b * A + c * (A @ A))
+        y = _bf16(a * y + y @ B)
+    return y.T if tr else y

@@ -25,7 +25,7 @@ from oracle import ns_oracle as O
 from synth import coeffs as C
 from synth import inputs as I
 from synth import polar_express as PE
-from tests.helpers import assert_parity, oracle_run
+from tests.helpers import assert_parity, bf16_model_out, oracle_run, relF
 
 pytestmark = pytest.mark.gpu
 
@@ -76,16 +76,24 @@ def test_aol_large_n_partials_tree(m, n):
 def test_polar_express_schedules(t):
     """Fig. 4's recomputed Polar-Express schedules (t = 1..9, default l, cushion and safety of
     App. D) through the CUDA path, AOL and Frobenius, against the oracle with the same
-    coefficient array.  t = 1 is a single large-coefficient step (a = 8.29, c = 17.3)."""
+    coefficient array.  t = 1 is a single large-coefficient step (a = 8.29, c = 17.3).
+    Gate: the north-star 2e-2, or 1.5 x the relF of ideal bf16 arithmetic where that model
+    itself exceeds it (unconverged t <= 4 schedules amplify storage rounding; DESIGN
+    reading R15, tests/helpers.bf16_model_relF)."""
     cf = [tuple(map(float, c)) for c in PE.polar_express(t)]
     x = I.gaussian(1024, 768, seed=I.matrix_seed(14, t))
+    q = O.polar_exact(x.astype(np.float64))
     for precond in ("aol", "frobenius"):
         out = _gpu(x, cf, precond)
         ref = oracle_run(x, cf, precond)
-        assert_parity(out, ref, BF16_TOL, f"PE t={t} {precond}")
-        if t >= 4:  # the polar-error comparison is meaningful once the iteration has converged
-            q = O.polar_exact(x.astype(np.float64))
-            assert O.polar_error(out, q) <= POLAR_SLACK * O.polar_error(ref, q)
+        model = bf16_model_out(x, cf, precond)
+        tol = max(BF16_TOL, 1.5 * relF(model, ref))
+        assert_parity(out, ref, tol, f"PE t={t} {precond}")
+        # polar error: converged schedules reach the bf16 noise floor (fp64 0.006 vs bf16
+        # ~0.009 at t >= 6), so the 5 % slack applies to the larger of the oracle's and the
+        # ideal-bf16 model's polar error
+        eg, eo, em = (O.polar_error(v, q) for v in (out, ref, model))
+        assert eg <= POLAR_SLACK * max(eo, em), (eg, eo, em)
 
 
 def test_levy_alpha1_gpt2_medium_shape():
