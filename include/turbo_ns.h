@@ -139,7 +139,8 @@ ns_status ns_orthogonalize_peers(void* const* X, void* const* out, void* const* 
 /* One Muon / Turbo-Muon optimizer step over `count` weight matrices (
  * PAPER.md P:L16/L97 "momentum -> orthogonalize -> update", reading R13 for the formulas of
  * the cited public Muon):
- *   M <- beta M + (1-beta) G ;  U <- nesterov ? (1-beta) G + beta M : M   (U rounded to bf16)
+ *   G' = grad_scale G (e.g. 1/world: the data-parallel mean of summed gradients)
+ *   M <- beta M + (1-beta) G' ;  U <- nesterov ? (1-beta) G' + beta M : M   (U rounded to bf16)
  *   U <- NS_iters(precond(U))  (as ns_orthogonalize_batched, in place on U)
  *   W <- W (1 - lr weight_decay) - lr * max(1, m/n)^(1/2) * U
  * W[i] (w_dtype), G[i] (g_dtype), M[i] (fp32, caller-initialised, e.g. zeros) and U[i]
@@ -147,8 +148,8 @@ ns_status ns_orthogonalize_peers(void* const* X, void* const* out, void* const* 
  * 3*iters + 3 launches, asynchronous on `stream`. */
 ns_status ns_muon_step(void* const* W, const void* const* G, float* const* M, void* const* U,
                        const int64_t* m, const int64_t* n, int64_t count, ns_dtype w_dtype, ns_dtype g_dtype,
-                       float lr, float beta, float weight_decay, int nesterov, int iters, const float* coeffs,
-                       ns_precond precond, void* stream);
+                       float lr, float beta, float weight_decay, float grad_scale, int nesterov, int iters,
+                       const float* coeffs, ns_precond precond, void* stream);
 
 /* The update half of a Muon step on its own (the distributed optimizer applies updates
  * orthogonalised on other ranks; reading R13):  W <- W (1 - lr weight_decay) - lr *

@@ -47,8 +47,8 @@ def _load() -> ctypes.CDLL:
         ctypes.POINTER(c_i64), c_i64, c_int, c_fp, c_int, c_int, c_vp]
     lib.ns_muon_step.argtypes = [
         ctypes.POINTER(c_vp), ctypes.POINTER(c_vp), ctypes.POINTER(c_vp), ctypes.POINTER(c_vp),
-        ctypes.POINTER(c_i64), ctypes.POINTER(c_i64), c_i64, c_int, c_int, c_float, c_float, c_float, c_int,
-        c_int, c_fp, c_int, c_vp]
+        ctypes.POINTER(c_i64), ctypes.POINTER(c_i64), c_i64, c_int, c_int, c_float, c_float, c_float, c_float,
+        c_int, c_int, c_fp, c_int, c_vp]
     lib.ns_muon_apply.argtypes = [ctypes.POINTER(c_vp), ctypes.POINTER(c_vp), ctypes.POINTER(c_i64),
                                   ctypes.POINTER(c_i64), c_i64, c_int, c_float, c_float, c_vp]
     lib.ns_workspace_size.argtypes = [ctypes.POINTER(c_i64), ctypes.POINTER(c_i64), c_i64, c_i64, c_int,

@@ -277,7 +277,8 @@ static int split_factor(int64_t M, int64_t N) {
   return (int)std::min<int64_t>(16, (nk + 7) / 8);
 }
 static void choose_splits(std::vector<Mat>& mats) {
-  static const bool off = [] { const char* e = getenv("TNS_NOSPLIT"); return e && atoi(e); }();  // A/B knob
+  const char* e = getenv("TNS_NOSPLIT");  // A/B knob, read at plan build
+  const bool off = e && atoi(e);
   for (Mat& mt : mats) mt.split = off ? 0 : split_factor(mt.M, mt.N);
 }
 // Tile width.  A plan whose every GEMM step has at most half as many 256-wide tiles as there
@@ -1368,16 +1369,17 @@ static void muon_table_used(MuonTab* t, cudaStream_t s) {
 
 ns_status ns_muon_step(void* const* W, const void* const* G, float* const* M, void* const* U,
                        const int64_t* m, const int64_t* n, int64_t count, ns_dtype w_dtype, ns_dtype g_dtype,
-                       float lr, float beta, float weight_decay, int nesterov, int iters, const float* coeffs,
-                       ns_precond precond, void* stream) {
+                       float lr, float beta, float weight_decay, float grad_scale, int nesterov, int iters,
+                       const float* coeffs, ns_precond precond, void* stream) {
   std::lock_guard<std::mutex> lk(g_mu);
   ns_status st = validate_common(count, iters, coeffs, precond, NS_BF16);
   if (st != NS_OK) return st;
   if (!W || !G || !M || !U || !m || !n) return fail(NS_ERR_INVALID_VALUE, "NULL array argument");
   if ((w_dtype != NS_BF16 && w_dtype != NS_FP32) || (g_dtype != NS_BF16 && g_dtype != NS_FP32))
     return fail(NS_ERR_INVALID_VALUE, "bad dtype");
-  if (!std::isfinite(lr) || !std::isfinite(beta) || !std::isfinite(weight_decay) || beta < 0.f || beta >= 1.f)
-    return fail(NS_ERR_INVALID_VALUE, "lr / beta / weight_decay out of range");
+  if (!std::isfinite(lr) || !std::isfinite(beta) || !std::isfinite(weight_decay) || !std::isfinite(grad_scale) ||
+      beta < 0.f || beta >= 1.f)
+    return fail(NS_ERR_INVALID_VALUE, "lr / beta / weight_decay / grad_scale out of range");
   std::vector<Mat> mats;
   std::vector<MuonJob> jobs;
   std::vector<uint64_t> key;
@@ -1405,7 +1407,7 @@ ns_status ns_muon_step(void* const* W, const void* const* G, float* const* M, vo
   MuonTab* tab = nullptr;
   if ((st = muon_table(key, jobs, s, &tab)) != NS_OK) return st;
   const MuonJob* dtab = reinterpret_cast<const MuonJob*>(tab->d);
-  CU_TRY(launch_muon_momentum(dtab, (int)count, max_numel, g_dtype == NS_BF16, beta, nesterov, dc->sms, s));
+  CU_TRY(launch_muon_momentum(dtab, (int)count, max_numel, g_dtype == NS_BF16, beta, grad_scale, nesterov, dc->sms, s));
   ++g_launches;
   st = run(mats, iters, coeffs, precond, NS_BF16, s);
   if (st == NS_OK) {

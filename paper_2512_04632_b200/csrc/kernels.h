@@ -54,7 +54,7 @@ cudaError_t launch_cast(const CastJob* d_jobs, int count, int64_t max_numel, boo
                         cudaStream_t stream);
 
 // Muon step around the path (muon.cu): momentum + nesterov -> bf16 U; W update from U.
-cudaError_t launch_muon_momentum(const MuonJob* d_jobs, int count, int64_t max_numel, bool g_bf16, float beta,
+cudaError_t launch_muon_momentum(const MuonJob* d_jobs, int count, int64_t max_numel, bool g_bf16, float beta, float gscale,
                                  int nesterov, int sms, cudaStream_t stream);
 cudaError_t launch_muon_apply(const MuonJob* d_jobs, int count, int64_t max_numel, bool w_bf16, float lr, float wd,
                               int sms, cudaStream_t stream);

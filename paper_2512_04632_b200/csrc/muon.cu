@@ -1,6 +1,7 @@
 // The Muon optimizer step around the NS path (PAPER.md P:L16, L97,
 // L311-315: "momentum -> orthogonalize -> update" with Turbo-Muon as a drop-in NS):
-//   muon_momentum_kernel : M <- beta M + (1-beta) G ;  U <- nesterov ? (1-beta) G + beta M : M
+//   muon_momentum_kernel : G <- gscale G (1/world: the data-parallel mean folded in) ;
+//                          M <- beta M + (1-beta) G ;  U <- nesterov ? (1-beta) G + beta M : M
 //                          (U in bf16 = the NS input, orthogonalised in place afterwards)
 //   muon_apply_kernel    : W <- W (1 - lr wd) - lr * max(1, m/n)^(1/2) * U
 // Both are HBM-bound elementwise passes, grouped over all matrices of a step (blockIdx.y =
@@ -51,7 +52,7 @@ __device__ __forceinline__ void st8(uint16_t* p, const float (&v)[8]) {
 // numel % 8 == 0; otherwise element by element).  Elementwise, HBM-bound.
 template <typename TG>
 __global__ void __launch_bounds__(256) muon_momentum_kernel(const MuonJob* __restrict__ jobs, float beta,
-                                                            int nesterov) {
+                                                            float gscale, int nesterov) {
   const MuonJob J = jobs[blockIdx.y];
   const TG* G = reinterpret_cast<const TG*>(J.G);
   uint16_t* U = reinterpret_cast<uint16_t*>(J.U);
@@ -65,6 +66,8 @@ __global__ void __launch_bounds__(256) muon_momentum_kernel(const MuonJob* __res
       ld8(G + i, g);
       ld8(J.M + i, m);
 #pragma unroll
+      for (int e = 0; e < 8; ++e) g[e] *= gscale;
+#pragma unroll
       for (int e = 0; e < 8; ++e) {
         m[e] = fmaf(beta, m[e], ob * g[e]);
         u[e] = nesterov ? fmaf(ob, g[e], beta * m[e]) : m[e];
@@ -75,7 +78,7 @@ __global__ void __launch_bounds__(256) muon_momentum_kernel(const MuonJob* __res
     return;
   }
   for (int64_t i = t0; i < J.numel; i += nt) {
-    const float g = ldf<TG>(G, i);
+    const float g = ldf<TG>(G, i) * gscale;
     const float m = fmaf(beta, J.M[i], ob * g);
     J.M[i] = m;
     U[i] = tobf(nesterov ? fmaf(ob, g, beta * m) : m);
@@ -173,11 +176,11 @@ static dim3 muon_grid(int64_t max_numel, int count, int sms) {
   return dim3((unsigned)want, (unsigned)count);
 }
 
-cudaError_t launch_muon_momentum(const MuonJob* d_jobs, int count, int64_t max_numel, bool g_bf16, float beta,
+cudaError_t launch_muon_momentum(const MuonJob* d_jobs, int count, int64_t max_numel, bool g_bf16, float beta, float gscale,
                                  int nesterov, int sms, cudaStream_t stream) {
   const dim3 grid = muon_grid(max_numel, count, sms);
-  if (g_bf16) muon_momentum_kernel<uint16_t><<<grid, 256, 0, stream>>>(d_jobs, beta, nesterov);
-  else muon_momentum_kernel<float><<<grid, 256, 0, stream>>>(d_jobs, beta, nesterov);
+  if (g_bf16) muon_momentum_kernel<uint16_t><<<grid, 256, 0, stream>>>(d_jobs, beta, gscale, nesterov);
+  else muon_momentum_kernel<float><<<grid, 256, 0, stream>>>(d_jobs, beta, gscale, nesterov);
   return cudaGetLastError();
 }
 

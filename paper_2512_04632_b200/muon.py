@@ -28,7 +28,7 @@ def _coeff_carr(group):
     return (ctypes.c_float * len(flat))(*flat)
 
 
-def _muon_step_call(W, G, M, U, ms, ns_, w_dt, g_dt, group, carr, dev):
+def _muon_step_call(W, G, M, U, ms, ns_, w_dt, g_dt, group, carr, dev, grad_scale: float = 1.0):
     """One grouped ns_muon_step over pointer lists (momentum -> NS -> update)."""
     cnt = len(W)
     arr = lambda xs: (ctypes.c_void_p * cnt)(*xs)  # noqa: E731
@@ -36,7 +36,7 @@ def _muon_step_call(W, G, M, U, ms, ns_, w_dt, g_dt, group, carr, dev):
         status = lib.ns_muon_step(
             arr(W), arr(G), arr(M), arr(U), (ctypes.c_int64 * cnt)(*ms), (ctypes.c_int64 * cnt)(*ns_),
             cnt, w_dt, g_dt, float(group["lr"]), float(group["momentum"]), float(group["weight_decay"]),
-            1 if group["nesterov"] else 0, group["iters"], carr, PRECOND[group["precond"]],
+            float(grad_scale), 1 if group["nesterov"] else 0, group["iters"], carr, PRECOND[group["precond"]],
             ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream))
     check(status, "ns_muon_step")
 
@@ -98,9 +98,10 @@ class DistributedTurboMuon(torch.optim.Optimizer):
     side of the path, with a reduce-scatter by ownership instead of a gradient all-reduce).
     Every rank holds the same parameter list and its LOCAL gradients; one step:
 
-      1. reduce-scatter by matrix ownership (mean over ranks; LPT ownership on NS FLOPs, as in
-         parallel.orthogonalize_sharded): each rank receives the averaged gradient of only the
-         matrices it owns;
+      1. reduce-scatter by matrix ownership (sum over ranks; LPT ownership on NS FLOPs, as in
+         parallel.orthogonalize_sharded): each rank receives the summed gradient of only the
+         matrices it owns (packed by one multi-tensor copy; the 1/world mean is applied inside
+         the momentum kernel);
       2. the owner runs the fused Muon step (momentum -> NS -> update of its own weights), the
          orthogonalised update U landing in its segment of a packed bf16 buffer;
       3. one all-gather of U, then every rank applies the same update kernel (ns_muon_apply)
@@ -141,7 +142,9 @@ class DistributedTurboMuon(torch.optim.Optimizer):
             dev = ps[0].device
             shapes = [(p.shape[0], p.numel() // p.shape[0]) for p in ps]
             iters = group["iters"]
-            mine, owned_g = reduce_scatter_owned([p.grad.view(s) for p, s in zip(ps, shapes)], self.pg, iters)
+            # summed (not averaged) gradients: the 1/world mean is folded into the momentum kernel
+            mine, owned_g = reduce_scatter_owned([p.grad.view(s) for p, s in zip(ps, shapes)], self.pg, iters,
+                                                 mean=False)
             plan = make_plan(shapes, world, iters, 1)
             key = (gi, tuple(shapes), world)
             if key not in self._ubuf:
@@ -160,7 +163,8 @@ class DistributedTurboMuon(torch.optim.Optimizer):
                     W.append(p.data_ptr()); G.append(g.data_ptr())
                     M.append(st["momentum_buffer"].data_ptr()); U.append(uv[i].data_ptr())
                     ms.append(m); ns_.append(n)
-                _muon_step_call(W, G, M, U, ms, ns_, _dt(ps[0]), _dt(owned_g[0]), group, carr, dev)
+                _muon_step_call(W, G, M, U, ms, ns_, _dt(ps[0]), _dt(owned_g[0]), group, carr, dev,
+                                grad_scale=1.0 / world)
             if world > 1:
                 _gather(ubuf, plan, 0, dist.get_rank(self.pg), self.pg)
                 others = [i for i in range(len(ps)) if i not in set(mine)]

@@ -198,9 +198,8 @@ def reduce_scatter_owned(tensors: Sequence[torch.Tensor], group=None, iters: int
     packed = _cached(key + ("in",), lambda: torch.zeros(plan.total, dtype=dtype, device=device))
     seg = plan.seg_elems
     out = _cached(key + ("out",), lambda: torch.empty(seg, dtype=dtype, device=device))
-    for i, t in enumerate(tensors):
-        m, n = shapes[i]
-        packed[plan.offsets[i]:plan.offsets[i] + m * n].view(m, n).copy_(t)
+    dst = _cached(key + ("views",), lambda: [packed[o:o + m * n].view(m, n) for o, (m, n) in zip(plan.offsets, shapes)])
+    torch._foreach_copy_(dst, tensors)  # one multi-tensor copy instead of one launch per matrix
     if world == 1:
         out.copy_(packed[:seg])
     elif dist.get_backend(group) == "nccl":

@@ -25,20 +25,26 @@ def polar_excess(gpu_out, oracle_out, x) -> tuple[float, float]:
     return O.polar_error(gpu_out, q), O.polar_error(oracle_out, q)
 
 
-def assert_parity(out, ref, tol: float, what: str = "") -> dict:
+def assert_parity(out, ref, tol: float, what: str = "", model=None) -> dict:
     """End-to-end gate of a CUDA result against the fp64 oracle, element by element.
 
     * global relative Frobenius difference <= tol (BASELINE north_star: 2e-2 bf16, 1e-4 fp32);
     * the same gate per row and per column (lines of >= 64 elements; shorter lines 2 tol), so
       a corrupted strip -- a ragged edge tile, one wrong row block -- cannot hide in the
       global norm;
-    * every element: |out - ref|_ij <= tol * max(rms(ref row i), rms(ref column j))
+    * every element: |out - ref|_ij <= tol * max(rms(ref row i), rms(ref column j), |ref_ij|)
       * sqrt(2 ln(numel) + 8).  Error model: each output element carries the sum of many
       independent bf16 roundings (stored X, A, B, fp32 accumulation), i.e. an approximately
-      Gaussian error whose deviation scales with the local magnitude of the result (rows and
-      columns of a heavy-tailed input's result differ by orders of magnitude, App. B) --
-      relF * (local rms); the gate's relF bound `tol` as that deviation and the Gaussian
-      maximum over numel samples (sqrt(2 ln numel), plus margin) bound the worst element.
+      Gaussian error whose deviation scales with the local magnitude of the result -- the
+      rms of its row and column, and, for the spikes a heavy-tailed input leaves in the
+      result (App. B), the element itself (its own storage rounding is 2^-9 |ref_ij|); the
+      gate's relF bound `tol` as that relative deviation and the Gaussian maximum over numel
+      samples (sqrt(2 ln numel), plus margin) bound the worst element.
+    Heavy-tailed inputs (Levy, App. B) break the Gaussian element model: a spike of X
+    spreads its storage rounding through the Gram into many elements, and even ideal bf16
+    arithmetic (bf16_model_out) exceeds the element bound there (Levy alpha = 1 at 4096 x 1024:
+    1.05 x).  Pass that model's output as `model` and the element gate becomes 1.5 x the
+    model's own worst element ratio (when that is above 1).
     Returns the measured values."""
     out = np.asarray(out, dtype=np.float64)
     ref = np.asarray(ref, dtype=np.float64)
@@ -60,11 +66,16 @@ def assert_parity(out, ref, tol: float, what: str = "") -> dict:
         res[name] = worst
     rr = np.sqrt(np.mean(ref * ref, axis=1))
     rc = np.sqrt(np.mean(ref * ref, axis=0))
-    scale = np.maximum(rr[:, None], rc[None, :]) * (tol * np.sqrt(2 * np.log(max(ref.size, 2)) + 8))
+    scale = np.maximum(np.maximum(rr[:, None], rc[None, :]), np.abs(ref)) * (
+        tol * np.sqrt(2 * np.log(max(ref.size, 2)) + 8))
     ratio = np.abs(d) / np.maximum(scale, 1e-300)
     worst = float(ratio.max())
     k = np.unravel_index(int(ratio.argmax()), ratio.shape)
-    assert worst <= 1.0, f"{what}: |diff| {abs(d[k]):.3e} at {k} > local bound {scale[k]:.3e}"
+    lim = 1.0
+    if model is not None:
+        lim = max(1.0, 1.5 * float((np.abs(np.asarray(model, dtype=np.float64) - ref) / np.maximum(scale, 1e-300)).max()))
+    assert worst <= lim, (f"{what}: |diff| {abs(d[k]):.3e} at {k} (ref {ref[k]:.3e}) > {lim:.2f} x local bound "
+                          f"{scale[k]:.3e}")
     res["max_abs_over_bound"] = worst
     return res
 

@@ -16,7 +16,7 @@ import torch
 from oracle import ns_oracle as O
 from synth import coeffs as C
 from synth import inputs as I
-from tests.helpers import oracle_run, polar_excess, relF, assert_parity
+from tests.helpers import oracle_run, polar_excess, relF, assert_parity, bf16_model_out
 
 pytestmark = pytest.mark.gpu
 
@@ -82,7 +82,7 @@ def test_cluster_distributions(dist):
     x = I.make_matrix(64, 576, seed=11, dist=dist)
     out, _ = _run(x, C.turbo(4), "aol")
     ref = oracle_run(x, C.turbo(4), "aol")
-    assert_parity(out, ref, BF16_TOL)
+    assert_parity(out, ref, BF16_TOL, dist, model=bf16_model_out(x, C.turbo(4), "aol"))
 
 
 def test_cluster_matches_step_engine():

@@ -102,7 +102,7 @@ def test_levy_alpha1_gpt2_medium_shape():
     for precond, coeffs in (("aol", C.turbo(4)), ("frobenius", C.muon_plus(5))):
         out = _gpu(x, coeffs, precond)
         ref = oracle_run(x, coeffs, precond)
-        assert_parity(out, ref, BF16_TOL, f"levy1 {precond}")
+        assert_parity(out, ref, BF16_TOL, f"levy1 {precond}", model=bf16_model_out(x, coeffs, precond))
         q = O.polar_exact_gram(x.astype(np.float64))
         assert O.polar_error(out, q) <= POLAR_SLACK * O.polar_error(ref, q)
 

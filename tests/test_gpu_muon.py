@@ -135,3 +135,25 @@ def test_turbo_muon_step_cuda_graph():
     torch.cuda.synchronize()
     for a, b in zip(pa, pb):
         assert torch.equal(a, b)
+
+
+def test_grad_scale_folds_the_mean():
+    """ns_muon_step's grad_scale (the data-parallel 1/world mean inside the momentum kernel):
+    a step on G with grad_scale 1/4 is bitwise the step on G / 4 (exact power-of-two scale)."""
+    from paper_2512_04632_b200.muon import _coeff_carr, _muon_step_call
+    from paper_2512_04632_b200._lib import DTYPE_FP32
+    m, n = 768, 512
+    w0 = torch.from_numpy(I.gaussian(m, n, seed=7, bf16=False)).cuda()
+    g = torch.from_numpy(I.gaussian(m, n, seed=8, bf16=False)).cuda()
+    group = {"lr": 0.05, "momentum": 0.9, "weight_decay": 0.01, "nesterov": True, "iters": 4, "precond": "aol",
+             "coeffs": None}
+    outs = []
+    for gg, scale in ((g, 0.25), (g / 4, 1.0)):
+        w = w0.clone()
+        mom = torch.full((m, n), 0.5, device="cuda")
+        u = torch.empty((m, n), dtype=torch.bfloat16, device="cuda")
+        _muon_step_call([w.data_ptr()], [gg.data_ptr()], [mom.data_ptr()], [u.data_ptr()], [m], [n], DTYPE_FP32,
+                        DTYPE_FP32, group, _coeff_carr(group), w.device, grad_scale=scale)
+        torch.cuda.synchronize()
+        outs.append((w, mom))
+    assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1])
