@@ -19,7 +19,7 @@ KEYS = {
     # counts against the real-time clock and reads lower -- kept for reference)
     "tensor_pct": ("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed", 1),
     "tensor_realtime_pct": ("sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed", 1),
-    "utchmma_ops": ("sm__ops_path_tensor_op_utchmma_src_bf16_dst_fp32.sum", 1),
+    "utchmma_ops": ("sm__ops_path_tensor_op_utchmma_src_bf16_dst_fp32_sparsity_off.sum", 1),
     "tensor_hmma_pct": ("sm__ops_path_tensor_op_hmma_src_bf16_dst_fp32_sparsity_off.avg.pct_of_peak_sustained_elapsed", 1),
     "sm_mhz": ("smsp__cycles_elapsed.avg.per_second", 1e-6),
     "l2_hit_pct": ("lts__t_sector_hit_rate.pct", 1),
