@@ -43,9 +43,23 @@ __device__ __forceinline__ float aol_rowsum_partials(const PrecondJob& J, int i)
   const int n1 = (N + 63) / 64, n2 = (N + 31) / 32;
   const float* pr = J.part + (int64_t)i * J.part_ld;
   const int d_end = min(4 * (bi + 1), n1), m_beg = min(8 * (bi + 1), n2);
+  // 8 loads in flight, added in slot order (the zeros past the end add nothing): the same
+  // sum, bitwise, as a plain sequential loop -- without 8 serialised L2 round trips
   float acc = 0.f;
-  for (int k = 0; k < d_end; ++k) acc += pr[k];
-  for (int k = m_beg; k < n2; ++k) acc += pr[n1 + k];
+  for (int k0 = 0; k0 < d_end; k0 += 8) {
+    float v[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) v[e] = (k0 + e < d_end) ? pr[k0 + e] : 0.f;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) acc += v[e];
+  }
+  for (int k0 = m_beg; k0 < n2; k0 += 8) {
+    float v[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) v[e] = (k0 + e < n2) ? pr[n1 + k0 + e] : 0.f;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) acc += v[e];
+  }
   return acc;
 }
 
@@ -70,16 +84,23 @@ __device__ __forceinline__ void precond_row_s(const PrecondJob& J, int i, int la
     const int n1 = (J.N + 63) / 64, n2 = (J.N + 31) / 32;
     const float* pr = J.part + (int64_t)i * J.part_ld;
     const int d_end = min(4 * (bi + 1), n1), m_beg = min(8 * (bi + 1), n2);
-    // two independent chains (lanes' even / odd passes), combined in a fixed order:
-    // deterministic, and twice the loads in flight of one chain
-    float acc = 0.f, acc2 = 0.f;
-    int k = lane;
-    for (; k + 32 < d_end; k += 64) { acc += pr[k]; acc2 += pr[k + 32]; }
-    if (k < d_end) acc += pr[k];
-    k = m_beg + lane;
-    for (; k + 32 < n2; k += 64) { acc += pr[n1 + k]; acc2 += pr[n1 + k + 32]; }
-    if (k < n2) acc += pr[n1 + k];
-    acc += acc2;
+    // per lane: slots lane, lane + 32, ... loaded 8 at a time and added in that order
+    // (fixed order: deterministic)
+    float acc = 0.f;
+    for (int k0 = lane; k0 < d_end; k0 += 256) {
+      float v[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) v[e] = (k0 + 32 * e < d_end) ? pr[k0 + 32 * e] : 0.f;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc += v[e];
+    }
+    for (int k0 = m_beg + lane; k0 < n2; k0 += 256) {
+      float v[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) v[e] = (k0 + 32 * e < n2) ? pr[n1 + k0 + 32 * e] : 0.f;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc += v[e];
+    }
     const float r = warp_sum(acc);
     if (lane == 0) {
       J.s[i] = r > 0.f ? rsqrtf(r) : 0.f;

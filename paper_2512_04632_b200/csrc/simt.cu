@@ -11,6 +11,7 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 #include "jobs.h"
@@ -157,7 +158,10 @@ __device__ __forceinline__ void grid_barrier(unsigned* bar) {
 template <typename T, bool VEC8>
 __global__ void __launch_bounds__(256, 3)
     precondition_kernel(const PrecondJob* __restrict__ jobs, int njobs, int64_t total_rows,
-                        int64_t total_segs, unsigned* barrier, uint32_t* __restrict__ flags, int lane_rows) {
+                        int64_t total_segs, unsigned* barrier, uint32_t* __restrict__ flags, int mode) {
+  // mode bit 0: AOL from partials with one lane per row; bits 1 / 2 (TNS_PRE_DBG, measurement
+  // only): skip phase 1 / phase 2
+  const int lane_rows = mode & 1;
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   asm volatile("griddepcontrol.wait;" ::: "memory");  // A0 comes from the preceding Gram launch
   const int lane = threadIdx.x & 31;
@@ -167,7 +171,8 @@ __global__ void __launch_bounds__(256, 3)
   // ---- phase 1: scaling vector s (Eq. 8 / Eq. 10); each warp owns a contiguous run of rows
   const int64_t per = (total_rows + nwarps - 1) / nwarps;
   const int64_t r_beg = gwarp * per, r_end = min(total_rows, r_beg + per);
-  if (lane_rows) {  // AOL from partials, every job with part_ld <= kSeqPartials
+  if (mode & 2) {
+  } else if (lane_rows) {  // AOL from partials, every job with part_ld <= kSeqPartials
     // AOL from partials: one LANE per row (<= 64 independent loads each), 32 rows per warp
     // at a time -- the row sums are short, so rows, not columns, carry the parallelism
     for (int64_t row0 = r_beg; row0 < r_end; row0 += 32) {
@@ -194,7 +199,7 @@ __global__ void __launch_bounds__(256, 3)
   // segments of stored rows (precond_segments): each warp takes an equal contiguous run of
   // segments -- equal bytes per warp under half storage, whatever the mix of matrix sizes --
   // ordered down 256-column strips (precond_seg_pos), 8 rows per lane in flight.
-  const int64_t sper = (total_segs + nwarps - 1) / nwarps;
+  const int64_t sper = (mode & 4) ? 0 : (total_segs + nwarps - 1) / nwarps;
   int64_t g = gwarp * sper;
   const int64_t g_end = min(total_segs, g + sper);
   if (g < g_end) {
@@ -227,6 +232,8 @@ static cudaError_t launch_precond_t(const PrecondJob* d_jobs, int njobs, int64_t
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, 0);
   if (occ < 1) occ = 1;
+  static const int occ_cap = [] { const char* e = getenv("TNS_PRE_OCC"); return e ? atoi(e) : 0; }();  // A/B knob
+  if (occ_cap > 0 && occ_cap < occ) occ = occ_cap;
   // one warp per row (phase 1) and per 4 segments (phase 2), at most the co-resident grid
   // (cooperative launch: the grid barrier needs every CTA resident)
   const int64_t warps = std::max<int64_t>(total_rows, (total_segs + 3) / 4);
@@ -244,7 +251,9 @@ static cudaError_t launch_precond_t(const PrecondJob* d_jobs, int njobs, int64_t
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 2;
-  return cudaLaunchKernelEx(&cfg, kern, d_jobs, njobs, total_rows, total_segs, d_barrier, d_flags, lane_rows);
+  static const int dbg = [] { const char* e = getenv("TNS_PRE_DBG"); return e ? atoi(e) : 0; }();
+  const int lr = (dbg & 8) ? 0 : lane_rows;  // bit 8: warp per row even for short partial rows (A/B)
+  return cudaLaunchKernelEx(&cfg, kern, d_jobs, njobs, total_rows, total_segs, d_barrier, d_flags, lr | (dbg & 6));
 }
 
 // ------------------------------------------------------------------------------ split-K Gram
