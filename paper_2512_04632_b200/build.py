@@ -12,7 +12,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libturbons.so")
-SOURCES = ["api.cu", "umma_gemm.cu", "simt.cu", "muon.cu", "cluster_ns.cu"]
+SOURCES = ["api.cu", "umma_gemm.cu", "simt.cu", "muon.cu", "cluster_ns.cu", "cluster_tc.cu"]
 HEADERS = ["ptx.cuh", "jobs.h", "kernels.h", "precond_rows.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [

@@ -75,6 +75,9 @@ struct DevCtx {
   // side stream for the cluster-resident small-matrix launch, joined back by events
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  // second side stream: the tcgen05 cluster kernel (mid-size matrices) beside the others
+  cudaStream_t side2 = nullptr;
+  cudaEvent_t ev_fork2 = nullptr, ev_join2 = nullptr;
   cudaStream_t cap = nullptr;  // private stream on which plans are captured into CUDA graphs
   // private stream on which evicted plans' device memory is released (cudaFreeAsync), ordered
   // after the plan's last use by an event -- eviction never synchronises the host
@@ -97,6 +100,9 @@ static ns_status dev_ctx(DevCtx** out) {
     CU_TRY(cudaStreamCreateWithFlags(&d.side, cudaStreamNonBlocking));
     CU_TRY(cudaEventCreateWithFlags(&d.ev_fork, cudaEventDisableTiming));
     CU_TRY(cudaEventCreateWithFlags(&d.ev_join, cudaEventDisableTiming));
+    CU_TRY(cudaStreamCreateWithFlags(&d.side2, cudaStreamNonBlocking));
+    CU_TRY(cudaEventCreateWithFlags(&d.ev_fork2, cudaEventDisableTiming));
+    CU_TRY(cudaEventCreateWithFlags(&d.ev_join2, cudaEventDisableTiming));
     CU_TRY(cudaStreamCreateWithFlags(&d.freer, cudaStreamNonBlocking));
     if (!g_encode) {
       cudaDriverEntryPointQueryResult q;
@@ -174,13 +180,14 @@ struct Mat {
   size_t stage_off = 0;
   // tensormap indices (tcgen05 path)
   int tm_x, tm_out, tm_w, tm_a, tm_b;
+  size_t tc_part_off = 0;  // cluster tcgen05 kernel: 16 * Np * Np fp32 Gram partials
   // fused collective: extra destinations of the final result (peers' buffers)
   std::vector<void*> peer;
   int tm_peer;
 };
 
 enum PhaseKind { PH_GEMM = 0, PH_SIMT = 1, PH_PRECOND = 2, PH_COPY = 3, PH_CLUSTER = 5, PH_SPLIT = 6,
-                 PH_CAST_IN = 7, PH_CAST_OUT = 8 };
+                 PH_CAST_IN = 7, PH_CAST_OUT = 8, PH_TC = 9 };
 struct Phase {
   PhaseKind kind;
   size_t dev_off;  // offset of the job array in the device table
@@ -212,6 +219,7 @@ struct Plan {
   ns_precond precond = NS_PRECOND_AOL;
   std::vector<Mat> mats;   // tcgen05 / SIMT step engine
   std::vector<Mat> tiny;   // cluster-resident whole-NS kernel (row a-10)
+  std::vector<Mat> tc;     // cluster-resident tcgen05 whole-NS kernel (mid-size, §8(f) rank 4)
   void* ws = nullptr;
   size_t ws_bytes = 0;
   void* dtab = nullptr;
@@ -306,16 +314,24 @@ static int choose_bn(const std::vector<Mat>& mats, int cg, int workers) {
 
 static size_t split_bytes(const Mat& mt) { return mt.split ? (size_t)mt.split * kSplitLd * kSplitLd * 4 : 0; }
 
+static size_t tc_part_bytes(int64_t N) { return (size_t)kTcCtas * tc_np(N) * tc_np(N) * 4; }
+
+// Workspace of a problem list as the step engine lays it out; a bf16 matrix the tcgen05
+// cluster kernel could take counts with the larger of its two footprints (an upper bound
+// whatever the routing).
 static size_t workspace_bytes_for(const std::vector<Mat>& mats, ns_dtype dt) {
-  size_t off = 1024;  // [0,1024): grid-barrier words and fused-mode phase counters
+  size_t off = 1024;  // [0,1024): grid-barrier words
   const size_t es = elem_size(dt);
   for (const Mat& mt : mats) {
-    off = align_up(off, 256) + (size_t)mt.M * mt.N * es;
-    off = align_up(off, 256) + (size_t)mt.N * mt.N * es;
-    off = align_up(off, 256) + (size_t)mt.N * mt.N * es;
-    off = align_up(off, 256) + s_floats(mt.N) * 4;
-    off = align_up(off, 256) + (size_t)mt.N * part_ld_for(mt.N) * 4;
-    if (dt == NS_BF16) off = align_up(off, 256) + (size_t)split_factor(mt.M, mt.N) * kSplitLd * kSplitLd * 4;
+    size_t o = 0;
+    o = align_up(o, 256) + (size_t)mt.M * mt.N * es;
+    o = align_up(o, 256) + (size_t)mt.N * mt.N * es;
+    o = align_up(o, 256) + (size_t)mt.N * mt.N * es;
+    o = align_up(o, 256) + s_floats(mt.N) * 4;
+    o = align_up(o, 256) + (size_t)mt.N * part_ld_for(mt.N) * 4;
+    if (dt == NS_BF16) o = align_up(o, 256) + (size_t)split_factor(mt.M, mt.N) * kSplitLd * kSplitLd * 4;
+    if (dt == NS_BF16 && tc_fits(mt.M, mt.N)) o = std::max(o, tc_part_bytes(mt.N));
+    off = align_up(off, 256) + align_up(o, 256);
   }
   return align_up(off, 256);
 }
@@ -398,9 +414,13 @@ static ns_status build_plan(Plan& P, HostTables& H, DevCtx* dc, const float* coe
     if (P.precond == NS_PRECOND_AOL && !P.simt) off += (size_t)mt.N * mt.part_ld * 4;
     off = align_up(off, 256); mt.split_off = off; off += split_bytes(mt);
   }
+  for (Mat& mt : P.tc) {  // Gram partials of the tcgen05 cluster kernel
+    off = align_up(off, 256); mt.tc_part_off = off; off += tc_part_bytes(mt.N);
+  }
   if (P.cast) {  // bf16 staging copies of the caller's fp32 matrices
     for (Mat& mt : P.mats) { off = align_up(off, 256); mt.stage_off = off; off += (size_t)mt.m * mt.n * 2; }
     for (Mat& mt : P.tiny) { off = align_up(off, 256); mt.stage_off = off; off += (size_t)mt.m * mt.n * 2; }
+    for (Mat& mt : P.tc) { off = align_up(off, 256); mt.stage_off = off; off += (size_t)mt.m * mt.n * 2; }
   }
   P.ws_bytes = align_up(off, 256);
   cudaError_t e = cudaSuccess;
@@ -438,7 +458,7 @@ static ns_status build_plan(Plan& P, HostTables& H, DevCtx* dc, const float* coe
   if (P.cast) {
     std::vector<CastJob> cin;
     int64_t mx = 0;
-    for (std::vector<Mat>* v : {&P.mats, &P.tiny})
+    for (std::vector<Mat>* v : {&P.mats, &P.tiny, &P.tc})
       for (Mat& mt : *v) {
         mt.user_x = mt.x; mt.user_out = mt.out;
         void* st = ws + mt.stage_off;
@@ -477,7 +497,19 @@ static ns_status build_plan(Plan& P, HostTables& H, DevCtx* dc, const float* coe
       }
     }
   }
+  for (Mat& mt : P.tc) {  // tcgen05 cluster kernel: 64 x 64-box maps of the input and output
+    ns_status st;
+    CUtensorMap tm;
+    if ((st = encode_tmap(&tm, mt.x, mt.m, mt.n, 64)) != NS_OK) return st;
+    mt.tm_x = (int)tmaps.size();
+    tmaps.push_back(tm);
+    if ((st = encode_tmap(&tm, mt.out, mt.m, mt.n, 64)) != NS_OK) return st;
+    mt.tm_out = (int)tmaps.size();
+    tmaps.push_back(tm);
+  }
   size_t tm_off = tmaps.empty() ? 0 : H.push(tmaps.data(), tmaps.size() * sizeof(CUtensorMap), 128);
+  struct TcFix { size_t job_off; int tin, tout; };
+  std::vector<TcFix> tc_fixes;
 
   // Device addresses of tensormaps are known only after allocation: record indices now,
   // patch pointers after cudaMalloc of the table (two-pass).  We first compute the final
@@ -543,6 +575,29 @@ static ns_status build_plan(Plan& P, HostTables& H, DevCtx* dc, const float* coe
       ph.ctas = ctas;
       P.phases.push_back(ph);
     }
+  }
+  // -- mid-size bf16 matrices: the whole NS on the tensor cores in one 16-CTA cluster each,
+  //    one launch for all of them (on a second side stream when other work is present)
+  if (!P.tc.empty()) {
+    std::vector<TcJob> jobs;
+    size_t smem = 0;
+    for (const Mat& mt : P.tc) {
+      TcJob J;
+      std::memset(&J, 0, sizeof(J));
+      J.m = (int)mt.m; J.n = (int)mt.n; J.M = (int)mt.M; J.N = (int)mt.N; J.wide = mt.wide ? 1 : 0;
+      J.Np = tc_np(mt.N); J.R = tc_rows(mt.M);
+      J.part = reinterpret_cast<float*>(ws + mt.tc_part_off);
+      tc_fixes.push_back({jobs.size() * sizeof(TcJob), mt.tm_x, mt.tm_out});
+      jobs.push_back(J);
+      smem = std::max(smem, tc_smem(J.Np, J.R));
+    }
+    Phase ph{PH_TC};
+    ph.dev_off = H.push(jobs.data(), jobs.size() * sizeof(TcJob), 64);
+    for (TcFix& f : tc_fixes) f.job_off += ph.dev_off;
+    ph.coeff_off = H.push(coeffs, (size_t)3 * T * sizeof(float), 16);
+    ph.njobs = (int)jobs.size();
+    ph.smem = smem;
+    P.phases.push_back(ph);
   }
   for (int k = 1; k <= T && !P.mats.empty(); ++k) {
     const float a = coeffs[3 * (k - 1)], b = coeffs[3 * (k - 1) + 1], c = coeffs[3 * (k - 1) + 2];
@@ -809,6 +864,11 @@ static ns_status build_plan(Plan& P, HostTables& H, DevCtx* dc, const float* coe
       J->tmAux = f.taux >= 0 ? dbase + tm_off + (size_t)(f.taux + 1) * sizeof(CUtensorMap) : nullptr;
       J->tmPeer = f.tpeer >= 0 ? dbase + tm_off + (size_t)f.tpeer * sizeof(CUtensorMap) : nullptr;
     }
+    for (const TcFix& f : tc_fixes) {
+      TcJob* J = reinterpret_cast<TcJob*>(H.bytes.data() + f.job_off);
+      J->tm_in = dbase + tm_off + (size_t)f.tin * sizeof(CUtensorMap);
+      J->tm_out = dbase + tm_off + (size_t)f.tout * sizeof(CUtensorMap);
+    }
     // pageable host -> device, stream-ordered: the runtime stages the bytes before returning
     // and does not wait for the stream's earlier work
     CU_TRY(cudaMemcpyAsync(P.dtab, H.bytes.data(), H.bytes.size(), cudaMemcpyHostToDevice, stream));
@@ -819,7 +879,7 @@ static ns_status build_plan(Plan& P, HostTables& H, DevCtx* dc, const float* coe
 
 static ns_status enqueue_plan(Plan& P, DevCtx* dc, cudaStream_t stream) {
   uint8_t* dbase = reinterpret_cast<uint8_t*>(P.dtab);
-  bool joined = true;
+  bool joined = true, joined2 = true;
   for (const Phase& ph : P.phases) {
     switch (ph.kind) {
       case PH_CLUSTER: {
@@ -840,6 +900,26 @@ static ns_status enqueue_plan(Plan& P, DevCtx* dc, cudaStream_t stream) {
         }
         ++g_launches;
         if (fork) CU_TRY(cudaEventRecord(dc->ev_join, dc->side));
+        break;
+      }
+      case PH_TC: {
+        // alone: on the caller's stream; beside other work: forked onto the second side stream
+        const bool fork = !P.mats.empty() || !P.tiny.empty();
+        cudaStream_t s = stream;
+        if (fork) {
+          CU_TRY(cudaEventRecord(dc->ev_fork2, stream));
+          CU_TRY(cudaStreamWaitEvent(dc->side2, dc->ev_fork2, 0));
+          s = dc->side2;
+          joined2 = false;
+        }
+        {
+          ProfScope ps(6, s);
+          CU_TRY(launch_cluster_tc_ns(reinterpret_cast<const TcJob*>(dbase + ph.dev_off), ph.njobs,
+                                      reinterpret_cast<const float*>(dbase + ph.coeff_off), P.iters, (int)P.precond,
+                                      ph.smem, dc->flags, s));
+        }
+        ++g_launches;
+        if (fork) CU_TRY(cudaEventRecord(dc->ev_join2, dc->side2));
         break;
       }
       case PH_COPY: {
@@ -869,6 +949,10 @@ static ns_status enqueue_plan(Plan& P, DevCtx* dc, cudaStream_t stream) {
           CU_TRY(cudaStreamWaitEvent(stream, dc->ev_join, 0));
           joined = true;
         }
+        if (ph.kind == PH_CAST_OUT && !joined2) {
+          CU_TRY(cudaStreamWaitEvent(stream, dc->ev_join2, 0));
+          joined2 = true;
+        }
         ProfScope ps(5, stream);
         CU_TRY(launch_cast(reinterpret_cast<const CastJob*>(dbase + ph.dev_off), ph.njobs, ph.max_numel,
                            ph.kind == PH_CAST_IN, dc->sms, stream));
@@ -893,6 +977,7 @@ static ns_status enqueue_plan(Plan& P, DevCtx* dc, cudaStream_t stream) {
     }
   }
   if (!joined) CU_TRY(cudaStreamWaitEvent(stream, dc->ev_join, 0));
+  if (!joined2) CU_TRY(cudaStreamWaitEvent(stream, dc->ev_join2, 0));
   return NS_OK;
 }
 
@@ -1012,6 +1097,21 @@ static bool to_cluster(const Mat& mt, ns_dtype dtype, bool any_peer, int cc_majo
   return g_path == 5 || dtype != NS_BF16 || (double)mt.M * (double)mt.N * (double)mt.N <= 2.2e6;
 }
 
+static bool tma_ok_call(const Mat& mt, ns_dtype dtype, bool cast);
+
+// Does matrix `mt` take the cluster-resident tcgen05 whole-NS kernel (cluster_tc.cu)?  bf16
+// matrices with short side N <= 256 whose slabs fit 16 CTAs (tc_fits: M <= 3072 for N > 128,
+// M <= 4096 for N <= 128) and that TMA can address, unless the FFMA cluster kernel takes them
+// (its small ones, to_cluster) -- paths 0 and 5; path 7 sends every such matrix here, path 4
+// none.  Shape-only (plus TMA alignment, as for the step engine): batching never changes a
+// result.
+static bool to_tc(const Mat& mt, ns_dtype dtype, bool any_peer, int cc_major, bool cast) {
+  if (dtype != NS_BF16 || any_peer || cc_major != 10) return false;
+  if (!(g_path == 0 || g_path == 5 || g_path == 7)) return false;
+  if (!tc_fits(mt.M, mt.N) || !tma_ok_call(mt, dtype, cast)) return false;
+  return g_path == 7 || !to_cluster(mt, dtype, any_peer, cc_major);
+}
+
 static bool tma_ok_call(const Mat& mt, ns_dtype dtype, bool cast) {
   Mat chk = mt;  // mixed precision: the step engine reads the 256-byte aligned staging copy
   if (cast) chk.x = chk.out = reinterpret_cast<void*>(256);
@@ -1053,10 +1153,14 @@ static void group_mats(const std::vector<Mat>& mats, ns_dtype dtype, bool cast, 
 // until unpinned, so a call can resolve all its plans before launching any.
 static ns_status resolve_plan(const std::vector<Mat>& mats_in, int iters, const float* coeffs, ns_precond precond,
                               ns_dtype dtype, cudaStream_t stream, bool cast, DevCtx* dc, Plan** out) {
-  std::vector<Mat> tiny, big;
+  std::vector<Mat> tiny, tcs, big;
   bool any_peer = false;
   for (const Mat& mt : mats_in) any_peer = any_peer || !mt.peer.empty();
-  for (const Mat& mt : mats_in) (to_cluster(mt, dtype, any_peer, dc->cc_major) ? tiny : big).push_back(mt);
+  for (const Mat& mt : mats_in) {
+    if (g_path != 7 && to_cluster(mt, dtype, any_peer, dc->cc_major)) tiny.push_back(mt);
+    else if (to_tc(mt, dtype, any_peer, dc->cc_major, cast)) tcs.push_back(mt);
+    else big.push_back(mt);
+  }
   bool simt = (g_path == 1) || dtype != NS_BF16 || dc->cc_major != 10;
   bool peers = false;
   for (const Mat& mt : big) {
@@ -1078,6 +1182,7 @@ static ns_status resolve_plan(const std::vector<Mat>& mats_in, int iters, const 
   key.push_back((uint64_t)iters); key.push_back((uint64_t)precond);
   for (int i = 0; i < 3 * iters; ++i) { uint32_t u; std::memcpy(&u, &coeffs[i], 4); key.push_back(u); }
   key.push_back((uint64_t)tiny.size());
+  key.push_back((uint64_t)tcs.size());
   for (const Mat& mt : mats_in) {
     key.push_back(reinterpret_cast<uint64_t>(mt.x)); key.push_back(reinterpret_cast<uint64_t>(mt.out));
     key.push_back((uint64_t)mt.m); key.push_back((uint64_t)mt.n);
@@ -1091,7 +1196,9 @@ static ns_status resolve_plan(const std::vector<Mat>& mats_in, int iters, const 
     // workspace than max(4 GiB, 2 x this list's): a caller that passes new buffers every step
     // (fresh pointers, fresh plans) must not accumulate workspaces.  Eviction releases the
     // victim's memory stream-ordered after its last launch (Plan::~Plan): no host sync.
-    const size_t need = workspace_bytes_for(big, dtype);
+    std::vector<Mat> sized(big);
+    sized.insert(sized.end(), tcs.begin(), tcs.end());
+    const size_t need = workspace_bytes_for(sized, dtype);
     const size_t budget = std::max<size_t>((size_t)4 << 30, 2 * need);
     auto held = [&]() {
       size_t b = 0;
@@ -1116,6 +1223,7 @@ static ns_status resolve_plan(const std::vector<Mat>& mats_in, int iters, const 
     np->cast = cast;
     np->mats = big;
     np->tiny = tiny;
+    np->tc = tcs;
     HostTables H;
     ns_status st = build_plan(*np, H, dc, coeffs, stream);
     if (st != NS_OK) {
@@ -1240,7 +1348,7 @@ ns_status nsx_epilogue_counters(uint64_t* out8, int reset) {
 
 int ns_set_path(int path) {
   std::lock_guard<std::mutex> lk(g_mu);
-  if (path != 0 && path != 1 && path != 2 && path != 4 && path != 5) return -1;
+  if (path != 0 && path != 1 && path != 2 && path != 4 && path != 5 && path != 7) return -1;
   int old = g_path;
   g_path = path;
   return old;
@@ -1531,6 +1639,9 @@ void ns_shutdown(void) {
     if (d.init && d.side) cudaStreamDestroy(d.side);
     if (d.init && d.ev_fork) cudaEventDestroy(d.ev_fork);
     if (d.init && d.ev_join) cudaEventDestroy(d.ev_join);
+    if (d.init && d.side2) cudaStreamDestroy(d.side2);
+    if (d.init && d.ev_fork2) cudaEventDestroy(d.ev_fork2);
+    if (d.init && d.ev_join2) cudaEventDestroy(d.ev_join2);
     if (d.init && d.cap) cudaStreamDestroy(d.cap);
     if (d.init && d.freer) cudaStreamDestroy(d.freer);
     d = DevCtx();

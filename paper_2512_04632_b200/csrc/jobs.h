@@ -211,4 +211,33 @@ __host__ __device__ inline bool cl_fits(int64_t M, int64_t N, int C = kClCtas) {
   return N >= 1 && N <= kClMaxN && M <= 4096 && cl_layout((int)M, (int)N, C).floats * 4 + kClHdr <= kClMaxSmem;
 }
 
+// ------------------------------------------------------------------ cluster-resident tcgen05 NS
+// Whole Newton-Schulz of one mid-size bf16 matrix (short side N <= 256) in ONE launch of a
+// 16-CTA cluster (cluster_tc.cu): Xh in row slabs of R rows per CTA,
+// N padded with zero columns to Np (128 or 256), A / B' copies in every CTA's shared memory,
+// Gram partials reduced through an fp32 scratch in L2 (16 * Np * Np floats per matrix).
+constexpr int kTcCtas = 16;
+constexpr size_t kTcMaxSmem = 227 * 1024;
+struct TcJob {
+  const void* tm_in;   // CUtensorMap (device) of the input X (m x n, 64 x 64 boxes, 128-byte swizzle)
+  const void* tm_out;  // CUtensorMap of the output (may address the same buffer)
+  float* part;         // 16 * Np * Np fp32 Gram partials
+  int32_t m, n, M, N, wide, Np, R, pad;
+};
+__host__ __device__ inline int tc_np(int64_t N) { return N <= 128 ? 128 : 256; }
+// Slab rows per CTA: a multiple of 64, at least 128 (one M = 128 UMMA per update accumulator).
+__host__ __device__ inline int tc_rows(int64_t M) {
+  const int64_t r = (M + kTcCtas - 1) / kTcCtas;
+  const int64_t r64 = (r + 63) / 64 * 64;
+  return (int)(r64 < 128 ? 128 : r64);
+}
+__host__ __device__ inline size_t tc_smem(int Np, int R) {
+  return (size_t)R * Np * 2 + (size_t)Np * Np * 2 + (size_t)Np * 4 + kTcCtas * 16 + 64 * 4 + 64 + 1024;
+}
+__host__ __device__ inline bool tc_fits(int64_t M, int64_t N) {
+  if (N < 1 || N > 256) return false;
+  const int R = tc_rows(M);
+  return R <= 256 && (int64_t)R * kTcCtas >= M && tc_smem(tc_np(N), R) <= kTcMaxSmem;
+}
+
 }  // namespace tns

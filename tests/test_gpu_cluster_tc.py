@@ -1,0 +1,119 @@
+"""Cluster-resident tcgen05 whole-NS kernel (csrc/cluster_tc.cu): every
+bf16 matrix with short side N <= 256 that fits 16 CTAs (M <= 3072 for N > 128) runs ALL steps
+of Alg. 2 in ONE launch -- CIFAR's 256 x 2304 and 256 x 576 conv weights, 768 x 256,
+1024 x 128, 64 x 576 (N padded to 128 with zero columns).  Same gates as the step engine
+against the fp64 oracle; plus launch count, determinism, batch invariance, flags and exact
+scale invariance."""
+import numpy as np
+import pytest
+import torch
+
+from synth import coeffs as C
+from synth import inputs as I
+from tests.helpers import assert_parity, oracle_run, polar_excess
+
+pytestmark = pytest.mark.gpu
+
+ns = pytest.importorskip("paper_2512_04632_b200")
+
+BF16_TOL = 2e-2
+
+SHAPES = [(256, 2304), (2304, 256), (256, 576), (576, 256), (768, 256), (1024, 128), (64, 576),
+          (256, 256), (200, 3000), (3072, 192), (136, 520)]
+
+
+def _run(x32, coeffs, precond, path=None):
+    old = ns.set_path(path) if path is not None else None
+    try:
+        t = torch.from_numpy(np.ascontiguousarray(x32, dtype=np.float32)).to(torch.bfloat16).cuda()
+        ns.orthogonalize(t, iters=len(coeffs), precond=precond, coeffs=coeffs)  # plan
+        t = torch.from_numpy(np.ascontiguousarray(x32, dtype=np.float32)).to(torch.bfloat16).cuda()
+        c0 = ns.launch_count()
+        ns.orthogonalize(t, iters=len(coeffs), precond=precond, coeffs=coeffs)
+        torch.cuda.synchronize()
+        n = ns.launch_count() - c0
+    finally:
+        if old is not None:
+            ns.set_path(old)
+    return t.float().cpu().numpy().astype(np.float64), n
+
+
+@pytest.mark.parametrize("m,n", SHAPES)
+@pytest.mark.parametrize("precond", ["aol", "frobenius"])
+def test_cluster_tc_against_oracle(m, n, precond):
+    x = I.gaussian(m, n, seed=I.matrix_seed(20, m * 7 + n))
+    coeffs = C.turbo(4) if precond == "aol" else C.muon_plus(5)
+    out, launches = _run(x, coeffs, precond)
+    assert launches == 1  # the whole NS in one cluster launch
+    ref = oracle_run(x, coeffs, precond)
+    assert_parity(out, ref, BF16_TOL, f"{m}x{n} {precond}")
+    eg, eo = polar_excess(out, ref, x)
+    assert eg <= 1.05 * eo, (eg, eo)
+    assert ns.read_flags() == 0
+
+
+def test_cluster_tc_precond_none_and_path7():
+    x = I.round_bf16(I.gaussian(384, 256, seed=22, bf16=False) / np.float32(40.0))
+    out, n = _run(x, C.turbo(4), "none")
+    assert n == 1
+    assert_parity(out, oracle_run(x, C.turbo(4), "none"), BF16_TOL)
+    # path 7 also takes the small matrices the FFMA cluster kernel would
+    x = I.gaussian(128, 128, seed=23)
+    out, n = _run(x, C.turbo(4), "aol", path=7)
+    assert n == 1
+    assert_parity(out, oracle_run(x, C.turbo(4), "aol"), BF16_TOL)
+
+
+def test_cluster_tc_deterministic_and_batch_invariant():
+    shapes = [(256, 2304), (256, 576), (64, 216), (768, 768), (1024, 128)]
+    xs = [I.gaussian(m, n, seed=400 + i) for i, (m, n) in enumerate(shapes)]
+    singles = [_run(x, C.turbo(4), "aol")[0] for x in xs]
+    again = _run(xs[0], C.turbo(4), "aol")[0]
+    assert np.array_equal(again, singles[0])
+    ts = [torch.from_numpy(x).to(torch.bfloat16).cuda() for x in xs]
+    outs = [torch.empty_like(t) for t in ts]
+    ns.orthogonalize_list(ts, out=outs, iters=4)
+    ns.orthogonalize_list(ts, out=outs, iters=4)  # graph replay
+    torch.cuda.synchronize()
+    for o, s in zip(outs, singles):
+        assert np.array_equal(o.float().cpu().numpy().astype(np.float64), s)
+
+
+def test_cluster_tc_scale_invariance_bitwise():
+    """NS(AOL(4 X)) == NS(AOL(X)) bitwise (reading R4: s from exponent-exact row sums)."""
+    x = I.gaussian(256, 2304, seed=61)
+    a, _ = _run(x, C.turbo(4), "aol")
+    b, _ = _run(x * np.float32(4.0), C.turbo(4), "aol")
+    assert np.array_equal(a, b)
+
+
+def test_cluster_tc_flags():
+    x = I.gaussian(576, 256, seed=65)
+    x[:, 5] = 0
+    ns.read_flags()
+    out, _ = _run(x, C.turbo(4), "aol")
+    assert ns.read_flags() & 1
+    assert np.all(np.isfinite(out)) and np.all(out[:, 5] == 0)
+    assert_parity(out, oracle_run(x, C.turbo(4), "aol"), BF16_TOL)
+    x = I.gaussian(576, 256, seed=66)
+    x[3, 2] = np.nan
+    ns.read_flags()
+    _run(x, C.turbo(4), "aol")
+    assert ns.read_flags() & 2
+
+
+def test_cluster_tc_out_of_place_and_cifar_set():
+    """The CIFAR conv set (config 3) in one grouped call: the four N = 256 matrices and 64 x 576
+    on the tcgen05 cluster kernel, 64 x 216 on the FFMA cluster kernel, concurrently."""
+    shapes = I.shape_set("cifar")
+    xs = [I.gaussian(m, n, seed=500 + i) for i, (m, n) in enumerate(shapes)]
+    ts = [torch.from_numpy(x).to(torch.bfloat16).cuda() for x in xs]
+    outs = [torch.empty_like(t) for t in ts]
+    ns.orthogonalize_list(ts, out=outs, iters=4)
+    c0 = ns.launch_count()
+    ns.orthogonalize_list(ts, out=outs, iters=4)
+    torch.cuda.synchronize()
+    assert ns.launch_count() - c0 == 2
+    for x, t, o in zip(xs, ts, outs):
+        assert np.array_equal(t.float().cpu().numpy(), x)  # input untouched
+        assert_parity(o.float().cpu().numpy().astype(np.float64), oracle_run(x, C.turbo(4), "aol"), BF16_TOL)
