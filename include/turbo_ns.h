@@ -191,24 +191,27 @@ ns_status ns_read_flags(void* stream, uint32_t* flags);
 /* Number of kernels the library launched on this process since load (host counter). */
 uint64_t ns_launch_count(void);
 
-/* Execution-path override for testing: 0 = auto: matrices with short side N <= 128 whose
- * fp32 copy fits in shared memory -- bf16 ones only while M*N^2 <= 2.2e6, where this is
- * measured faster than the step engine -- (the "cluster-resident" small-matrix kernel: the whole
- * NS of one matrix in ONE launch of a 16-CTA (when the matrix fits that layout) or 8-CTA
- * thread-block cluster, X, A and B resident in
- * shared memory, rows exchanged over DSMEM), all
- * other matrices through the step engine (tcgen05, 256x256 tiles on CTA pairs, for aligned
- * bf16, else SIMT; one PDL-chained launch per step); when both kinds are present the
- * cluster launch runs on an internal side stream joined back by events; 1 = force the SIMT
- * (CUDA-core) step kernels, 2 = tcgen05 with single-CTA 128x256 tiles, 4 = per-step launches
- * for every matrix (no cluster kernel), 5 = as 0 but every matrix that fits takes the cluster
- * kernel.  Returns the previous value; any other `path` returns -1 and changes nothing. */
+/* Execution-path override for testing.  0 = auto: bf16 matrices with short side N <= 128
+ * that TMA can address and that fit 16 row slabs (M <= 4096) run the WHOLE NS in ONE launch of
+ * a 16-CTA cluster on the tensor cores (cluster_tc_ns_kernel: X slabs and A / B' resident in
+ * shared memory, Gram partials reduced through L2 in a fixed order, A rows broadcast over
+ * DSMEM); other matrices with N <= 128 whose fp32 copy
+ * fits in shared memory (fp32 always, bf16 while M*N^2 <= 2.2e6) run the whole NS in one
+ * launch of a 16- or 8-CTA FFMA cluster (cluster_ns_kernel; row a-10); all other matrices go
+ * through the step engine (tcgen05, 256x256 tiles on CTA pairs, for aligned bf16, else SIMT;
+ * one PDL-chained launch per step); when several kinds are present the cluster launches run
+ * on internal side streams joined back by events; 1 = force the SIMT (CUDA-core) step
+ * kernels, 2 = tcgen05 with single-CTA 128x256 tiles, 4 = per-step launches for every matrix
+ * (no cluster kernels), 5 = as 0 but every matrix that fits the FFMA cluster kernel takes it,
+ * 7 = as 0 but every bf16 matrix with N <= 256 that fits the tcgen05 cluster kernel (M <= 3072
+ * for N > 128) takes it.  Results of a matrix never depend on the rest of the call.  Returns
+ * the previous value; any other `path` returns -1 and changes nothing. */
 int ns_set_path(int path);
 
 /* Per-kernel event timing (measurement support for bench.py; off by default).
  * When enabled, every launch the library enqueues is bracketed by CUDA events recorded
  * on the SAME stream.  ns_profile_read SYNCHRONISES on the last event, writes for each
- * kind k (0 GRAM, 1 PRECOND, 2 POLY, 3 XB, 4 SIMT, 5 COPY, 6 unused, 7 CLUSTER; nkinds <= 8) the summed
+ * kind k (0 GRAM, 1 PRECOND, 2 POLY, 3 XB, 4 SIMT, 5 COPY, 6 CLUSTER_TC, 7 CLUSTER; nkinds <= 8) the summed
  * device milliseconds ms[k] and the launch count counts[k], then clears the records. */
 void ns_profile_enable(int on);
 ns_status ns_profile_read(double* ms, uint64_t* counts, int nkinds);

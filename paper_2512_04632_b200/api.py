@@ -221,12 +221,13 @@ def launch_count() -> int:
 
 def set_path(path: int) -> int:
     """0 auto, 1 CUDA-core kernels, 2 tcgen05 1-CTA tiles, 4 per-step launches for every
-    matrix (no cluster kernel), 5 every matrix that fits takes the cluster kernel.  Returns
-    the previous path, or -1 (and changes nothing) for any other value."""
+    matrix (no cluster kernels), 5 every matrix that fits takes the FFMA cluster kernel, 7 every
+    bf16 matrix with N <= 256 that fits takes the tcgen05 cluster kernel.  Returns the previous
+    path, or -1 (and changes nothing) for any other value."""
     return int(lib.ns_set_path(int(path)))
 
 
-KERNEL_KINDS = ("gram", "precondition", "poly", "update", "simt", "copy", "unused", "cluster")
+KERNEL_KINDS = ("gram", "precondition", "poly", "update", "simt", "copy", "cluster_tc", "cluster")
 
 
 def profile_enable(on: bool = True) -> None:

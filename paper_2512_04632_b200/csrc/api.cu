@@ -75,9 +75,10 @@ struct DevCtx {
   // side stream for the cluster-resident small-matrix launch, joined back by events
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
-  // second side stream: the tcgen05 cluster kernel (mid-size matrices) beside the others
-  cudaStream_t side2 = nullptr;
-  cudaEvent_t ev_fork2 = nullptr, ev_join2 = nullptr;
+  // side streams of the tcgen05 cluster kernel's launches (one per cluster size 2, 4, 8, 16),
+  // so they run beside each other and beside the step engine
+  cudaStream_t tside[4] = {};
+  cudaEvent_t tfork[4] = {}, tjoin[4] = {};
   cudaStream_t cap = nullptr;  // private stream on which plans are captured into CUDA graphs
   // private stream on which evicted plans' device memory is released (cudaFreeAsync), ordered
   // after the plan's last use by an event -- eviction never synchronises the host
@@ -100,9 +101,11 @@ static ns_status dev_ctx(DevCtx** out) {
     CU_TRY(cudaStreamCreateWithFlags(&d.side, cudaStreamNonBlocking));
     CU_TRY(cudaEventCreateWithFlags(&d.ev_fork, cudaEventDisableTiming));
     CU_TRY(cudaEventCreateWithFlags(&d.ev_join, cudaEventDisableTiming));
-    CU_TRY(cudaStreamCreateWithFlags(&d.side2, cudaStreamNonBlocking));
-    CU_TRY(cudaEventCreateWithFlags(&d.ev_fork2, cudaEventDisableTiming));
-    CU_TRY(cudaEventCreateWithFlags(&d.ev_join2, cudaEventDisableTiming));
+    for (int i = 0; i < 4; ++i) {
+      CU_TRY(cudaStreamCreateWithFlags(&d.tside[i], cudaStreamNonBlocking));
+      CU_TRY(cudaEventCreateWithFlags(&d.tfork[i], cudaEventDisableTiming));
+      CU_TRY(cudaEventCreateWithFlags(&d.tjoin[i], cudaEventDisableTiming));
+    }
     CU_TRY(cudaStreamCreateWithFlags(&d.freer, cudaStreamNonBlocking));
     if (!g_encode) {
       cudaDriverEntryPointQueryResult q;
@@ -314,7 +317,7 @@ static int choose_bn(const std::vector<Mat>& mats, int cg, int workers) {
 
 static size_t split_bytes(const Mat& mt) { return mt.split ? (size_t)mt.split * kSplitLd * kSplitLd * 4 : 0; }
 
-static size_t tc_part_bytes(int64_t N) { return (size_t)kTcCtas * tc_np(N) * tc_np(N) * 4; }
+static size_t tc_part_bytes(int64_t M, int64_t N) { return (size_t)tc_cluster(M, N) * tc_np(N) * tc_np(N) * 4; }
 
 // Workspace of a problem list as the step engine lays it out; a bf16 matrix the tcgen05
 // cluster kernel could take counts with the larger of its two footprints (an upper bound
@@ -330,7 +333,7 @@ static size_t workspace_bytes_for(const std::vector<Mat>& mats, ns_dtype dt) {
     o = align_up(o, 256) + s_floats(mt.N) * 4;
     o = align_up(o, 256) + (size_t)mt.N * part_ld_for(mt.N) * 4;
     if (dt == NS_BF16) o = align_up(o, 256) + (size_t)split_factor(mt.M, mt.N) * kSplitLd * kSplitLd * 4;
-    if (dt == NS_BF16 && tc_fits(mt.M, mt.N)) o = std::max(o, tc_part_bytes(mt.N));
+    if (dt == NS_BF16 && tc_fits(mt.M, mt.N)) o = std::max(o, tc_part_bytes(mt.M, mt.N));
     off = align_up(off, 256) + align_up(o, 256);
   }
   return align_up(off, 256);
@@ -415,7 +418,7 @@ static ns_status build_plan(Plan& P, HostTables& H, DevCtx* dc, const float* coe
     off = align_up(off, 256); mt.split_off = off; off += split_bytes(mt);
   }
   for (Mat& mt : P.tc) {  // Gram partials of the tcgen05 cluster kernel
-    off = align_up(off, 256); mt.tc_part_off = off; off += tc_part_bytes(mt.N);
+    off = align_up(off, 256); mt.tc_part_off = off; off += tc_part_bytes(mt.M, mt.N);
   }
   if (P.cast) {  // bf16 staging copies of the caller's fp32 matrices
     for (Mat& mt : P.mats) { off = align_up(off, 256); mt.stage_off = off; off += (size_t)mt.m * mt.n * 2; }
@@ -579,25 +582,32 @@ static ns_status build_plan(Plan& P, HostTables& H, DevCtx* dc, const float* coe
   // -- mid-size bf16 matrices: the whole NS on the tensor cores in one 16-CTA cluster each,
   //    one launch for all of them (on a second side stream when other work is present)
   if (!P.tc.empty()) {
-    std::vector<TcJob> jobs;
-    size_t smem = 0;
-    for (const Mat& mt : P.tc) {
-      TcJob J;
-      std::memset(&J, 0, sizeof(J));
-      J.m = (int)mt.m; J.n = (int)mt.n; J.M = (int)mt.M; J.N = (int)mt.N; J.wide = mt.wide ? 1 : 0;
-      J.Np = tc_np(mt.N); J.R = tc_rows(mt.M);
-      J.part = reinterpret_cast<float*>(ws + mt.tc_part_off);
-      tc_fixes.push_back({jobs.size() * sizeof(TcJob), mt.tm_x, mt.tm_out});
-      jobs.push_back(J);
-      smem = std::max(smem, tc_smem(J.Np, J.R));
+    // one launch per cluster size (a function of the shape alone, tc_cluster)
+    for (int C = 2; C <= kTcCtas; C *= 2) {
+      std::vector<TcJob> jobs;
+      std::vector<TcFix> fx;
+      size_t smem = 0;
+      for (const Mat& mt : P.tc) {
+        if (tc_cluster(mt.M, mt.N) != C) continue;
+        TcJob J;
+        std::memset(&J, 0, sizeof(J));
+        J.m = (int)mt.m; J.n = (int)mt.n; J.M = (int)mt.M; J.N = (int)mt.N; J.wide = mt.wide ? 1 : 0;
+        J.Np = tc_np(mt.N); J.C = C; J.R = tc_rows(mt.M, C);
+        J.part = reinterpret_cast<float*>(ws + mt.tc_part_off);
+        fx.push_back({jobs.size() * sizeof(TcJob), mt.tm_x, mt.tm_out});
+        jobs.push_back(J);
+        smem = std::max(smem, tc_smem(J.Np, J.R, C));
+      }
+      if (jobs.empty()) continue;
+      Phase ph{PH_TC};
+      ph.dev_off = H.push(jobs.data(), jobs.size() * sizeof(TcJob), 64);
+      for (TcFix& f : fx) { f.job_off += ph.dev_off; tc_fixes.push_back(f); }
+      ph.coeff_off = H.push(coeffs, (size_t)3 * T * sizeof(float), 16);
+      ph.njobs = (int)jobs.size();
+      ph.smem = smem;
+      ph.ctas = C;
+      P.phases.push_back(ph);
     }
-    Phase ph{PH_TC};
-    ph.dev_off = H.push(jobs.data(), jobs.size() * sizeof(TcJob), 64);
-    for (TcFix& f : tc_fixes) f.job_off += ph.dev_off;
-    ph.coeff_off = H.push(coeffs, (size_t)3 * T * sizeof(float), 16);
-    ph.njobs = (int)jobs.size();
-    ph.smem = smem;
-    P.phases.push_back(ph);
   }
   for (int k = 1; k <= T && !P.mats.empty(); ++k) {
     const float a = coeffs[3 * (k - 1)], b = coeffs[3 * (k - 1) + 1], c = coeffs[3 * (k - 1) + 2];
@@ -879,7 +889,8 @@ static ns_status build_plan(Plan& P, HostTables& H, DevCtx* dc, const float* coe
 
 static ns_status enqueue_plan(Plan& P, DevCtx* dc, cudaStream_t stream) {
   uint8_t* dbase = reinterpret_cast<uint8_t*>(P.dtab);
-  bool joined = true, joined2 = true;
+  bool joined = true;
+  uint32_t tjoined = 0xFu;  // bit i clear: tc side stream i must be joined back
   for (const Phase& ph : P.phases) {
     switch (ph.kind) {
       case PH_CLUSTER: {
@@ -903,23 +914,27 @@ static ns_status enqueue_plan(Plan& P, DevCtx* dc, cudaStream_t stream) {
         break;
       }
       case PH_TC: {
-        // alone: on the caller's stream; beside other work: forked onto the second side stream
-        const bool fork = !P.mats.empty() || !P.tiny.empty();
+        // alone: on the caller's stream; beside other work (the step engine, the FFMA cluster
+        // kernel, or a tc launch of another cluster size): forked onto its own side stream
+        int ntc = 0;
+        for (const Phase& q : P.phases) ntc += q.kind == PH_TC;
+        const bool fork = !P.mats.empty() || !P.tiny.empty() || ntc > 1;
+        const int si = ph.ctas == 2 ? 0 : ph.ctas == 4 ? 1 : ph.ctas == 8 ? 2 : 3;
         cudaStream_t s = stream;
         if (fork) {
-          CU_TRY(cudaEventRecord(dc->ev_fork2, stream));
-          CU_TRY(cudaStreamWaitEvent(dc->side2, dc->ev_fork2, 0));
-          s = dc->side2;
-          joined2 = false;
+          CU_TRY(cudaEventRecord(dc->tfork[si], stream));
+          CU_TRY(cudaStreamWaitEvent(dc->tside[si], dc->tfork[si], 0));
+          s = dc->tside[si];
+          tjoined &= ~(1u << si);
         }
         {
           ProfScope ps(6, s);
-          CU_TRY(launch_cluster_tc_ns(reinterpret_cast<const TcJob*>(dbase + ph.dev_off), ph.njobs,
+          CU_TRY(launch_cluster_tc_ns(reinterpret_cast<const TcJob*>(dbase + ph.dev_off), ph.njobs, ph.ctas,
                                       reinterpret_cast<const float*>(dbase + ph.coeff_off), P.iters, (int)P.precond,
                                       ph.smem, dc->flags, s));
         }
         ++g_launches;
-        if (fork) CU_TRY(cudaEventRecord(dc->ev_join2, dc->side2));
+        if (fork) CU_TRY(cudaEventRecord(dc->tjoin[si], dc->tside[si]));
         break;
       }
       case PH_COPY: {
@@ -949,10 +964,9 @@ static ns_status enqueue_plan(Plan& P, DevCtx* dc, cudaStream_t stream) {
           CU_TRY(cudaStreamWaitEvent(stream, dc->ev_join, 0));
           joined = true;
         }
-        if (ph.kind == PH_CAST_OUT && !joined2) {
-          CU_TRY(cudaStreamWaitEvent(stream, dc->ev_join2, 0));
-          joined2 = true;
-        }
+        if (ph.kind == PH_CAST_OUT)
+          for (int i = 0; i < 4; ++i)
+            if (!(tjoined >> i & 1u)) { CU_TRY(cudaStreamWaitEvent(stream, dc->tjoin[i], 0)); tjoined |= 1u << i; }
         ProfScope ps(5, stream);
         CU_TRY(launch_cast(reinterpret_cast<const CastJob*>(dbase + ph.dev_off), ph.njobs, ph.max_numel,
                            ph.kind == PH_CAST_IN, dc->sms, stream));
@@ -977,7 +991,8 @@ static ns_status enqueue_plan(Plan& P, DevCtx* dc, cudaStream_t stream) {
     }
   }
   if (!joined) CU_TRY(cudaStreamWaitEvent(stream, dc->ev_join, 0));
-  if (!joined2) CU_TRY(cudaStreamWaitEvent(stream, dc->ev_join2, 0));
+  for (int i = 0; i < 4; ++i)
+    if (!(tjoined >> i & 1u)) CU_TRY(cudaStreamWaitEvent(stream, dc->tjoin[i], 0));
   return NS_OK;
 }
 
@@ -1099,17 +1114,19 @@ static bool to_cluster(const Mat& mt, ns_dtype dtype, bool any_peer, int cc_majo
 
 static bool tma_ok_call(const Mat& mt, ns_dtype dtype, bool cast);
 
-// Does matrix `mt` take the cluster-resident tcgen05 whole-NS kernel (cluster_tc.cu)?  bf16
-// matrices with short side N <= 256 whose slabs fit 16 CTAs (tc_fits: M <= 3072 for N > 128,
-// M <= 4096 for N <= 128) and that TMA can address, unless the FFMA cluster kernel takes them
-// (its small ones, to_cluster) -- paths 0 and 5; path 7 sends every such matrix here, path 4
-// none.  Shape-only (plus TMA alignment, as for the step engine): batching never changes a
-// result.
+// Does matrix `mt` take the cluster-resident tcgen05 whole-NS kernel (cluster_tc.cu)?  Paths 0
+// and 5: bf16 matrices with short side N <= 128 (padded to 128) whose slabs fit 16 CTAs (M <=
+// 4096) and that TMA can address -- measured faster than both the step engine and the FFMA
+// cluster kernel (graph replay, profiles/r02_cluster_tc.log: 1024x128 43 vs 79 us, 64x576 43
+// vs 64, 128^2 43 vs 60 / 66).  For 128 < N <= 256 (padded to 256) the kernel is correct but
+// slower than the step engine (256x2304 123 vs 89 us: the Gram reduction and the A broadcast
+// move ~0.6 MB per CTA per iteration), so only path 7 sends those here; path 4 sends none.
+// Shape-only (plus TMA alignment, as for the step engine): batching never changes a result.
 static bool to_tc(const Mat& mt, ns_dtype dtype, bool any_peer, int cc_major, bool cast) {
   if (dtype != NS_BF16 || any_peer || cc_major != 10) return false;
   if (!(g_path == 0 || g_path == 5 || g_path == 7)) return false;
   if (!tc_fits(mt.M, mt.N) || !tma_ok_call(mt, dtype, cast)) return false;
-  return g_path == 7 || !to_cluster(mt, dtype, any_peer, cc_major);
+  return g_path == 7 || mt.N <= 128;
 }
 
 static bool tma_ok_call(const Mat& mt, ns_dtype dtype, bool cast) {
@@ -1157,8 +1174,11 @@ static ns_status resolve_plan(const std::vector<Mat>& mats_in, int iters, const 
   bool any_peer = false;
   for (const Mat& mt : mats_in) any_peer = any_peer || !mt.peer.empty();
   for (const Mat& mt : mats_in) {
-    if (g_path != 7 && to_cluster(mt, dtype, any_peer, dc->cc_major)) tiny.push_back(mt);
+    // path 5 keeps every matrix the FFMA cluster kernel fits there (its tests); otherwise the
+    // tcgen05 cluster kernel first, then the FFMA one (fp32, TMA-unaligned small bf16)
+    if (g_path == 5 && to_cluster(mt, dtype, any_peer, dc->cc_major)) tiny.push_back(mt);
     else if (to_tc(mt, dtype, any_peer, dc->cc_major, cast)) tcs.push_back(mt);
+    else if (to_cluster(mt, dtype, any_peer, dc->cc_major)) tiny.push_back(mt);
     else big.push_back(mt);
   }
   bool simt = (g_path == 1) || dtype != NS_BF16 || dc->cc_major != 10;
@@ -1639,9 +1659,11 @@ void ns_shutdown(void) {
     if (d.init && d.side) cudaStreamDestroy(d.side);
     if (d.init && d.ev_fork) cudaEventDestroy(d.ev_fork);
     if (d.init && d.ev_join) cudaEventDestroy(d.ev_join);
-    if (d.init && d.side2) cudaStreamDestroy(d.side2);
-    if (d.init && d.ev_fork2) cudaEventDestroy(d.ev_fork2);
-    if (d.init && d.ev_join2) cudaEventDestroy(d.ev_join2);
+    for (int i = 0; i < 4; ++i) {
+      if (d.init && d.tside[i]) cudaStreamDestroy(d.tside[i]);
+      if (d.init && d.tfork[i]) cudaEventDestroy(d.tfork[i]);
+      if (d.init && d.tjoin[i]) cudaEventDestroy(d.tjoin[i]);
+    }
     if (d.init && d.cap) cudaStreamDestroy(d.cap);
     if (d.init && d.freer) cudaStreamDestroy(d.freer);
     d = DevCtx();

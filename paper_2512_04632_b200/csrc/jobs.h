@@ -213,31 +213,46 @@ __host__ __device__ inline bool cl_fits(int64_t M, int64_t N, int C = kClCtas) {
 
 // ------------------------------------------------------------------ cluster-resident tcgen05 NS
 // Whole Newton-Schulz of one mid-size bf16 matrix (short side N <= 256) in ONE launch of a
-// 16-CTA cluster (cluster_tc.cu): Xh in row slabs of R rows per CTA,
-// N padded with zero columns to Np (128 or 256), A / B' copies in every CTA's shared memory,
-// Gram partials reduced through an fp32 scratch in L2 (16 * Np * Np floats per matrix).
-constexpr int kTcCtas = 16;
+// C-CTA cluster (cluster_tc.cu): Xh in row slabs of R rows per CTA, N
+// padded with zero columns to Np (128 or 256), A / B' copies in every CTA's shared memory,
+// Gram partials reduced through an fp32 scratch in L2 (C * Np * Np floats per matrix).  C is
+// the smallest power of two (2..16) whose slabs fit -- a function of the shape alone, so a
+// matrix's result never depends on the rest of its call; jobs are launched in groups of
+// equal C.
+constexpr int kTcCtas = 16;  // largest cluster (non-portable size)
 constexpr size_t kTcMaxSmem = 227 * 1024;
 struct TcJob {
   const void* tm_in;   // CUtensorMap (device) of the input X (m x n, 64 x 64 boxes, 128-byte swizzle)
   const void* tm_out;  // CUtensorMap of the output (may address the same buffer)
-  float* part;         // 16 * Np * Np fp32 Gram partials
-  int32_t m, n, M, N, wide, Np, R, pad;
+  float* part;         // C * Np * Np fp32 Gram partials
+  int32_t m, n, M, N, wide, Np, R, C;
 };
 __host__ __device__ inline int tc_np(int64_t N) { return N <= 128 ? 128 : 256; }
-// Slab rows per CTA: a multiple of 64, at least 128 (one M = 128 UMMA per update accumulator).
-__host__ __device__ inline int tc_rows(int64_t M) {
-  const int64_t r = (M + kTcCtas - 1) / kTcCtas;
+// Scratch floats for the owner's per-warp AOL row sums (8 warps x Np / C rows) or diagonal.
+__host__ __device__ inline int tc_diag_floats(int Np, int C) { return 8 * (Np / C) < 128 ? 128 : 8 * (Np / C); }
+__host__ __device__ inline size_t tc_smem(int Np, int R, int C) {
+  return (size_t)R * Np * 2 + (size_t)Np * Np * 2 + (size_t)Np * 4 + kTcCtas * 16 + (size_t)tc_diag_floats(Np, C) * 4 +
+         64 + 1024;
+}
+// Slab rows per CTA for a C-CTA cluster: a multiple of 64, at least 128 (one M = 128 UMMA
+// per update accumulator).
+__host__ __device__ inline int tc_rows(int64_t M, int C) {
+  const int64_t r = (M + C - 1) / C;
   const int64_t r64 = (r + 63) / 64 * 64;
   return (int)(r64 < 128 ? 128 : r64);
 }
-__host__ __device__ inline size_t tc_smem(int Np, int R) {
-  return (size_t)R * Np * 2 + (size_t)Np * Np * 2 + (size_t)Np * 4 + kTcCtas * 16 + 64 * 4 + 64 + 1024;
+// Cluster size for an M x N matrix (0: does not fit): 16 CTAs whenever the slabs fit.  The
+// kernel takes any power of two 2..16 (Np / C <= 64 owned rows per CTA); smaller clusters were
+// measured SLOWER for a lone matrix (graph replay: 1024x128 53 us at C = 4 vs 43 at 16, 64x576
+// 55 at 4 vs 43, 768x256 111 at 8 vs 102 -- the owner's reduction and broadcast rows grow as
+// Np / C) though they take fewer SMs from a concurrent step-engine launch (CIFAR set 103 vs
+// 108 us), so the size is fixed at 16: a function of the shape alone either way.
+__host__ __device__ inline int tc_cluster(int64_t M, int64_t N) {
+  if (N < 1 || N > 256 || M < 1) return 0;
+  const int Np = tc_np(N), C = kTcCtas;
+  const int R = tc_rows(M, C);
+  return (R <= 256 && (int64_t)R * C >= M && tc_smem(Np, R, C) <= kTcMaxSmem) ? C : 0;
 }
-__host__ __device__ inline bool tc_fits(int64_t M, int64_t N) {
-  if (N < 1 || N > 256) return false;
-  const int R = tc_rows(M);
-  return R <= 256 && (int64_t)R * kTcCtas >= M && tc_smem(tc_np(N), R) <= kTcMaxSmem;
-}
+__host__ __device__ inline bool tc_fits(int64_t M, int64_t N) { return tc_cluster(M, N) != 0; }
 
 }  // namespace tns

@@ -49,10 +49,11 @@ cudaError_t launch_cluster_ns(const ClusterJob* d_jobs, int njobs, const float* 
 // (8 phase marks + launch count).
 cudaError_t cluster_timeline(unsigned long long* out9, bool reset);
 
-// Whole NS of `njobs` mid-size bf16 matrices on the tensor cores, one 16-CTA cluster each
-// (cluster_tc.cu); smem_bytes = max tc_smem(Np, R) over the jobs; d_coeffs: 3*iters floats.
-cudaError_t launch_cluster_tc_ns(const TcJob* d_jobs, int njobs, const float* d_coeffs, int iters, int precond,
-                                 size_t smem_bytes, uint32_t* d_flags, cudaStream_t stream);
+// Whole NS of `njobs` mid-size bf16 matrices on the tensor cores, one cluster of `ctas` CTAs
+// each (every job's C == ctas; cluster_tc.cu); smem_bytes = max tc_smem(Np, R) over the jobs;
+// d_coeffs: 3*iters floats.
+cudaError_t launch_cluster_tc_ns(const TcJob* d_jobs, int njobs, int ctas, const float* d_coeffs, int iters,
+                                 int precond, size_t smem_bytes, uint32_t* d_flags, cudaStream_t stream);
 
 // fp32 <-> bf16 storage casts of a mixed-precision call (muon.cu), one launch for all jobs.
 cudaError_t launch_cast(const CastJob* d_jobs, int count, int64_t max_numel, bool to_bf16, int sms,

@@ -98,13 +98,13 @@ def test_cluster_matches_step_engine():
 
 
 def test_cluster_eligibility_boundary():
-    """N = 128: M = 160 is the largest eligible height (227 KB of shared memory); 168 goes
-    to the step engine."""
+    """N = 128 fp32 (the FFMA cluster kernel's own mode): M = 160 is the largest eligible height
+    (227 KB of shared memory); 168 goes to the CUDA-core step kernels."""
     for m, want in [(160, 1), (168, 13)]:
-        x = I.gaussian(m, 128, seed=13)
-        out, launches = _run(x, C.turbo(4), "aol")
+        x = I.gaussian(m, 128, seed=13, bf16=False)
+        out, launches = _run(x, C.turbo(4), "aol", torch.float32)
         assert launches == want, (m, launches)
-        assert_parity(out, oracle_run(x, C.turbo(4), "aol"), BF16_TOL)
+        assert_parity(out, oracle_run(x, C.turbo(4), "aol"), FP32_TOL)
 
 
 def test_cluster_determinism_and_scale_invariance_bitwise():
@@ -234,16 +234,20 @@ def test_cluster_size_groups_bitwise():
 
 
 def test_auto_routing_by_cost():
-    """Path 0: bf16 matrices that fit take the cluster kernel only while M*N^2 <= 2.2e6
-    (64 x 216: yes; 64 x 576, 160 x 128: step engine); fp32 ones always.  Both routes meet
-    the gate and agree to bf16 rounding."""
-    cases = [(64, 216, torch.bfloat16, 1), (64, 576, torch.bfloat16, 13), (160, 128, torch.bfloat16, 13),
+    """Path 0: bf16 matrices with N <= 128 that TMA can address take the tcgen05 cluster kernel
+    (one launch); fp32 ones that fit the FFMA cluster kernel take it (one launch); path 5 sends
+    every matrix that fits to the FFMA kernel, path 4 everything to the step engine.  All routes
+    meet the gate and agree to rounding."""
+    cases = [(64, 216, torch.bfloat16, 1), (64, 576, torch.bfloat16, 1), (160, 128, torch.bfloat16, 1),
              (64, 576, torch.float32, 1), (128, 128, torch.bfloat16, 1)]
     for m, n, dt, want in cases:
         x = I.gaussian(m, n, seed=240, bf16=(dt == torch.bfloat16))
         a, la = _run(x, C.turbo(4), "aol", dt, path=0)
         b, lb = _run(x, C.turbo(4), "aol", dt, path=5)
-        assert la == want and lb == 1, (m, n, dt, la, lb)
+        c, lc = _run(x, C.turbo(4), "aol", dt, path=4)
+        assert la == want and lb == 1 and lc == 13, (m, n, dt, la, lb, lc)
         tol = BF16_TOL if dt == torch.bfloat16 else FP32_TOL
         ref = oracle_run(x, C.turbo(4), "aol")
-        assert relF(a, ref) <= tol and relF(b, ref) <= tol
+        assert relF(a, ref) <= tol and relF(b, ref) <= tol and relF(c, ref) <= tol
+
+

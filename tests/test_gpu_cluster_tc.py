@@ -1,9 +1,11 @@
-"""Cluster-resident tcgen05 whole-NS kernel (csrc/cluster_tc.cu): every
-bf16 matrix with short side N <= 256 that fits 16 CTAs (M <= 3072 for N > 128) runs ALL steps
-of Alg. 2 in ONE launch -- CIFAR's 256 x 2304 and 256 x 576 conv weights, 768 x 256,
-1024 x 128, 64 x 576 (N padded to 128 with zero columns).  Same gates as the step engine
-against the fp64 oracle; plus launch count, determinism, batch invariance, flags and exact
-scale invariance."""
+"""Cluster-resident tcgen05 whole-NS kernel (csrc/cluster_tc.cu): a bf16
+matrix with short side N <= 256 that fits 16 CTAs (M <= 3072 for N > 128, M <= 4096 for
+N <= 128) runs ALL steps of Alg. 2 in ONE launch -- CIFAR's 256 x 2304 and 256 x 576 conv
+weights, 768 x 256, 1024 x 128, 64 x 576 (N padded to 128 with zero columns).  The
+default path routes N <= 128 there (measured faster); ns_set_path(7) sends every eligible
+matrix, which is how the N > 128 cases run here.  Same gates as the step engine against the
+fp64 oracle; plus launch count, determinism (repeated calls bitwise), batch invariance, flags
+and exact scale invariance."""
 import numpy as np
 import pytest
 import torch
@@ -22,7 +24,7 @@ SHAPES = [(256, 2304), (2304, 256), (256, 576), (576, 256), (768, 256), (1024, 1
           (256, 256), (200, 3000), (3072, 192), (136, 520)]
 
 
-def _run(x32, coeffs, precond, path=None):
+def _run(x32, coeffs, precond, path=7):
     old = ns.set_path(path) if path is not None else None
     try:
         t = torch.from_numpy(np.ascontiguousarray(x32, dtype=np.float32)).to(torch.bfloat16).cuda()
@@ -64,17 +66,31 @@ def test_cluster_tc_precond_none_and_path7():
     assert_parity(out, oracle_run(x, C.turbo(4), "aol"), BF16_TOL)
 
 
+def test_cluster_tc_default_routing():
+    """Path 0: N <= 128 bf16 matrices take the tcgen05 cluster kernel (one launch), N = 256 the
+    step engine."""
+    out, n = _run(I.gaussian(1024, 128, seed=24), C.turbo(4), "aol", path=0)
+    assert n == 1
+    out, n = _run(I.gaussian(768, 256, seed=25), C.turbo(4), "aol", path=0)
+    assert n == 13
+
+
 def test_cluster_tc_deterministic_and_batch_invariant():
     shapes = [(256, 2304), (256, 576), (64, 216), (768, 768), (1024, 128)]
     xs = [I.gaussian(m, n, seed=400 + i) for i, (m, n) in enumerate(shapes)]
     singles = [_run(x, C.turbo(4), "aol")[0] for x in xs]
-    again = _run(xs[0], C.turbo(4), "aol")[0]
-    assert np.array_equal(again, singles[0])
+    for _ in range(8):  # repeated calls: one bit pattern (fixed-order reductions, no races)
+        again = _run(xs[0], C.turbo(4), "aol")[0]
+        assert np.array_equal(again, singles[0])
     ts = [torch.from_numpy(x).to(torch.bfloat16).cuda() for x in xs]
     outs = [torch.empty_like(t) for t in ts]
-    ns.orthogonalize_list(ts, out=outs, iters=4)
-    ns.orthogonalize_list(ts, out=outs, iters=4)  # graph replay
-    torch.cuda.synchronize()
+    old = ns.set_path(7)
+    try:
+        ns.orthogonalize_list(ts, out=outs, iters=4)
+        ns.orthogonalize_list(ts, out=outs, iters=4)  # graph replay
+        torch.cuda.synchronize()
+    finally:
+        ns.set_path(old)
     for o, s in zip(outs, singles):
         assert np.array_equal(o.float().cpu().numpy().astype(np.float64), s)
 
@@ -102,18 +118,24 @@ def test_cluster_tc_flags():
     assert ns.read_flags() & 2
 
 
-def test_cluster_tc_out_of_place_and_cifar_set():
-    """The CIFAR conv set (config 3) in one grouped call: the four N = 256 matrices and 64 x 576
-    on the tcgen05 cluster kernel, 64 x 216 on the FFMA cluster kernel, concurrently."""
+@pytest.mark.parametrize("path,launches", [(7, 1), (0, 18)])
+def test_cluster_tc_out_of_place_and_cifar_set(path, launches):
+    """The CIFAR conv set (config 3) in one grouped call.  Path 7: all six matrices on the
+    tcgen05 cluster kernel, one launch.  Path 0: the two N = 64 ones there (one launch, on a
+    side stream), the four N = 256 ones on the step engine (13 launches + 4 split-K reductions)."""
     shapes = I.shape_set("cifar")
     xs = [I.gaussian(m, n, seed=500 + i) for i, (m, n) in enumerate(shapes)]
     ts = [torch.from_numpy(x).to(torch.bfloat16).cuda() for x in xs]
     outs = [torch.empty_like(t) for t in ts]
-    ns.orthogonalize_list(ts, out=outs, iters=4)
-    c0 = ns.launch_count()
-    ns.orthogonalize_list(ts, out=outs, iters=4)
-    torch.cuda.synchronize()
-    assert ns.launch_count() - c0 == 2
+    old = ns.set_path(path)
+    try:
+        ns.orthogonalize_list(ts, out=outs, iters=4)
+        c0 = ns.launch_count()
+        ns.orthogonalize_list(ts, out=outs, iters=4)
+        torch.cuda.synchronize()
+        assert ns.launch_count() - c0 == launches
+    finally:
+        ns.set_path(old)
     for x, t, o in zip(xs, ts, outs):
         assert np.array_equal(t.float().cpu().numpy(), x)  # input untouched
         assert_parity(o.float().cpu().numpy().astype(np.float64), oracle_run(x, C.turbo(4), "aol"), BF16_TOL)

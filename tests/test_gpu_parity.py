@@ -608,7 +608,7 @@ def test_failed_second_plan_leaves_first_group_untouched():
     built before either launches, so when the second does not fit a caller workspace sized
     for the first only, the call fails with NS_ERR_WORKSPACE and no matrix is modified
     (header contract)."""
-    shapes = [(300, 201), (768, 768)]
+    shapes = [(300, 301), (768, 768)]  # 301: TMA-unaligned, and N > 256 (no cluster kernel)
     xs = [torch.from_numpy(I.gaussian(m, n, seed=320 + i)).to(torch.bfloat16).cuda() for i, (m, n) in enumerate(shapes)]
     keep = [x.clone() for x in xs]
     need_first = ns.workspace_size([shapes[0]])
