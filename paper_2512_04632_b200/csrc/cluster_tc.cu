@@ -268,12 +268,13 @@ __global__ void __launch_bounds__(kTcThreads, 1)
           const float4* src = reinterpret_cast<const float4*>(J.part) +
                               (size_t)(((a0 * 4 + qd0) * nch + c) * 8 + v) * 32 + l0;
           float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-          for (int t0 = 0; t0 < g.C; t0 += 2) {  // partials 0..C-1 summed in order (C even)
-            float4 pv[2];
+          for (int t0 = 0; t0 < g.C; t0 += 8) {  // partials 0..C-1 summed in order, 8 loads in flight
+            float4 pv[8];
 #pragma unroll
-            for (int t = 0; t < 2; ++t) pv[t] = __ldcg(src + (size_t)(t0 + t) * g.Np * g.Np / 4);
+            for (int t = 0; t < 8; ++t)
+              pv[t] = (t0 + t < g.C) ? __ldcg(src + (size_t)(t0 + t) * g.Np * g.Np / 4) : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-            for (int t = 0; t < 2; ++t) { acc.x += pv[t].x; acc.y += pv[t].y; acc.z += pv[t].z; acc.w += pv[t].w; }
+            for (int t = 0; t < 8; ++t) { acc.x += pv[t].x; acc.y += pv[t].y; acc.z += pv[t].z; acc.w += pv[t].w; }
           }
           const int q = c * 32 + v * 4;
           const uint32_t w0 = pk_bf2(acc.x, acc.y), w1 = pk_bf2(acc.z, acc.w);
@@ -307,28 +308,27 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncthreads();
     TC_TL();
-    if (threadIdx.x == 0) {
-      if (k == 0 && precond == 1) {  // my rows' share of tr(A0), in row order
-        float tr = 0.f;
-        for (int i = 0; i < g.rows; ++i) tr += diag[i];
-        trbuf[4 * rank] = tr;
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    if (threadIdx.x == 0 && k == 0 && precond == 1) {  // my rows' share of tr(A0), in row order
+      float tr = 0.f;
+      for (int i = 0; i < g.rows; ++i) tr += diag[i];
+      trbuf[4 * rank] = tr;
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    if (k == 0 && precond == 1) __syncthreads();
+    if (threadIdx.x >= 1 && (int)threadIdx.x < g.C) {  // one thread per peer issues its copies
+      const uint32_t peer = (rank + threadIdx.x) % g.C;
+      const uint32_t rbar = tc_mapa(smem_u32(bar_rx), peer);
+      for (int j = 0; j < g.nb; ++j) {
+        const uint32_t src = base + a_box(g, o0 >> 6, j) + (uint32_t)(o0 & 63) * 128u;
+        tc_bulk_s2s(tc_mapa(src, peer), src, (uint32_t)g.rows * 128u, rbar);
       }
-      for (int pr = 1; pr < g.C; ++pr) {
-        const uint32_t peer = (rank + pr) % g.C;
-        const uint32_t rbar = tc_mapa(smem_u32(bar_rx), peer);
-        for (int j = 0; j < g.nb; ++j) {
-          const uint32_t src = base + a_box(g, o0 >> 6, j) + (uint32_t)(o0 & 63) * 128u;
-          tc_bulk_s2s(tc_mapa(src, peer), src, (uint32_t)g.rows * 128u, rbar);
-        }
-        if (k == 0 && precond == 2) {
-          const uint32_t src = base + g.svec + (uint32_t)o0 * 4u;
-          tc_bulk_s2s(tc_mapa(src, peer), src, (uint32_t)g.rows * 4u, rbar);
-        }
-        if (k == 0 && precond == 1) {
-          const uint32_t src = base + g.trbuf + rank * 16u;
-          tc_bulk_s2s(tc_mapa(src, peer), src, 16u, rbar);
-        }
+      if (k == 0 && precond == 2) {
+        const uint32_t src = base + g.svec + (uint32_t)o0 * 4u;
+        tc_bulk_s2s(tc_mapa(src, peer), src, (uint32_t)g.rows * 4u, rbar);
+      }
+      if (k == 0 && precond == 1) {
+        const uint32_t src = base + g.trbuf + rank * 16u;
+        tc_bulk_s2s(tc_mapa(src, peer), src, 16u, rbar);
       }
     }
     tc_wait_cluster(bar_rx, (uint32_t)(k & 1));
