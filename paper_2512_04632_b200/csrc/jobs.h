@@ -241,17 +241,22 @@ __host__ __device__ inline int tc_rows(int64_t M, int C) {
   const int64_t r64 = (r + 63) / 64 * 64;
   return (int)(r64 < 128 ? 128 : r64);
 }
-// Cluster size for an M x N matrix (0: does not fit): 16 CTAs whenever the slabs fit.  The
-// kernel takes any power of two 2..16 (Np / C <= 64 owned rows per CTA); smaller clusters were
-// measured SLOWER for a lone matrix (graph replay: 1024x128 53 us at C = 4 vs 43 at 16, 64x576
-// 55 at 4 vs 43, 768x256 111 at 8 vs 102 -- the owner's reduction and broadcast rows grow as
-// Np / C) though they take fewer SMs from a concurrent step-engine launch (CIFAR set 103 vs
-// 108 us), so the size is fixed at 16: a function of the shape alone either way.
+// Cluster size for an M x N matrix (0: does not fit): the smallest power of two C in 4..16
+// that keeps the slabs at the minimum R = 128 rows (C >= M / 128); past M = 2048 it is 16 with
+// taller slabs.  Measured (graph replay, profiles/r02_cluster_tc.log): a lone matrix is
+// fastest with many CTAs and short slabs (64x576: 43 us at C = 16 or 8 with R = 128, 55 at 4
+// with R = 192; C = 2 with 64 owned rows per CTA: 64x216 55 vs 47 at 4), but a call that also
+// runs step-engine launches loses fewer SMs to small clusters (CIFAR set 103 us vs 108 at
+// C = 16); R = 128 with the fewest CTAs keeps both.  A function of the shape alone.
 __host__ __device__ inline int tc_cluster(int64_t M, int64_t N) {
   if (N < 1 || N > 256 || M < 1) return 0;
-  const int Np = tc_np(N), C = kTcCtas;
-  const int R = tc_rows(M, C);
-  return (R <= 256 && (int64_t)R * C >= M && tc_smem(Np, R, C) <= kTcMaxSmem) ? C : 0;
+  const int Np = tc_np(N);
+  for (int C = Np / 64 > 4 ? Np / 64 : 4; C <= kTcCtas; C *= 2) {  // C = 2 measured slower (64x216 55 vs 45 us)
+    if ((int64_t)128 * C < M && C < kTcCtas) continue;
+    const int R = tc_rows(M, C);
+    if (R <= 256 && (int64_t)R * C >= M && tc_smem(Np, R, C) <= kTcMaxSmem) return C;
+  }
+  return 0;
 }
 __host__ __device__ inline bool tc_fits(int64_t M, int64_t N) { return tc_cluster(M, N) != 0; }
 

@@ -118,11 +118,12 @@ def test_cluster_tc_flags():
     assert ns.read_flags() & 2
 
 
-@pytest.mark.parametrize("path,launches", [(7, 1), (0, 18)])
+@pytest.mark.parametrize("path,launches", [(7, 3), (0, 19)])
 def test_cluster_tc_out_of_place_and_cifar_set(path, launches):
     """The CIFAR conv set (config 3) in one grouped call.  Path 7: all six matrices on the
-    tcgen05 cluster kernel, one launch.  Path 0: the two N = 64 ones there (one launch, on a
-    side stream), the four N = 256 ones on the step engine (13 launches + 4 split-K reductions)."""
+    tcgen05 cluster kernel, one launch per cluster size (16: the 256 x 2304 ones, 8: 256 x 576
+    and 64 x 576, 4: 64 x 216).  Path 0: the two N = 64 ones there (two launches on side
+    streams), the four N = 256 ones on the step engine (13 launches + 4 split-K reductions)."""
     shapes = I.shape_set("cifar")
     xs = [I.gaussian(m, n, seed=500 + i) for i, (m, n) in enumerate(shapes)]
     ts = [torch.from_numpy(x).to(torch.bfloat16).cuda() for x in xs]
