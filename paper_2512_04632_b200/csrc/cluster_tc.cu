@@ -37,6 +37,8 @@
 
 namespace tns {
 
+__device__ long long g_tc_tl[64];  // TNS_DBG bit 4096: phase stamps of CTA 0 (measurement only)
+
 namespace {
 
 constexpr int kBox = 64 * 64 * 2;  // one 64 x 64 bf16 box, 128-byte rows, 128-byte swizzle
@@ -136,10 +138,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   bool bad = false, zero = false;
   // TNS_DBG bit 4096 (measurement only): cycle stamps of CTA 0 of the first cluster, printed
   const bool tl = (dbg & 4096) && blockIdx.x == 0 && threadIdx.x == 0;
-  long long tls[40];
   int ntl = 0;
-  const long long T0 = clock64();
-#define TC_TL() do { if (tl && ntl < 40) tls[ntl++] = clock64() - T0; } while (0)
+  const long long T0 = tl ? clock64() : 0;
+#define TC_TL() do { if (tl && ntl < 64) g_tc_tl[ntl++] = clock64() - T0; } while (0)
 
   if (threadIdx.x == 0) {
     mbar_init(bar_load, 1);
@@ -259,7 +260,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       const int per = 32 / rl;                     // column units per warp pass
       const int r0 = lane % rl, sub = lane / rl;
       float rs[2] = {0.f, 0.f};
-      for (int gi = 0; gi * rl < g.rows; ++gi) {   // rows > 32 (C = 2 or 4): two row groups
+#pragma unroll
+      for (int gi = 0; gi < 2; ++gi) {             // rows > 32 (C = 2 or 4): two row groups
+        if (gi * rl >= g.rows) break;
         const int r = gi * rl + r0, i = o0 + r;
         const int a0 = i >> 7, qd0 = (i >> 5) & 3, l0 = i & 31;
         for (int u0 = warp * per; u0 < units; u0 += 8 * per) {
@@ -289,7 +292,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         }
       }
       if (k == 0 && precond == 2) {  // Eq. 8 on the stored bf16 A0 row: fixed-order reduction
-        for (int gi = 0; gi * rl < g.rows; ++gi) {
+#pragma unroll
+        for (int gi = 0; gi < 2; ++gi) {
+          if (gi * rl >= g.rows) break;
           float v = rs[gi];
           for (int o = rl; o < 32; o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
           if (lane < rl) diag[warp * g.rows + gi * rl + lane] = v;  // per-warp row sums (scratch)
@@ -534,8 +539,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     bulk_wait<0>();
     TC_TL();
     if (tl) {
-      printf("tc timeline (cycles since entry, CTA 0): load %lld |", tls[0]);
-      for (int i = 1; i < ntl; ++i) printf(" %lld", tls[i] - tls[i - 1]);
+      printf("tc timeline (cycles since entry, CTA 0): load %lld |", g_tc_tl[0]);
+      for (int i = 1; i < ntl; ++i) printf(" %lld", g_tc_tl[i] - g_tc_tl[i - 1]);
       printf("\n");
     }
   }
