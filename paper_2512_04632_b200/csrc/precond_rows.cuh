@@ -43,22 +43,20 @@ __device__ __forceinline__ float aol_rowsum_partials(const PrecondJob& J, int i)
   const int n1 = (N + 63) / 64, n2 = (N + 31) / 32;
   const float* pr = J.part + (int64_t)i * J.part_ld;
   const int d_end = min(4 * (bi + 1), n1), m_beg = min(8 * (bi + 1), n2);
-  // 8 loads in flight, added in slot order (the zeros past the end add nothing): the same
-  // sum, bitwise, as a plain sequential loop -- without 8 serialised L2 round trips
+  // the row's slots as one list (direct ones, then mirrored ones), loaded up to 32 at a time and
+  // added in list order (the zeros past the end add nothing): the same sum, bitwise, as a
+  // plain sequential loop -- in one L2 round trip for N <= 1024 instead of one per slot
+  const int nd = d_end, nt = d_end + (n2 - m_beg);
   float acc = 0.f;
-  for (int k0 = 0; k0 < d_end; k0 += 8) {
-    float v[8];
+  for (int t0 = 0; t0 < nt; t0 += 32) {
+    float v[32];
 #pragma unroll
-    for (int e = 0; e < 8; ++e) v[e] = (k0 + e < d_end) ? pr[k0 + e] : 0.f;
+    for (int e = 0; e < 32; ++e) {
+      const int t = t0 + e;
+      v[e] = t < nd ? pr[t] : (t < nt ? pr[n1 + m_beg + (t - nd)] : 0.f);
+    }
 #pragma unroll
-    for (int e = 0; e < 8; ++e) acc += v[e];
-  }
-  for (int k0 = m_beg; k0 < n2; k0 += 8) {
-    float v[8];
-#pragma unroll
-    for (int e = 0; e < 8; ++e) v[e] = (k0 + e < n2) ? pr[n1 + k0 + e] : 0.f;
-#pragma unroll
-    for (int e = 0; e < 8; ++e) acc += v[e];
+    for (int e = 0; e < 32; ++e) acc += v[e];
   }
   return acc;
 }
