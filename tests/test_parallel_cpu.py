@@ -112,28 +112,29 @@ def test_sharded_gloo_matches_single(world, buckets):
             assert np.array_equal(a, b.numpy())
 
 
-def _rs_worker(rank, world, port, shapes, q):
+def _rs_worker(rank, world, port, shapes, q, mean=True):
     from paper_2512_04632_b200.parallel import reduce_scatter_owned
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     # rank-dependent local "gradients": g_r[i] = gaussian(i) * (r + 1)
     gs = [torch.from_numpy(I.gaussian(m, n, seed=300 + i, bf16=False)) * (rank + 1) for i, (m, n) in enumerate(shapes)]
-    mine, views = reduce_scatter_owned(gs)
+    mine, views = reduce_scatter_owned(gs, mean=mean)
     q.put((rank, mine, [v.clone().numpy() for v in views]))
     dist.barrier()
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 4])
-def test_reduce_scatter_owned_gloo(world):
-    """Each rank receives the cross-rank mean of exactly the matrices it owns (LPT
-    ownership identical to the sharded NS), and the owners partition the list."""
+@pytest.mark.parametrize("world,mean", [(2, True), (4, True), (2, False)])
+def test_reduce_scatter_owned_gloo(world, mean):
+    """Each rank receives the cross-rank mean (or, for DistributedTurboMuon, which folds the
+    1/world into its momentum kernel, the sum) of exactly the matrices it owns (LPT ownership
+    identical to the sharded NS), and the owners partition the list."""
     shapes = [(96, 64), (64, 160), (128, 128), (40, 24), (200, 56), (64, 64), (32, 96)]
     ctx = mp.get_context("spawn")
     q = ctx.SimpleQueue()
     port = _free_port()
-    procs = [ctx.Process(target=_rs_worker, args=(r, world, port, shapes, q)) for r in range(world)]
+    procs = [ctx.Process(target=_rs_worker, args=(r, world, port, shapes, q, mean)) for r in range(world)]
     for p in procs:
         p.start()
     results = [q.get() for _ in range(world)]
@@ -142,7 +143,7 @@ def test_reduce_scatter_owned_gloo(world):
         assert p.exitcode == 0
     owners = lpt_owners(shapes, world)
     seen = []
-    mean_factor = sum(r + 1 for r in range(world)) / world
+    mean_factor = sum(r + 1 for r in range(world)) / (world if mean else 1)
     for rank, mine, views in results:
         assert mine == [i for i in range(len(shapes)) if owners[i] == rank]
         seen += mine
