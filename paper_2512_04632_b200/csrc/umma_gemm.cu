@@ -244,7 +244,14 @@ __device__ __forceinline__ void epi_math(int var, const Epi& E, int p, int q, co
     }
   }
   // non-finite check of the 32 stored bf16 values: per half, (h & 0x7F80) + 0x80 reaches
-  // bit 15 iff the exponent is all ones (Inf/NaN); OR over the words, one test at the end
+  // bit 15 iff the exponent is all ones (Inf/NaN); OR over the words, one test at the end.
+  // Only the update's outputs are checked: a non-finite A or B' always reaches X_{k+1}
+  // (NaN and Inf propagate through the products; an overflowing Gram gives s = 0 and
+  // 0 * Inf = NaN), so flag bit 1 is raised all the same, and the Gram / A^2 epilogues --
+  // the ones as long as their short main loops -- save the instructions.
+#ifndef TNS_CHECK_ALL_STEPS
+  if (E.mode != MODE_XB) return;
+#endif
   uint32_t nf = 0;
 #pragma unroll
   for (int i = 0; i < 16; ++i) nf |= (o[i] & 0x7F807F80u) + 0x00800080u;
