@@ -183,7 +183,7 @@ struct Mat {
   size_t stage_off = 0;
   // tensormap indices (tcgen05 path)
   int tm_x, tm_out, tm_w, tm_a, tm_b;
-  size_t tc_part_off = 0;  // cluster tcgen05 kernel: 16 * Np * Np fp32 Gram partials
+  size_t tc_part_off = 0;  // cluster tcgen05 kernel: Gram partials + A image (tc_part_floats)
   // fused collective: extra destinations of the final result (peers' buffers)
   std::vector<void*> peer;
   int tm_peer;
@@ -317,7 +317,10 @@ static int choose_bn(const std::vector<Mat>& mats, int cg, int workers) {
 
 static size_t split_bytes(const Mat& mt) { return mt.split ? (size_t)mt.split * kSplitLd * kSplitLd * 4 : 0; }
 
-static size_t tc_part_bytes(int64_t M, int64_t N) { return (size_t)tc_cluster(M, N) * tc_np(N) * tc_np(N) * 4; }
+static size_t tc_part_bytes(int64_t M, int64_t N) {
+  const int C = tc_cluster(M, N);
+  return C ? tc_part_floats(tc_np(N), C) * 4 : 0;
+}
 
 // Workspace of a problem list as the step engine lays it out; a bf16 matrix the tcgen05
 // cluster kernel could take counts with the larger of its two footprints (an upper bound

@@ -2,24 +2,29 @@
 // small and mid-size matrices are latency/communication-bound, and P:L327: the CIFAR
 // conv weights reshaped to 2-D, e.g. 256 x 2304).
 //
-// One thread-block cluster of C CTAs (a power of two, 2..16, set by the shape: tc_cluster)
+// One thread-block cluster of C CTAs (a power of two, 4..16, set by the shape: tc_cluster)
 // runs ALL steps of Alg. 2 for one matrix in ONE launch.  Xh (M x N, the short-side orientation, N padded with zero columns to
 // Np in {128, 256}) is split into row slabs of R in {128, 192, 256} rows, one per CTA,
 // resident in shared memory for the whole call in the 64 x 64-box / 128-byte-swizzle layout
 // the TMA loads it in (X itself, not a transposed copy: wide inputs are oriented by the UMMA
 // major bits, as in the step engine).  Every CTA also holds a full copy of A (Np x Np bf16),
 // which the polynomial step turns into B' in place.  Per iteration k (Eqs. 3-5):
-//   Gram  : each CTA P_r = slab_r^T slab_r (tcgen05, fp32 in TMEM), written to an fp32
-//           scratch in L2; cluster barrier; CTA r sums rows [r Np/C, (r+1) Np/C) of the C
-//           partials in a fixed order (deterministic), rounds them to bf16 -- A_k rows -- and
-//           broadcasts them to every CTA's A copy by bulk DSMEM copies (mbarrier complete_tx).
-//           k = 1: the owner also forms s_i = (sum_j |A0_ij|)^(-1/2) (AOL, Eq. 8) or the
-//           trace (Frobenius, Eq. 10) for its rows and broadcasts it; every CTA then forms
-//           A1 = diag(s) A0 diag(s) and X1 = X0 diag(s) in its own copies (Alg. 2 l.3-4).
+//   Gram  : each CTA P_r = slab_r^T slab_r (tcgen05, fp32 in TMEM); its lower-triangle 32 x 32
+//           chunks go to an fp32 scratch in L2; cluster barrier; CTA r sums an equal share of
+//           the chunk elements over the C partials in a fixed order (deterministic), rounds them
+//           to bf16 -- A_k -- and writes them, mirrored, into a global A image laid out like the
+//           shared-memory A buffer; cluster barrier; every CTA bulk-loads the whole image
+//           (measured on B200, tools/xfer_probe.cu: L2 stores ~30 B/cycle/SM, bulk L2 loads
+//           55-65, DSMEM bulk copies ~13 -- so the triangle halves the dominant store traffic
+//           and the L2 image replaces a DSMEM broadcast).
+//           k = 1: every CTA forms s_i = (sum_j |A0_ij|)^(-1/2) (AOL, Eq. 8) or tr(A0)^(-1/2)
+//           (Frobenius, Eq. 10) from its copy of A0, then A1 = diag(s) A0 diag(s) and
+//           X1 = X0 diag(s) in its own copies (Alg. 2 l.3-4).
 //   Poly  : every CTA computes B' = a_k I + b_k A + c_k A^2 for the full matrix (tcgen05, A
 //           as both operands; redundant per CTA, no communication), in place over A (Eq. 4
 //           with Eq. 5's a_k folded in, reading R15).
-//   Update: slab_r <- slab_r B'^T (tcgen05), written back over the slab in place (Eq. 5).
+//   Update: slab_r <- slab_r B'^T (tcgen05; wide inputs: X_r <- B' X_r, the same product with
+//           the slab as the B operand), written back over the slab in place (Eq. 5).
 // After T iterations each CTA TMA-stores its slab.  Rounding: bf16 storage of X, A, B' (every
 // stored value rounded once, RNE), fp32 accumulation and fp32 scaling -- reading R6; X1 is
 // materialised here (Alg. 2 l.3 literally), where the step engine folds diag(s) into B'1, so
@@ -44,16 +49,6 @@ namespace {
 constexpr int kBox = 64 * 64 * 2;  // one 64 x 64 bf16 box, 128-byte rows, 128-byte swizzle
 constexpr int kTcThreads = 256;    // 8 warps: TMEM lane quarter = warp % 4
 
-__device__ __forceinline__ uint32_t tc_mapa(uint32_t local, uint32_t rank) {
-  uint32_t r;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local), "r"(rank));
-  return r;
-}
-__device__ __forceinline__ void tc_bulk_s2s(uint32_t dst, uint32_t src, uint32_t bytes, uint32_t bar) {
-  asm volatile("cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
-               "r"(src), "r"(bytes), "r"(bar)
-               : "memory");
-}
 __device__ __forceinline__ void tc_wait_cluster(uint64_t* bar, uint32_t parity) {
   const uint32_t a = smem_u32(bar);
   uint32_t ok = 0;
@@ -74,7 +69,6 @@ __device__ __forceinline__ uint32_t pk_bf2(float lo, float hi) {
   asm("cvt.rn.bf16x2.f32 %0, %2, %1;" : "=r"(r) : "f"(lo), "f"(hi));
   return r;
 }
-__device__ __forceinline__ uint16_t to_bf(float f) { return __bfloat16_as_ushort(__float2bfloat16_rn(f)); }
 // byte offset of element column c (0..63) of row r (0..63) inside a 128-byte-swizzled box
 __device__ __forceinline__ uint32_t swz(uint32_t r, uint32_t c) {
   return r * 128u + ((((c >> 3) ^ (r & 7u)) << 4) | ((c & 7u) << 1));
@@ -85,20 +79,18 @@ __device__ __forceinline__ bool bad16(uint32_t w) {  // either bf16 of the pair 
 
 struct TcGeo {
   int Np, R, nb, rb;     // padded short side, slab rows, Np / 64, R / 64
-  int rows;              // rows of A owned per CTA in the reduction: Np / C (<= 64)
   int C;                 // CTAs in the cluster
+  int L;                 // lower-triangle 32 x 32 chunks of a Gram partial (tc_tri_chunks)
   uint32_t slab, abuf;   // smem offsets (relative to the 1024-aligned base)
-  uint32_t svec, trbuf, diag, bars;  // diag: tc_diag_floats (Frobenius diagonal / AOL per-warp row sums)
+  uint32_t svec, bars;
 };
 __device__ __forceinline__ TcGeo tc_geo(const TcJob& J) {
   TcGeo g;
-  g.Np = J.Np; g.R = J.R; g.nb = J.Np / 64; g.rb = J.R / 64; g.C = J.C; g.rows = J.Np / J.C;
+  g.Np = J.Np; g.R = J.R; g.nb = J.Np / 64; g.rb = J.R / 64; g.C = J.C; g.L = tc_tri_chunks(J.Np);
   g.slab = 0;
   g.abuf = (uint32_t)J.R * J.Np * 2;
   g.svec = g.abuf + (uint32_t)J.Np * J.Np * 2;
-  g.trbuf = g.svec + (uint32_t)J.Np * 4;
-  g.diag = g.trbuf + kTcCtas * 16;
-  g.bars = g.diag + (uint32_t)tc_diag_floats(J.Np, J.C) * 4;  // 3 mbarriers + the TMEM address slot (tc_smem() budgets 64 bytes)
+  g.bars = g.svec + (uint32_t)J.Np * 4;  // 4 mbarriers + the TMEM address slot (tc_smem() budgets 64 bytes)
   return g;
 }
 
@@ -111,9 +103,87 @@ __device__ __forceinline__ uint32_t slab_box(const TcGeo& g, int wide, int i, in
   return g.slab + (uint32_t)(wide ? (i * g.nb + j) : (j * g.rb + i)) * kBox;
 }
 // A box (row block i, column block j): row blocks fastest (K-major operands, 64-row blocks
-// adjacent).
+// adjacent).  The global A image (TcJob::part) has the same layout, offsets relative to abuf.
 __device__ __forceinline__ uint32_t a_box(const TcGeo& g, int i, int j) {
   return g.abuf + (uint32_t)(j * g.nb + i) * kBox;
+}
+// byte offset of element (i, j) of A in the image / relative to abuf
+__device__ __forceinline__ uint32_t a_img(const TcGeo& g, int i, int j) {
+  return (uint32_t)((j >> 6) * g.nb + (i >> 6)) * kBox + swz((uint32_t)(i & 63), (uint32_t)(j & 63));
+}
+
+// The Gram all-reduce, owner side: float4 units [rank per, (rank + 1) per) of the lower-triangle
+// chunk order, summed over the CC partials in order 0..CC-1 (16 loads in flight per thread:
+// 16 / CC units per batch), rounded to bf16 once, written into the A image with their mirrors.
+template <int CC>
+__device__ __forceinline__ void reduce_share(const TcGeo& g, float* part, uint32_t rank, bool& bad) {
+  constexpr int kUpb = 16 / CC;
+  const int U = g.L * 256, per = U / CC;
+  const float4* Pb = reinterpret_cast<const float4*>(part);
+  uint8_t* img = reinterpret_cast<uint8_t*>(part + (size_t)CC * g.L * 1024);
+  for (int w0 = (int)threadIdx.x; w0 < per; w0 += kTcThreads * kUpb) {
+    float4 pv[kUpb][CC];
+#pragma unroll
+    for (int i = 0; i < kUpb; ++i) {
+      const int w = w0 + i * kTcThreads;
+#pragma unroll
+      for (int t = 0; t < CC; ++t)
+        pv[i][t] = w < per ? __ldcg(Pb + (size_t)t * U + (size_t)rank * per + w) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int i = 0; i < kUpb; ++i) {
+      const int w = w0 + i * kTcThreads;
+      if (w >= per) break;
+      float4 a4 = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int t = 0; t < CC; ++t) { a4.x += pv[i][t].x; a4.y += pv[i][t].y; a4.z += pv[i][t].z; a4.w += pv[i][t].w; }
+      const int u = (int)rank * per + w;
+      const int ci = u >> 8, v = (u >> 5) & 7, l = u & 31;
+      int rb = 0;
+      while ((rb + 1) * (rb + 2) / 2 <= ci) ++rb;
+      const int row = rb * 32 + l, col = (ci - rb * (rb + 1) / 2) * 32 + v * 4;
+      const uint32_t w0b = pk_bf2(a4.x, a4.y), w1b = pk_bf2(a4.z, a4.w);
+      bad |= bad16(w0b) | bad16(w1b);
+      const uint16_t hv[4] = {(uint16_t)(w0b & 0xFFFFu), (uint16_t)(w0b >> 16), (uint16_t)(w1b & 0xFFFFu), (uint16_t)(w1b >> 16)};
+      if (col + 3 <= row) {
+        *reinterpret_cast<uint2*>(img + a_img(g, row, col)) = make_uint2(w0b, w1b);
+      } else {  // a diagonal chunk: the elements on or below the diagonal only
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          if (col + e <= row) *reinterpret_cast<uint16_t*>(img + a_img(g, row, col + e)) = hv[e];
+      }
+#pragma unroll
+      for (int e = 0; e < 4; ++e)  // mirrored: A_k is stored symmetric, bit for bit
+        if (col + e < row) *reinterpret_cast<uint16_t*>(img + a_img(g, col + e, row)) = hv[e];
+    }
+  }
+}
+
+// B' = a_k I + b_k A + c_k A^2 for 32 columns [q0, q0 + 32) of row p, in place over the bf16
+// A row (Eq. 4 with Eq. 5's a_k folded in, reading R15); nf accumulates the non-finite test of
+// the stored pairs (bit 15 / 31 set iff a half is Inf / NaN).
+template <bool DIAG>
+__device__ __forceinline__ void poly_chunk(uint8_t* sm, const TcGeo& g, int p, int q0, const uint32_t (&r)[32],
+                                           const uint4 (&xv)[4], float ca, float cb, float cc, uint32_t& nf) {
+#pragma unroll
+  for (int h = 0; h < 4; ++h) {  // 8 columns per 16-byte swizzle chunk
+    const int q = q0 + 8 * h;
+    const uint32_t x[4] = {xv[h].x, xv[h].y, xv[h].z, xv[h].w};
+    uint32_t o[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      float w0 = fmaf(cc, __uint_as_float(r[8 * h + 2 * e]), cb * bf_lo(x[e]));
+      float w1 = fmaf(cc, __uint_as_float(r[8 * h + 2 * e + 1]), cb * bf_hi(x[e]));
+      if (DIAG) {
+        w0 = (q + 2 * e == p) ? w0 + ca : w0;
+        w1 = (q + 2 * e + 1 == p) ? w1 + ca : w1;
+      }
+      o[e] = pk_bf2(w0, w1);
+      nf |= (o[e] & 0x7F807F80u) + 0x00800080u;
+    }
+    *reinterpret_cast<uint4*>(sm + a_box(g, p >> 6, q >> 6) + swz((uint32_t)(p & 63), (uint32_t)(q & 63))) =
+        make_uint4(o[0], o[1], o[2], o[3]);
+  }
 }
 
 __global__ void __launch_bounds__(kTcThreads, 1)
@@ -133,8 +203,6 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   uint64_t* bar_mma1 = bar_load + 3;  // second accumulator of a batch (its epilogue overlaps)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar_load + 4);
   float* svec = reinterpret_cast<float*>(sm + g.svec);
-  float* trbuf = reinterpret_cast<float*>(sm + g.trbuf);
-  float* diag = reinterpret_cast<float*>(sm + g.diag);
   bool bad = false, zero = false;
   // TNS_DBG bit 4096 (measurement only): cycle stamps of CTA 0 of the first cluster, printed
   const bool tl = (dbg & 4096) && blockIdx.x == 0 && threadIdx.x == 0;
@@ -205,157 +273,111 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         umma_commit<1>(a ? bar_mma1 : bar_mma);  // accumulator a done: its epilogue may start
       }
     }
-    {  // TMEM -> fp32 partial in L2, in the TMEM-natural order pidx(): every store instruction
-       // of a warp writes 32 consecutive float4 (512 contiguous bytes).  Accumulator 0 drains
-       // while accumulator 1 is still being computed; two TMEM loads in flight per wait.
-      float* P = J.part + (size_t)rank * g.Np * g.Np;
-      const int nch = g.Np / 32;
-#ifdef TNS_TC_NO_OVERLAP
-      mbar_wait(bar_mma, ph0);
-      if (nacc_g > 1) mbar_wait(bar_mma1, ph1);
-#endif
+    {
+      // TMEM -> fp32 partial in L2: only the lower-triangle 32 x 32 chunks (A is symmetric),
+      // chunk (rb, c) at index rb (rb + 1) / 2 + c, inside a chunk float4 unit v * 32 + lane =
+      // row 32 rb + lane, columns 32 c + 4 v .. + 3 (every store instruction of a warp writes
+      // 512 contiguous bytes).  Accumulator 0 drains while accumulator 1 is being computed;
+      // two TMEM loads in flight per wait.
+      float4* P = reinterpret_cast<float4*>(J.part) + (size_t)rank * g.L * 256;
+      const int h = warp >> 2;
       for (int a = 0; a < nacc_g; ++a) {
-#ifndef TNS_TC_NO_OVERLAP
         mbar_wait(a ? bar_mma1 : bar_mma, a ? ph1 : ph0);
-#endif
         if (a == 0) TC_TL();
         tc_fence_after();
-        for (int c = warp >> 2; c < nch; c += 4) {
+        const int rb = a * 4 + qd;  // this warp's 32-row block
+        for (int c = h; c <= rb; c += 4) {  // chunks c and c + 2 of the row block
+          const bool two = c + 2 <= rb;       // warp-uniform
           uint32_t r[2][32];
           tmem_ld_32x32b_x32(tmem + lane_base + (uint32_t)(a * g.Np + c * 32), r[0]);
-          tmem_ld_32x32b_x32(tmem + lane_base + (uint32_t)(a * g.Np + (c + 2) * 32), r[1]);
+          if (two) tmem_ld_32x32b_x32(tmem + lane_base + (uint32_t)(a * g.Np + (c + 2) * 32), r[1]);
           tmem_ld_wait_regs(r[0]);
-          tmem_ld_wait_regs(r[1]);
+          if (two) tmem_ld_wait_regs(r[1]);
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            float4* dst = reinterpret_cast<float4*>(P) + (size_t)(((a * 4 + qd) * nch + c + 2 * h) * 8) * 32 + lane;
+          for (int hh = 0; hh < 2; ++hh) {
+            if (hh && !two) break;
+            float4* dst = P + (size_t)(rb * (rb + 1) / 2 + c + 2 * hh) * 256 + lane;
 #pragma unroll
             for (int v = 0; v < 8; ++v)
-              __stcg(dst + v * 32, make_float4(__uint_as_float(r[h][4 * v]), __uint_as_float(r[h][4 * v + 1]),
-                                               __uint_as_float(r[h][4 * v + 2]), __uint_as_float(r[h][4 * v + 3])));
+              __stcg(dst + v * 32, make_float4(__uint_as_float(r[hh][4 * v]), __uint_as_float(r[hh][4 * v + 1]),
+                                               __uint_as_float(r[hh][4 * v + 2]), __uint_as_float(r[hh][4 * v + 3])));
           }
         }
       }
       ph0 ^= 1;
       if (nacc_g > 1) ph1 ^= 1;
+      asm volatile("fence.proxy.async.global;" ::: "memory");  // read back by bulk copies
     }
     tc_fence_before();
     TC_TL();
     cluster_sync();  // every partial of this iteration is in L2 (release / acquire)
+    asm volatile("fence.proxy.async.global;" ::: "memory");
     TC_TL();
-    // ===================================================== reduce my rows of A_k, broadcast
-    const int o0 = (int)rank * g.rows;
-    if (threadIdx.x == 0) {
-      uint32_t bytes = (uint32_t)(g.C - 1) * g.rows * 128u * g.nb;
-      if (k == 0 && precond == 2) bytes += (uint32_t)(g.C - 1) * g.rows * 4u;
-      if (k == 0 && precond == 1) bytes += (uint32_t)(g.C - 1) * 16u;
-      mbar_arrive_expect_tx(bar_rx, bytes);
-    }
+    // ===================================================== reduce my share of A_k into the image
     {
-      // The partials are stored as float4 units pidx(p, q) = ((((a*4 + qd)*nch + c)*8 + v)*32 + l),
-      // p = 128 a + 32 qd + l, q = 32 c + 4 v.  My rows [o0, o0 + rows) share (a, qd); a lane
-      // takes one row (l) of one column unit (c, v): loads of consecutive lanes are consecutive.
-      const int nch = g.Np / 32, units = nch * 8;
-      const int rl = g.rows < 32 ? g.rows : 32;   // lanes per column unit (one row each)
-      const int per = 32 / rl;                     // column units per warp pass
-      const int r0 = lane % rl, sub = lane / rl;
-      float rs[2] = {0.f, 0.f};
-#pragma unroll
-      for (int gi = 0; gi < 2; ++gi) {             // rows > 32 (C = 2 or 4): two row groups
-        if (gi * rl >= g.rows) break;
-        const int r = gi * rl + r0, i = o0 + r;
-        const int a0 = i >> 7, qd0 = (i >> 5) & 3, l0 = i & 31;
-        for (int u0 = warp * per; u0 < units; u0 += 8 * per) {
-          const int unit = u0 + sub;
-          const int c = unit >> 3, v = unit & 7;
-          const float4* src = reinterpret_cast<const float4*>(J.part) +
-                              (size_t)(((a0 * 4 + qd0) * nch + c) * 8 + v) * 32 + l0;
-          float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-          for (int t0 = 0; t0 < g.C; t0 += 8) {  // partials 0..C-1 summed in order, 8 loads in flight
-            float4 pv[8];
-#pragma unroll
-            for (int t = 0; t < 8; ++t)
-              pv[t] = (t0 + t < g.C) ? __ldcg(src + (size_t)(t0 + t) * g.Np * g.Np / 4) : make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-            for (int t = 0; t < 8; ++t) { acc.x += pv[t].x; acc.y += pv[t].y; acc.z += pv[t].z; acc.w += pv[t].w; }
-          }
-          const int q = c * 32 + v * 4;
-          const uint32_t w0 = pk_bf2(acc.x, acc.y), w1 = pk_bf2(acc.z, acc.w);
-          bad |= bad16(w0) | bad16(w1);
-          rs[gi] += fabsf(bf_lo(w0)) + fabsf(bf_hi(w0)) + fabsf(bf_lo(w1)) + fabsf(bf_hi(w1));
-          if (k == 0 && precond == 1 && q <= i && i < q + 4) {  // the diagonal element of row i
-            const float dv[4] = {bf_lo(w0), bf_hi(w0), bf_lo(w1), bf_hi(w1)};
-            diag[i - o0] = dv[i - q];
-          }
-          *reinterpret_cast<uint2*>(sm + a_box(g, i >> 6, q >> 6) + swz((uint32_t)(i & 63), (uint32_t)(q & 63))) =
-              make_uint2(w0, w1);
-        }
-      }
-      if (k == 0 && precond == 2) {  // Eq. 8 on the stored bf16 A0 row: fixed-order reduction
-#pragma unroll
-        for (int gi = 0; gi < 2; ++gi) {
-          if (gi * rl >= g.rows) break;
-          float v = rs[gi];
-          for (int o = rl; o < 32; o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-          if (lane < rl) diag[warp * g.rows + gi * rl + lane] = v;  // per-warp row sums (scratch)
-        }
-        __syncthreads();
-        if (threadIdx.x < g.rows) {
-          float t = 0.f;
-          for (int w = 0; w < 8; ++w) t += diag[w * g.rows + threadIdx.x];
-          const int ii = o0 + (int)threadIdx.x;
-          svec[ii] = t > 0.f ? rsqrtf(t) : 0.f;
-          if (!(t > 0.f) && ii < J.N) zero = true;
-        }
-      }
+      // CTA r owns float4 units [r U / C, (r + 1) U / C) of the chunk order (equal shares of the
+      // triangle); it sums them over the C partials in the fixed order 0..C-1 (deterministic),
+      // rounds to bf16 once and writes the elements, and the mirrored ones, into the A image.
+      // (Staging the slices in shared memory by bulk copies measured slower: 8.3 vs 5.3 k cycles.)
+      if (g.C == 16) reduce_share<16>(g, J.part, rank, bad);
+      else if (g.C == 8) reduce_share<8>(g, J.part, rank, bad);
+      else reduce_share<4>(g, J.part, rank, bad);
+      // generic stores, read next by the bulk (async-proxy) copies of every CTA
+      asm volatile("fence.proxy.async.global;" ::: "memory");
     }
-    // my rows were written by generic stores and go out through the async proxy (bulk copies)
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    __syncthreads();
     TC_TL();
-    if (threadIdx.x == 0 && k == 0 && precond == 1) {  // my rows' share of tr(A0), in row order
-      float tr = 0.f;
-      for (int i = 0; i < g.rows; ++i) tr += diag[i];
-      trbuf[4 * rank] = tr;
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    }
-    if (k == 0 && precond == 1) __syncthreads();
-    if (threadIdx.x >= 1 && (int)threadIdx.x < g.C) {  // one thread per peer issues its copies
-      const uint32_t peer = (rank + threadIdx.x) % g.C;
-      const uint32_t rbar = tc_mapa(smem_u32(bar_rx), peer);
-      for (int j = 0; j < g.nb; ++j) {
-        const uint32_t src = base + a_box(g, o0 >> 6, j) + (uint32_t)(o0 & 63) * 128u;
-        tc_bulk_s2s(tc_mapa(src, peer), src, (uint32_t)g.rows * 128u, rbar);
-      }
-      if (k == 0 && precond == 2) {
-        const uint32_t src = base + g.svec + (uint32_t)o0 * 4u;
-        tc_bulk_s2s(tc_mapa(src, peer), src, (uint32_t)g.rows * 4u, rbar);
-      }
-      if (k == 0 && precond == 1) {
-        const uint32_t src = base + g.trbuf + rank * 16u;
-        tc_bulk_s2s(tc_mapa(src, peer), src, 16u, rbar);
-      }
+    cluster_sync();  // the A_k image is complete
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+    if (threadIdx.x == 0) {  // every CTA loads the whole image into its A buffer
+      const uint32_t bytes = (uint32_t)g.Np * g.Np * 2, piece = bytes / 16;
+      const uint8_t* img = reinterpret_cast<const uint8_t*>(J.part + (size_t)g.C * g.L * 1024);
+      mbar_arrive_expect_tx(bar_rx, bytes);
+      for (uint32_t o = 0; o < bytes; o += piece)
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                         base + g.abuf + o), "l"(img + o), "r"(piece), "r"(smem_u32(bar_rx))
+                     : "memory");
     }
     tc_wait_cluster(bar_rx, (uint32_t)(k & 1));
-    // My bulk copies to the peers read my rows of A, which the preconditioner (k = 1) or the
-    // A^2 epilogue overwrites next: every peer having received everything (its rx wait) is
-    // the only completion signal, so a split cluster barrier -- arrive here, wait before the
-    // first store into A -- orders them (the A^2 MMAs in between hide its latency).
-    cluster_arrive_relaxed();
-    bool a_pending = true;
     TC_TL();
     // ===================================================== k = 1: the preconditioner
     if (k == 0 && precond != 0) {
-      cluster_wait();
-      a_pending = false;
-      if (precond == 1) {
-        float tr = 0.f;
-        for (int r = 0; r < g.C; ++r) tr += trbuf[4 * r];
-        const float s = tr > 0.f ? rsqrtf(tr) : 0.f;
-        if (!(tr > 0.f) && rank == 0 && threadIdx.x == 0) zero = true;
-        for (int i = threadIdx.x; i < g.Np; i += kTcThreads) svec[i] = s;
+      // s from the bf16 A0 every CTA now holds (no communication): AOL s_i = (sum_j |A0_ij|)^(-1/2)
+      // (Eq. 8, columns in order), Frobenius s = tr(A0)^(-1/2) (Eq. 10)
+      if (precond == 2) {
+        if ((int)threadIdx.x < g.Np) {
+          const int i = threadIdx.x;
+          float t = 0.f;
+          for (int jb = 0; jb < g.nb; ++jb)
+#pragma unroll
+            for (int ch = 0; ch < 8; ++ch) {
+              const uint4 u4 = *reinterpret_cast<const uint4*>(sm + a_box(g, i >> 6, jb) + (uint32_t)(i & 63) * 128u +
+                                                               (uint32_t)((ch ^ (i & 7)) << 4));
+              t += fabsf(bf_lo(u4.x)) + fabsf(bf_hi(u4.x)) + fabsf(bf_lo(u4.y)) + fabsf(bf_hi(u4.y)) +
+                   fabsf(bf_lo(u4.z)) + fabsf(bf_hi(u4.z)) + fabsf(bf_lo(u4.w)) + fabsf(bf_hi(u4.w));
+            }
+          svec[i] = t > 0.f ? rsqrtf(t) : 0.f;
+          if (!(t > 0.f) && i < J.N) zero = true;
+        }
+      } else {
+        if ((int)threadIdx.x < g.Np) {
+          const int i = threadIdx.x;
+          svec[i] = bf_lo(*reinterpret_cast<const uint16_t*>(sm + g.abuf + a_img(g, i, i)));
+        }
         __syncthreads();
+        float tr = 0.f;
+        if (warp == 0) {  // fixed order: lane sums its strided diagonal entries, then a fixed tree
+          for (int i = lane; i < g.Np; i += 32) tr += svec[i];
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) tr += __shfl_xor_sync(0xffffffffu, tr, o);
+        }
+        __syncthreads();
+        if (warp == 0 && lane == 0) {
+          const float s = tr > 0.f ? rsqrtf(tr) : 0.f;
+          if (!(tr > 0.f)) zero = true;
+          for (int i = 0; i < g.Np; ++i) svec[i] = s;
+        }
       }
+      __syncthreads();
       // A1 = diag(s) A0 diag(s) (Alg. 2 l.4), X1 = X0 diag(s) (Alg. 2 l.3): 16-byte chunks
       const int achunks = g.Np * g.Np / 8;
       for (int t = threadIdx.x; t < achunks; t += kTcThreads) {
@@ -366,9 +388,11 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         uint4 u = *p;
         uint32_t wv[4] = {u.x, u.y, u.z, u.w};
         const float si = svec[row];
+        const float4 s0 = *reinterpret_cast<const float4*>(svec + col0), s1 = *reinterpret_cast<const float4*>(svec + col0 + 4);
+        const float sc[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
 #pragma unroll
         for (int e = 0; e < 4; ++e)
-          wv[e] = pk_bf2((si * bf_lo(wv[e])) * svec[col0 + 2 * e], (si * bf_hi(wv[e])) * svec[col0 + 2 * e + 1]);
+          wv[e] = pk_bf2((si * bf_lo(wv[e])) * sc[2 * e], (si * bf_hi(wv[e])) * sc[2 * e + 1]);
         *p = make_uint4(wv[0], wv[1], wv[2], wv[3]);
       }
       const int xchunks = g.R * g.Np / 8;
@@ -380,8 +404,10 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         uint32_t wv[4] = {u.x, u.y, u.z, u.w};
         if (!wide) {  // box (i, j) at j * rb + i: columns are N indices
           const int n0 = (bx / g.rb) * 64 + cpos;
+          const float4 s0 = *reinterpret_cast<const float4*>(svec + n0), s1 = *reinterpret_cast<const float4*>(svec + n0 + 4);
+          const float sc[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
 #pragma unroll
-          for (int e = 0; e < 4; ++e) wv[e] = pk_bf2(bf_lo(wv[e]) * svec[n0 + 2 * e], bf_hi(wv[e]) * svec[n0 + 2 * e + 1]);
+          for (int e = 0; e < 4; ++e) wv[e] = pk_bf2(bf_lo(wv[e]) * sc[2 * e], bf_hi(wv[e]) * sc[2 * e + 1]);
         } else {      // box (i, j) at i * nb + j: box rows are N indices
           const float sn = svec[(bx % g.nb) * 64 + r];
 #pragma unroll
@@ -409,10 +435,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     }
     {
       // B' overwrites A in place, and A is the B operand of both accumulators' UMMAs: wait
-      // for all of them before the first store, and for every peer to hold my rows of A
+      // for all of them before the first store
       mbar_wait(bar_mma, ph0);
       if (nacc_g > 1) mbar_wait(bar_mma1, ph1);
-      if (a_pending) cluster_wait();
       TC_TL();
       tc_fence_after();
       const int nch = g.Np / 32;
@@ -422,30 +447,26 @@ __global__ void __launch_bounds__(kTcThreads, 1)
           uint32_t r[2][32];
           tmem_ld_32x32b_x32(tmem + lane_base + (uint32_t)(a * g.Np + c * 32), r[0]);
           tmem_ld_32x32b_x32(tmem + lane_base + (uint32_t)(a * g.Np + (c + 2) * 32), r[1]);
+          uint4 xv[2][4];  // the b_k A term's bf16 A, loaded while the TMEM loads are in flight
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh)
+#pragma unroll
+            for (int h = 0; h < 4; ++h) {
+              const int q = (c + 2 * hh) * 32 + 8 * h;
+              xv[hh][h] = *reinterpret_cast<const uint4*>(sm + a_box(g, p >> 6, q >> 6) + swz((uint32_t)(p & 63), (uint32_t)(q & 63)));
+            }
           tmem_ld_wait_regs(r[0]);
           tmem_ld_wait_regs(r[1]);
+          uint32_t nf = 0;
 #pragma unroll
           for (int hh = 0; hh < 2; ++hh) {
             const int q0 = (c + 2 * hh) * 32;
-#pragma unroll
-            for (int h = 0; h < 4; ++h) {  // 8 columns per 16-byte chunk
-              const int q = q0 + 8 * h;
-              uint4* ptr = reinterpret_cast<uint4*>(sm + a_box(g, p >> 6, q >> 6) + swz((uint32_t)(p & 63), (uint32_t)(q & 63)));
-              const uint4 u4 = *ptr;
-              const uint32_t x[4] = {u4.x, u4.y, u4.z, u4.w};
-              uint32_t o[4];
-#pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                float w0 = fmaf(cc, __uint_as_float(r[hh][8 * h + 2 * e]), cb * bf_lo(x[e]));
-                float w1 = fmaf(cc, __uint_as_float(r[hh][8 * h + 2 * e + 1]), cb * bf_hi(x[e]));
-                if (q + 2 * e == p) w0 += ca;
-                if (q + 2 * e + 1 == p) w1 += ca;
-                o[e] = pk_bf2(w0, w1);
-                bad |= bad16(o[e]);
-              }
-              *ptr = make_uint4(o[0], o[1], o[2], o[3]);
-            }
+            // the chunk holds this warp's diagonal elements iff its 32 columns are the warp's
+            // 32 rows (warp-uniform): only then the a_k I term needs per-element selects
+            if (q0 == p - lane) poly_chunk<true>(sm, g, p, q0, r[hh], xv[hh], ca, cb, cc, nf);
+            else poly_chunk<false>(sm, g, p, q0, r[hh], xv[hh], ca, cb, cc, nf);
           }
+          bad |= (nf & 0x80008000u) != 0;
         }
       }
       ph0 ^= 1;
@@ -458,23 +479,36 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     TC_TL();
     if (threadIdx.x == 0) {
       tc_fence_after();
-      const uint32_t idesc = make_idesc_bf16(128, (uint32_t)g.Np, wide ? 1u : 0u, 0u);
-      for (int a = 0; a < nacc_x; ++a) {
-        const int rb0 = (a == 0) ? 0 : (g.R == 192 ? 1 : 2);  // first 64-row block of the accumulator
-        for (int ks = 0; ks < g.Np / 16; ++ks) {
-          const int kb = ks >> 2, kk = ks & 3;
-          uint64_t ad;
-          if (!wide)  // Aop[p][k] = slab[p][k]: K-major, row blocks adjacent
-            ad = make_sdesc(base + slab_box(g, 0, rb0, kb) + kk * 32, 16, 1024);
-          else        // Aop[p][k] = X[k][p]: MN-major, 64-wide p chunks one slab block apart
-            ad = make_sdesc(base + slab_box(g, 1, rb0, kb) + kk * 2048, (uint32_t)g.nb * kBox, 1024);
-          const uint64_t bd = make_sdesc(base + a_box(g, 0, kb) + kk * 32, 16, 1024);
-          umma_bf16<1>(tmem + (uint32_t)(a * g.Np), ad, bd, idesc, ks ? 1u : 0u);
+      if (!wide) {  // D[p][q] = sum_k slab[p][k] B'[q][k]: R slab rows in 128-row accumulators
+        const uint32_t idesc = make_idesc_bf16(128, (uint32_t)g.Np, 0u, 0u);
+        for (int a = 0; a < nacc_x; ++a) {
+          const int rb0 = (a == 0) ? 0 : (g.R == 192 ? 1 : 2);  // first 64-row block of the accumulator
+          for (int ks = 0; ks < g.Np / 16; ++ks) {
+            const int kb = ks >> 2, kk = ks & 3;
+            // Aop[p][k] = slab[p][k]: K-major, row blocks adjacent
+            const uint64_t ad = make_sdesc(base + slab_box(g, 0, rb0, kb) + kk * 32, 16, 1024);
+            const uint64_t bd = make_sdesc(base + a_box(g, 0, kb) + kk * 32, 16, 1024);
+            umma_bf16<1>(tmem + (uint32_t)(a * g.Np), ad, bd, idesc, ks ? 1u : 0u);
+          }
+          umma_commit<1>(a ? bar_mma1 : bar_mma);
         }
-        umma_commit<1>(a ? bar_mma1 : bar_mma);
+      } else {
+        // wide: the slab holds X itself ([n][m] boxes), and X' = B' X (B' symmetric): D[n][m] =
+        // sum_j B'[n][j] X[j][m] -- A operand B' (K-major), B operand the slab (MN-major, UMMA
+        // N = R), so the accumulator rows are slab box rows (vector stores, no 64-row overlap)
+        const uint32_t idesc = make_idesc_bf16(128, (uint32_t)g.R, 0u, 1u);
+        for (int a = 0; a < nacc_g; ++a) {
+          for (int ks = 0; ks < g.Np / 16; ++ks) {
+            const int kb = ks >> 2, kk = ks & 3;
+            const uint64_t ad = make_sdesc(base + a_box(g, 2 * a, kb) + kk * 32, 16, 1024);
+            const uint64_t bd = make_sdesc(base + slab_box(g, 1, 0, kb) + kk * 2048, (uint32_t)g.nb * kBox, 1024);
+            umma_bf16<1>(tmem + (uint32_t)(a * 256), ad, bd, idesc, ks ? 1u : 0u);
+          }
+          umma_commit<1>(a ? bar_mma1 : bar_mma);
+        }
       }
     }
-    {
+    if (!wide) {
       // X' overwrites the slab in place, which both accumulators' UMMAs read (R = 192: their
       // rows overlap): wait for all of them
       mbar_wait(bar_mma, ph0);
@@ -487,11 +521,11 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         const int p = prow0 + qd * 32 + lane;
         if (a == 1 && g.R == 192 && qd < 2) continue;  // R = 192: rows 64..127 belong to accumulator 0
         for (int c = warp >> 2; c < nch; c += 2) {
-        uint32_t r[32];
-        tmem_ld_32x32b_x32(tmem + lane_base + (uint32_t)(a * g.Np + c * 32), r);
-        tmem_ld_wait_regs(r);
-        const int q0 = c * 32;
-        if (!wide) {
+          uint32_t r[32];
+          tmem_ld_32x32b_x32(tmem + lane_base + (uint32_t)(a * g.Np + c * 32), r);
+          tmem_ld_wait_regs(r);
+          const int q0 = c * 32;
+          uint32_t nf = 0;
 #pragma unroll
           for (int h = 0; h < 4; ++h) {
             const int q = q0 + 8 * h;
@@ -499,24 +533,45 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
               o[e] = pk_bf2(__uint_as_float(r[8 * h + 2 * e]), __uint_as_float(r[8 * h + 2 * e + 1]));
-              bad |= bad16(o[e]);
+              nf |= (o[e] & 0x7F807F80u) + 0x00800080u;
             }
             *reinterpret_cast<uint4*>(sm + slab_box(g, 0, p >> 6, q >> 6) + swz((uint32_t)(p & 63), (uint32_t)(q & 63))) =
                 make_uint4(o[0], o[1], o[2], o[3]);
           }
-        } else {  // wide: the slab stores [n][m] boxes: element (p, q) at row q, column p
-          const uint32_t bx = slab_box(g, 1, p >> 6, q0 >> 6);
-#pragma unroll
-          for (int e = 0; e < 32; ++e) {
-            const uint16_t h = to_bf(__uint_as_float(r[e]));
-            bad |= ((h & 0x7F80u) == 0x7F80u);
-            *reinterpret_cast<uint16_t*>(sm + bx + swz((uint32_t)((q0 + e) & 63), (uint32_t)(p & 63))) = h;
-          }
-        }
+          bad |= (nf & 0x80008000u) != 0;
         }
       }
       ph0 ^= 1;
       if (nacc_x > 1) ph1 ^= 1;
+    } else {
+      mbar_wait(bar_mma, ph0);  // the slab is the B operand of both accumulators
+      if (nacc_g > 1) mbar_wait(bar_mma1, ph1);
+      TC_TL();
+      tc_fence_after();
+      for (int a = 0; a < nacc_g; ++a) {
+        const int n = a * 128 + qd * 32 + lane;
+        for (int c = warp >> 2; c < g.R / 32; c += 2) {
+          uint32_t r[32];
+          tmem_ld_32x32b_x32(tmem + lane_base + (uint32_t)(a * 256 + c * 32), r);
+          tmem_ld_wait_regs(r);
+          uint32_t nf = 0;
+#pragma unroll
+          for (int h = 0; h < 4; ++h) {
+            const int m = c * 32 + 8 * h;
+            uint32_t o[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              o[e] = pk_bf2(__uint_as_float(r[8 * h + 2 * e]), __uint_as_float(r[8 * h + 2 * e + 1]));
+              nf |= (o[e] & 0x7F807F80u) + 0x00800080u;
+            }
+            *reinterpret_cast<uint4*>(sm + slab_box(g, 1, m >> 6, n >> 6) + swz((uint32_t)(n & 63), (uint32_t)(m & 63))) =
+                make_uint4(o[0], o[1], o[2], o[3]);
+          }
+          bad |= (nf & 0x80008000u) != 0;
+        }
+      }
+      ph0 ^= 1;
+      if (nacc_g > 1) ph1 ^= 1;
     }
     tc_fence_before();
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the next Gram's MMAs read the slab

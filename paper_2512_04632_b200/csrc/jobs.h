@@ -214,9 +214,11 @@ __host__ __device__ inline bool cl_fits(int64_t M, int64_t N, int C = kClCtas) {
 // ------------------------------------------------------------------ cluster-resident tcgen05 NS
 // Whole Newton-Schulz of one mid-size bf16 matrix (short side N <= 256) in ONE launch of a
 // C-CTA cluster (cluster_tc.cu): Xh in row slabs of R rows per CTA, N
-// padded with zero columns to Np (128 or 256), A / B' copies in every CTA's shared memory,
-// Gram partials reduced through an fp32 scratch in L2 (C * Np * Np floats per matrix).  C is
-// the smallest power of two (2..16) whose slabs fit -- a function of the shape alone, so a
+// padded with zero columns to Np (128 or 256), A / B' copies in every CTA's shared memory.
+// Gram all-reduce through an L2 scratch (`part`): each CTA's fp32 partial, lower-triangle
+// 32 x 32 chunks only (tc_tri_chunks), then the bf16 A image (Np x Np, the shared-memory box
+// layout) that the owners of its chunk ranges write and every CTA bulk-loads.  C is the
+// smallest power of two (4..16) whose slabs fit -- a function of the shape alone, so a
 // matrix's result never depends on the rest of its call; jobs are launched in groups of
 // equal C.
 constexpr int kTcCtas = 16;  // largest cluster (non-portable size)
@@ -224,15 +226,17 @@ constexpr size_t kTcMaxSmem = 227 * 1024;
 struct TcJob {
   const void* tm_in;   // CUtensorMap (device) of the input X (m x n, 64 x 64 boxes, 128-byte swizzle)
   const void* tm_out;  // CUtensorMap of the output (may address the same buffer)
-  float* part;         // C * Np * Np fp32 Gram partials
+  float* part;         // tc_part_floats(Np, C) floats of scratch (partials, then the A image)
   int32_t m, n, M, N, wide, Np, R, C;
 };
 __host__ __device__ inline int tc_np(int64_t N) { return N <= 128 ? 128 : 256; }
-// Scratch floats for the owner's per-warp AOL row sums (8 warps x Np / C rows) or diagonal.
-__host__ __device__ inline int tc_diag_floats(int Np, int C) { return 8 * (Np / C) < 128 ? 128 : 8 * (Np / C); }
-__host__ __device__ inline size_t tc_smem(int Np, int R, int C) {
-  return (size_t)R * Np * 2 + (size_t)Np * Np * 2 + (size_t)Np * 4 + kTcCtas * 16 + (size_t)tc_diag_floats(Np, C) * 4 +
-         64 + 1024;
+// Lower-triangle 32 x 32 chunks (row block >= column block) of an Np x Np Gram partial.
+__host__ __device__ inline int tc_tri_chunks(int Np) { return (Np / 32) * (Np / 32 + 1) / 2; }
+__host__ __device__ inline size_t tc_part_floats(int Np, int C) {
+  return (size_t)C * tc_tri_chunks(Np) * 1024 + (size_t)Np * Np / 2;
+}
+__host__ __device__ inline size_t tc_smem(int Np, int R, int /*C*/) {
+  return (size_t)R * Np * 2 + (size_t)Np * Np * 2 + (size_t)Np * 4 + 64 + 1024;
 }
 // Slab rows per CTA for a C-CTA cluster: a multiple of 64, at least 128 (one M = 128 UMMA
 // per update accumulator).

@@ -10,7 +10,7 @@ import paper_2512_04632_b200 as ns  # noqa: E402
 
 ns.set_path(7)  # every eligible matrix on the tcgen05 cluster kernel
 
-for m, n in ((256, 2304), (768, 256), (1024, 128)):
+for m, n in ((256, 2304), (2304, 256), (256, 576), (768, 256), (1024, 128)):
     x = torch.randn(m, n, device="cuda").bfloat16()
     for _ in range(3):
         ns.orthogonalize(x, iters=4)
