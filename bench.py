@@ -678,6 +678,16 @@ def run_extras(args, peaks, extra_outs=None):
     us, gus, nl = small(lambda: ns.orthogonalize_list(xs, out=outs, iters=4))
     keep("cifar", xs_np, outs, list(range(len(shapes))), C.turbo(4), 2e-2)
     out["cifar"] = {"us": round(us, 1), "us_graph_replay": round(gus, 1), "launches": nl, "matrices": len(shapes)}
+    # the same set with every matrix on the tcgen05 cluster kernel (ns_set_path(7)): not the
+    # default -- routing is per shape and N = 256 matrices stay on the step engine
+    outs7 = [torch.empty_like(t) for t in xs]
+    old_path = ns.set_path(7)
+    try:
+        us7, gus7, nl7 = small(lambda: ns.orthogonalize_list(xs, out=outs7, iters=4))
+    finally:
+        ns.set_path(old_path)
+    keep("cifar-path7", xs_np, outs7, list(range(len(shapes))), C.turbo(4), 2e-2)
+    out["cifar"].update({"path7_us": round(us7, 1), "path7_us_graph_replay": round(gus7, 1), "path7_launches": nl7})
     # --- config 1: one 128 x 128 fp32 matrix, fp32 "exact" mode (cluster-resident kernel)
     x1_np = I.gaussian(128, 128, seed=I.matrix_seed(1, 0), bf16=False)
     x1 = torch.from_numpy(x1_np).cuda()
