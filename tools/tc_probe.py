@@ -42,7 +42,11 @@ def replay_us(xs, outs):
 
 cases = {"cifar": I.shape_set("cifar"), "256x2304": [(256, 2304)], "256x576": [(256, 576)],
          "768x256": [(768, 256)], "1024x128": [(1024, 128)], "64x576": [(64, 576)], "64x216": [(64, 216)],
-         "128x128": [(128, 128)], "3072x192": [(3072, 192)], "gpt2-small-like 16x768x256": [(768, 256)] * 16}
+         "128x128": [(128, 128)], "3072x192": [(3072, 192)], "gpt2-small-like 16x768x256": [(768, 256)] * 16,
+         "batch 64x1024x128": [(1024, 128)] * 64, "batch 64x64x576": [(64, 576)] * 64,
+         "batch 16x1024x128": [(1024, 128)] * 16}
+if len(sys.argv) > 1:  # a subset by name prefix
+    cases = {k: v for k, v in cases.items() if any(k.startswith(a) for a in sys.argv[1:])}
 for name, shapes in cases.items():
     xs = [torch.randn(m, n, device="cuda").bfloat16() for m, n in shapes]
     outs = [torch.empty_like(x) for x in xs]
