@@ -20,8 +20,10 @@ ns = pytest.importorskip("paper_2512_04632_b200")
 
 BF16_TOL = 2e-2
 
+# wide and tall, Np = 128 / 256, C = 4 / 8 / 16, slab rows R = 128 / 192 / 256 (R = 256: the
+# wide update's UMMA N = 256), ragged N (zero-padded columns) and ragged M (rows past M)
 SHAPES = [(256, 2304), (2304, 256), (256, 576), (576, 256), (768, 256), (1024, 128), (64, 576),
-          (256, 256), (200, 3000), (3072, 192), (136, 520)]
+          (256, 256), (200, 3000), (3072, 192), (136, 520), (96, 4000), (4000, 96), (64, 216)]
 
 
 def _run(x32, coeffs, precond, path=7):
