@@ -18,18 +18,19 @@
 //           55-65, DSMEM bulk copies ~13 -- so the triangle halves the dominant store traffic
 //           and the L2 image replaces a DSMEM broadcast).
 //           k = 1: every CTA forms s_i = (sum_j |A0_ij|)^(-1/2) (AOL, Eq. 8) or tr(A0)^(-1/2)
-//           (Frobenius, Eq. 10) from its copy of A0, then A1 = diag(s) A0 diag(s) and
-//           X1 = X0 diag(s) in its own copies (Alg. 2 l.3-4).
+//           (Frobenius, Eq. 10) from its copy of A0, then A1 = diag(s) A0 diag(s) in its own
+//           copy (Alg. 2 l.4); X1 = X0 diag(s) (l.3) is never formed: diag(s) is folded into
+//           B'1 (its columns), as in the step engine (reading R15).
 //   Poly  : every CTA computes B' = a_k I + b_k A + c_k A^2 for the full matrix (tcgen05, A
 //           as both operands; redundant per CTA, no communication), in place over A (Eq. 4
-//           with Eq. 5's a_k folded in, reading R15).
+//           with Eq. 5's a_k folded in, reading R15; k = 1: times diag(s) on the right).
 //   Update: slab_r <- slab_r B'^T (tcgen05; wide inputs: X_r <- B' X_r, the same product with
 //           the slab as the B operand), written back over the slab in place (Eq. 5).
 // After T iterations each CTA TMA-stores its slab.  Rounding: bf16 storage of X, A, B' (every
-// stored value rounded once, RNE), fp32 accumulation and fp32 scaling -- reading R6; X1 is
-// materialised here (Alg. 2 l.3 literally), where the step engine folds diag(s) into B'1, so
-// the two engines agree to bf16 rounding, not bitwise (routing is shape-only: a matrix always
-// takes the same engine, batching never changes its result).
+// stored value rounded once, RNE), fp32 accumulation and fp32 scaling -- readings R6 / R15,
+// the same roundings as the step engine; the two engines still agree to bf16 rounding only,
+// not bitwise (their fp32 sums run in different orders), and routing is shape-only: a matrix
+// always takes the same engine, batching never changes its result.
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -160,26 +161,46 @@ __device__ __forceinline__ void reduce_share(const TcGeo& g, float* part, uint32
 }
 
 // B' = a_k I + b_k A + c_k A^2 for 32 columns [q0, q0 + 32) of row p, in place over the bf16
-// A row (Eq. 4 with Eq. 5's a_k folded in, reading R15); nf accumulates the non-finite test of
-// the stored pairs (bit 15 / 31 set iff a half is Inf / NaN).
-template <bool DIAG>
+// A row (Eq. 4 with Eq. 5's a_k folded in, reading R15), two columns per packed fp32x2
+// FMUL2 / FFMA2 (the same fp32 roundings as fmaf(c, r, b * x) per element).  No non-finite
+// test here: a non-finite A or B' always reaches X_{k+1}, whose stores are checked.
+__device__ __forceinline__ uint64_t pk2(float lo, float hi) {
+  uint64_t d;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(d) : "f"(lo), "f"(hi));
+  return d;
+}
+template <bool DIAG, bool SCALE>
 __device__ __forceinline__ void poly_chunk(uint8_t* sm, const TcGeo& g, int p, int q0, const uint32_t (&r)[32],
-                                           const uint4 (&xv)[4], float ca, float cb, float cc, uint32_t& nf) {
+                                           const uint4 (&xv)[4], float ca, float cb, float cc, const float* sv) {
+  const uint64_t cb2 = pk2(cb, cb), cc2 = pk2(cc, cc);
 #pragma unroll
   for (int h = 0; h < 4; ++h) {  // 8 columns per 16-byte swizzle chunk
     const int q = q0 + 8 * h;
     const uint32_t x[4] = {xv[h].x, xv[h].y, xv[h].z, xv[h].w};
+    float sc[8];
+    if (SCALE) {  // k = 1: B'1 diag(s) -- column q scaled by s_q (X1 = X0 diag(s) never formed)
+      const float4 a0 = *reinterpret_cast<const float4*>(sv + q), a1 = *reinterpret_cast<const float4*>(sv + q + 4);
+      sc[0] = a0.x; sc[1] = a0.y; sc[2] = a0.z; sc[3] = a0.w; sc[4] = a1.x; sc[5] = a1.y; sc[6] = a1.z; sc[7] = a1.w;
+    }
     uint32_t o[4];
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-      float w0 = fmaf(cc, __uint_as_float(r[8 * h + 2 * e]), cb * bf_lo(x[e]));
-      float w1 = fmaf(cc, __uint_as_float(r[8 * h + 2 * e + 1]), cb * bf_hi(x[e]));
+      uint64_t t, w;
+      asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(t) : "l"(cb2), "l"(pk2(bf_lo(x[e]), bf_hi(x[e]))));
+      asm("fma.rn.f32x2 %0, %1, %2, %3;"
+          : "=l"(w)
+          : "l"(cc2), "l"(pk2(__uint_as_float(r[8 * h + 2 * e]), __uint_as_float(r[8 * h + 2 * e + 1]))), "l"(t));
+      float w0, w1;
+      asm("mov.b64 {%0, %1}, %2;" : "=f"(w0), "=f"(w1) : "l"(w));
       if (DIAG) {
         w0 = (q + 2 * e == p) ? w0 + ca : w0;
         w1 = (q + 2 * e + 1 == p) ? w1 + ca : w1;
       }
+      if (SCALE) {
+        w0 *= sc[2 * e];
+        w1 *= sc[2 * e + 1];
+      }
       o[e] = pk_bf2(w0, w1);
-      nf |= (o[e] & 0x7F807F80u) + 0x00800080u;
     }
     *reinterpret_cast<uint4*>(sm + a_box(g, p >> 6, q >> 6) + swz((uint32_t)(p & 63), (uint32_t)(q & 63))) =
         make_uint4(o[0], o[1], o[2], o[3]);
@@ -190,7 +211,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     cluster_tc_ns_kernel(const TcJob* __restrict__ jobs, const float* __restrict__ coeffs, int iters, int precond,
                          uint32_t* __restrict__ flags, int dbg) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-byte aligned by pointer arithmetic on the __shared__ array (not through an integer
+  // cast), so the compiler keeps the shared state space: LDS / STS, not generic LD / ST
+  uint8_t* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const uint32_t base = smem_u32(sm);
   const TcJob& J = jobs[blockIdx.x / jobs[0].C];  // every job of a launch has the same C
   const uint32_t rank = cluster_ctarank();
@@ -306,12 +329,10 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       }
       ph0 ^= 1;
       if (nacc_g > 1) ph1 ^= 1;
-      asm volatile("fence.proxy.async.global;" ::: "memory");  // read back by bulk copies
     }
     tc_fence_before();
     TC_TL();
     cluster_sync();  // every partial of this iteration is in L2 (release / acquire)
-    asm volatile("fence.proxy.async.global;" ::: "memory");
     TC_TL();
     // ===================================================== reduce my share of A_k into the image
     {
@@ -378,43 +399,38 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         }
       }
       __syncthreads();
-      // A1 = diag(s) A0 diag(s) (Alg. 2 l.4), X1 = X0 diag(s) (Alg. 2 l.3): 16-byte chunks
-      const int achunks = g.Np * g.Np / 8;
-      for (int t = threadIdx.x; t < achunks; t += kTcThreads) {
-        const int bx = t >> 9, w = t & 511, r = w >> 3, ch = w & 7;  // 512 chunks per box
-        const int bi = bx % g.nb, bj = bx / g.nb;                    // a_box order
-        const int row = bi * 64 + r, col0 = bj * 64 + ((ch ^ (r & 7)) << 3);
-        uint4* p = reinterpret_cast<uint4*>(sm + g.abuf + (uint32_t)bx * kBox + r * 128 + ch * 16);
-        uint4 u = *p;
-        uint32_t wv[4] = {u.x, u.y, u.z, u.w};
-        const float si = svec[row];
-        const float4 s0 = *reinterpret_cast<const float4*>(svec + col0), s1 = *reinterpret_cast<const float4*>(svec + col0 + 4);
-        const float sc[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
+      // A1 = diag(s) A0 diag(s) (Alg. 2 l.4) in this CTA's copy, box by box (no index division:
+      // the box walk gives row and column blocks), two boxes x two 16-byte chunks per thread in
+      // flight (all loads of a group before its stores).  X1 = X0 diag(s) (l.3) is never formed:
+      // s goes into the k = 1 A^2 epilogue (B'1 diag(s), as in the step engine, reading R15).
+      for (int bj = 0; bj < g.nb; ++bj)
+        for (int bi = 0; bi < g.nb; bi += 2) {
+          uint4 u[4];
+          float si[4];
+          float4 s0[4], s1[4];
+          uint4* pp[4];
 #pragma unroll
-        for (int e = 0; e < 4; ++e)
-          wv[e] = pk_bf2((si * bf_lo(wv[e])) * sc[2 * e], (si * bf_hi(wv[e])) * sc[2 * e + 1]);
-        *p = make_uint4(wv[0], wv[1], wv[2], wv[3]);
-      }
-      const int xchunks = g.R * g.Np / 8;
-      for (int t = threadIdx.x; t < xchunks; t += kTcThreads) {
-        const int bx = t >> 9, w = t & 511, r = w >> 3, ch = w & 7;
-        const int cpos = (ch ^ (r & 7)) << 3;
-        uint4* p = reinterpret_cast<uint4*>(sm + g.slab + (uint32_t)bx * kBox + r * 128 + ch * 16);
-        uint4 u = *p;
-        uint32_t wv[4] = {u.x, u.y, u.z, u.w};
-        if (!wide) {  // box (i, j) at j * rb + i: columns are N indices
-          const int n0 = (bx / g.rb) * 64 + cpos;
-          const float4 s0 = *reinterpret_cast<const float4*>(svec + n0), s1 = *reinterpret_cast<const float4*>(svec + n0 + 4);
-          const float sc[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
+          for (int j = 0; j < 4; ++j) {
+            const int w = (int)threadIdx.x + (j & 1) * kTcThreads, r = w >> 3, ch = w & 7;  // 512 chunks per box
+            const int bx = bj * g.nb + bi + (j >> 1);
+            const int col0 = bj * 64 + ((ch ^ (r & 7)) << 3);
+            pp[j] = reinterpret_cast<uint4*>(sm + g.abuf + (uint32_t)bx * kBox + r * 128 + ch * 16);
+            u[j] = *pp[j];
+            si[j] = svec[(bi + (j >> 1)) * 64 + r];
+            s0[j] = *reinterpret_cast<const float4*>(svec + col0);
+            s1[j] = *reinterpret_cast<const float4*>(svec + col0 + 4);
+          }
 #pragma unroll
-          for (int e = 0; e < 4; ++e) wv[e] = pk_bf2(bf_lo(wv[e]) * sc[2 * e], bf_hi(wv[e]) * sc[2 * e + 1]);
-        } else {      // box (i, j) at i * nb + j: box rows are N indices
-          const float sn = svec[(bx % g.nb) * 64 + r];
+          for (int j = 0; j < 4; ++j) {
+            const uint32_t wv[4] = {u[j].x, u[j].y, u[j].z, u[j].w};
+            const float sc[8] = {s0[j].x, s0[j].y, s0[j].z, s0[j].w, s1[j].x, s1[j].y, s1[j].z, s1[j].w};
+            uint32_t o[4];
 #pragma unroll
-          for (int e = 0; e < 4; ++e) wv[e] = pk_bf2(bf_lo(wv[e]) * sn, bf_hi(wv[e]) * sn);
+            for (int e = 0; e < 4; ++e)
+              o[e] = pk_bf2((si[j] * bf_lo(wv[e])) * sc[2 * e], (si[j] * bf_hi(wv[e])) * sc[2 * e + 1]);
+            *pp[j] = make_uint4(o[0], o[1], o[2], o[3]);
+          }
         }
-        *p = make_uint4(wv[0], wv[1], wv[2], wv[3]);
-      }
     }
     // ===================================================== B' = a I + b A + c A^2 (in place)
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -441,6 +457,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       TC_TL();
       tc_fence_after();
       const int nch = g.Np / 32;
+      const bool scale1 = k == 0 && precond != 0;  // B'1 diag(s): X1 = X0 diag(s) folded in
       for (int a = 0; a < nacc_g; ++a) {
         const int p = a * 128 + qd * 32 + lane;
         for (int c = warp >> 2; c < nch; c += 4) {
@@ -457,16 +474,20 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             }
           tmem_ld_wait_regs(r[0]);
           tmem_ld_wait_regs(r[1]);
-          uint32_t nf = 0;
 #pragma unroll
           for (int hh = 0; hh < 2; ++hh) {
             const int q0 = (c + 2 * hh) * 32;
             // the chunk holds this warp's diagonal elements iff its 32 columns are the warp's
             // 32 rows (warp-uniform): only then the a_k I term needs per-element selects
-            if (q0 == p - lane) poly_chunk<true>(sm, g, p, q0, r[hh], xv[hh], ca, cb, cc, nf);
-            else poly_chunk<false>(sm, g, p, q0, r[hh], xv[hh], ca, cb, cc, nf);
+            const bool dg = q0 == p - lane;
+            if (!scale1) {
+              if (dg) poly_chunk<true, false>(sm, g, p, q0, r[hh], xv[hh], ca, cb, cc, svec);
+              else poly_chunk<false, false>(sm, g, p, q0, r[hh], xv[hh], ca, cb, cc, svec);
+            } else {
+              if (dg) poly_chunk<true, true>(sm, g, p, q0, r[hh], xv[hh], ca, cb, cc, svec);
+              else poly_chunk<false, true>(sm, g, p, q0, r[hh], xv[hh], ca, cb, cc, svec);
+            }
           }
-          bad |= (nf & 0x80008000u) != 0;
         }
       }
       ph0 ^= 1;
