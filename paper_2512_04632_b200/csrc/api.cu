@@ -1121,13 +1121,12 @@ static bool tma_ok_call(const Mat& mt, ns_dtype dtype, bool cast);
 // and 5: bf16 matrices with short side N <= 128 (padded to 128) whose slabs fit 16 CTAs (M <=
 // 4096) and that TMA can address -- measured faster than both the step engine and the FFMA
 // cluster kernel (graph replay, profiles/r02_cluster_tc.log: 1024x128 43 vs 79 us, 64x576 43
-// vs 64, 128^2 43 vs 60 / 66).  For 128 < N <= 256 (padded to 256) the kernel (round 2: lower-
-// triangle Gram partials, L2 A image) ties the step engine on a lone 256x2304 (90 us) and
-// loses on the others (256x576 84 vs 75, 3072x192 94 vs 88); it also holds 16 SMs per matrix
-// for the whole call, so a batch of such matrices runs in waves (64 x 256x2304 ~7 waves) where
-// the step engine shares tiles across the GPU.  Routing wide C = 16 shapes here made the CIFAR
-// set 104 -> 95.5 us but would halve large batches, and routing is per shape (batching never
-// changes a result), so only path 7 sends N > 128 here; path 4 sends none.
+// vs 64, 128^2 43 vs 60 / 66; round-2 third pass: 37-39 us).  For 128 < N <= 256 (padded to
+// 256) the kernel now beats the step engine on lone matrices (256x2304 82 vs 91 us, 768x256 76
+// vs 78, 3072x192 86 vs 88; 256x576 77 vs 76) but holds 16 SMs per matrix for the whole call,
+// so a batch of such matrices runs in waves (64 x 256x2304 ~7 waves) where the step engine
+// shares tiles across the GPU; routing is per shape (batching never changes a result), so only
+// path 7 sends N > 128 here (the CIFAR set: 86 us on path 7, 104 on path 0); path 4 sends none.
 // Shape-only (plus TMA alignment, as for the step engine): batching never changes a result.
 static bool to_tc(const Mat& mt, ns_dtype dtype, bool any_peer, int cc_major, bool cast) {
   if (dtype != NS_BF16 || any_peer || cc_major != 10) return false;
