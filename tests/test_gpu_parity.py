@@ -259,19 +259,23 @@ def test_sharded_nccl_world1():
 def test_fused_peer_stores_c_abi():
     """ns_orthogonalize_peers: the last iteration's epilogue writes every output tile to the
     extra destinations as well (here two local buffers standing in for peers' NVLink-mapped
-    gather buffers): all copies are bitwise the regular result."""
+    gather buffers, NaN-filled so that a missed tile shows): all copies are bitwise the regular
+    result, and a peer copy of the ragged matrix matches the fp64 oracle on its own."""
     shapes = [(1024, 1024), (3072, 768), (768, 3072), (520, 136)]
-    xs = [torch.from_numpy(I.gaussian(m, n, seed=130 + i)).to(torch.bfloat16).cuda() for i, (m, n) in enumerate(shapes)]
+    xs_np = [I.gaussian(m, n, seed=130 + i) for i, (m, n) in enumerate(shapes)]
+    xs = [torch.from_numpy(x).to(torch.bfloat16).cuda() for x in xs_np]
     ref = [x.clone() for x in xs]
     ns.orthogonalize_list(ref, iters=4)
     outs = [torch.empty_like(x) for x in xs]
-    peers = [[torch.zeros_like(x) for _ in range(2)] for x in xs]
+    peers = [[torch.full_like(x, float("nan")) for _ in range(2)] for x in xs]
     ns.orthogonalize_list(xs, out=outs, iters=4, peer_ptrs=[[p.data_ptr() for p in ps] for ps in peers])
     torch.cuda.synchronize()
     for r, o, ps in zip(ref, outs, peers):
         assert torch.equal(o, r)
         for p in ps:
             assert torch.equal(p, r)
+    peer = peers[3][1].float().cpu().numpy().astype(np.float64)
+    assert_parity(peer, oracle_run(xs_np[3], C.turbo(4), "aol"), 2e-2, "peer copy 520x136")
 
 
 def test_sharded_fused_collective_world1():
