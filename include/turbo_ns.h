@@ -164,7 +164,9 @@ ns_status ns_muon_apply(void* const* W, const void* const* U, const int64_t* m, 
  * times (ns_orthogonalize with `batch`, or a grouped list) -- per matrix W (m x n), A and B
  * (N x N), s and the AOL partials (Eq. 8 row sums), plus a 1 KiB header per plan
  * (a list mixing TMA-unaligned bf16 shapes runs as two plans).  An upper bound for any
- * device and path: matrices served by the cluster-resident kernel need none.  Host only
+ * device and path: a matrix served by the tcgen05 cluster kernel needs only its Gram-partial
+ * scratch and A image (counted with the larger of the two footprints), the FFMA cluster
+ * kernel none.  Host only
  * (no device call).  NS_ERR_INVALID_VALUE for NULL pointers, count/batch/m/n < 1, bad
  * dtype. */
 ns_status ns_workspace_size(const int64_t* m, const int64_t* n, int64_t count, int64_t batch,
@@ -193,9 +195,10 @@ uint64_t ns_launch_count(void);
 
 /* Execution-path override for testing.  0 = auto: bf16 matrices with short side N <= 128
  * that TMA can address and that fit 16 row slabs (M <= 4096) run the WHOLE NS in ONE launch of
- * a 16-CTA cluster on the tensor cores (cluster_tc_ns_kernel: X slabs and A / B' resident in
- * shared memory, Gram partials reduced through L2 in a fixed order, A rows broadcast over
- * DSMEM); other matrices with N <= 128 whose fp32 copy
+ * a 4- to 16-CTA cluster on the tensor cores (cluster_tc_ns_kernel: X slabs and A / B'
+ * resident in shared memory, lower-triangle Gram partials reduced through L2 in a fixed
+ * order into an A image every CTA bulk-loads); other
+ * matrices with N <= 128 whose fp32 copy
  * fits in shared memory (fp32 always, bf16 while M*N^2 <= 2.2e6) run the whole NS in one
  * launch of a 16- or 8-CTA FFMA cluster (cluster_ns_kernel; row a-10); all other matrices go
  * through the step engine (tcgen05, 256x256 tiles on CTA pairs, for aligned bf16, else SIMT;

@@ -3,8 +3,9 @@
 // conv weights reshaped to 2-D, e.g. 256 x 2304).
 //
 // One thread-block cluster of C CTAs (a power of two, 4..16, set by the shape: tc_cluster)
-// runs ALL steps of Alg. 2 for one matrix in ONE launch.  Xh (M x N, the short-side orientation, N padded with zero columns to
-// Np in {128, 256}) is split into row slabs of R in {128, 192, 256} rows, one per CTA,
+// runs ALL steps of Alg. 2 for one matrix in ONE launch.  Xh (M x N, the
+// short-side orientation, N padded with zero columns to Np in {128, 256}) is split into row
+// slabs of R in {128, 192, 256} rows, one per CTA,
 // resident in shared memory for the whole call in the 64 x 64-box / 128-byte-swizzle layout
 // the TMA loads it in (X itself, not a transposed copy: wide inputs are oriented by the UMMA
 // major bits, as in the step engine).  Every CTA also holds a full copy of A (Np x Np bf16),
