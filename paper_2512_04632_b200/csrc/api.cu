@@ -184,6 +184,7 @@ struct Mat {
   // tensormap indices (tcgen05 path)
   int tm_x, tm_out, tm_w, tm_a, tm_b;
   size_t tc_part_off = 0;  // cluster tcgen05 kernel: Gram partials + A image (tc_part_floats)
+  size_t cl_off = 0;       // FFMA cluster kernel: row-exchange scratch (cl_xchg_floats)
   // fused collective: extra destinations of the final result (peers' buffers)
   std::vector<void*> peer;
   int tm_peer;
@@ -321,6 +322,15 @@ static size_t tc_part_bytes(int64_t M, int64_t N) {
   const int C = tc_cluster(M, N);
   return C ? tc_part_floats(tc_np(N), C) * 4 : 0;
 }
+// CTAs of the FFMA cluster kernel for a matrix (16 when it fits that layout; TNS_CL_CTAS=8
+// forces 8 -- an A/B knob), and its exchange scratch
+static int cl_ctas(int64_t M, int64_t N) {
+  static const bool only8 = [] { const char* e = getenv("TNS_CL_CTAS"); return e && atoi(e) == 8; }();
+  return !only8 && cl_fits(M, N, kClCtasMax) ? kClCtasMax : kClCtas;
+}
+static size_t cl_xchg_bytes(int64_t M, int64_t N) {
+  return cl_fits(M, N) ? cl_xchg_floats((int)M, (int)N, cl_ctas(M, N)) * 4 : 0;
+}
 
 // Workspace of a problem list as the step engine lays it out; a bf16 matrix the tcgen05
 // cluster kernel could take counts with the larger of its two footprints (an upper bound
@@ -337,6 +347,7 @@ static size_t workspace_bytes_for(const std::vector<Mat>& mats, ns_dtype dt) {
     o = align_up(o, 256) + (size_t)mt.N * part_ld_for(mt.N) * 4;
     if (dt == NS_BF16) o = align_up(o, 256) + (size_t)split_factor(mt.M, mt.N) * kSplitLd * kSplitLd * 4;
     if (dt == NS_BF16 && tc_fits(mt.M, mt.N)) o = std::max(o, tc_part_bytes(mt.M, mt.N));
+    o = std::max(o, cl_xchg_bytes(mt.M, mt.N));  // or the FFMA cluster kernel's exchange scratch
     off = align_up(off, 256) + align_up(o, 256);
   }
   return align_up(off, 256);
@@ -422,6 +433,9 @@ static ns_status build_plan(Plan& P, HostTables& H, DevCtx* dc, const float* coe
   }
   for (Mat& mt : P.tc) {  // Gram partials of the tcgen05 cluster kernel
     off = align_up(off, 256); mt.tc_part_off = off; off += tc_part_bytes(mt.M, mt.N);
+  }
+  for (Mat& mt : P.tiny) {  // row-exchange scratch of the FFMA cluster kernel
+    off = align_up(off, 256); mt.cl_off = off; off += cl_xchg_bytes(mt.M, mt.N);
   }
   if (P.cast) {  // bf16 staging copies of the caller's fp32 matrices
     for (Mat& mt : P.mats) { off = align_up(off, 256); mt.stage_off = off; off += (size_t)mt.m * mt.n * 2; }
@@ -562,12 +576,11 @@ static ns_status build_plan(Plan& P, HostTables& H, DevCtx* dc, const float* coe
       std::vector<ClusterJob> cj;
       size_t smem = 0;
       for (const Mat& mt : P.tiny) {
-        static const bool only8 = [] { const char* e = getenv("TNS_CL_CTAS"); return e && atoi(e) == 8; }();
-        const bool fits16 = !only8 && cl_fits(mt.M, mt.N, kClCtasMax);  // TNS_CL_CTAS=8: A/B knob
-        if (fits16 != (ctas == kClCtasMax)) continue;
+        if (cl_ctas(mt.M, mt.N) != ctas) continue;
         ClusterJob J;
         std::memset(&J, 0, sizeof(J));
         J.x = mt.x; J.out = mt.out;
+        J.xchg = reinterpret_cast<float*>(ws + mt.cl_off);
         J.m = (int)mt.m; J.n = (int)mt.n; J.M = (int)mt.M; J.N = (int)mt.N; J.wide = mt.wide ? 1 : 0;
         cj.push_back(J);
         smem = std::max(smem, cl_layout(J.M, J.N, ctas).floats * 4 + kClHdr);

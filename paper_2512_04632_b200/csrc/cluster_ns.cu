@@ -14,6 +14,9 @@
 //     X: CTA r computes its rows of X_{k+1} = a X_k + X_k B_k               (Eq. 5)
 //        -> DSMEM broadcast into every CTA's Xh copy, cluster barrier
 //   store this CTA's rows of X_{T+1} (caller layout, transposed back for m < n)
+// A phase whose full matrix is at least kClL2Bytes (jobs.h) exchanges through an L2 buffer
+// instead of DSMEM (each CTA stores its rows once, cluster barrier, every CTA bulk-loads the
+// matrix): the same data, measured faster for the larger matrices only.
 // Arithmetic is fp32 FFMA; in bf16 mode every stored X, A, B value is rounded to bf16
 // (the same storage points as the tcgen05 path, reading R7).  The symmetric operands are
 // read through their transposes (A_ik = A_ki, bitwise: the products are computed in the
@@ -62,6 +65,12 @@ __device__ __forceinline__ uint32_t dsmem_addr(uint32_t local, uint32_t rank) {
 __device__ __forceinline__ void dsmem_bulk(uint32_t dst, uint32_t src, uint32_t bytes, uint32_t bar) {
   asm volatile("cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
                "r"(src), "r"(bytes), "r"(bar)
+               : "memory");
+}
+// Bulk copy (TMA engine) global -> this CTA's shared memory, counted on mbarrier `bar`.
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(bar)
                : "memory");
 }
 __device__ __forceinline__ void cl_wait(const uint64_t* bar, uint32_t parity) {
@@ -186,6 +195,33 @@ __global__ void __launch_bounds__(kClThreads, 1)
   };
   // bytes each CTA receives per phase: the other CTAs' rows
   const uint32_t bytes_ab = (uint32_t)(N - nr) * lda * 4, bytes_x = (uint32_t)(M - mr) * ldx * 4;
+  // Large phases go through L2 instead (kClL2Bytes): every thread stores its share of this
+  // CTA's rows [row0, row0 + nrows) into the buffer g; after a cluster barrier the whole
+  // matrix [0, total_rows) is bulk-loaded into dst (the own rows included: identical values),
+  // completing on barrier b.  A function of the shape: the same choice in every CTA.
+  const bool l2_ab = (uint32_t)N * lda * 4 >= kClL2Bytes, l2_x = (uint32_t)M * ldx * 4 >= kClL2Bytes;
+  auto exchange = [&](int b, float* g, float* dst, const float* src, int row0, int nrows, int total_rows, int ld,
+                      uint32_t par) {
+    __syncthreads();  // every thread's epilogue rows are in src
+    const int n4 = nrows * ld / 4;
+    const float4* s4 = reinterpret_cast<const float4*>(src);
+    float4* g4 = reinterpret_cast<float4*>(g + (size_t)row0 * ld);
+    for (int e = tid; e < n4; e += kClThreads) __stcg(g4 + e, s4[e]);
+    asm volatile("fence.proxy.async.global;" ::: "memory");  // read back by the async proxy
+    cluster_sync();  // every CTA's rows are in L2 (release / acquire); all reads of dst are done
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+    const uint32_t bytes = (uint32_t)total_rows * ld * 4;
+    if (tid == 0) mbar_arrive_expect_tx(&bars[b], bytes);
+    __syncthreads();  // the expected byte count is registered before any copy can complete
+    constexpr uint32_t kPiece = 16384;
+    for (uint32_t off = (uint32_t)tid * kPiece; off < bytes; off += kClThreads * kPiece)
+      bulk_g2s(smem_u32(dst) + off, reinterpret_cast<const uint8_t*>(g) + off, min(kPiece, bytes - off),
+               smem_u32(&bars[b]));
+    cl_wait(&bars[b], par);
+  };
+  float* gA = J.xchg;
+  float* gB = gA + (size_t)L.N4 * lda;
+  float* gX = gB + (size_t)L.N4 * lda;
 
   if (tid == 0) {
     for (int b = 0; b < 3; ++b) mbar_init(&bars[b], 1);
@@ -224,13 +260,17 @@ __global__ void __launch_bounds__(kClThreads, 1)
     const float a = coeffs[3 * k], b = coeffs[3 * k + 1], c = coeffs[3 * k + 2];
     const uint32_t par = (uint32_t)k & 1u;
     // ---- G: rows [r0, r0+nr) of A = Xh^T Xh  (L(i, kk) = Xh[kk][r0+i]: k-major)
-    if (tid == 0) mbar_arrive_expect_tx(&bars[0], bytes_ab);
+    if (tid == 0 && !l2_ab) mbar_arrive_expect_tx(&bars[0], bytes_ab);
     cl_gemm<true>(Xf + r0, ldx, Xf, ldx, nr, C4, M, [&](int i, int j, float4 v) {
       v.x = rnd<S>(v.x); v.y = rnd<S>(v.y); v.z = rnd<S>(v.z); v.w = rnd<S>(v.w);
       *reinterpret_cast<float4*>(A + (size_t)(r0 + i) * lda + j) = v;
     }, dbg);
-    publish(0, L.offA + (size_t)r0 * lda, A + (size_t)r0 * lda, (uint32_t)nr * lda * 4);
-    cl_wait(&bars[0], par);
+    if (l2_ab) {
+      exchange(0, gA, A, A + (size_t)r0 * lda, r0, nr, N, lda, par);
+    } else {
+      publish(0, L.offA + (size_t)r0 * lda, A + (size_t)r0 * lda, (uint32_t)nr * lda * 4);
+      cl_wait(&bars[0], par);
+    }
     if (k == 0) CL_TL(1);
     if (k == 0 && precond != 0) {
       // A0 is rescaled IN PLACE below, including this CTA's own rows, which the bulk copies
@@ -298,33 +338,42 @@ __global__ void __launch_bounds__(kClThreads, 1)
     }
     if (k == 0) CL_TL(2);
     // ---- P: rows [r0, r0+nr) of B = b A + c A A  (L(i, kk) = A[i][kk] = A[kk][i])
-    if (tid == 0) mbar_arrive_expect_tx(&bars[1], bytes_ab);
+    if (tid == 0 && !l2_ab) mbar_arrive_expect_tx(&bars[1], bytes_ab);
     cl_gemm<true>(A + r0, lda, A, lda, nr, C4, N, [&](int i, int j, float4 v) {
       const float4 av = *reinterpret_cast<const float4*>(A + (size_t)(r0 + i) * lda + j);
       v.x = rnd<S>(fmaf(c, v.x, b * av.x)); v.y = rnd<S>(fmaf(c, v.y, b * av.y));
       v.z = rnd<S>(fmaf(c, v.z, b * av.z)); v.w = rnd<S>(fmaf(c, v.w, b * av.w));
       *reinterpret_cast<float4*>(B + (size_t)(r0 + i) * lda + j) = v;
     }, dbg);
-    publish(1, L.offB + (size_t)r0 * lda, B + (size_t)r0 * lda, (uint32_t)nr * lda * 4);
-    cl_wait(&bars[1], par);
+    if (l2_ab) {
+      exchange(1, gB, B, B + (size_t)r0 * lda, r0, nr, N, lda, par);
+    } else {
+      publish(1, L.offB + (size_t)r0 * lda, B + (size_t)r0 * lda, (uint32_t)nr * lda * 4);
+      cl_wait(&bars[1], par);
+    }
     if (k == 0) CL_TL(3);
     // ---- X: rows [o, o+mr) of X_{k+1} = a X_k + X_k B_k  (L = X_k rows, row-major)
-    if (tid == 0) mbar_arrive_expect_tx(&bars[2], bytes_x);
+    if (tid == 0 && !l2_x) mbar_arrive_expect_tx(&bars[2], bytes_x);
     cl_gemm<false>(Xf + (size_t)o * ldx, ldx, B, lda, mr, C4, N, [&](int i, int j, float4 v) {
       const float4 xv = *reinterpret_cast<const float4*>(Xf + (size_t)(o + i) * ldx + j);
       v.x = rnd<S>(fmaf(a, xv.x, v.x)); v.y = rnd<S>(fmaf(a, xv.y, v.y));
       v.z = rnd<S>(fmaf(a, xv.z, v.z)); v.w = rnd<S>(fmaf(a, xv.w, v.w));
       *reinterpret_cast<float4*>(Xn + (size_t)i * ldx + j) = v;
     }, dbg);
-    // (publish's barrier also ends every read of this CTA's X_k rows)
-    publish(2, L.offX + (size_t)o * ldx, Xn, (uint32_t)mr * ldx * 4);
-    if (k == 0) CL_TL(4);
-    for (int e = tid; e < mr * C4; e += kClThreads) {  // own rows: local copy
-      const int i = e / C4, j = (e % C4) * 4;
-      *reinterpret_cast<float4*>(Xf + (size_t)(o + i) * ldx + j) = *reinterpret_cast<const float4*>(Xn + (size_t)i * ldx + j);
+    if (l2_x) {  // (the exchange's cluster barrier also ends every read of this CTA's X_k rows)
+      exchange(2, gX, Xf, Xn, o, mr, M, ldx, par);
+      if (k == 0) CL_TL(4);
+    } else {
+      // (publish's barrier also ends every read of this CTA's X_k rows)
+      publish(2, L.offX + (size_t)o * ldx, Xn, (uint32_t)mr * ldx * 4);
+      if (k == 0) CL_TL(4);
+      for (int e = tid; e < mr * C4; e += kClThreads) {  // own rows: local copy
+        const int i = e / C4, j = (e % C4) * 4;
+        *reinterpret_cast<float4*>(Xf + (size_t)(o + i) * ldx + j) = *reinterpret_cast<const float4*>(Xn + (size_t)i * ldx + j);
+      }
+      __syncthreads();
+      cl_wait(&bars[2], par);
     }
-    __syncthreads();
-    cl_wait(&bars[2], par);
     if (k == 0) CL_TL(5);
   }
   CL_TL(6);

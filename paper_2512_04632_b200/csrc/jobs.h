@@ -185,6 +185,7 @@ constexpr int kClHdr = 64;                  // bytes before the float region (mb
 struct ClusterJob {
   const void* x;  // input, caller layout (m x n row-major)
   void* out;      // output, caller layout (may equal x)
+  float* xchg;    // cl_xchg_floats(M, N, C) floats of L2 scratch for the large row exchanges
   int32_t m, n, M, N, wide, pad;
 };
 struct ClLayout {
@@ -206,6 +207,19 @@ __host__ __device__ inline ClLayout cl_layout(int M, int N, int C = kClCtas) {
   o += L.N4;  // s
   L.floats = o;
   return L;
+}
+// Row exchanges of the FFMA cluster kernel: a phase whose matrix (the rows every CTA must
+// receive) has at least kClL2Bytes goes through an L2 buffer -- every CTA stores its rows once,
+// cluster barrier, every CTA bulk-loads the whole matrix -- instead of one DSMEM bulk copy per
+// peer (measured per SM: DSMEM ~13 B/cycle, L2 stores ~30, bulk L2 loads 55-65,
+// tools/xfer_probe.cu); the small exchanges would lose the extra barrier + L2 round trip
+// (64x27 bf16 33 -> 39 us all-L2), so only the large ones switch (graph replay, interleaved:
+// 128^2 fp32 59.5 -> 58.6 us, 64x216 fp32 41.1 -> 39.2, 256x64 fp32 43.6 -> 41.0, small bf16
+// unchanged).  Data movement only: the results are bitwise the same either way.
+constexpr uint32_t kClL2Bytes = 32768;
+__host__ __device__ inline size_t cl_xchg_floats(int M, int N, int C) {
+  const ClLayout L = cl_layout(M, N, C);
+  return 2 * (size_t)L.N4 * L.lda + (size_t)C * L.Mr * L.ldx;
 }
 __host__ __device__ inline bool cl_fits(int64_t M, int64_t N, int C = kClCtas) {
   return N >= 1 && N <= kClMaxN && M <= 4096 && cl_layout((int)M, (int)N, C).floats * 4 + kClHdr <= kClMaxSmem;
