@@ -18,7 +18,9 @@
 // instead of DSMEM (each CTA stores its rows once, cluster barrier, every CTA bulk-loads the
 // matrix): the same data, measured faster for the larger matrices only.
 // Arithmetic is fp32 FFMA; in bf16 mode every stored X, A, B value is rounded to bf16
-// (the same storage points as the tcgen05 path, reading R7).  The symmetric operands are
+// (the same storage points as the tcgen05 path, reading R7).  In fp32 mode, when a CTA's own
+// rows of X fit its B buffer, P and X fuse into X' = aX + b(XA) + c((XA)A) per row (reading
+// R16): B is never formed, one exchange per iteration fewer.  The symmetric operands are
 // read through their transposes (A_ik = A_ki, bitwise: the products are computed in the
 // same order for (i, k) and (k, i)), so every shared-memory operand load is a 16-byte
 // vector along a row.  Reductions have a fixed order: results are deterministic.
@@ -200,6 +202,9 @@ __global__ void __launch_bounds__(kClThreads, 1)
   // matrix [0, total_rows) is bulk-loaded into dst (the own rows included: identical values),
   // completing on barrier b.  A function of the shape: the same choice in every CTA.
   const bool l2_ab = (uint32_t)N * lda * 4 >= kClL2Bytes, l2_x = (uint32_t)M * ldx * 4 >= kClL2Bytes;
+  // fp32 mode whose own X rows fit the B buffer: no B phase (reading R16, below)
+  constexpr bool kF32 = sizeof(S) == 4;
+  const bool reassoc = kF32 && L.Mr <= L.N4;
   auto exchange = [&](int b, float* g, float* dst, const float* src, int row0, int nrows, int total_rows, int ld,
                       uint32_t par) {
     __syncthreads();  // every thread's epilogue rows are in src
@@ -337,6 +342,24 @@ __global__ void __launch_bounds__(kClThreads, 1)
       __syncthreads();
     }
     if (k == 0) CL_TL(2);
+    if (reassoc) {
+      // fp32 mode (reading R16): X_{k+1} = a X_k + b (X_k A_k) + c ((X_k A_k) A_k), Eq. 4-5 with
+      // the product associated per row -- this CTA's rows need only A_k, so B_k is never
+      // formed or exchanged (one row exchange per iteration fewer; no storage rounding in fp32)
+      if (tid == 0 && !l2_x) mbar_arrive_expect_tx(&bars[2], bytes_x);
+      cl_gemm<false>(Xf + (size_t)o * ldx, ldx, A, lda, mr, C4, N, [&](int i, int j, float4 v) {
+        *reinterpret_cast<float4*>(B + (size_t)i * lda + j) = v;  // Y = X_k A_k (own rows)
+      }, dbg);
+      __syncthreads();
+      if (k == 0) CL_TL(3);
+      cl_gemm<false>(B, lda, A, lda, mr, C4, N, [&](int i, int j, float4 v) {
+        const float4 xv = *reinterpret_cast<const float4*>(Xf + (size_t)(o + i) * ldx + j);
+        const float4 yv = *reinterpret_cast<const float4*>(B + (size_t)i * lda + j);
+        v.x = fmaf(a, xv.x, fmaf(b, yv.x, c * v.x)); v.y = fmaf(a, xv.y, fmaf(b, yv.y, c * v.y));
+        v.z = fmaf(a, xv.z, fmaf(b, yv.z, c * v.z)); v.w = fmaf(a, xv.w, fmaf(b, yv.w, c * v.w));
+        *reinterpret_cast<float4*>(Xn + (size_t)i * ldx + j) = v;
+      }, dbg);
+    } else {
     // ---- P: rows [r0, r0+nr) of B = b A + c A A  (L(i, kk) = A[i][kk] = A[kk][i])
     if (tid == 0 && !l2_ab) mbar_arrive_expect_tx(&bars[1], bytes_ab);
     cl_gemm<true>(A + r0, lda, A, lda, nr, C4, N, [&](int i, int j, float4 v) {
@@ -360,6 +383,7 @@ __global__ void __launch_bounds__(kClThreads, 1)
       v.z = rnd<S>(fmaf(a, xv.z, v.z)); v.w = rnd<S>(fmaf(a, xv.w, v.w));
       *reinterpret_cast<float4*>(Xn + (size_t)i * ldx + j) = v;
     }, dbg);
+    }
     if (l2_x) {  // (the exchange's cluster barrier also ends every read of this CTA's X_k rows)
       exchange(2, gX, Xf, Xn, o, mr, M, ldx, par);
       if (k == 0) CL_TL(4);
