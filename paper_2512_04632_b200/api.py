@@ -35,14 +35,37 @@ def _check_tensor(t: torch.Tensor, name: str = "tensor") -> None:
         raise ValueError(f"{name} must be contiguous (row-major)")
 
 
+class _Nothing:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        return False
+
+
+_NOTHING = _Nothing()
+
+
+def _on_device(dev: torch.device):
+    """torch.cuda.device(dev), skipped when dev is already current (a per-call host cost)."""
+    return _NOTHING if dev.index == torch.cuda.current_device() else torch.cuda.device(dev)
+
+
 def _stream(t: torch.Tensor | None = None) -> ctypes.c_void_p:
     dev = t.device if t is not None else None
     return ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
 
 
+_DEFAULT_COEFFS: dict = {}
+
+
 def _coeff_array(iters: int, coeffs, precond: str):
-    if coeffs is None:
-        coeffs = default_coeffs(iters, precond)
+    if coeffs is None:  # the default schedules are data: one ctypes array per (iters, precond)
+        key = (iters, precond)
+        arr = _DEFAULT_COEFFS.get(key)
+        if arr is None:
+            arr = _DEFAULT_COEFFS[key] = _coeff_array(iters, default_coeffs(iters, precond), precond)
+        return arr
     flat = [float(v) for t in coeffs for v in t] if len(coeffs) and hasattr(coeffs[0], "__len__") \
         else [float(v) for v in coeffs]
     if len(flat) != 3 * iters:
@@ -67,7 +90,7 @@ def orthogonalize(x: torch.Tensor, iters: int = 4, precond: str = "aol", coeffs=
     if x.numel() == 0:
         return x
     c = _coeff_array(iters, coeffs, precond)
-    with torch.cuda.device(x.device):
+    with _on_device(x.device):
         st = lib.ns_orthogonalize(ctypes.c_void_p(x.data_ptr()), m, n, batch, iters, c,
                                   PRECOND[precond], _dtype_code(x), _stream(x))
     check(st, "ns_orthogonalize")
@@ -115,7 +138,7 @@ def orthogonalize_list(xs: Sequence[torch.Tensor], out: Sequence[torch.Tensor] |
     mixed = compute is not None and compute != xs[0].dtype
     if mixed and (xs[0].dtype != torch.float32 or compute != torch.bfloat16 or peer_ptrs is not None):
         raise ValueError("mixed precision: fp32 matrices with compute=torch.bfloat16 (no peer stores)")
-    with torch.cuda.device(xs[0].device):
+    with _on_device(xs[0].device):
         if mixed:
             st = lib.ns_orthogonalize_cast(X, O, M, N, cnt, iters, c, PRECOND[precond], _stream(xs[0]))
             check(st, "ns_orthogonalize_cast")
