@@ -354,6 +354,35 @@ def test_many_matrices_one_call_bitwise():
         assert torch.equal(t, outs[k]), (k, shapes[k])
 
 
+@pytest.mark.parametrize("dtype,shapes,path", [
+    (torch.float32, [(128, 128), (64, 216), (256, 64)], 0),          # FFMA cluster kernel + L2 exchange scratch
+    (torch.bfloat16, [(1024, 128), (64, 576), (256, 2304)], 0),       # tcgen05 cluster kernel beside the step engine
+    (torch.bfloat16, [(1024, 128), (64, 576), (256, 2304), (768, 256)], 7),  # every one on the tcgen05 cluster kernel
+])
+def test_exact_workspace_covers_cluster_kernels(dtype, shapes, path):
+    """A caller workspace of exactly ns_workspace_size bytes is enough when matrices take the
+    cluster-resident kernels (their Gram-partial / A-image and row-exchange scratch), and the
+    results are bitwise those of library-owned workspace."""
+    xs = [torch.from_numpy(I.gaussian(m, n, seed=700 + i, bf16=dtype == torch.bfloat16)).to(dtype).cuda()
+          for i, (m, n) in enumerate(shapes)]
+    old = ns.set_path(path)
+    try:
+        ref = [torch.empty_like(x) for x in xs]
+        ns.orthogonalize_list(xs, out=ref, iters=4)
+        buf = torch.empty(ns.workspace_size(shapes, dtype=dtype), dtype=torch.uint8, device="cuda")
+        try:
+            ns.set_workspace(buf)
+            outs = [torch.empty_like(x) for x in xs]
+            ns.orthogonalize_list(xs, out=outs, iters=4)
+            torch.cuda.synchronize()
+        finally:
+            ns.set_workspace(None)
+        for r, o in zip(ref, outs):
+            assert torch.equal(r, o)
+    finally:
+        ns.set_path(old)
+
+
 def test_caller_owned_workspace():
     """ns_set_workspace: plans carve their workspace from a caller buffer (results bitwise
     equal to library-owned workspace); a too-small buffer fails with NS_ERR_WORKSPACE."""
