@@ -44,7 +44,10 @@ def assert_parity(out, ref, tol: float, what: str = "", model=None) -> dict:
     spreads its storage rounding through the Gram into many elements, and even ideal bf16
     arithmetic (bf16_model_out) exceeds the element bound there (Levy alpha = 1 at 4096 x 1024:
     1.05 x).  Pass that model's output as `model` and the element gate becomes 1.5 x the
-    model's own worst element ratio (when that is above 1).
+    model's own worst element ratio (when that is above 1); likewise the row / column gates
+    become 1.5 x the model's own worst row / column relF where that exceeds them (unconverged
+    large-coefficient schedules on small N: Polar-Express t = 3 at 256 x 2304, ideal bf16
+    worst row 0.12 against a global 0.05).
     Returns the measured values."""
     out = np.asarray(out, dtype=np.float64)
     ref = np.asarray(ref, dtype=np.float64)
@@ -61,6 +64,9 @@ def assert_parity(out, ref, tol: float, what: str = "", model=None) -> dict:
         ok = rn > 0
         worst = float((dn[ok] / rn[ok]).max()) if ok.any() else 0.0
         lim = tol if ln >= 64 else 2 * tol
+        if model is not None and ok.any():
+            dm = np.linalg.norm(np.asarray(model, dtype=np.float64) - ref, axis=axis)
+            lim = max(lim, 1.5 * float((dm[ok] / rn[ok]).max()))
         assert worst <= lim, f"{what}: worst {name} relF {worst:.3e} > {lim}"
         assert np.all(dn[~ok] == 0), f"{what}: {name} with zero reference is not zero"
         res[name] = worst
