@@ -65,16 +65,21 @@ def test_cluster_aol4(m, n, dtype):
         assert eg <= 1.05 * eo + (1e-6 if dtype == torch.float32 else 0.0), (eg, eo)
 
 
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32], ids=["bf16", "fp32"])
 @pytest.mark.parametrize("m,n", [(128, 128), (64, 576), (100, 37)])
 @pytest.mark.parametrize("precond,coeffs", [("frobenius", C.muon_plus(5)), ("aol", C.muon_plus(5)),
                                             ("none", C.turbo(4))])
-def test_cluster_preconds_and_odd_iters(m, n, precond, coeffs):
-    x = I.gaussian(m, n, seed=3)
+def test_cluster_preconds_and_odd_iters(m, n, precond, coeffs, dtype):
+    """Every preconditioner and an odd iteration count, bf16 and fp32 (fp32: the row-wise
+    X' = aX + b(XA) + c((XA)A) of reading R16 where it applies, 128^2 and 64x576)."""
+    x = I.gaussian(m, n, seed=3, bf16=dtype == torch.bfloat16)
     if precond == "none":
-        x = I.round_bf16(x / np.float32(4 * np.sqrt(max(m, n))))
-    out, launches = _run(x, coeffs, precond)
+        x = x / np.float32(4 * np.sqrt(max(m, n)))
+        if dtype == torch.bfloat16:
+            x = I.round_bf16(x)
+    out, launches = _run(x, coeffs, precond, dtype)
     assert launches == 1
-    assert_parity(out, oracle_run(x, coeffs, precond), BF16_TOL)
+    assert_parity(out, oracle_run(x, coeffs, precond), BF16_TOL if dtype == torch.bfloat16 else FP32_TOL)
 
 
 @pytest.mark.parametrize("dist", ["lowrank", "levy1.0", "levy1.5"])
