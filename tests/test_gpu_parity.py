@@ -665,3 +665,45 @@ def test_failed_second_plan_leaves_first_group_untouched():
         t = x.clone()
         ns.orthogonalize(t, iters=4)
         assert torch.equal(t, o)
+
+
+def test_concurrent_streams_distinct_lists():
+    """Thread-safety contract (turbo_ns.h): calls from several host threads, each on its own
+    stream with its own problem list (step engine, tcgen05 cluster kernel and FFMA cluster
+    kernel matrices mixed, so the internal side streams are shared), give bitwise the
+    results of the same calls made one at a time."""
+    import threading
+    lists = [[(768, 768), (1024, 128), (64, 216)], [(3072, 768), (256, 2304)], [(512, 512), (64, 576), (128, 128)],
+             [(2048, 256), (100, 37)]]
+    inputs = [[torch.from_numpy(I.gaussian(m, n, seed=900 + 10 * j + i)).to(torch.bfloat16).cuda()
+               for i, (m, n) in enumerate(shapes)] for j, shapes in enumerate(lists)]
+    ref = []
+    for xs in inputs:
+        outs = [torch.empty_like(x) for x in xs]
+        ns.orthogonalize_list(xs, out=outs, iters=4)
+        ref.append(outs)
+    torch.cuda.synchronize()
+    results = [None] * len(lists)
+    errors = []
+
+    def worker(j):
+        try:
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                outs = [torch.empty_like(x) for x in inputs[j]]
+                for _ in range(10):
+                    ns.orthogonalize_list(inputs[j], out=outs, iters=4)
+            s.synchronize()
+            results[j] = outs
+        except Exception as e:  # surfaced below
+            errors.append(e)
+
+    threads = [threading.Thread(target=worker, args=(j,)) for j in range(len(lists))]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errors, errors
+    for r, o in zip(ref, results):
+        for a, b in zip(r, o):
+            assert torch.equal(a, b)
