@@ -645,7 +645,10 @@ static ns_status build_plan(Plan& P, HostTables& H, DevCtx* dc, const float* coe
             J.sym = 1; J.P = J.Q = (int)mt.N; J.K = (int)mt.M;
             J.out = Am(mt); J.aux = nullptr; J.ld = mt.N;
             J.half = hs;  // A: lower-triangle blocks only (readers take the upper transposed)
-            if (k == 1 && use_part) { J.part = Part(mt); J.part_ld = mt.part_ld; }
+            if (k == 1 && use_part) {
+              J.part = Part(mt); J.part_ld = mt.part_ld;
+              J.part_sm = mt.part_ld <= kSeqPartials;  // slot-major for the lane-per-row sums
+            }
             if (mt.split) {  // partials only; the reduction launch writes A (and the AOL sums)
               J.split_ws = reinterpret_cast<float*>(ws + mt.split_off);
               J.split_stride = kSplitLd * kSplitLd;
@@ -703,7 +706,7 @@ static ns_status build_plan(Plan& P, HostTables& H, DevCtx* dc, const float* coe
             S.stride = kSplitLd * kSplitLd; S.ld = (int)kSplitLd;
             S.S = mt.split; S.N = (int)mt.N;
             S.A = Am(mt);
-            if (k == 1 && use_part) { S.part = Part(mt); S.part_ld = mt.part_ld; }
+            if (k == 1 && use_part) { S.part = Part(mt); S.part_ld = mt.part_ld; S.part_sm = mt.part_ld <= kSeqPartials; }
             S.row_start = red.rows;
             red.rows += mt.N;
             red.sj.push_back(S);
@@ -768,7 +771,7 @@ static ns_status build_plan(Plan& P, HostTables& H, DevCtx* dc, const float* coe
           PrecondJob J;
           std::memset(&J, 0, sizeof(J));
           J.A = Am(mt); J.s = Sv(mt); J.N = (int)mt.N; J.precond = (int)P.precond;
-          if (use_part) { J.part = Part(mt); J.part_ld = mt.part_ld; }
+          if (use_part) { J.part = Part(mt); J.part_ld = mt.part_ld; J.part_sm = mt.part_ld <= kSeqPartials; }
           J.half = P.simt ? 0 : hs;
           J.row_start = rows; J.seg_start = items;
           rows += mt.N;

@@ -51,10 +51,11 @@ struct GemmJob {
   int32_t s_by_row;    // XB: scale a*aux by s[p] (1) or s[q] (0)
   float a, b, c;
   // GRAM with AOL (iteration 1): per-tile |A0| row-sum partials, written once each (no
-  // atomics): part[i * part_ld + slot]; slots [0, ceil(N/64)) = direct 64-column blocks,
-  // [ceil(N/64), + ceil(N/32)) = mirrored 32-row blocks.  nullptr = not collected.
+  // atomics): part_ld slots per row -- [0, ceil(N/64)) direct 64-column blocks,
+  // [ceil(N/64), + ceil(N/32)) mirrored 32-row blocks -- at part_at(); nullptr = not collected.
   float* part;
   int32_t part_ld;
+  int32_t part_sm;  // 1: slot-major layout (see part_at)
   // XB of the last iteration, fused collective: also store every output tile into `npeer`
   // more destinations (peers' gather buffers over NVLink); tmPeer -> npeer consecutive
   // 32x32-box CUtensorMaps.
@@ -108,11 +109,20 @@ struct CastJob {
 // AOL rows with at most this many Gram-epilogue partial slots (N <= 1344) are summed by
 // one lane in slot order; larger ones by a warp tree (precond_rows.cuh).
 constexpr int kSeqPartials = 64;
+// Slot t of row i of an N-row partial array: row-major part[i * part_ld + t], or slot-major
+// part[t * N + i] (sm = 1: the plans' layout when part_ld <= kSeqPartials -- then the
+// preconditioner reads one row per lane, and consecutive lanes read consecutive floats; the
+// Gram epilogue's stores of a slot are coalesced the same way).  The single-step entry points
+// (nsx_gram / nsx_precondition) keep row-major.
+__host__ __device__ inline int64_t part_at(int part_ld, int sm, int N, int i, int t) {
+  return sm ? (int64_t)t * N + i : (int64_t)i * part_ld + t;
+}
 struct PrecondJob {
   void* A;          // N x N symmetric Gram, in place -> A1
   float* s;         // N
   const float* part;  // row-sum partials from the Gram epilogue (GemmJob::part) or nullptr
   int32_t part_ld;
+  int32_t part_sm;    // layout of part (part_at)
   int32_t half;       // A stored as lower-triangle 256-blocks: rescale only those
   int32_t N;
   int32_t precond;  // 1 Frobenius, 2 AOL
@@ -162,6 +172,7 @@ struct SplitJob {
   void* A;          // N x N, ld N, storage type of the plan
   float* part;
   int32_t part_ld;
+  int32_t part_sm;    // layout of part (part_at)
   int64_t row_start;  // prefix over jobs of N (one warp per row)
 };
 constexpr int kSplitMaxN = 256;

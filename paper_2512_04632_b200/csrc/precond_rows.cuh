@@ -41,7 +41,6 @@ __device__ __forceinline__ float warp_sum(float v) {
 __device__ __forceinline__ float aol_rowsum_partials(const PrecondJob& J, int i) {
   const int N = J.N, bi = i / 256;
   const int n1 = (N + 63) / 64, n2 = (N + 31) / 32;
-  const float* pr = J.part + (int64_t)i * J.part_ld;
   const int d_end = min(4 * (bi + 1), n1), m_beg = min(8 * (bi + 1), n2);
   // the row's slots as one list (direct ones, then mirrored ones), loaded up to 32 at a time and
   // added in list order (the zeros past the end add nothing): the same sum, bitwise, as a
@@ -53,7 +52,8 @@ __device__ __forceinline__ float aol_rowsum_partials(const PrecondJob& J, int i)
 #pragma unroll
     for (int e = 0; e < 32; ++e) {
       const int t = t0 + e;
-      v[e] = t < nd ? pr[t] : (t < nt ? pr[n1 + m_beg + (t - nd)] : 0.f);
+      v[e] = t < nd ? J.part[part_at(J.part_ld, J.part_sm, N, i, t)]
+                    : (t < nt ? J.part[part_at(J.part_ld, J.part_sm, N, i, n1 + m_beg + (t - nd))] : 0.f);
     }
 #pragma unroll
     for (int e = 0; e < 32; ++e) acc += v[e];
@@ -77,7 +77,8 @@ __device__ __forceinline__ void precond_row_s(const PrecondJob& J, int i, int la
       if (!isfinite(r)) fl |= 2u;
     }
   } else if (J.precond == 2 && J.part != nullptr) {
-    // many partials per row (large N): warp-parallel, fixed-order tree
+    // many partials per row (large N): warp-parallel, fixed-order tree (row-major partials:
+    // part_sm is only set where part_ld <= kSeqPartials)
     const int bi = i / 256;
     const int n1 = (J.N + 63) / 64, n2 = (J.N + 31) / 32;
     const float* pr = J.part + (int64_t)i * J.part_ld;

@@ -302,7 +302,7 @@ __global__ void __launch_bounds__(256)
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) rs += __shfl_xor_sync(0xffffffffu, rs, o);
-  if (J.part != nullptr && lane == 0) J.part[(int64_t)i * J.part_ld] = rs;
+  if (J.part != nullptr && lane == 0) J.part[part_at(J.part_ld, J.part_sm, J.N, i, 0)] = rs;
   if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(flags, 2u);
 }
 

@@ -112,7 +112,7 @@ struct Epi {
   const float* s;
   float a, b, c;
   float* part;
-  int part_ld;
+  int part_ld, part_sm;
   const uint8_t* tmPeer;
   int npeer;
   float diag_add;
@@ -130,7 +130,7 @@ __device__ __forceinline__ Epi load_epi(const GemmJob* __restrict__ J) {
   e.aux = reinterpret_cast<const uint16_t*>(J->aux);
   e.s = J->s;
   e.a = J->a; e.b = J->b; e.c = J->c;
-  e.part = J->part; e.part_ld = J->part_ld;
+  e.part = J->part; e.part_ld = J->part_ld; e.part_sm = J->part_sm;
   e.tmPeer = reinterpret_cast<const uint8_t*>(J->tmPeer); e.npeer = J->npeer;
   e.diag_add = J->diag_add;
   e.half = J->half;
@@ -591,13 +591,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                   fabsf(lo_bf(u.z)) + fabsf(hi_bf(u.z)) + fabsf(lo_bf(u.w)) + fabsf(hi_bf(u.w));
           }
           if (q + lane < E.Q && prow < E.P)
-            E.part[(int64_t)(q + lane) * E.part_ld + (E.Q + 63) / 64 + prow / 32] = cs;
+            E.part[part_at(E.part_ld, E.part_sm, E.P, q + lane, (E.Q + 63) / 64 + prow / 32)] = cs;
         }
         if (prof) { t1 = clock64(); EPC(6, t1 - t0); t0 = t1; }
       }
       if (E.part != nullptr && p < E.P) {
-        if (qh < E.Q) E.part[(int64_t)p * E.part_ld + qh / 64] = rsum;
-        if (G::kChunks > 2 && qh + 64 < E.Q) E.part[(int64_t)p * E.part_ld + qh / 64 + 1] = rsum1;
+        if (qh < E.Q) E.part[part_at(E.part_ld, E.part_sm, E.P, p, qh / 64)] = rsum;
+        if (G::kChunks > 2 && qh + 64 < E.Q) E.part[part_at(E.part_ld, E.part_sm, E.P, p, qh / 64 + 1)] = rsum1;
       }
       if (++as == 2) { as = 0; aphase ^= 1; }
     }
