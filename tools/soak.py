@@ -28,38 +28,41 @@ fails = 0
 for case in range(a.cases):
     cnt = int(rng.integers(1, 6))
     shapes = [(int(rng.choice(DIMS)), int(rng.choice(DIMS))) for _ in range(cnt)]
-    dtype = torch.bfloat16 if rng.random() < 0.8 else torch.float32
+    u = rng.random()
+    dtype = torch.bfloat16 if u < 0.7 else torch.float32
+    cast = 0.7 <= u < 0.85  # fp32 matrices, bf16 compute (ns_orthogonalize_cast)
     precond = ["aol", "frobenius", "none"][int(rng.integers(0, 3))]
     iters = int(rng.integers(1, 6))
     coeffs = C.turbo(iters) if precond == "aol" else C.muon_plus(iters)
     path = int(rng.choice([0, 4, 5, 7]))
     xs_np = []
     for i, (m, n) in enumerate(shapes):
-        x = I.gaussian(m, n, seed=int(rng.integers(0, 1 << 30)), bf16=dtype == torch.bfloat16)
+        x = I.gaussian(m, n, seed=int(rng.integers(0, 1 << 30)), bf16=dtype == torch.bfloat16 or cast)
         if precond == "none":
             x = (x / np.float32(4 * np.sqrt(max(m, n)))).astype(np.float32)
-            if dtype == torch.bfloat16:
+            if dtype == torch.bfloat16 or cast:  # cast: bf16-exact values, so the oracle sees the GPU's input
                 x = I.round_bf16(x)
         xs_np.append(x)
     old = ns.set_path(path)
     try:
         xs = [torch.from_numpy(x).to(dtype).cuda() for x in xs_np]
         grouped = [torch.empty_like(x) for x in xs]
-        ns.orthogonalize_list(xs, out=grouped, iters=iters, precond=precond, coeffs=coeffs)
+        kw = dict(iters=iters, precond=precond, coeffs=coeffs, compute=torch.bfloat16 if cast else None)
+        ns.orthogonalize_list(xs, out=grouped, **kw)
         again = [torch.empty_like(x) for x in xs]
-        ns.orthogonalize_list(xs, out=again, iters=iters, precond=precond, coeffs=coeffs)  # graph replay
+        ns.orthogonalize_list(xs, out=again, **kw)  # graph replay
         singles = []
         for x in xs:
             o = torch.empty_like(x)
-            ns.orthogonalize_list([x], out=[o], iters=iters, precond=precond, coeffs=coeffs)
+            ns.orthogonalize_list([x], out=[o], **kw)
             singles.append(o)
         torch.cuda.synchronize()
         flags = ns.read_flags()
     finally:
         ns.set_path(old)
-    tol = 2e-2 if dtype == torch.bfloat16 else 1e-4
+    tol = 2e-2 if (dtype == torch.bfloat16 or cast) else 1e-4
     for i, (x, g, r, s1) in enumerate(zip(xs_np, grouped, again, singles)):
-        msg = f"case {case} path {path} {dtype} {precond} T={iters} {shapes[i]} in {shapes}"
+        msg = f"case {case} path {path} {dtype}{' cast' if cast else ''} {precond} T={iters} {shapes[i]} in {shapes}"
         if not torch.equal(g, r):
             print("REPEAT MISMATCH", msg, flush=True)
             fails += 1
