@@ -199,7 +199,8 @@ struct Phase {
   int64_t total;    // tiles (GEMM/SIMT) or items (PRECOND)
   int64_t total_rows;
   bool vec8;
-  bool lane_rows = false;  // PH_PRECOND: AOL partials, every part_ld <= kSeqPartials
+  bool lane_rows = false;  // PH_PRECOND: AOL from the Gram partials for every job
+  int row_kinds = 0;       // PH_PRECOND: OR of precond_lane_kind over the jobs
   int gemm_kind;  // profiling kind: 0 GRAM, 2 POLY, 3 XB
   size_t tiles_off = 0;   // offset of the TaskDesc list (PH_GEMM)
   int64_t max_tiles = 0;  // tiles of the GEMM step
@@ -647,7 +648,7 @@ static ns_status build_plan(Plan& P, HostTables& H, DevCtx* dc, const float* coe
             J.half = hs;  // A: lower-triangle blocks only (readers take the upper transposed)
             if (k == 1 && use_part) {
               J.part = Part(mt); J.part_ld = mt.part_ld;
-              J.part_sm = mt.part_ld <= kSeqPartials;  // slot-major for the lane-per-row sums
+              J.part_sm = precond_part_sm(mt.part_ld);  // precond_rows.cuh: per-N summation
             }
             if (mt.split) {  // partials only; the reduction launch writes A (and the AOL sums)
               J.split_ws = reinterpret_cast<float*>(ws + mt.split_off);
@@ -706,7 +707,7 @@ static ns_status build_plan(Plan& P, HostTables& H, DevCtx* dc, const float* coe
             S.stride = kSplitLd * kSplitLd; S.ld = (int)kSplitLd;
             S.S = mt.split; S.N = (int)mt.N;
             S.A = Am(mt);
-            if (k == 1 && use_part) { S.part = Part(mt); S.part_ld = mt.part_ld; S.part_sm = mt.part_ld <= kSeqPartials; }
+            if (k == 1 && use_part) { S.part = Part(mt); S.part_ld = mt.part_ld; S.part_sm = precond_part_sm(mt.part_ld); }
             S.row_start = red.rows;
             red.rows += mt.N;
             red.sj.push_back(S);
@@ -771,7 +772,7 @@ static ns_status build_plan(Plan& P, HostTables& H, DevCtx* dc, const float* coe
           PrecondJob J;
           std::memset(&J, 0, sizeof(J));
           J.A = Am(mt); J.s = Sv(mt); J.N = (int)mt.N; J.precond = (int)P.precond;
-          if (use_part) { J.part = Part(mt); J.part_ld = mt.part_ld; J.part_sm = mt.part_ld <= kSeqPartials; }
+          if (use_part) { J.part = Part(mt); J.part_ld = mt.part_ld; J.part_sm = precond_part_sm(mt.part_ld); }
           J.half = P.simt ? 0 : hs;
           J.row_start = rows; J.seg_start = items;
           rows += mt.N;
@@ -860,8 +861,10 @@ static ns_status build_plan(Plan& P, HostTables& H, DevCtx* dc, const float* coe
         ph.total_rows = st.rows;
         ph.vec8 = st.vec8;
         ph.lane_rows = true;
-        for (const PrecondJob& pj : st.pj)
-          ph.lane_rows = ph.lane_rows && pj.precond == 2 && pj.part != nullptr && pj.part_ld <= kSeqPartials;
+        for (const PrecondJob& pj : st.pj) {
+          ph.lane_rows = ph.lane_rows && pj.precond == 2 && pj.part != nullptr;
+          if (pj.part != nullptr) ph.row_kinds |= precond_lane_kind(pj.part_ld);
+        }
         P.phases.push_back(ph);
       }
     }
@@ -1003,7 +1006,7 @@ static ns_status enqueue_plan(Plan& P, DevCtx* dc, cudaStream_t stream) {
         ProfScope ps(1, stream);
         CU_TRY(launch_precondition(reinterpret_cast<const PrecondJob*>(dbase + ph.dev_off), ph.njobs,
                                    ph.total_rows, ph.total, ph.vec8, P.dtype == NS_BF16, P.barrier,
-                                   dc->flags, ph.lane_rows, stream));
+                                   dc->flags, ph.lane_rows ? 1 | ph.row_kinds : 0, stream));
         ++g_launches;
         break;
       }
@@ -1869,14 +1872,15 @@ ns_status nsx_precondition(void* A, int64_t N, ns_precond precond, const float* 
       return fail(NS_ERR_INVALID_VALUE, "partials are AOL row sums of a bf16 Gram");
     J.part = part; J.part_ld = part_ld_for(N);
   }
-  const bool lane_rows = part && J.part_ld <= kSeqPartials;
+  const bool lane_rows = part != nullptr;
   void* dmem = nullptr;
   CU_TRY(cudaMalloc(&dmem, 256 + sizeof(J)));
   CU_TRY(cudaMemset(dmem, 0, 256));  // grid-barrier words
   CU_TRY(cudaMemcpy(reinterpret_cast<uint8_t*>(dmem) + 256, &J, sizeof(J), cudaMemcpyHostToDevice));
   cudaError_t e = launch_precondition(reinterpret_cast<const PrecondJob*>(reinterpret_cast<uint8_t*>(dmem) + 256), 1,
                                       N, precond_segments((int)N, 0), vec8, dtype == NS_BF16,
-                                      reinterpret_cast<unsigned*>(dmem), dc->flags, lane_rows, strm);
+                                      reinterpret_cast<unsigned*>(dmem), dc->flags,
+                                      lane_rows ? 1 | precond_lane_kind(J.part_ld) : 0, strm);
   ++g_launches;
   cudaError_t e2 = cudaStreamSynchronize(strm);
   cudaFree(dmem);

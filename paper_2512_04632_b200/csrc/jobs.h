@@ -107,8 +107,13 @@ struct CastJob {
 
 // Per-matrix descriptor for the preconditioning kernel (AOL / Frobenius).
 // AOL rows with at most this many Gram-epilogue partial slots (N <= 1344) are summed by
-// one lane in slot order; larger ones by a warp tree (precond_rows.cuh).
+// one lane in slot order; longer ones by four lanes or a warp (precond_rows.cuh
+// kQuarterPartials).
 constexpr int kSeqPartials = 64;
+constexpr int kQuarterPartials = 256;  // four lanes per row up to here, a warp per row beyond
+// Layout of a plan's partials (part_at): slot-major where the rows are summed by one or four
+// lanes (consecutive rows in consecutive lanes), row-major for the warp-per-row sums.
+__host__ __device__ inline int precond_part_sm(int part_ld) { return part_ld <= kQuarterPartials ? 1 : 0; }
 // Slot t of row i of an N-row partial array: row-major part[i * part_ld + t], or slot-major
 // part[t * N + i] (sm = 1: the plans' layout when part_ld <= kSeqPartials -- then the
 // preconditioner reads one row per lane, and consecutive lanes read consecutive floats; the

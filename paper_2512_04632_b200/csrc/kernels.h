@@ -35,7 +35,12 @@ cudaError_t launch_simt_gemm(const SimtJob* d_jobs, int njobs, int64_t total_til
 // runs one lane per row (precond_rows.cuh).
 cudaError_t launch_precondition(const PrecondJob* d_jobs, int njobs, int64_t total_rows,
                                 int64_t total_segs, bool vec8, bool is_bf16,
-                                unsigned* d_barrier, uint32_t* d_flags, bool lane_rows, cudaStream_t stream);
+                                unsigned* d_barrier, uint32_t* d_flags, int lane_mode, cudaStream_t stream);
+// lane_mode: bit 0 = AOL from the Gram partials for every job (lane loops); with it, bits
+// 3 / 4 / 5 = some job's rows are summed by four lanes / a warp / one lane (precond_rows.cuh)
+__host__ __device__ inline int precond_lane_kind(int part_ld) {
+  return part_ld <= kSeqPartials ? 32 : (part_ld <= kQuarterPartials ? 8 : 16);
+}
 
 // Split-K Gram reduction (simt.cu): one warp per row of every job (bf16 storage).
 cudaError_t launch_split_reduce(const SplitJob* d_jobs, int njobs, int64_t total_rows, uint32_t* d_flags,

@@ -61,52 +61,71 @@ __device__ __forceinline__ float aol_rowsum_partials(const PrecondJob& J, int i)
   return acc;
 }
 
+// How the AOL row sums of a matrix are formed from its partials (a function of N alone,
+// reading R11): part_ld <= kSeqPartials (N <= 1344) one lane per row, slots in order;
+// <= kQuarterPartials (N <= 5440) four lanes per row, a contiguous quarter of the slot list
+// each, the quarters added in order (both slot-major: consecutive rows in consecutive lanes);
+// beyond, one warp per row over the row-major slots, lane-strided and a fixed tree.  (Measured:
+// four lanes beat the warp tree at 2048^2 / 4096^2, lose at 8192^2, where every row is long
+// and a warp per row keeps its loads in whole 128-byte lines.)
+// (kQuarterPartials, precond_part_sm: jobs.h)
+// Quarter qt of the slot list of row i (kSeqPartials < part_ld <= kQuarterPartials): list
+// positions [qt c, min(nt, (qt + 1) c)), c = ceil(nt / 4), summed in order, 32 loads in flight.
+__device__ __forceinline__ float aol_rowsum_quarter(const PrecondJob& J, int i, int qt) {
+  const int N = J.N, bi = i / 256;
+  const int n1 = (N + 63) / 64, n2 = (N + 31) / 32;
+  const int d_end = min(4 * (bi + 1), n1), m_beg = min(8 * (bi + 1), n2);
+  const int nd = d_end, nt = d_end + (n2 - m_beg);
+  const int c = (nt + 3) / 4, t_beg = qt * c, t_end = min(nt, t_beg + c);
+  float acc = 0.f;
+  for (int t0 = t_beg; t0 < t_end; t0 += 32) {
+    float v[32];
+#pragma unroll
+    for (int e = 0; e < 32; ++e) {
+      const int t = t0 + e;
+      v[e] = t < t_end ? (t < nd ? J.part[part_at(J.part_ld, J.part_sm, N, i, t)]
+                                 : J.part[part_at(J.part_ld, J.part_sm, N, i, n1 + m_beg + (t - nd))])
+                       : 0.f;
+    }
+#pragma unroll
+    for (int e = 0; e < 32; ++e) acc += v[e];
+  }
+  return acc;
+}
+// Warp-wide row sum (part_ld > kQuarterPartials, row-major partials): lane k sums slots k,
+// k + 32, ... of the list in that order, then a fixed xor tree; every lane returns the sum.
+__device__ __forceinline__ float aol_rowsum_tree(const PrecondJob& J, int i, int lane) {
+  const int bi = i / 256;
+  const int n1 = (J.N + 63) / 64, n2 = (J.N + 31) / 32;
+  const float* pr = J.part + (int64_t)i * J.part_ld;
+  const int d_end = min(4 * (bi + 1), n1), m_beg = min(8 * (bi + 1), n2);
+  float acc = 0.f;
+  for (int k0 = lane; k0 < d_end; k0 += 256) {
+    float v[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) v[e] = (k0 + 32 * e < d_end) ? pr[k0 + 32 * e] : 0.f;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) acc += v[e];
+  }
+  for (int k0 = m_beg + lane; k0 < n2; k0 += 256) {
+    float v[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) v[e] = (k0 + 32 * e < n2) ? pr[n1 + k0 + 32 * e] : 0.f;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) acc += v[e];
+  }
+  return warp_sum(acc);
+}
+
 // Phase 1 for row i: s_i (AOL, Eq. 8) or, for row 0, the whole Frobenius s (Eq. 10).
 // Fixed-order reductions: deterministic.
 template <typename T, bool VEC8>
 __device__ __forceinline__ void precond_row_s(const PrecondJob& J, int i, int lane, uint32_t& fl) {
   const T* __restrict__ A = reinterpret_cast<const T*>(J.A);
   const int N = J.N;
-  if (J.precond == 2 && J.part != nullptr && J.part_ld <= kSeqPartials) {
-    // AOL from the Gram epilogue's partials, few per row: one lane sums them in slot order
-    // (the same order as the standalone kernel's lane-per-row loop: bitwise equal s)
-    if (lane == 0) {
-      const float r = aol_rowsum_partials(J, i);
-      J.s[i] = r > 0.f ? rsqrtf(r) : 0.f;
-      if (!(r > 0.f)) fl |= 1u;
-      if (!isfinite(r)) fl |= 2u;
-    }
-  } else if (J.precond == 2 && J.part != nullptr) {
-    // many partials per row (large N): warp-parallel, fixed-order tree (row-major partials:
-    // part_sm is only set where part_ld <= kSeqPartials)
-    const int bi = i / 256;
-    const int n1 = (J.N + 63) / 64, n2 = (J.N + 31) / 32;
-    const float* pr = J.part + (int64_t)i * J.part_ld;
-    const int d_end = min(4 * (bi + 1), n1), m_beg = min(8 * (bi + 1), n2);
-    // per lane: slots lane, lane + 32, ... loaded 8 at a time and added in that order
-    // (fixed order: deterministic)
-    float acc = 0.f;
-    for (int k0 = lane; k0 < d_end; k0 += 256) {
-      float v[8];
-#pragma unroll
-      for (int e = 0; e < 8; ++e) v[e] = (k0 + 32 * e < d_end) ? pr[k0 + 32 * e] : 0.f;
-#pragma unroll
-      for (int e = 0; e < 8; ++e) acc += v[e];
-    }
-    for (int k0 = m_beg + lane; k0 < n2; k0 += 256) {
-      float v[8];
-#pragma unroll
-      for (int e = 0; e < 8; ++e) v[e] = (k0 + 32 * e < n2) ? pr[n1 + k0 + 32 * e] : 0.f;
-#pragma unroll
-      for (int e = 0; e < 8; ++e) acc += v[e];
-    }
-    const float r = warp_sum(acc);
-    if (lane == 0) {
-      J.s[i] = r > 0.f ? rsqrtf(r) : 0.f;
-      if (!(r > 0.f)) fl |= 1u;
-      if (!isfinite(r)) fl |= 2u;
-    }
-  } else if (J.precond == 2) {  // AOL from A0 itself: s_i = (sum_j |A0_ij|)^(-1/2)
+  // (AOL from the Gram epilogue's partials runs in the kernel's lane loop instead:
+  // aol_rowsum_partials / aol_rowsum_quarter / aol_rowsum_tree)
+  if (J.precond == 2) {  // AOL from A0 itself: s_i = (sum_j |A0_ij|)^(-1/2)
     float acc = 0.f;
     const T* Ai = A + (int64_t)i * N;
     if (VEC8 && sizeof(T) == 2) {

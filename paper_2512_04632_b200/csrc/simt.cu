@@ -159,7 +159,8 @@ template <typename T, bool VEC8>
 __global__ void __launch_bounds__(256, 3)
     precondition_kernel(const PrecondJob* __restrict__ jobs, int njobs, int64_t total_rows,
                         int64_t total_segs, unsigned* barrier, uint32_t* __restrict__ flags, int mode) {
-  // mode bit 0: AOL from partials with one lane per row; bits 1 / 2 (TNS_PRE_DBG, measurement
+  // mode bit 0: AOL from the Gram partials (lane loops), bits 3 / 4 / 5: the launch has rows
+  // summed by four lanes / a warp / one lane (host flags); bits 1 / 2 (TNS_PRE_DBG, measurement
   // only): skip phase 1 / phase 2
   const int lane_rows = mode & 1;
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
@@ -172,19 +173,68 @@ __global__ void __launch_bounds__(256, 3)
   const int64_t per = (total_rows + nwarps - 1) / nwarps;
   const int64_t r_beg = gwarp * per, r_end = min(total_rows, r_beg + per);
   if (mode & 2) {
-  } else if (lane_rows) {  // AOL from partials, every job with part_ld <= kSeqPartials
-    // AOL from partials: one LANE per row (<= 64 independent loads each), 32 rows per warp
-    // at a time -- the row sums are short, so rows, not columns, carry the parallelism
-    for (int64_t row0 = r_beg; row0 < r_end; row0 += 32) {
-      const int64_t row = row0 + lane;
-      if (row < r_end) {
-        const int jb = find_pjob(jobs, njobs, row);
+  } else if (lane_rows) {  // AOL from the Gram epilogue's partials (every job)
+    // Short partial rows (part_ld <= kSeqPartials, N <= 1344): one LANE per row, 32 rows per
+    // warp at a time -- the row sums are short, so rows, not columns, carry the parallelism.
+    // Longer ones: four lanes per row or a warp per row (precond_rows.cuh kQuarterPartials).
+    // Which summation a row gets depends on its matrix's N alone (reading R11); the host
+    // flags which kinds the launch holds (bit 5 one lane, bit 3 four lanes, bit 4 a warp per
+    // row), and only those loops run.
+    if (mode & 32) {
+      for (int64_t row0 = r_beg; row0 < r_end; row0 += 32) {
+        const int64_t row = row0 + lane;
+        if (row < r_end) {
+          const int jb = find_pjob(jobs, njobs, row);
+          const PrecondJob& J = jobs[jb];
+          if (J.part_ld <= kSeqPartials) {
+            const int i = (int)(row - J.row_start);
+            const float r = aol_rowsum_partials(J, i);
+            J.s[i] = r > 0.f ? rsqrtf(r) : 0.f;
+            if (!(r > 0.f)) fl |= 1u;
+            if (!isfinite(r)) fl |= 2u;
+          }
+        }
+      }
+    }
+    const unsigned kinds = ((mode & 8) ? 1u : 0u) | ((mode & 16) ? 2u : 0u);
+    if (kinds & 1u) {  // four lanes per row, 8 rows at a time
+      const int qt = lane >> 3;
+      for (int64_t row0 = r_beg; row0 < r_end; row0 += 8) {
+        const int64_t row = row0 + (lane & 7);
+        float v = 0.f;
+        bool mine = false;
+        int jb = 0, i = 0;
+        if (row < r_end) {
+          jb = find_pjob(jobs, njobs, row);
+          mine = jobs[jb].part_ld > kSeqPartials && jobs[jb].part_ld <= kQuarterPartials;
+          i = (int)(row - jobs[jb].row_start);
+          if (mine) v = aol_rowsum_quarter(jobs[jb], i, qt);
+        }
+        const float q1 = __shfl_sync(0xffffffffu, v, (lane & 7) + 8);   // quarters 1..3 of
+        const float q2 = __shfl_sync(0xffffffffu, v, (lane & 7) + 16);  // this lane's row,
+        const float q3 = __shfl_sync(0xffffffffu, v, (lane & 7) + 24);  // added in order
+        if (mine && qt == 0) {
+          const float r = ((v + q1) + q2) + q3;
+          const PrecondJob& J = jobs[jb];
+          J.s[i] = r > 0.f ? rsqrtf(r) : 0.f;
+          if (!(r > 0.f)) fl |= 1u;
+          if (!isfinite(r)) fl |= 2u;
+        }
+      }
+    }
+    if (kinds & 2u) {  // one warp per row
+      int jb = find_pjob(jobs, njobs, r_beg);
+      for (int64_t row = r_beg; row < r_end; ++row) {
+        while (jb + 1 < njobs && jobs[jb + 1].row_start <= row) ++jb;
         const PrecondJob& J = jobs[jb];
+        if (J.part_ld <= kQuarterPartials) continue;
         const int i = (int)(row - J.row_start);
-        const float r = aol_rowsum_partials(J, i);
-        J.s[i] = r > 0.f ? rsqrtf(r) : 0.f;
-        if (!(r > 0.f)) fl |= 1u;
-        if (!isfinite(r)) fl |= 2u;
+        const float r = aol_rowsum_tree(J, i, lane);
+        if (lane == 0) {
+          J.s[i] = r > 0.f ? rsqrtf(r) : 0.f;
+          if (!(r > 0.f)) fl |= 1u;
+          if (!isfinite(r)) fl |= 2u;
+        }
       }
     }
   } else if (r_beg < r_end) {
@@ -252,8 +302,9 @@ static cudaError_t launch_precond_t(const PrecondJob* d_jobs, int njobs, int64_t
   cfg.attrs = attr;
   cfg.numAttrs = 2;
   static const int dbg = [] { const char* e = getenv("TNS_PRE_DBG"); return e ? atoi(e) : 0; }();
-  const int lr = (dbg & 8) ? 0 : lane_rows;  // bit 8: warp per row even for short partial rows (A/B)
-  return cudaLaunchKernelEx(&cfg, kern, d_jobs, njobs, total_rows, total_segs, d_barrier, d_flags, lr | (dbg & 6));
+  const int lr = lane_rows;
+  return cudaLaunchKernelEx(&cfg, kern, d_jobs, njobs, total_rows, total_segs, d_barrier, d_flags,
+                            lr | (dbg & 6));
 }
 
 // ------------------------------------------------------------------------------ split-K Gram
@@ -323,8 +374,8 @@ cudaError_t launch_split_reduce(const SplitJob* d_jobs, int njobs, int64_t total
 
 cudaError_t launch_precondition(const PrecondJob* d_jobs, int njobs, int64_t total_rows,
                                 int64_t total_segs, bool vec8, bool is_bf16, unsigned* d_barrier,
-                                uint32_t* d_flags, bool lane_rows, cudaStream_t stream) {
-  const int lr = lane_rows ? 1 : 0;
+                                uint32_t* d_flags, int lane_mode, cudaStream_t stream) {
+  const int lr = lane_mode & (1 | 8 | 16 | 32);
   if (is_bf16) {
     return vec8 ? launch_precond_t<uint16_t, true>(d_jobs, njobs, total_rows, total_segs, d_barrier, d_flags, lr, stream)
                 : launch_precond_t<uint16_t, false>(d_jobs, njobs, total_rows, total_segs, d_barrier, d_flags, lr, stream);
