@@ -62,8 +62,9 @@ def test_square_sweep_full_size(n):
 
 @pytest.mark.parametrize("m,n", [(1536, 1536), (1400, 3000)])
 def test_aol_large_n_partials_tree(m, n):
-    """N >= 1376 (part_ld > 64): the AOL row sums run the warp-tree branch; a wide shape
-    (m < n, orientation by descriptors) with a ragged last 256-block (1400 = 5 * 256 + 120)."""
+    """N >= 1376 (part_ld > 64): the AOL row sums run the four-lanes-per-row branch (the
+    warp-per-row one, N > 5440, runs in the 8192^2 tests); a wide shape (m < n, orientation by
+    descriptors) with a ragged last 256-block (1400 = 5 * 256 + 120)."""
     x = I.gaussian(m, n, seed=I.matrix_seed(13, m + n))
     out = _gpu(x, C.turbo(4), "aol")
     ref = oracle_run(x, C.turbo(4), "aol")
@@ -110,8 +111,8 @@ def test_levy_alpha1_gpt2_medium_shape():
 @pytest.mark.parametrize("m,n", [(768, 512), (2048, 1536), (1000, 2048)])
 def test_precondition_from_gram_partials(m, n):
     """nsx_gram emits the iteration-1 Gram epilogue's AOL partials; nsx_precondition sums
-    them (one lane per row while N <= 1344, a warp tree above) exactly as the production
-    launch does.  s must equal the oracle's Eq. 8 on the GPU's stored bf16 A0 (fp32 sums of
+    them (one lane per row while N <= 1344, four lanes per row up to N = 5440, a warp per row
+    above) exactly as the production launch does.  s must equal the oracle's Eq. 8 on the GPU's stored bf16 A0 (fp32 sums of
     the same bf16 values: relative 1e-5), and A1 = diag(s) A0 diag(s) rounded once."""
     x = I.gaussian(m, n, seed=I.matrix_seed(16, m + n))
     t = torch.from_numpy(x).to(torch.bfloat16).cuda()
