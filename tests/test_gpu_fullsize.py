@@ -5,7 +5,7 @@
   Muon+ comparator (Frobenius, T = 5), element by element against the fp64 oracle (global,
   per-row, per-column and max-abs gates, tests/helpers.assert_parity) and the polar error
   of both against the exact polar factor (X (X^T X)^(-1/2) via syevd at these
-  sizes, oracle.polar_exact_gram).  N >= 1376 runs the warp-tree branch of the AOL row-sum
+  sizes, oracle.polar_exact_gram).  N >= 1376 runs the four-lane (and at 8192^2 the warp-per-row) branch of the AOL row-sum
   reduction over the Gram epilogue's partials (precond_rows.cuh) and, at 8192^2, the
   32-block partial layout.
 * Polar-Express schedules t = 1..9 (Fig. 4, App. D; reading R14):
