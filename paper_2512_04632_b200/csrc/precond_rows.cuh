@@ -117,6 +117,42 @@ __device__ __forceinline__ float aol_rowsum_tree(const PrecondJob& J, int i, int
   return warp_sum(acc);
 }
 
+// Two rows of one matrix at once (the loads of both in flight together); each row's sum is
+// formed exactly as aol_rowsum_tree forms it (same per-lane order, same tree).
+__device__ __forceinline__ void aol_rowsum_tree2(const PrecondJob& J, int i0, int i1, int lane, float& r0, float& r1) {
+  const int n1 = (J.N + 63) / 64, n2 = (J.N + 31) / 32;
+  const float* p0 = J.part + (int64_t)i0 * J.part_ld;
+  const float* p1 = J.part + (int64_t)i1 * J.part_ld;
+  const int b0 = i0 / 256, b1 = i1 / 256;
+  const int d0 = min(4 * (b0 + 1), n1), m0 = min(8 * (b0 + 1), n2);
+  const int d1 = min(4 * (b1 + 1), n1), m1 = min(8 * (b1 + 1), n2);
+  float a0 = 0.f, a1 = 0.f;
+  for (int k0 = lane; k0 < max(d0, d1); k0 += 256) {
+    float v0[8], v1[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      v0[e] = (k0 + 32 * e < d0) ? p0[k0 + 32 * e] : 0.f;
+      v1[e] = (k0 + 32 * e < d1) ? p1[k0 + 32 * e] : 0.f;
+    }
+#pragma unroll
+    for (int e = 0; e < 8; ++e) { a0 += v0[e]; a1 += v1[e]; }
+  }
+  // the mirrored slots: each row walks its own range m.. n2 in steps of 256 from m + lane
+  for (int j = 0; m0 + lane + j < n2 || m1 + lane + j < n2; j += 256) {
+    float v0[8], v1[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const int k0 = m0 + lane + j + 32 * e, k1 = m1 + lane + j + 32 * e;
+      v0[e] = (k0 < n2) ? p0[n1 + k0] : 0.f;
+      v1[e] = (k1 < n2) ? p1[n1 + k1] : 0.f;
+    }
+#pragma unroll
+    for (int e = 0; e < 8; ++e) { a0 += v0[e]; a1 += v1[e]; }
+  }
+  r0 = warp_sum(a0);
+  r1 = warp_sum(a1);
+}
+
 // Phase 1 for row i: s_i (AOL, Eq. 8) or, for row 0, the whole Frobenius s (Eq. 10).
 // Fixed-order reductions: deterministic.
 template <typename T, bool VEC8>

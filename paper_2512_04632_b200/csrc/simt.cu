@@ -222,19 +222,28 @@ __global__ void __launch_bounds__(256, 3)
         }
       }
     }
-    if (kinds & 2u) {  // one warp per row
+    if (kinds & 2u) {  // one warp per row (two rows of a matrix at a time)
       int jb = find_pjob(jobs, njobs, r_beg);
-      for (int64_t row = r_beg; row < r_end; ++row) {
+      for (int64_t row = r_beg; row < r_end;) {
         while (jb + 1 < njobs && jobs[jb + 1].row_start <= row) ++jb;
         const PrecondJob& J = jobs[jb];
-        if (J.part_ld <= kQuarterPartials) continue;
+        if (J.part_ld <= kQuarterPartials) { ++row; continue; }
         const int i = (int)(row - J.row_start);
-        const float r = aol_rowsum_tree(J, i, lane);
-        if (lane == 0) {
-          J.s[i] = r > 0.f ? rsqrtf(r) : 0.f;
-          if (!(r > 0.f)) fl |= 1u;
-          if (!isfinite(r)) fl |= 2u;
+        float r[2];
+        int nr = 1;
+        if (row + 1 < r_end && i + 1 < J.N) {
+          aol_rowsum_tree2(J, i, i + 1, lane, r[0], r[1]);
+          nr = 2;
+        } else {
+          r[0] = aol_rowsum_tree(J, i, lane);
         }
+        if (lane == 0)
+          for (int u = 0; u < nr; ++u) {
+            J.s[i + u] = r[u] > 0.f ? rsqrtf(r[u]) : 0.f;
+            if (!(r[u] > 0.f)) fl |= 1u;
+            if (!isfinite(r[u])) fl |= 2u;
+          }
+        row += nr;
       }
     }
   } else if (r_beg < r_end) {
