@@ -50,6 +50,26 @@ def test_invalid_arguments_rejected_on_host():
     assert lib.ns_last_error()
 
 
+def test_call_limits_rejected_on_host():
+    """Header limits checked before anything touches the device (tile words pack
+    the job index in 20 bits): 2^20 matrices in one call, a matrix pointer not aligned to
+    its element size, a dimension beyond 2^30."""
+    import numpy as np
+    from paper_2512_04632_b200._lib import NS_ERR_INVALID_VALUE, NS_ERR_NOT_SUPPORTED, lib
+    c = (ctypes.c_float * 12)(*([1.0] * 12))
+    cnt = 1 << 20
+    ptrs = np.full(cnt, 0x1000, dtype=np.uint64)
+    dims = np.full(cnt, 8, dtype=np.int64)
+    X = ptrs.ctypes.data_as(ctypes.POINTER(ctypes.c_void_p))
+    M = dims.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))
+    assert lib.ns_orthogonalize_batched(X, None, M, M, cnt, 4, c, 2, 0, None) == NS_ERR_NOT_SUPPORTED
+    assert b"2^20" in lib.ns_last_error()
+    odd = ctypes.c_void_p(0x1001)
+    assert lib.ns_orthogonalize(odd, 8, 8, 1, 4, c, 2, 0, None) == NS_ERR_NOT_SUPPORTED
+    v = ctypes.c_void_p(0x1000)
+    assert lib.ns_orthogonalize(v, (1 << 30) + 1, 8, 1, 4, c, 2, 0, None) == NS_ERR_INVALID_VALUE
+
+
 def test_workspace_size_host_only():
     import paper_2512_04632_b200 as ns
     b = ns.workspace_size([(768, 768)])
