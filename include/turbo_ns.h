@@ -45,7 +45,9 @@
  *     not while `stream` is itself being captured; TNS_NOGRAPH=1 disables it).
  *   - Thread-safety: calls are serialised by an internal mutex; distinct streams are
  *     fine for distinct problem lists.  Calls with the SAME problem list share its cached
- *     workspace: on different streams the caller must order them (events).
+ *     workspace: a call on another stream than the previous call with that list waits
+ *     (cudaStreamWaitEvent) for the previous call's last launch; only while `stream` is
+ *     being captured must the caller order such calls itself.
  *   - Determinism: results are bitwise reproducible for identical inputs, and
  *     independent of how matrices are grouped into calls: every routing and tiling
  *     decision that changes the arithmetic (cluster kernel vs step engine, split-K Gram

@@ -240,6 +240,7 @@ struct Plan {
   bool graph_failed = false;
   bool pinned = false;             // resolved for a call in progress: never evicted
   cudaEvent_t last = nullptr;      // recorded on the caller's stream after every launch
+  cudaStream_t last_stream = nullptr;  // ... on this stream (a call on another stream waits for it)
   ~Plan() {
     // an executable graph still in flight is released on completion (cudaGraphExecDestroy);
     // device memory is freed stream-ordered after the last launch (release_async)
@@ -1073,6 +1074,15 @@ static ns_status launch_plan(Plan& P, DevCtx* dc, cudaStream_t stream) {
       graph = false;
     }
   }
+  // the plan's workspace is shared by every call with this problem list: a call on another
+  // stream than the previous one waits for that call's last launch (not while `stream` is
+  // being captured -- the caller's graph then owns the ordering)
+  if (P.last && P.last_stream != stream) {
+    cudaStreamCaptureStatus cs0 = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(stream, &cs0) == cudaSuccess && cs0 == cudaStreamCaptureStatusNone)
+      CU_TRY(cudaStreamWaitEvent(stream, P.last, 0));
+    cudaGetLastError();
+  }
   if (graph && !P.gexec && P.uses >= 1) capture_plan(P, dc);
   ++P.uses;
   ns_status st = NS_OK;
@@ -1087,7 +1097,10 @@ static ns_status launch_plan(Plan& P, DevCtx* dc, cudaStream_t stream) {
   cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
   if (st == NS_OK && cudaStreamIsCapturing(stream, &cs) == cudaSuccess && cs == cudaStreamCaptureStatusNone) {
     if (!P.last && cudaEventCreateWithFlags(&P.last, cudaEventDisableTiming) != cudaSuccess) P.last = nullptr;
-    if (P.last) CU_TRY(cudaEventRecord(P.last, stream));
+    if (P.last) {
+      CU_TRY(cudaEventRecord(P.last, stream));
+      P.last_stream = stream;
+    }
   }
   cudaGetLastError();
   return st;

@@ -667,6 +667,27 @@ def test_failed_second_plan_leaves_first_group_untouched():
         assert torch.equal(t, o)
 
 
+def test_same_list_on_two_streams_is_ordered():
+    """Thread-safety contract (turbo_ns.h): calls with the SAME problem list share its cached
+    workspace; a call on another stream than the previous one waits for that call's last
+    launch inside the library, so alternating streams with no caller-side events gives the
+    results of one stream (both engines: step engine and tcgen05 cluster kernel)."""
+    shapes = [(2048, 2048), (1024, 1024), (3072, 768), (1024, 128)]
+    xs = [torch.from_numpy(I.gaussian(m, n, seed=950 + i)).to(torch.bfloat16).cuda() for i, (m, n) in enumerate(shapes)]
+    outs = [torch.empty_like(x) for x in xs]
+    ns.orthogonalize_list(xs, out=outs, iters=4)
+    ref = [o.clone() for o in outs]
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    s1.wait_stream(torch.cuda.current_stream())
+    s2.wait_stream(torch.cuda.current_stream())
+    for i in range(8):
+        with torch.cuda.stream(s1 if i % 2 == 0 else s2):
+            ns.orthogonalize_list(xs, out=outs, iters=4)
+    torch.cuda.synchronize()
+    for a, b in zip(outs, ref):
+        assert torch.equal(a, b)
+
+
 def test_concurrent_streams_distinct_lists():
     """Thread-safety contract (turbo_ns.h): calls from several host threads, each on its own
     stream with its own problem list (step engine, tcgen05 cluster kernel and FFMA cluster
